@@ -1,0 +1,132 @@
+/*
+ * foe_b200.h -- C ABI of the B200-native FoE Poisson-denoise hot path.
+ *
+ * The reference (foepoisson, pure Python) has no FFI layer; its operator
+ * boundary is a set of numpy functions.  Each entry point below replaces one
+ * of them and keeps its argument meaning and error behaviour; citations are
+ * /root/reference/pkg/src/foepoisson/<file>:<line>.
+ *
+ * Conventions
+ *  - All image pointers are DEVICE pointers (row-major, contiguous), sizes are
+ *    plain ints; `stream` is a cudaStream_t passed as void* (NULL = legacy).
+ *  - Every call returns FOE_OK (0) or a negative FOE_E* code; the message of the
+ *    last failure on the calling host thread is available from foe_last_error().
+ *  - Calls are stream-ordered and re-entrant across host threads as long as
+ *    each call gets its own workspace (reference: independent denoise() jobs may
+ *    run concurrently, benchmark.py:117-121).
+ *  - Arithmetic is fp32 on device with fp64 reductions and fp64 solver scalars;
+ *    host-visible scalars (energies, trace) are fp64 like the reference.
+ */
+#ifndef FOE_B200_H
+#define FOE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum foe_status {
+    FOE_OK = 0,
+    FOE_E_INVALID = -1,   /* ValueError in the reference (image.py:23-34, prior.py:87-92, solver.py:94-118) */
+    FOE_E_CUDA = -2,      /* CUDA runtime failure */
+    FOE_E_NUMERICAL = -3, /* NumericalFailure (solver.py:26-31) -- per-image detail in foe_image_status */
+    FOE_E_UNSUPPORTED = -4
+};
+
+enum foe_boundary { FOE_SYMMETRIC = 0, FOE_PERIODIC = 1 }; /* image.py:17 BOUNDARY_RULES */
+enum foe_branch { FOE_QUADRATIC = 0, FOE_IDIV = 1 };       /* pipeline.py:193-204 */
+
+/* per-image solver outcome (solver.py:128-175) */
+enum foe_solve_status {
+    FOE_SOLVE_OK = 0,
+    FOE_SOLVE_NONFINITE = 1, /* non-finite smooth energy (solver.py:143-144) */
+    FOE_SOLVE_STALLED = 2    /* backtracking past max_lipschitz (solver.py:159-160) */
+};
+
+typedef struct foe_bank foe_bank; /* opaque device-resident filter bank */
+
+/* SolverConfig (solver.py:34-65) */
+typedef struct foe_solver_cfg {
+    double gamma;            /* inertial weight, default 0.8 */
+    double lipschitz_init;   /* L_{-1}, default 1.0 */
+    double backtrack_factor; /* eta, default 1.2 */
+    double relax_factor;     /* default 1.05 */
+    double rel_tol;          /* default 1e-6 */
+    double max_lipschitz;    /* default 1e15 */
+} foe_solver_cfg;
+
+/* per-image result of foe_solve; trace rows are in the caller's trace buffer */
+typedef struct foe_image_status {
+    int status;     /* foe_solve_status */
+    int n_iters;    /* accepted iterations == len(SolverTrace) */
+    int n_trials;   /* trial energies evaluated (backtracking included) */
+    int failed_at;  /* iteration index of the failure, -1 if none */
+} foe_image_status;
+
+int foe_abi_version(void);
+const char *foe_last_error(void);
+int foe_device_sm_count(int device);
+
+/* ---- filter bank: FoEModel.filters (prior.py:75-78) + weights --------------------------------
+ * filters: host float64 (n, m, m) in true-convolution orientation (what convolve_same takes,
+ * image.py:37-58); weights: host float64 (n), strictly positive (prior.py:64-66).
+ * m odd in {1,3,5,7}; n*m*m <= 4096.  Uploaded to the current device. */
+int foe_bank_create(const double *filters, const double *weights, int n, int m, int boundary,
+                    foe_bank **out);
+int foe_bank_destroy(foe_bank *bank);
+int foe_bank_info(const foe_bank *bank, int *n, int *m, int *boundary);
+
+/* ---- elementwise ------------------------------------------------------------------------------ */
+/* anscombe_forward, anscombe.py:19-24: v = 2 sqrt(y + 3/8) (y validated >= 0 by the caller) */
+int foe_anscombe_forward(const double *y, float *v, int64_t n, void *stream);
+/* denoise_direct obs, pipeline.py:165: obs = where(y == 0, c, y) */
+int foe_direct_obs(const double *y, float *obs, double c, int64_t n, void *stream);
+/* anscombe_inverse_exact_unbiased, anscombe.py:33-51; fp64 output from fp32 z.
+ * counts (device, 2 x uint64, nullable): [n_clamped_input, n_clamped_output] (added to) */
+int foe_anscombe_inverse_exact_unbiased(const float *z, double *x, int64_t n,
+                                        unsigned long long *counts, void *stream);
+/* prox_quadratic, solver.py:92-100 and prox_idiv, solver.py:103-125 (t >= 0) */
+int foe_prox_quadratic(const float *u_tilde, const float *v, float *out, double t, int64_t n,
+                       void *stream);
+int foe_prox_idiv(const float *u_tilde, const float *obs, float *out, double t, int64_t n,
+                  void *stream);
+
+/* ---- operators ---------------------------------------------------------------------------------
+ * convolve_same (image.py:37-58) / convolve_adjoint (image.py:68-83) with filter `index` of the
+ * bank, B images of H x W.  Reference-operator surface for tests; the solve uses the fused pass. */
+int foe_convolve_same(const foe_bank *bank, int index, const float *x, float *out, int B, int H,
+                      int W, void *stream);
+int foe_convolve_adjoint(const foe_bank *bank, int index, const float *y, float *out, int B, int H,
+                         int W, void *stream);
+
+/* foe_energy (prior.py:95-101) + foe_gradient (prior.py:104-110) fused in one pass.
+ * u, grad: device (B, H, W) fp32; energy: device fp64 (B).  workspace >= foe_eval_workspace_size. */
+size_t foe_eval_workspace_size(const foe_bank *bank, int B, int H, int W);
+int foe_energy_grad(const foe_bank *bank, const float *u, float *grad, double *energy, int B, int H,
+                    int W, void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---- the solver --------------------------------------------------------------------------------
+ * ipiano_minimize (solver.py:128-175) with FoE callbacks (pipeline.py:167-172, 205-208) for B
+ * independent images, fully device-resident: every backtracking decision is taken on the device.
+ *   u0, obs      device (B,H,W) fp32: start point and data-term observation (v or y-with-c)
+ *   lam, branch, max_iters   host arrays (B): data weight, foe_branch, iteration budget
+ *   u_out        device (B,H,W) fp32: final iterate
+ *   status       host (B) results;  trace  host (B, trace_cap, 6) fp64 rows F,G,L,step,slack,tol
+ *   trace_cap >= max(max_iters).  Returns FOE_E_NUMERICAL if any image failed (others valid). */
+size_t foe_solve_workspace_size(const foe_bank *bank, int B, int H, int W, int trace_cap);
+int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfg, int B, int H, int W,
+              const float *u0, const float *obs, const double *lam, const int *branch,
+              const int *max_iters, float *u_out, foe_image_status *status, double *trace,
+              int trace_cap, void *workspace, size_t workspace_bytes, void *stream);
+
+/* benchmark hook: run `reps` back-to-back trial passes of the fused kernel on the state left by
+ * the last foe_solve in `workspace` without changing it (decisions suppressed). */
+int foe_bench_trial_pass(const foe_bank *bank, int B, int H, int W, int trace_cap, int reps,
+                         void *workspace, size_t workspace_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FOE_B200_H */

@@ -1,0 +1,307 @@
+"""CPU oracle for the FoE denoise hot path -- TEST INFRASTRUCTURE ONLY.
+
+Python face of ``oracle/foe_oracle.c`` (float64 restatement of the reference
+``foepoisson`` hot path) plus the host-side rules of ``pipeline.py`` restated in
+plain Python/numpy.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py`` (cpu_baseline leg and ``--impl reference`` arm) may import this
+module; the product package never does.
+
+Pinned against golden vectors produced by the reference itself
+(``tests/golden/make_golden.py`` -> ``tests/golden/*.npz``), see
+``tests/test_oracle.py``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_lp = ctypes.POINTER(ctypes.c_long)
+_ip = ctypes.POINTER(ctypes.c_int)
+
+BOUNDARY_CODES = {"symmetric": 0, "periodic": 1}
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with oracle/Makefile (gcc, no GPU needed)."""
+    src = os.path.join(_HERE, "foe_oracle.c")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = ctypes.CDLL(_LIB_PATH)
+        L.orc_convolve_same.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp, ctypes.c_int, ctypes.c_int, _dp]
+        L.orc_convolve_adjoint.argtypes = L.orc_convolve_same.argtypes
+        L.orc_foe_energy.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.orc_foe_energy.restype = ctypes.c_double
+        L.orc_foe_gradient.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp, _dp, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, _dp]
+        L.orc_prox_quadratic.argtypes = [_dp, _dp, ctypes.c_double, ctypes.c_long, _dp]
+        L.orc_prox_idiv.argtypes = [_dp, _dp, ctypes.c_double, ctypes.c_long, _dp]
+        L.orc_anscombe_forward.argtypes = [_dp, ctypes.c_long, _dp]
+        L.orc_anscombe_inverse_exact_unbiased.argtypes = [_dp, ctypes.c_long, _dp, _lp]
+        L.orc_ipiano_foe.argtypes = [_dp, _dp, ctypes.c_int, ctypes.c_int, _dp, _dp, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                     ctypes.c_double, _dp, _dp, _ip, _ip]
+        L.orc_ipiano_foe.restype = ctypes.c_int
+        L.orc_num_threads.restype = ctypes.c_int
+        L.orc_set_num_threads.argtypes = [ctypes.c_int]
+        _lib = L
+    return _lib
+
+
+def num_threads() -> int:
+    return lib().orc_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    lib().orc_set_num_threads(int(n))
+
+
+def _c(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a):
+    return a.ctypes.data_as(_dp)
+
+
+# --------------------------------------------------------------------------
+# filter basis / model decode: image.py:117-130 (dct_basis), prior.py:75-78
+
+
+def dct_atoms(m: int) -> np.ndarray:
+    """Zero-mean orthonormal 2-D DCT-II atoms (m*m - 1, m, m); image.py:117-130."""
+    i = np.arange(m)
+    d = np.cos(np.pi * (2 * i[None, :] + 1) * i[:, None] / (2 * m))
+    d[0] *= np.sqrt(1.0 / m)
+    d[1:] *= np.sqrt(2.0 / m)
+    return np.einsum("pi,qj->pqij", d, d).reshape(m * m, m, m)[1:].copy()
+
+
+@dataclass
+class OracleModel:
+    """Filter bank in the reference's terms: filters (N, m, m), weights (N,)."""
+
+    filters: np.ndarray
+    weights: np.ndarray
+    boundary: str = "symmetric"
+    domain_tag: str = "anscombe"
+
+    @property
+    def m(self) -> int:
+        return self.filters.shape[1]
+
+    @property
+    def n(self) -> int:
+        return self.filters.shape[0]
+
+
+def read_foe(path) -> OracleModel:
+    """Minimal FOE 1 reader (fileio.py:51-79) for the oracle side."""
+    with open(path) as fh:
+        lines = [ln.strip() for ln in fh if ln.strip()]
+    assert lines[0] == "FOE 1"
+    tag, nf, m, basis, boundary = lines[1].split()
+    nf, m = int(nf), int(m)
+    assert basis == f"dct{m}"
+    rows = np.array([[float(t) for t in ln.split()] for ln in lines[2:2 + nf]])
+    atoms = dct_atoms(m)
+    filters = np.tensordot(rows[:, 1:], atoms, axes=1)
+    return OracleModel(filters=filters, weights=rows[:, 0].copy(), boundary=boundary, domain_tag=tag)
+
+
+# --------------------------------------------------------------------------
+# numerics core (foe_oracle.c)
+
+
+def convolve_same(x, k, boundary="symmetric"):
+    """image.py:37-58."""
+    x = _c(x)
+    k = _c(k)
+    out = np.empty_like(x)
+    lib().orc_convolve_same(_p(x), x.shape[0], x.shape[1], _p(k), k.shape[0], BOUNDARY_CODES[boundary], _p(out))
+    return out
+
+
+def convolve_adjoint(y, k, boundary="symmetric"):
+    """image.py:68-83."""
+    y = _c(y)
+    k = _c(k)
+    out = np.empty_like(y)
+    lib().orc_convolve_adjoint(_p(y), y.shape[0], y.shape[1], _p(k), k.shape[0], BOUNDARY_CODES[boundary], _p(out))
+    return out
+
+
+def foe_energy(u, model: OracleModel) -> float:
+    """prior.py:95-101."""
+    u = _c(u)
+    f = _c(model.filters)
+    w = _c(model.weights)
+    return float(lib().orc_foe_energy(_p(u), u.shape[0], u.shape[1], _p(f), _p(w), model.n, model.m,
+                                      BOUNDARY_CODES[model.boundary]))
+
+
+def foe_gradient(u, model: OracleModel) -> np.ndarray:
+    """prior.py:104-110."""
+    u = _c(u)
+    f = _c(model.filters)
+    w = _c(model.weights)
+    g = np.empty_like(u)
+    lib().orc_foe_gradient(_p(u), u.shape[0], u.shape[1], _p(f), _p(w), model.n, model.m,
+                           BOUNDARY_CODES[model.boundary], _p(g))
+    return g
+
+
+def prox_quadratic(ut, t, v):
+    """solver.py:92-100."""
+    ut = _c(ut)
+    v = _c(v)
+    out = np.empty_like(ut)
+    lib().orc_prox_quadratic(_p(ut), _p(v), float(t), ut.size, _p(out))
+    return out
+
+
+def prox_idiv(ut, t, obs):
+    """solver.py:103-125."""
+    ut = _c(ut)
+    obs = _c(obs)
+    out = np.empty_like(ut)
+    lib().orc_prox_idiv(_p(ut), _p(obs), float(t), ut.size, _p(out))
+    return out
+
+
+def anscombe_forward(y):
+    """anscombe.py:19-24."""
+    y = _c(y)
+    if y.min() < 0:
+        raise ValueError("counts must be nonnegative")
+    v = np.empty_like(y)
+    lib().orc_anscombe_forward(_p(y), y.size, _p(v))
+    return v
+
+
+def anscombe_inverse_exact_unbiased(z, diagnostics=None):
+    """anscombe.py:33-51."""
+    z = _c(z)
+    x = np.empty_like(z)
+    cnt = (ctypes.c_long * 2)()
+    lib().orc_anscombe_inverse_exact_unbiased(_p(z), z.size, _p(x), cnt)
+    if diagnostics is not None:
+        diagnostics["n_clamped_input"] = int(cnt[0])
+        diagnostics["n_clamped_output"] = int(cnt[1])
+    return x
+
+
+@dataclass
+class OracleTrace:
+    F: list = field(default_factory=list)
+    G: list = field(default_factory=list)
+    L: list = field(default_factory=list)
+    step_norm: list = field(default_factory=list)
+    descent_slack: list = field(default_factory=list)
+    slack_tol: list = field(default_factory=list)
+    n_trials: int = 0
+    status: int = 0
+
+
+def ipiano_foe(u0, obs, model: OracleModel, lam, branch, *, gamma=0.8, lipschitz_init=1.0,
+               backtrack_factor=1.2, relax_factor=1.05, max_iters=150, rel_tol=1e-6,
+               max_lipschitz=1e15):
+    """ipiano_minimize (solver.py:128-175) with FoE callbacks (pipeline.py:167-172, 205-208).
+
+    branch: "quadratic" or "idiv" (prox and energy_G, pipeline.py:197-204).
+    Returns (u, OracleTrace)."""
+    u0 = _c(u0)
+    obs = _c(obs)
+    f = _c(model.filters)
+    w = _c(model.weights)
+    H, W = u0.shape
+    u = np.empty_like(u0)
+    trace = np.zeros((max_iters, 6))
+    it = ctypes.c_int(0)
+    tr = ctypes.c_int(0)
+    status = lib().orc_ipiano_foe(_p(u0), _p(obs), H, W, _p(f), _p(w), model.n, model.m,
+                                  BOUNDARY_CODES[model.boundary], float(lam),
+                                  0 if branch == "quadratic" else 1, gamma, lipschitz_init,
+                                  backtrack_factor, relax_factor, int(max_iters), rel_tol,
+                                  max_lipschitz, _p(u), _p(trace), ctypes.byref(it), ctypes.byref(tr))
+    n = it.value
+    t = OracleTrace(F=list(trace[:n, 0]), G=list(trace[:n, 1]), L=list(trace[:n, 2]),
+                    step_norm=list(trace[:n, 3]), descent_slack=list(trace[:n, 4]),
+                    slack_tol=list(trace[:n, 5]), n_trials=tr.value, status=status)
+    return u, t
+
+
+# --------------------------------------------------------------------------
+# pipeline rules (pipeline.py:83-131) restated
+
+
+QUADRATIC_PEAK_THRESHOLD = 5.0  # pipeline.py:25
+BIN_FACTOR = 3  # noise.py:9
+
+
+def load_lambda_table(path):
+    with open(path) as fh:
+        return json.load(fh)
+
+
+def solver_budget(peak: float) -> int:
+    """pipeline.py:83-87: 150 iterations below peak 5, else 60."""
+    return 150 if peak < QUADRATIC_PEAK_THRESHOLD else 60
+
+
+def select_lambda(peak, variant, table, force_branch=None) -> float:
+    """pipeline.py:98-131: log-log interpolation, clamped at the ends."""
+    if variant == "direct":
+        name, p = "direct", peak
+    else:
+        p = peak * BIN_FACTOR ** 2 if variant == "transform_binned" else peak
+        if force_branch is not None:
+            name = f"transform_{force_branch}"
+        elif p >= QUADRATIC_PEAK_THRESHOLD:
+            name = "transform_quadratic"
+        else:
+            name = "transform_idiv"
+    rows = sorted(table["tables"][name])
+    peaks = np.array([r[0] for r in rows])
+    lams = np.array([r[1] for r in rows])
+    return float(np.exp(np.interp(np.log(p), np.log(peaks), np.log(lams))))
+
+
+def denoise(noisy, peak, model: OracleModel, variant, table, lam="auto", zero_offset_c=0.1,
+            force_branch=None, rel_tol=1e-6, max_iters=None):
+    """denoise_transform / denoise_direct (pipeline.py:152-211) on the C oracle.
+
+    max_iters=None applies solver_budget (pipeline.py:83-87); an explicit value
+    bypasses it (the truncated-oracle mode of SURVEY.md Appendix B)."""
+    noisy = _c(noisy)
+    lam_v = select_lambda(peak, variant, table, force_branch) if lam == "auto" else float(lam)
+    iters = solver_budget(peak) if max_iters is None else int(max_iters)
+    if variant == "direct":
+        obs = np.where(noisy == 0, zero_offset_c, noisy)
+        u, tr = ipiano_foe(obs, obs, model, lam_v, "idiv", max_iters=iters, rel_tol=rel_tol)
+        return {"image": u, "branch": "direct_idiv", "lam": lam_v, "trace": tr, "transformed": None}
+    v = anscombe_forward(noisy)
+    quadratic = (force_branch == "quadratic") if force_branch is not None else peak >= QUADRATIC_PEAK_THRESHOLD
+    branch = "quadratic" if quadratic else "idiv"
+    u, tr = ipiano_foe(v, v, model, lam_v, branch, max_iters=iters, rel_tol=rel_tol)
+    return {"image": anscombe_inverse_exact_unbiased(u), "branch": f"transform_{branch}", "lam": lam_v,
+            "trace": tr, "transformed": u}

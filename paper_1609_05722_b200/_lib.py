@@ -1,0 +1,127 @@
+"""Build and load ``libfoe_b200.so`` (the sm_100a CUDA library behind ``include/foe_b200.h``).
+
+There is no CPU fallback: every operator of this package runs through this
+library, and loading it fails loudly when it has not been built.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(PKG)
+SRC = os.path.join(PKG, "csrc", "foe_b200.cu")
+INCLUDE = os.path.join(REPO, "include")
+LIB_PATH = os.path.join(PKG, "libfoe_b200.so")
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+FOE_OK, FOE_E_INVALID, FOE_E_CUDA, FOE_E_NUMERICAL, FOE_E_UNSUPPORTED = 0, -1, -2, -3, -4
+
+
+def _sources():
+    d = os.path.join(PKG, "csrc")
+    return [os.path.join(d, f) for f in sorted(os.listdir(d)) if f.endswith((".cu", ".cuh", ".h"))] + \
+        [os.path.join(INCLUDE, f) for f in sorted(os.listdir(INCLUDE))]
+
+
+def needs_build() -> bool:
+    if not os.path.exists(LIB_PATH):
+        return True
+    t = os.path.getmtime(LIB_PATH)
+    return any(os.path.getmtime(s) > t for s in _sources())
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """nvcc -gencode arch=compute_100a,code=sm_100a ... -> libfoe_b200.so (no GPU needed)."""
+    if not force and not needs_build():
+        return LIB_PATH
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-I" + INCLUDE, "-o", LIB_PATH + ".tmp", SRC]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stderr[-4000:])
+    os.replace(LIB_PATH + ".tmp", LIB_PATH)
+    if verbose:
+        print(res.stderr)
+    return LIB_PATH
+
+
+class FoeError(RuntimeError):
+    pass
+
+
+_lib = None
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+
+
+class SolverCfgC(ctypes.Structure):
+    _fields_ = [("gamma", ctypes.c_double), ("lipschitz_init", ctypes.c_double),
+                ("backtrack_factor", ctypes.c_double), ("relax_factor", ctypes.c_double),
+                ("rel_tol", ctypes.c_double), ("max_lipschitz", ctypes.c_double)]
+
+
+class ImageStatusC(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int), ("n_iters", ctypes.c_int), ("n_trials", ctypes.c_int),
+                ("failed_at", ctypes.c_int)]
+
+
+def lib():
+    """The loaded CUDA library; raises if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise FoeError(f"{LIB_PATH} is not built; run paper_1609_05722_b200._lib.build() "
+                       "(or __graft_entry__.build()) -- there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    L.foe_last_error.restype = ctypes.c_char_p
+    L.foe_abi_version.restype = ctypes.c_int
+    L.foe_device_sm_count.argtypes = [ctypes.c_int]
+    L.foe_bank_create.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]
+    L.foe_bank_destroy.argtypes = [_vp]
+    L.foe_bank_info.argtypes = [_vp, _vp, _vp, _vp]
+    L.foe_anscombe_forward.argtypes = [_vp, _vp, _i64, _vp]
+    L.foe_direct_obs.argtypes = [_vp, _vp, ctypes.c_double, _i64, _vp]
+    L.foe_anscombe_inverse_exact_unbiased.argtypes = [_vp, _vp, _i64, _vp, _vp]
+    L.foe_prox_quadratic.argtypes = [_vp, _vp, _vp, ctypes.c_double, _i64, _vp]
+    L.foe_prox_idiv.argtypes = [_vp, _vp, _vp, ctypes.c_double, _i64, _vp]
+    L.foe_convolve_same.argtypes = [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp]
+    L.foe_convolve_adjoint.argtypes = L.foe_convolve_same.argtypes
+    L.foe_eval_workspace_size.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    L.foe_eval_workspace_size.restype = ctypes.c_size_t
+    L.foe_energy_grad.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                  ctypes.c_size_t, _vp]
+    L.foe_solve_workspace_size.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    L.foe_solve_workspace_size.restype = ctypes.c_size_t
+    L.foe_solve.argtypes = [_vp, ctypes.POINTER(SolverCfgC), ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp,
+                            _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
+    L.foe_bench_trial_pass.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       _vp, ctypes.c_size_t, _vp]
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str = "") -> int:
+    if rc == FOE_OK:
+        return rc
+    msg = lib().foe_last_error().decode(errors="replace")
+    if rc == FOE_E_INVALID:
+        raise ValueError(f"{what}: {msg}" if what else msg)
+    raise FoeError(f"{what} failed ({rc}): {msg}")
+
+
+EXPORTED_SYMBOLS = [
+    "foe_abi_version", "foe_last_error", "foe_device_sm_count", "foe_bank_create", "foe_bank_destroy",
+    "foe_bank_info", "foe_anscombe_forward", "foe_direct_obs", "foe_anscombe_inverse_exact_unbiased",
+    "foe_prox_quadratic", "foe_prox_idiv", "foe_convolve_same", "foe_convolve_adjoint",
+    "foe_eval_workspace_size", "foe_energy_grad", "foe_solve_workspace_size", "foe_solve",
+    "foe_bench_trial_pass",
+]

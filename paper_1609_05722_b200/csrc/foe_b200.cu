@@ -1,0 +1,1057 @@
+// foe_b200.cu -- B200 (sm_100a) kernels and C ABI for the FoE Poisson-denoise hot path.
+//
+// Reference path (/root/reference/pkg/src/foepoisson):
+//   denoise (pipeline.py:242-244) -> anscombe_forward (anscombe.py:19-24)
+//   -> ipiano_minimize (solver.py:128-175) over foe_energy / foe_gradient (prior.py:95-110)
+//      with prox_quadratic / prox_idiv (solver.py:92-125)
+//   -> anscombe_inverse_exact_unbiased (anscombe.py:33-51)
+//
+// Design:
+//  * One fused "pass" kernel evaluates one iPiano trial for every live image of a batch:
+//    trial point + prox (elementwise, in a shared-memory tile with a 2r halo), the forward
+//    responses K_i u_new and K_i du of all filters, rho'(z), the exact adjoint K_i^T with the
+//    symmetric-boundary fold done in-tile, the energy change dF = sum a_i log1p(dz(2z_o+dz)/(1+z_o^2))
+//    and the dot products <du,du>, <g,du>, |u|^2, G(u_new) -- one HBM pass per trial.
+//  * Per-tile fp64 partials are summed in a fixed order by the last CTA of each image, which also
+//    takes the accept/reject decision, updates L and rotates the state buffers: no host round trip.
+//  * A trial that is accepted already carries grad F(u_new) for the next iteration (speculative
+//    gradient), so every pass is one trial: ~1.37 passes per accepted iteration.
+#include "foe_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+struct foe_bank {
+    int n, m, boundary, device;
+    float *d_kf, *d_alpha;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define FOE_CUDA(x)                                                                              \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess) return fail(FOE_E_CUDA, "%s: %s", #x, cudaGetErrorString(e_));    \
+    } while (0)
+
+constexpr int kMaxTaps = 4096;
+constexpr int kMaxFilters = 512;
+constexpr int kNumPartials = 7;  // dF|F, sq, gd, |u|^2, G_a, G_b, G_bad
+constexpr int kPartialStride = 8;
+
+enum PassMode { MODE_EVAL = 0, MODE_INIT = 1, MODE_TRIAL = 2 };
+
+struct ImgCtl {
+    double L, f_u, lam;
+    int n, max_iters, trials, status, done, branch, failed_at;
+    int iu, iup, inew, ig, ignew;
+    int pad[2];
+};
+
+struct PassArgs {
+    int B, H, W, n_filters, tiles_x, tiles_y, mode, no_decide;
+    size_t plane;  // B*H*W: distance between state slots
+    const float *kf;     // (n, M*M) flipped taps (correlation orientation of the forward conv)
+    const float *alpha;  // (n)
+    // state (solve modes)
+    float *U;        // 3 slots
+    float *Gs;       // 2 slots
+    const float *obs;
+    ImgCtl *ctl;
+    double *trace;
+    int trace_cap;
+    int *n_active;
+    // eval mode
+    const float *u_in;
+    float *g_out;
+    double *energy_out;
+    // reductions
+    double *partials;     // (B, tiles, kPartialStride)
+    unsigned *tickets;    // (B)
+    // solver constants
+    double gamma, step_num, eta, relax, rel_tol, max_L;
+};
+
+// ------------------------------------------------------------------------------------------------
+// geometry
+
+// Owned-row partition of the image into tiles of T rows; the last tile is pulled up so it owns at
+// least r rows: every pixel within r of the far edge then lies in a tile whose region also holds
+// the padded pixels that fold onto it (symmetric boundary, image.py:61-83).
+__host__ __device__ __forceinline__ int tile_start(int k, int nt, int T, int n, int r) {
+    if (k >= nt) return n;
+    int s = k * T;
+    if (k == nt - 1 && nt > 1) s = (s < n - r) ? s : n - r;
+    return s;
+}
+
+// np.pad index map (image.py:61-65): "symmetric" (edge-inclusive mirror) or "wrap"; clamped so
+// far-out (don't-care) positions of partial tiles stay in bounds.
+template <bool SYM>
+__device__ __forceinline__ int src_idx(int q, int n) {
+    if (SYM) {
+        if (q < 0) q = -1 - q;
+        if (q >= n) q = 2 * n - 1 - q;
+        return q < 0 ? 0 : (q >= n ? n - 1 : q);
+    } else {
+        q %= n;
+        return q < 0 ? q + n : q;
+    }
+}
+
+template <int M_>
+struct PassCfg {
+    static constexpr int M = M_;
+    static constexpr int R = M / 2;
+    static constexpr int RH = 48, RW = 48;  // region = owned tile + r ring
+    static constexpr int MY = 6;            // micro-tile: MY rows x 4 cols per thread
+    static constexpr int G = 3;             // filter groups per CTA
+    static constexpr int FG = 2;            // filters per group between barriers
+    static constexpr int NTX = RW / 4, NTY = RH / MY, NTG = NTX * NTY, NT = G * NTG;
+    static constexpr int CW = RW + 2 * R;  // staged columns
+    static constexpr int SH = RH + 2 * R;  // staged rows
+    // row pitch: multiple of 4 (float4) with MY*SW == 16 (mod 32) -> conflict-free LDS.128
+    static constexpr int pitch() {
+        int p = (CW + 3) & ~3;
+        while ((MY * p) % 32 != 16) p += 4;
+        return p;
+    }
+    static constexpr int SW = pitch();
+    static constexpr int PLANE = SH * SW;
+    static constexpr int TH = RH - 2 * R, TW = RW - 2 * R;  // max owned tile
+    static_assert(NTG % 32 == 0, "filter groups must be whole warps");
+    static_assert(TH >= 2 * R, "tile too small for the fold rule");
+};
+
+template <int W>
+__device__ __forceinline__ void load_row(const float *p, float (&r)[W]) {
+#pragma unroll
+    for (int k = 0; k + 4 <= W; k += 4) {
+        const float4 v = *reinterpret_cast<const float4 *>(p + k);
+        r[k] = v.x; r[k + 1] = v.y; r[k + 2] = v.z; r[k + 3] = v.w;
+    }
+    if constexpr ((W & 3) >= 2) {
+        const float2 v = *reinterpret_cast<const float2 *>(p + (W & ~3));
+        r[W & ~3] = v.x; r[(W & ~3) + 1] = v.y;
+    }
+    if constexpr ((W & 1) == 1) r[W - 1] = p[W - 1];
+}
+
+__device__ __forceinline__ float prox_quad(float ut, float t, float v) {
+    return (ut + t * v) / (1.0f + t);  // solver.py:100
+}
+
+__device__ __forceinline__ float prox_idv(float ut, float t, float ob) {
+    if (t == 0.0f) return ut;  // solver.py:119-120
+    const float a = ut - t;
+    const float root = sqrtf(fmaf(a, a, 4.0f * t * ob));
+    float o = (a >= 0.0f) ? 0.5f * (a + root) : (2.0f * t * ob) / (root - a);  // solver.py:121-124
+    if (ob == 0.0f && a < 0.0f) o = 0.0f;                                      // solver.py:125
+    return o;
+}
+
+// ------------------------------------------------------------------------------------------------
+// decision (the body of the backtracking loop, solver.py:147-174), run by one thread per image
+
+__device__ void finish_image(const PassArgs &a, ImgCtl &c) {
+    c.done = 1;
+    atomicSub(a.n_active, 1);
+}
+
+__device__ void decide(const PassArgs &a, int b, const double *s) {
+    ImgCtl &c = a.ctl[b];
+    if (a.mode == MODE_INIT) {
+        c.f_u = s[0];
+        if (!isfinite(s[0])) {  // solver.py:142-144
+            c.status = FOE_SOLVE_NONFINITE;
+            c.failed_at = c.n;
+            finish_image(a, c);
+        }
+        return;
+    }
+    const double L = c.L;
+    const double dF = s[0], sq = s[1], gd = s[2], un2 = s[3];
+    const double f_new = c.f_u + dF;
+    // slack = f_new - (f_u + gd + L/2 sq), evaluated from dF directly (solver.py:154-155)
+    const double slack = dF - (gd + 0.5 * L * sq);
+    const double tol = 1e-12 * (fabs(c.f_u) + fabs(f_new) + fabs(gd) + 0.5 * L * sq);
+    c.trials++;
+    if (isfinite(f_new) && slack <= tol) {  // solver.py:156
+        double Gv;
+        if (c.branch == FOE_QUADRATIC) Gv = 0.5 * c.lam * s[4];  // pipeline.py:200
+        else Gv = (s[6] > 0.0) ? INFINITY : c.lam * (s[4] - s[5]);  // pipeline.py:141-149
+        const double step = sqrt(sq);
+        double *row = a.trace + ((size_t)b * a.trace_cap + c.n) * 6;  // solver.py:162-169
+        row[0] = f_new; row[1] = Gv; row[2] = L; row[3] = step; row[4] = slack; row[5] = tol;
+        const int old_up = c.iup;  // u_prev, u = u, u_new (solver.py:171)
+        c.iup = c.iu; c.iu = c.inew; c.inew = old_up;
+        const int og = c.ig; c.ig = c.ignew; c.ignew = og;
+        c.f_u = f_new;
+        c.L = L / a.relax;  // solver.py:172
+        c.n++;
+        const double un = sqrt(un2);
+        if (step < a.rel_tol * fmax(un, 1e-300) || c.n >= c.max_iters) finish_image(a, c);  // :173-174
+    } else {
+        c.L = L * a.eta;  // solver.py:158-160
+        if (c.L > a.max_L) {
+            c.status = FOE_SOLVE_STALLED;
+            c.failed_at = c.n;
+            finish_image(a, c);
+        }
+    }
+}
+
+// fixed-order block reduction of kNumPartials doubles (deterministic)
+template <int NT>
+__device__ __forceinline__ void block_reduce(double (&v)[kNumPartials], double (*red)[kNumPartials],
+                                             double *out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) {
+        double x = v[k];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+        if (lane == 0) red[warp][k] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < kNumPartials) {
+        double s = 0.0;
+#pragma unroll 1
+        for (int w = 0; w < NT / 32; ++w) s += red[w][threadIdx.x];
+        out[threadIdx.x] = s;
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// the fused pass
+
+template <int M, bool TRIAL, bool SYM>
+__global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
+    using C = PassCfg<M>;
+    constexpr int R = C::R, SW = C::SW, CW = C::CW, SH = C::SH, MY = C::MY, NT = C::NT;
+    constexpr int WIN = 4 + 2 * R;
+
+    extern __shared__ __align__(16) float sm[];
+    __shared__ double red[NT / 32][kNumPartials];
+    __shared__ double s_sum[kNumPartials];
+    __shared__ int s_last;
+
+    const int tid = threadIdx.x;
+    const int b = blockIdx.y;
+    const int H = a.H, W = a.W, nf = a.n_filters;
+
+    int iu = 0, iup = 0, inew = 0, ig = 0, ignew = 0, branch = 0;
+    float tau32 = 0.f, t32 = 0.f, gam32 = 0.f;
+    if (a.mode != MODE_EVAL) {
+        const ImgCtl &c = a.ctl[b];
+        if (c.done && !a.no_decide) return;
+        iu = c.iu; iup = c.iup; inew = c.inew; ig = c.ig; ignew = c.ignew; branch = c.branch;
+        if (TRIAL) {
+            const double tau = a.step_num / c.L;  // SolverConfig.step_size, solver.py:64-65
+            tau32 = (float)tau;
+            t32 = (float)(tau * c.lam);
+            gam32 = (float)a.gamma;
+        }
+    }
+    const size_t HW = (size_t)H * W;
+    const size_t ioff = (size_t)b * HW;
+    const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
+    float *gout, *uout = nullptr;
+    if (a.mode == MODE_EVAL) {
+        uin = a.u_in + ioff;
+        gout = a.g_out + ioff;
+    } else {
+        uin = a.U + iu * a.plane + ioff;
+        if (TRIAL) {
+            upv = a.U + iup * a.plane + ioff;
+            gin = a.Gs + ig * a.plane + ioff;
+            obs = a.obs + ioff;
+            uout = a.U + inew * a.plane + ioff;
+            gout = a.Gs + ignew * a.plane + ioff;
+        } else {
+            gout = a.Gs + ig * a.plane + ioff;
+        }
+    }
+
+    const int t = blockIdx.x;
+    const int tyi = t / a.tiles_x, txi = t - tyi * a.tiles_x;
+    const int s0 = tile_start(tyi, a.tiles_y, C::TH, H, R), s1 = tile_start(tyi + 1, a.tiles_y, C::TH, H, R);
+    const int c0 = tile_start(txi, a.tiles_x, C::TW, W, R), c1 = tile_start(txi + 1, a.tiles_x, C::TW, W, R);
+    const int ry0 = s0 - R, rx0 = c0 - R;  // region origin; staged cell (i,j) <-> (ry0-R+i, rx0-R+j)
+
+    float *Un = sm;
+    float *Du = Un + C::PLANE;
+    float *Psi = TRIAL ? Du + C::PLANE : Du;
+    float *s_taps = Psi + C::G * C::FG * C::PLANE;
+    float *s_alpha = s_taps + nf * M * M;
+
+    for (int k = tid; k < nf * M * M; k += NT) s_taps[k] = a.kf[k];
+    for (int k = tid; k < nf; k += NT) s_alpha[k] = a.alpha[k];
+    // zero ring of every psi plane: psi_0 = 0 outside the region (and outside the image)
+    if constexpr (R > 0) {
+        constexpr int RING = SH * CW - C::RH * C::RW;
+        for (int k = tid; k < C::G * C::FG * RING; k += NT) {
+            const int pl = k / RING, e = k - pl * RING;
+            int i, j;
+            if (e < R * CW) { i = e / CW; j = e - i * CW; }
+            else if (e < 2 * R * CW) { const int e2 = e - R * CW; i = C::RH + R + e2 / CW; j = e2 % CW; }
+            else { const int e3 = e - 2 * R * CW; i = R + e3 / (2 * R); const int jj = e3 % (2 * R); j = jj < R ? jj : C::RW + jj; }
+            Psi[pl * C::PLANE + i * SW + j] = 0.0f;
+        }
+    }
+
+    // ---- prologue: stage u (EVAL/INIT) or the trial point u_new and du (TRIAL) -------------------
+    double acc[kNumPartials];
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
+    for (int k = tid; k < SH * CW; k += NT) {
+        const int i = k / CW, j = k - i * CW;
+        const int gy = ry0 - R + i, gx = rx0 - R + j;
+        const size_t o = (size_t)src_idx<SYM>(gy, H) * W + src_idx<SYM>(gx, W);
+        if (TRIAL) {
+            const float u = __ldg(uin + o), up = __ldg(upv + o), g = __ldg(gin + o), ob = __ldg(obs + o);
+            // u - tau g + gamma (u - u_prev)  (solver.py:146-149)
+            const float ut = (u - tau32 * g) + gam32 * (u - up);
+            const float un = (branch == FOE_QUADRATIC) ? prox_quad(ut, t32, ob) : prox_idv(ut, t32, ob);
+            const float du = un - u;
+            Un[i * SW + j] = un;
+            Du[i * SW + j] = du;
+            if (gy >= s0 && gy < s1 && gx >= c0 && gx < c1) {
+                acc[1] += (double)du * (double)du;  // vdot(du, du)  solver.py:152
+                acc[2] += (double)g * (double)du;   // vdot(g, du)   solver.py:153
+                acc[3] += (double)u * (double)u;    // |u|^2 for the stop test, solver.py:173
+                if (branch == FOE_QUADRATIC) {
+                    const double d = (double)un - (double)ob;
+                    acc[4] += d * d;
+                } else {
+                    acc[4] += (double)un;
+                    if (ob > 0.0f) {
+                        if (un > 0.0f) acc[5] += (double)ob * (double)logf(un);
+                        else acc[6] += 1.0;
+                    }
+                }
+            }
+        } else {
+            Un[i * SW + j] = __ldg(uin + o);
+        }
+    }
+    __syncthreads();
+
+    // ---- filter loop -----------------------------------------------------------------------------
+    const int grp = tid / C::NTG, lt = tid - grp * C::NTG;
+    const int tx = lt % C::NTX, ty = lt / C::NTX;
+    const int fpg = (nf + C::G - 1) / C::G;
+    const int fbeg = grp * fpg, fend = min(nf, fbeg + fpg);
+    const int ly0 = ty * MY, lx0 = tx * 4;  // region-local origin of this thread's micro-tile
+
+    bool own_r[MY], img_r[MY], own_c[4], img_c[4];
+#pragma unroll
+    for (int o = 0; o < MY; ++o) {
+        const int gy = ry0 + ly0 + o;
+        own_r[o] = gy >= s0 && gy < s1;
+        img_r[o] = gy >= 0 && gy < H;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int gx = rx0 + lx0 + c;
+        own_c[c] = gx >= c0 && gx < c1;
+        img_c[c] = gx >= 0 && gx < W;
+    }
+
+    float gacc[MY][4];
+#pragma unroll
+    for (int o = 0; o < MY; ++o)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) gacc[o][c] = 0.0f;
+
+    const float *ubase = Un + ly0 * SW + lx0;
+    const float *dbase = Du + ly0 * SW + lx0;
+
+#pragma unroll 1
+    for (int fr = 0; fr < fpg; fr += C::FG) {
+#pragma unroll 1
+        for (int q = 0; q < C::FG; ++q) {
+            const int f = fbeg + fr + q;
+            if (fr + q >= fpg || f >= fend) continue;
+            float w[M * M];
+#pragma unroll
+            for (int k = 0; k < M * M; ++k) w[k] = s_taps[f * M * M + k];
+            const float al = s_alpha[f];
+            float z[MY][4], dz[MY][4];
+#pragma unroll
+            for (int o = 0; o < MY; ++o)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { z[o][c] = 0.0f; dz[o][c] = 0.0f; }
+            // forward responses: z = K_f u_new (image.py:37-58), dz = K_f du
+#pragma unroll
+            for (int i = 0; i < MY + 2 * R; ++i) {
+                float ru[WIN], rd[WIN];
+                load_row<WIN>(ubase + i * SW, ru);
+                if (TRIAL) load_row<WIN>(dbase + i * SW, rd);
+#pragma unroll
+                for (int o = 0; o < MY; ++o) {
+                    const int aa = i - o;
+                    if (aa < 0 || aa >= M) continue;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) {
+                        const float wt = w[aa * M + bb];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            z[o][c] = fmaf(wt, ru[c + bb], z[o][c]);
+                            if (TRIAL) dz[o][c] = fmaf(wt, rd[c + bb], dz[o][c]);
+                        }
+                    }
+                }
+            }
+            // pointwise: psi = a_f rho'(z) (prior.py:31-32), energy terms on owned pixels
+            float *ps = Psi + (grp * C::FG + q) * C::PLANE + (ly0 + R) * SW + lx0 + R;
+            double e = 0.0;
+#pragma unroll
+            for (int o = 0; o < MY; ++o) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float zz = z[o][c];
+                    float psi = __fdividef(2.0f * al * zz, fmaf(zz, zz, 1.0f));
+                    if (SYM && !(img_r[o] && img_c[c])) psi = 0.0f;
+                    ps[o * SW + c] = psi;
+                    if (own_r[o] && own_c[c]) {
+                        if (TRIAL) {
+                            // F(u_new) - F(u) per response: log1p(dz (2 z_old + dz) / (1 + z_old^2))
+                            const float d = dz[o][c];
+                            const float zo = zz - d;
+                            const float x = d * fmaf(2.0f, zo, d) / fmaf(zo, zo, 1.0f);
+                            e += (double)log1pf(x);
+                        } else {
+                            e += (double)log1pf(zz * zz);  // potential order 0, prior.py:30
+                        }
+                    }
+                }
+            }
+            acc[0] += (double)al * e;
+        }
+        __syncthreads();
+        // adjoint: gacc += K_f^T psi_f  (correlation with the unflipped kernel, image.py:84-87)
+#pragma unroll 1
+        for (int q = 0; q < C::FG; ++q) {
+            const int f = fbeg + fr + q;
+            if (fr + q >= fpg || f >= fend) continue;
+            float w[M * M];
+#pragma unroll
+            for (int k = 0; k < M * M; ++k) w[k] = s_taps[f * M * M + (M * M - 1 - k)];
+            const float *pb = Psi + (grp * C::FG + q) * C::PLANE + ly0 * SW + lx0;
+#pragma unroll
+            for (int i = 0; i < MY + 2 * R; ++i) {
+                float rp[WIN];
+                load_row<WIN>(pb + i * SW, rp);
+#pragma unroll
+                for (int o = 0; o < MY; ++o) {
+                    const int aa = i - o;
+                    if (aa < 0 || aa >= M) continue;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) {
+                        const float wt = w[aa * M + bb];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) gacc[o][c] = fmaf(wt, rp[c + bb], gacc[o][c]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- combine filter groups, fold padded pixels (P^T, image.py:88-90), write ------------------
+    float *gb = Psi;  // G planes of RH x RW
+#pragma unroll
+    for (int o = 0; o < MY; ++o)
+        *reinterpret_cast<float4 *>(gb + grp * C::RH * C::RW + (ly0 + o) * C::RW + lx0) =
+            make_float4(gacc[o][0], gacc[o][1], gacc[o][2], gacc[o][3]);
+    __syncthreads();
+    auto gsum = [&](int ly, int lx) {
+        float s = gb[ly * C::RW + lx];
+#pragma unroll
+        for (int g2 = 1; g2 < C::G; ++g2) s += gb[g2 * C::RH * C::RW + ly * C::RW + lx];
+        return s;
+    };
+    const int oh = s1 - s0, ow = c1 - c0;
+    for (int k = tid; k < oh * ow; k += NT) {
+        const int yy = k / ow, xx = k - yy * ow;
+        const int gy = s0 + yy, gx = c0 + xx;
+        const int ly = gy - ry0, lx = gx - rx0;
+        float val = gsum(ly, lx);
+        if (SYM && R > 0) {
+            int my = -1, mx = -1;
+            if (gy < R) my = (-1 - gy) - ry0;
+            else if (gy >= H - R) my = (2 * H - 1 - gy) - ry0;
+            if (gx < R) mx = (-1 - gx) - rx0;
+            else if (gx >= W - R) mx = (2 * W - 1 - gx) - rx0;
+            if (my >= 0) val += gsum(my, lx);
+            if (mx >= 0) val += gsum(ly, mx);
+            if (my >= 0 && mx >= 0) val += gsum(my, mx);
+        }
+        const size_t o = (size_t)gy * W + gx;
+        gout[o] = val;
+        if (TRIAL) uout[o] = Un[(ly + R) * SW + lx + R];
+    }
+
+    // ---- per-tile partials, last CTA of the image reduces and decides ----------------------------
+    const int ntiles = a.tiles_x * a.tiles_y;
+    block_reduce<NT>(acc, red, s_sum);
+    if (tid < kNumPartials) {
+        a.partials[((size_t)b * ntiles + t) * kPartialStride + tid] = s_sum[tid];
+        __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(a.tickets + b, 1u) == (unsigned)(ntiles - 1));
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double tot[kNumPartials];
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) tot[k] = 0.0;
+    const double *pp = a.partials + (size_t)b * ntiles * kPartialStride;
+    for (int tt = tid; tt < ntiles; tt += NT)
+#pragma unroll
+        for (int k = 0; k < kNumPartials; ++k) tot[k] += __ldcg(pp + (size_t)tt * kPartialStride + k);
+    __syncthreads();
+    block_reduce<NT>(tot, red, s_sum);
+    __syncthreads();
+    if (tid == 0) {
+        a.tickets[b] = 0u;
+        if (a.mode == MODE_EVAL) {
+            a.energy_out[b] = s_sum[0];
+        } else if (!a.no_decide) {
+            decide(a, b, s_sum);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// elementwise kernels
+
+__global__ void k_anscombe_fwd(const double *__restrict__ y, float *__restrict__ v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = (float)(2.0 * sqrt(y[i] + 0.375));  // anscombe.py:24
+}
+
+__global__ void k_direct_obs(const double *__restrict__ y, float *__restrict__ obs, double c, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        obs[i] = (float)(y[i] == 0.0 ? c : y[i]);  // pipeline.py:165
+}
+
+__global__ void k_inverse_exact_unbiased(const float *__restrict__ z, double *__restrict__ x, int64_t n,
+                                         unsigned long long *counts) {
+    const double S = 1.2247448713915890491;  // sqrt(3/2), anscombe.py:13
+    unsigned c_low = 0, c_neg = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double zi = (double)z[i];
+        const bool low = zi < S;
+        const double zc = low ? S : zi;
+        const double v = zc * zc / 4.0 + S / (4.0 * zc) - 11.0 / (8.0 * zc * zc) + 5.0 * S / (8.0 * zc * zc * zc) - 0.125;
+        const bool neg = v < 0.0;
+        c_low += low;
+        c_neg += (neg && !low);
+        x[i] = neg ? 0.0 : v;  // anscombe.py:48-51
+    }
+    if (counts) {
+        for (int off = 16; off > 0; off >>= 1) {
+            c_low += __shfl_down_sync(0xffffffffu, c_low, off);
+            c_neg += __shfl_down_sync(0xffffffffu, c_neg, off);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (c_low) atomicAdd(counts, (unsigned long long)c_low);
+            if (c_neg) atomicAdd(counts + 1, (unsigned long long)c_neg);
+        }
+    }
+}
+
+__global__ void k_prox_quadratic(const float *__restrict__ ut, const float *__restrict__ v, float *__restrict__ out,
+                                 float t, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = prox_quad(ut[i], t, v[i]);
+}
+
+__global__ void k_prox_idiv(const float *__restrict__ ut, const float *__restrict__ ob, float *__restrict__ out,
+                            float t, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = prox_idv(ut[i], t, ob[i]);
+}
+
+// single-filter reference operators (image.py:37-83); simple gathers, not on the solve path
+template <bool SYM>
+__global__ void k_conv_same(const float *__restrict__ x, float *__restrict__ out, const float *__restrict__ kf, int m,
+                            int B, int H, int W) {
+    const int r = m / 2;
+    const int64_t n = (int64_t)B * H * W;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / ((int64_t)H * W);
+        const int p = (int)(i - b * H * W), y = p / W, xx = p - y * W;
+        const float *img = x + b * H * W;
+        float s = 0.0f;
+        for (int a = 0; a < m; ++a)
+            for (int c = 0; c < m; ++c)
+                s = fmaf(kf[a * m + c], img[(size_t)src_idx<SYM>(y + a - r, H) * W + src_idx<SYM>(xx + c - r, W)], s);
+        out[i] = s;
+    }
+}
+
+template <bool SYM>
+__global__ void k_conv_adjoint(const float *__restrict__ yv, float *__restrict__ out, const float *__restrict__ k,
+                               int m, int B, int H, int W) {
+    const int r = m / 2;
+    const int64_t n = (int64_t)B * H * W;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / ((int64_t)H * W);
+        const int p = (int)(i - b * H * W), y = p / W, xx = p - y * W;
+        const float *img = yv + b * H * W;
+        // padded positions q with src(q) == p (image.py:88-90)
+        int qy[3], qx[3], ny = 0, nx = 0;
+        const int cy[3] = {y, SYM ? -1 - y : y - H, SYM ? 2 * H - 1 - y : y + H};
+        const int cx[3] = {xx, SYM ? -1 - xx : xx - W, SYM ? 2 * W - 1 - xx : xx + W};
+        for (int e = 0; e < 3; ++e) {
+            if (cy[e] >= -r && cy[e] < H + r && (e == 0 || cy[e] != y)) qy[ny++] = cy[e];
+            if (cx[e] >= -r && cx[e] < W + r && (e == 0 || cx[e] != xx)) qx[nx++] = cx[e];
+        }
+        float s = 0.0f;
+        for (int ey = 0; ey < ny; ++ey)
+            for (int ex = 0; ex < nx; ++ex)
+                for (int a = 0; a < m; ++a) {
+                    const int py = qy[ey] + a - r;
+                    if (py < 0 || py >= H) continue;
+                    for (int c = 0; c < m; ++c) {
+                        const int px = qx[ex] + c - r;
+                        if (px < 0 || px >= W) continue;
+                        s = fmaf(k[a * m + c], img[(size_t)py * W + px], s);
+                    }
+                }
+        out[i] = s;
+    }
+}
+
+__global__ void k_gather_final(const float *__restrict__ U, size_t plane, const ImgCtl *__restrict__ ctl,
+                               float *__restrict__ out, size_t HW, int B) {
+    const int b = blockIdx.y;
+    const float *src = U + (size_t)ctl[b].iu * plane + (size_t)b * HW;
+    float *dst = out + (size_t)b * HW;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < HW; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+// ------------------------------------------------------------------------------------------------
+// host side
+
+int grid_1d(int64_t n, int block = 256) {
+    int64_t g = (n + block - 1) / block;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
+}
+
+template <int M>
+size_t pass_smem_bytes(int nf, bool trial) {
+    using C = PassCfg<M>;
+    return sizeof(float) * ((size_t)(trial ? 2 : 1) * C::PLANE + (size_t)C::G * C::FG * C::PLANE + (size_t)nf * M * M + nf);
+}
+
+template <int M, bool TRIAL, bool SYM>
+int launch_pass_t(const PassArgs &a, cudaStream_t st) {
+    using C = PassCfg<M>;
+    const size_t smem = pass_smem_bytes<M>(a.n_filters, TRIAL);
+    static unsigned long long configured = 0;  // one bit per device
+    int dev = 0;
+    FOE_CUDA(cudaGetDevice(&dev));
+    if (!(configured >> (dev & 63) & 1ull)) {
+        FOE_CUDA(cudaFuncSetAttribute(k_pass<M, TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured |= 1ull << (dev & 63);
+    }
+    dim3 grid(a.tiles_x * a.tiles_y, a.B);
+    k_pass<M, TRIAL, SYM><<<grid, C::NT, smem, st>>>(a);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+template <bool TRIAL, bool SYM>
+int launch_pass_m(int m, const PassArgs &a, cudaStream_t st) {
+    switch (m) {
+        case 1: return launch_pass_t<1, TRIAL, SYM>(a, st);
+        case 3: return launch_pass_t<3, TRIAL, SYM>(a, st);
+        case 5: return launch_pass_t<5, TRIAL, SYM>(a, st);
+        case 7: return launch_pass_t<7, TRIAL, SYM>(a, st);
+        default: return fail(FOE_E_UNSUPPORTED, "filter size %d not compiled (1,3,5,7)", m);
+    }
+}
+
+int launch_pass(int m, bool sym, const PassArgs &a, cudaStream_t st) {
+    const bool trial = a.mode == MODE_TRIAL;
+    if (trial) return sym ? launch_pass_m<true, true>(m, a, st) : launch_pass_m<true, false>(m, a, st);
+    return sym ? launch_pass_m<false, true>(m, a, st) : launch_pass_m<false, false>(m, a, st);
+}
+
+void tile_counts(int m, int H, int W, int *tx, int *ty) {
+    const int r = m / 2;
+    const int T = 48 - 2 * r;  // PassCfg<M>::TH == TW for every M
+    *ty = (H + T - 1) / T;
+    *tx = (W + T - 1) / T;
+}
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct SolveLayout {
+    size_t U, G, ctl, partials, tickets, trace, n_active, total;
+};
+
+SolveLayout solve_layout(int m, int B, int H, int W, int trace_cap) {
+    int tx, ty;
+    tile_counts(m, H, W, &tx, &ty);
+    const size_t plane = (size_t)B * H * W * sizeof(float);
+    SolveLayout L;
+    size_t off = 0;
+    L.U = off; off = align_up(off + 3 * plane);
+    L.G = off; off = align_up(off + 2 * plane);
+    L.ctl = off; off = align_up(off + sizeof(ImgCtl) * B);
+    L.partials = off; off = align_up(off + sizeof(double) * kPartialStride * (size_t)B * tx * ty);
+    L.tickets = off; off = align_up(off + sizeof(unsigned) * B);
+    L.trace = off; off = align_up(off + sizeof(double) * 6 * (size_t)B * trace_cap);
+    L.n_active = off; off = align_up(off + sizeof(int) * 4);
+    L.total = off;
+    return L;
+}
+
+int check_dims(const foe_bank *bank, int B, int H, int W) {
+    if (!bank) return fail(FOE_E_INVALID, "null bank");
+    if (B < 1 || B > 65535) return fail(FOE_E_INVALID, "batch %d out of range", B);
+    if (H < bank->m || W < bank->m)  // prior.py:87-92
+        return fail(FOE_E_INVALID, "image shape (%d, %d) smaller than filter size %d", H, W, bank->m);
+    return FOE_OK;
+}
+
+struct PinnedFlags {
+    int *p = nullptr;
+    ~PinnedFlags() { if (p) cudaFreeHost(p); }
+};
+thread_local PinnedFlags t_flags;
+
+}  // namespace
+
+extern "C" {
+
+int foe_abi_version(void) { return 1; }
+const char *foe_last_error(void) { return g_err.c_str(); }
+
+int foe_device_sm_count(int device) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+    return v;
+}
+
+int foe_bank_create(const double *filters, const double *weights, int n, int m, int boundary, foe_bank **out) {
+    if (!filters || !weights || !out) return fail(FOE_E_INVALID, "null argument");
+    if (n < 1 || n > kMaxFilters) return fail(FOE_E_INVALID, "filter count %d out of range", n);
+    if (m < 1 || m % 2 != 1) return fail(FOE_E_INVALID, "kernel side must be odd, got %d", m);  // image.py:23-29
+    if (m > 7) return fail(FOE_E_UNSUPPORTED, "filter size %d not compiled (1,3,5,7)", m);
+    if (n * m * m > kMaxTaps) return fail(FOE_E_UNSUPPORTED, "bank too large (%d taps)", n * m * m);
+    if (boundary != FOE_SYMMETRIC && boundary != FOE_PERIODIC)
+        return fail(FOE_E_INVALID, "boundary must be symmetric or periodic");
+    for (int i = 0; i < n; ++i)
+        if (!(weights[i] > 0)) return fail(FOE_E_INVALID, "expert weights must be strictly positive");
+    std::vector<float> kf((size_t)n * m * m), al(n);
+    for (int i = 0; i < n; ++i) {
+        al[i] = (float)weights[i];
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b)  // cv2.filter2D correlates with the flipped kernel, image.py:49-50
+                kf[(size_t)i * m * m + a * m + b] = (float)filters[(size_t)i * m * m + (m - 1 - a) * m + (m - 1 - b)];
+    }
+    foe_bank *bk = new foe_bank();
+    bk->n = n; bk->m = m; bk->boundary = boundary;
+    cudaGetDevice(&bk->device);
+    if (cudaMalloc(&bk->d_kf, kf.size() * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&bk->d_alpha, al.size() * sizeof(float)) != cudaSuccess) {
+        delete bk;
+        return fail(FOE_E_CUDA, "cudaMalloc failed for the filter bank");
+    }
+    FOE_CUDA(cudaMemcpy(bk->d_kf, kf.data(), kf.size() * sizeof(float), cudaMemcpyHostToDevice));
+    FOE_CUDA(cudaMemcpy(bk->d_alpha, al.data(), al.size() * sizeof(float), cudaMemcpyHostToDevice));
+    *out = bk;
+    return FOE_OK;
+}
+
+int foe_bank_destroy(foe_bank *bank) {
+    if (!bank) return FOE_OK;
+    cudaFree(bank->d_kf);
+    cudaFree(bank->d_alpha);
+    delete bank;
+    return FOE_OK;
+}
+
+int foe_bank_info(const foe_bank *bank, int *n, int *m, int *boundary) {
+    if (!bank) return fail(FOE_E_INVALID, "null bank");
+    if (n) *n = bank->n;
+    if (m) *m = bank->m;
+    if (boundary) *boundary = bank->boundary;
+    return FOE_OK;
+}
+
+int foe_anscombe_forward(const double *y, float *v, int64_t n, void *stream) {
+    if (n <= 0) return FOE_OK;
+    k_anscombe_fwd<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(y, v, n);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_direct_obs(const double *y, float *obs, double c, int64_t n, void *stream) {
+    if (c < 0) return fail(FOE_E_INVALID, "zero_offset_c must be non-negative");
+    if (n <= 0) return FOE_OK;
+    k_direct_obs<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(y, obs, c, n);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_anscombe_inverse_exact_unbiased(const float *z, double *x, int64_t n, unsigned long long *counts,
+                                        void *stream) {
+    if (n <= 0) return FOE_OK;
+    k_inverse_exact_unbiased<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(z, x, n, counts);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_prox_quadratic(const float *ut, const float *v, float *out, double t, int64_t n, void *stream) {
+    if (t < 0) return fail(FOE_E_INVALID, "t must be >= 0, got %g", t);  // solver.py:94-95
+    if (n <= 0) return FOE_OK;
+    k_prox_quadratic<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(ut, v, out, (float)t, n);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_prox_idiv(const float *ut, const float *obs, float *out, double t, int64_t n, void *stream) {
+    if (t < 0) return fail(FOE_E_INVALID, "t must be >= 0, got %g", t);  // solver.py:111-112
+    if (n <= 0) return FOE_OK;
+    k_prox_idiv<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(ut, obs, out, (float)t, n);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_convolve_same(const foe_bank *bank, int index, const float *x, float *out, int B, int H, int W,
+                      void *stream) {
+    int rc = check_dims(bank, B, H, W);
+    if (rc) return rc;
+    if (index < 0 || index >= bank->n) return fail(FOE_E_INVALID, "filter index %d out of range", index);
+    const int64_t n = (int64_t)B * H * W;
+    const float *kf = bank->d_kf + (size_t)index * bank->m * bank->m;
+    if (bank->boundary == FOE_SYMMETRIC)
+        k_conv_same<true><<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(x, out, kf, bank->m, B, H, W);
+    else
+        k_conv_same<false><<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(x, out, kf, bank->m, B, H, W);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_convolve_adjoint(const foe_bank *bank, int index, const float *y, float *out, int B, int H, int W,
+                         void *stream) {
+    // the adjoint correlates with the unflipped kernel: reverse the stored flipped taps on the fly
+    int rc = check_dims(bank, B, H, W);
+    if (rc) return rc;
+    if (index < 0 || index >= bank->n) return fail(FOE_E_INVALID, "filter index %d out of range", index);
+    const int m = bank->m;
+    std::vector<float> kf((size_t)m * m), k((size_t)m * m);
+    FOE_CUDA(cudaMemcpy(kf.data(), bank->d_kf + (size_t)index * m * m, sizeof(float) * m * m, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m * m; ++i) k[i] = kf[m * m - 1 - i];
+    float *dk = nullptr;
+    FOE_CUDA(cudaMallocAsync(&dk, sizeof(float) * m * m, (cudaStream_t)stream));
+    FOE_CUDA(cudaMemcpyAsync(dk, k.data(), sizeof(float) * m * m, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    const int64_t n = (int64_t)B * H * W;
+    if (bank->boundary == FOE_SYMMETRIC)
+        k_conv_adjoint<true><<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(y, out, dk, m, B, H, W);
+    else
+        k_conv_adjoint<false><<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(y, out, dk, m, B, H, W);
+    FOE_CUDA(cudaGetLastError());
+    FOE_CUDA(cudaFreeAsync(dk, (cudaStream_t)stream));
+    FOE_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return FOE_OK;
+}
+
+size_t foe_eval_workspace_size(const foe_bank *bank, int B, int H, int W) {
+    if (!bank) return 0;
+    int tx, ty;
+    tile_counts(bank->m, H, W, &tx, &ty);
+    return align_up(sizeof(double) * kPartialStride * (size_t)B * tx * ty) + align_up(sizeof(unsigned) * B);
+}
+
+int foe_energy_grad(const foe_bank *bank, const float *u, float *grad, double *energy, int B, int H, int W,
+                    void *workspace, size_t workspace_bytes, void *stream) {
+    int rc = check_dims(bank, B, H, W);
+    if (rc) return rc;
+    if (workspace_bytes < foe_eval_workspace_size(bank, B, H, W)) return fail(FOE_E_INVALID, "workspace too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    PassArgs a{};
+    a.B = B; a.H = H; a.W = W; a.n_filters = bank->n;
+    tile_counts(bank->m, H, W, &a.tiles_x, &a.tiles_y);
+    a.mode = MODE_EVAL;
+    a.kf = bank->d_kf; a.alpha = bank->d_alpha;
+    a.u_in = u; a.g_out = grad; a.energy_out = energy;
+    a.partials = (double *)workspace;
+    a.tickets = (unsigned *)((char *)workspace + align_up(sizeof(double) * kPartialStride * (size_t)B * a.tiles_x * a.tiles_y));
+    FOE_CUDA(cudaMemsetAsync(a.tickets, 0, sizeof(unsigned) * B, st));
+    return launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, st);
+}
+
+size_t foe_solve_workspace_size(const foe_bank *bank, int B, int H, int W, int trace_cap) {
+    if (!bank) return 0;
+    return solve_layout(bank->m, B, H, W, trace_cap).total;
+}
+
+static void fill_solve_args(PassArgs &a, const foe_bank *bank, const foe_solver_cfg &cfg, int B, int H, int W,
+                            int trace_cap, char *ws, const SolveLayout &L) {
+    a.B = B; a.H = H; a.W = W; a.n_filters = bank->n;
+    tile_counts(bank->m, H, W, &a.tiles_x, &a.tiles_y);
+    a.plane = (size_t)B * H * W;
+    a.kf = bank->d_kf; a.alpha = bank->d_alpha;
+    a.U = (float *)(ws + L.U);
+    a.Gs = (float *)(ws + L.G);
+    a.ctl = (ImgCtl *)(ws + L.ctl);
+    a.partials = (double *)(ws + L.partials);
+    a.tickets = (unsigned *)(ws + L.tickets);
+    a.trace = (double *)(ws + L.trace);
+    a.trace_cap = trace_cap;
+    a.n_active = (int *)(ws + L.n_active);
+    a.gamma = cfg.gamma;
+    a.step_num = 1.99 * (1.0 - cfg.gamma);  // solver.py:64-65
+    a.eta = cfg.backtrack_factor;
+    a.relax = cfg.relax_factor;
+    a.rel_tol = cfg.rel_tol;
+    a.max_L = cfg.max_lipschitz;
+}
+
+int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, int W, const float *u0,
+              const float *obs, const double *lam, const int *branch, const int *max_iters, float *u_out,
+              foe_image_status *status, double *trace, int trace_cap, void *workspace, size_t workspace_bytes,
+              void *stream) {
+    int rc = check_dims(bank, B, H, W);
+    if (rc) return rc;
+    if (!cfgp || !u0 || !obs || !lam || !branch || !max_iters || !u_out || !status || !trace)
+        return fail(FOE_E_INVALID, "null argument");
+    const foe_solver_cfg cfg = *cfgp;
+    // SolverConfig.__post_init__, solver.py:54-62
+    if (!(cfg.gamma >= 0.0 && cfg.gamma < 1.0)) return fail(FOE_E_INVALID, "gamma must be in [0, 1), got %g", cfg.gamma);
+    if (!(cfg.lipschitz_init > 0)) return fail(FOE_E_INVALID, "lipschitz_init must be positive");
+    if (!(cfg.backtrack_factor > 1)) return fail(FOE_E_INVALID, "backtrack_factor must exceed 1");
+    int max_it = 0, min_it = 1 << 30;
+    for (int b = 0; b < B; ++b) {
+        if (max_iters[b] < 1) return fail(FOE_E_INVALID, "max_iters must be at least 1");
+        if (!(lam[b] > 0)) return fail(FOE_E_INVALID, "lambda must be positive, got %g", lam[b]);
+        if (branch[b] != FOE_QUADRATIC && branch[b] != FOE_IDIV) return fail(FOE_E_INVALID, "bad branch");
+        max_it = std::max(max_it, max_iters[b]);
+        min_it = std::min(min_it, max_iters[b]);
+    }
+    if (trace_cap < max_it) return fail(FOE_E_INVALID, "trace_cap %d < max_iters %d", trace_cap, max_it);
+    const SolveLayout L = solve_layout(bank->m, B, H, W, trace_cap);
+    if (workspace_bytes < L.total) return fail(FOE_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, L.total);
+    cudaStream_t st = (cudaStream_t)stream;
+    char *ws = (char *)workspace;
+    PassArgs a{};
+    fill_solve_args(a, bank, cfg, B, H, W, trace_cap, ws, L);
+
+    std::vector<ImgCtl> hc(B);
+    for (int b = 0; b < B; ++b) {
+        ImgCtl &c = hc[b];
+        memset(&c, 0, sizeof(c));
+        c.L = cfg.lipschitz_init;
+        c.lam = lam[b];
+        c.max_iters = max_iters[b];
+        c.branch = branch[b];
+        c.failed_at = -1;
+        c.iu = 0; c.iup = 0; c.inew = 1;  // u_prev = u = u0 (solver.py:136-137)
+        c.ig = 0; c.ignew = 1;
+    }
+    const size_t HWB = (size_t)B * H * W;
+    FOE_CUDA(cudaMemcpyAsync(a.ctl, hc.data(), sizeof(ImgCtl) * B, cudaMemcpyHostToDevice, st));
+    FOE_CUDA(cudaMemsetAsync(a.tickets, 0, sizeof(unsigned) * B, st));
+    FOE_CUDA(cudaMemcpyAsync(a.n_active, &B, sizeof(int), cudaMemcpyHostToDevice, st));
+    FOE_CUDA(cudaMemcpyAsync(a.U, u0, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
+
+    // iteration 0 needs F(u0) and grad F(u0)
+    a.mode = MODE_INIT;
+    if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, st))) return rc;
+
+    if (!t_flags.p) FOE_CUDA(cudaHostAlloc(&t_flags.p, 4 * sizeof(int), cudaHostAllocDefault));
+    cudaEvent_t ev[2];
+    FOE_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    FOE_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    a.mode = MODE_TRIAL;
+    // every image needs >= 1 trial per accepted iteration; afterwards poll the live count every chunk
+    const long hard_cap = (long)max_it * 200 + 64;
+    long launched = 0;
+    int slot = 0, pending = -1;
+    int chunk = std::max(1, min_it);
+    for (;;) {
+        for (int k = 0; k < chunk; ++k)
+            if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, st))) return rc;
+        launched += chunk;
+        FOE_CUDA(cudaMemcpyAsync(t_flags.p + slot, a.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+        FOE_CUDA(cudaEventRecord(ev[slot], st));
+        if (pending >= 0) {
+            FOE_CUDA(cudaEventSynchronize(ev[pending]));
+            if (t_flags.p[pending] == 0) break;
+        }
+        pending = slot;
+        slot ^= 1;
+        chunk = 8;
+        if (launched > hard_cap) {
+            cudaEventDestroy(ev[0]);
+            cudaEventDestroy(ev[1]);
+            return fail(FOE_E_NUMERICAL, "solver did not terminate after %ld passes", launched);
+        }
+    }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    {
+        dim3 grid(std::max(1, std::min(148, (int)((size_t)H * W / 1024 + 1))), B);
+        k_gather_final<<<grid, 256, 0, st>>>(a.U, a.plane, a.ctl, u_out, (size_t)H * W, B);
+        FOE_CUDA(cudaGetLastError());
+    }
+    FOE_CUDA(cudaMemcpyAsync(hc.data(), a.ctl, sizeof(ImgCtl) * B, cudaMemcpyDeviceToHost, st));
+    FOE_CUDA(cudaMemcpyAsync(trace, a.trace, sizeof(double) * 6 * (size_t)B * trace_cap, cudaMemcpyDeviceToHost, st));
+    FOE_CUDA(cudaStreamSynchronize(st));
+    int any_fail = 0;
+    for (int b = 0; b < B; ++b) {
+        status[b].status = hc[b].status;
+        status[b].n_iters = hc[b].n;
+        status[b].n_trials = hc[b].trials;
+        status[b].failed_at = hc[b].status ? hc[b].failed_at : -1;
+        any_fail |= hc[b].status != 0;
+    }
+    return any_fail ? fail(FOE_E_NUMERICAL, "numerical failure in at least one image") : FOE_OK;
+}
+
+int foe_bench_trial_pass(const foe_bank *bank, int B, int H, int W, int trace_cap, int reps, void *workspace,
+                         size_t workspace_bytes, void *stream) {
+    int rc = check_dims(bank, B, H, W);
+    if (rc) return rc;
+    const SolveLayout L = solve_layout(bank->m, B, H, W, trace_cap);
+    if (workspace_bytes < L.total) return fail(FOE_E_INVALID, "workspace too small");
+    foe_solver_cfg cfg{0.8, 1.0, 1.2, 1.05, 1e-6, 1e15};
+    PassArgs a{};
+    fill_solve_args(a, bank, cfg, B, H, W, trace_cap, (char *)workspace, L);
+    a.mode = MODE_TRIAL;
+    a.no_decide = 1;
+    for (int k = 0; k < reps; ++k)
+        if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, (cudaStream_t)stream))) return rc;
+    return FOE_OK;
+}
+
+}  // extern "C"
