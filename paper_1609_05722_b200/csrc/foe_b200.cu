@@ -713,7 +713,7 @@ void tile_counts(int m, int H, int W, int *tx, int *ty) {
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct SolveLayout {
-    size_t U, G, ctl, partials, tickets, trace, n_active, total;
+    size_t U, G, O, ctl, partials, tickets, trace, n_active, total;
 };
 
 SolveLayout solve_layout(int m, int B, int H, int W, int trace_cap) {
@@ -724,6 +724,7 @@ SolveLayout solve_layout(int m, int B, int H, int W, int trace_cap) {
     size_t off = 0;
     L.U = off; off = align_up(off + 3 * plane);
     L.G = off; off = align_up(off + 2 * plane);
+    L.O = off; off = align_up(off + plane);
     L.ctl = off; off = align_up(off + sizeof(ImgCtl) * B);
     L.partials = off; off = align_up(off + sizeof(double) * kPartialStride * (size_t)B * tx * ty);
     L.tickets = off; off = align_up(off + sizeof(unsigned) * B);
@@ -923,6 +924,7 @@ static void fill_solve_args(PassArgs &a, const foe_bank *bank, const foe_solver_
     a.kf = bank->d_kf; a.alpha = bank->d_alpha;
     a.U = (float *)(ws + L.U);
     a.Gs = (float *)(ws + L.G);
+    a.obs = (const float *)(ws + L.O);
     a.ctl = (ImgCtl *)(ws + L.ctl);
     a.partials = (double *)(ws + L.partials);
     a.tickets = (unsigned *)(ws + L.tickets);
@@ -975,7 +977,7 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
         c.max_iters = max_iters[b];
         c.branch = branch[b];
         c.failed_at = -1;
-        c.iu = 0; c.iup = 0; c.inew = 1;  // u_prev = u = u0 (solver.py:136-137)
+        c.iu = 0; c.iup = 2; c.inew = 1;  // u_prev = u = u0 (solver.py:136-137), distinct slots
         c.ig = 0; c.ignew = 1;
     }
     const size_t HWB = (size_t)B * H * W;
@@ -983,6 +985,8 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     FOE_CUDA(cudaMemsetAsync(a.tickets, 0, sizeof(unsigned) * B, st));
     FOE_CUDA(cudaMemcpyAsync(a.n_active, &B, sizeof(int), cudaMemcpyHostToDevice, st));
     FOE_CUDA(cudaMemcpyAsync(a.U, u0, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
+    FOE_CUDA(cudaMemcpyAsync(a.U + 2 * a.plane, u0, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
+    FOE_CUDA(cudaMemcpyAsync((float *)(ws + L.O), obs, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
 
     // iteration 0 needs F(u0) and grad F(u0)
     a.mode = MODE_INIT;

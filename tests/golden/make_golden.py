@@ -90,7 +90,8 @@ def main():
         "fallback": (fallback_bank(), v),
         "rand_periodic": (random_model(np.random.default_rng(5), 3, 5, boundary="periodic"), v),
         "rand_m7_sym": (random_model(np.random.default_rng(6), 4, 7), v[:13, :11].copy()),
-        "rand_m3_periodic_tiny": (random_model(np.random.default_rng(8), 2, 3, boundary="periodic"), v[:5, :7].copy()),
+        "rand_m3_periodic_tiny": (random_model(np.random.default_rng(8), 2, 3, boundary="periodic"),
+                                  np.random.default_rng(9).normal(size=(5, 7)) + 3.0),
     }
     for name, (model, u) in cases.items():
         out[f"u_{name}"] = u
