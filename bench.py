@@ -1,0 +1,276 @@
+"""Benchmark of the FoE Poisson-denoise hot path on B200 (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): one 512x512 image from the frozen synthetic
+generator, peak 1, Anscombe-domain model foe_a (24 filters 5x5), quadratic data
+term, the reference's iPiano solver with its own 150-iteration budget
+(pipeline.py:83-87).  A "step" = one full denoise: Anscombe forward -> device
+iPiano solve (all backtracking on device) -> exact unbiased inverse, with the
+counts already resident in HBM.  With N GPUs every rank denoises its own image
+(seed = rank): weak scaling, no data-path collective.
+
+Metric: Mpixel*iter/s = pixels x accepted iterations / time (whole job).
+L2 handling: the 512^2 working set (~6 MB) lives in L2 by design; a 256 MiB
+buffer is rewritten between timed steps so every step starts cold.
+
+--impl reference times the CPU oracle port (oracle/foe_oracle.c, fp64, all host
+threads) on the same config: the reference is pure Python and cannot be
+compiled, and it cannot run on the GPU box.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+H = W = 512
+PEAK = 1.0
+N_FILT, K = 24, 5
+ALG_FLOP_PER_PX_IT = 4 * N_FILT * K * K  # forward + adjoint
+METRIC = "Mpixel·iter/s of FoE solver (fp32, % FP32 peak); 512² denoise ms"
+CONFIG = {"workload": "cfg2: 512x512 synthetic, peak 1, transform/quadratic, foe_a 24x5x5, 150 iters",
+          "model": "foe_a (24 filters 5x5, dct5, symmetric)", "image": "512x512", "peak": PEAK,
+          "iterations": 150, "l2": "flushed between steps (256 MiB rewrite); working set L2-resident within a step"}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_oracle_rate(y, iters, threads=None):
+    """Oracle port (fp64 C, OpenMP) on a truncated 512^2 solve: Mpixel*iter/s, seconds, cores."""
+    from oracle import cpu as orc
+    orc.build()
+    if threads:
+        orc.set_num_threads(threads)
+    m = orc.read_foe(os.path.join(REPO, "paper_1609_05722_b200", "assets", "foe_a.foe"))
+    v = orc.anscombe_forward(y)
+    lam = 0.6075  # select_lambda(1, transform, quadratic), lambda_table.json
+    t0 = time.perf_counter()
+    u, tr = orc.ipiano_foe(v, v, m, lam, "quadratic", max_iters=iters, rel_tol=0.0)
+    orc.anscombe_inverse_exact_unbiased(u)
+    dt = time.perf_counter() - t0
+    return y.size * len(tr.F) / dt / 1e6, dt, orc.num_threads()
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle port on the box's host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_1609_05722_b200.synth import make_counts
+    _, y = make_counts(H, W, 0, PEAK)
+    iters = args.ref_iters
+    for _ in range(args.warmup):
+        cpu_oracle_rate(y, iters)
+    rates, secs = [], 0.0
+    for _ in range(args.steps):
+        r, dt, cores = cpu_oracle_rate(y, iters)
+        rates.append(r)
+        secs += dt
+    value = y.size * iters * args.steps / secs / 1e6
+    sample = f"512x512 cfg2 solve truncated to {iters} accepted iterations per step (incl. the iteration-0 backtracking climb)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Mpixel*iter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": CONFIG,
+            "cpu_baseline": {"value": value, "unit": "Mpixel*iter/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "Mpixel*iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-iters", type=int, default=8)
+    ap.add_argument("--cpu-iters", type=int, default=30)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pass-reps", type=int, default=100)
+    args = ap.parse_args()
+    rank, local_rank, world = dist_env()
+    args.warmup = max(args.warmup, 0)
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1609_05722_b200 as fp
+    from paper_1609_05722_b200 import _lib
+    from paper_1609_05722_b200.anscombe import forward_device, inverse_exact_unbiased_device
+    from paper_1609_05722_b200.synth import make_counts
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    model = fp.load_packaged_model("foe_a")
+    clean, y = make_counts(H, W, rank, PEAK)
+    y_dev = torch.from_numpy(y).to(dev)
+    lam = fp.select_lambda(PEAK, "transform", force_branch="quadratic")
+    cfg = fp.solver_budget(PEAK, fp.SolverConfig())  # the reference's own budget: 150 iterations
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        v = forward_device(y_dev)
+        res = fp.solve_device(model, v, v, lam, "quadratic", cfg.max_iters, cfg)
+        x = inverse_exact_unbiased_device(res.u)
+        return res, x
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    L = _lib.lib()
+    launches0 = L.foe_kernel_launch_count()
+    total_ms, iters, trials = 0.0, 0, 0
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res, x = step()
+            e1.record(stream)
+            e1.synchronize()
+            total_ms += e0.elapsed_time(e1)
+            iters += len(res.traces[0])
+            trials += res.traces[0].n_trials
+    torch.cuda.synchronize()
+    launches = L.foe_kernel_launch_count() - launches0
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    px_it_per_step = H * W * iters / args.steps
+    value = world * px_it_per_step / (ms_per_step * 1e-3) / 1e6
+
+    # dominant kernel: the fused trial pass, timed back to back on the solved state
+    ws = res._workspace
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _lib.check(L.foe_bench_trial_pass(res._bank.handle, 1, H, W, res._cap, 5, ws.data_ptr(), ws.numel(),
+                                      stream.cuda_stream))
+    e0.record(stream)
+    _lib.check(L.foe_bench_trial_pass(res._bank.handle, 1, H, W, res._cap, args.pass_reps, ws.data_ptr(),
+                                      ws.numel(), stream.cuda_stream))
+    e1.record(stream)
+    e1.synchronize()
+    pass_ms = e0.elapsed_time(e1) / args.pass_reps
+    props = torch.cuda.get_device_properties(dev)
+    sm_count = props.multi_processor_count
+    peak_clock = clk.max_mhz or 1965.0
+    fp32_peak_tflops = sm_count * 128 * 2 * peak_clock * 1e6 / 1e12
+    alg_flop_pass = ALG_FLOP_PER_PX_IT * H * W
+    achieved = alg_flop_pass / (pass_ms * 1e-3) / 1e12
+    solve_frac = value * 1e6 * ALG_FLOP_PER_PX_IT / (world * fp32_peak_tflops * 1e12)
+
+    # end to end through the public API with host buffers (H2D counts, D2H image + transformed)
+    e2e_ms = []
+    for i in range(max(1, min(args.steps, 5)) + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fp.denoise(fp.DenoiseRequest(noisy=y, peak=PEAK, model=model, variant="transform",
+                                          force_branch="quadratic"))
+        dt = time.perf_counter() - t0
+        if i:
+            e2e_ms.append(dt * 1e3)
+    e2e_iters = len(r.trace)
+    e2e_t = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world * H * W * e2e_iters / (float(e2e_t.item()) * 1e-3) / 1e6
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, secs, cores = cpu_oracle_rate(y, args.cpu_iters)
+        cpu = {"value": rate, "unit": "Mpixel*iter/s", "cores": cores, "kind": "port",
+               "sample": f"512x512 cfg2 solve truncated to {args.cpu_iters} iterations ({secs:.1f} s, fp64 C oracle)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "Mpixel*iter/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+                "config": dict(CONFIG, parallelism=f"replicas{world}" if world > 1 else "single"),
+                "denoise_ms_512": ms_per_step, "iterations_per_step": iters / args.steps,
+                "trials_per_step": trials / args.steps,
+                "algorithmic_fp32_frac": solve_frac,
+                "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
+                             "frac": achieved / fp32_peak_tflops, "traffic": None,
+                             "kernel": "k_pass<5,TRIAL,SYM> (fused trial pass)", "pass_ms": pass_ms,
+                             "flop_per_launch": alg_flop_pass,
+                             "peak_source": f"{sm_count} SMs x 128 FP32 lanes x 2 x {peak_clock} MHz (nominal; "
+                                            "MEASURED_PEAKS.json has no FP32 figure)"},
+                "e2e": {"value": e2e_value, "unit": "Mpixel*iter/s", "ms_per_denoise": float(e2e_t.item()),
+                        "h2d_bytes_per_step": int(y.nbytes), "d2h_bytes_per_step": int(2 * y.nbytes)},
+                "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+                "clocks": clk.summary(),
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

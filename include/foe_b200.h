@@ -68,6 +68,8 @@ typedef struct foe_image_status {
 int foe_abi_version(void);
 const char *foe_last_error(void);
 int foe_device_sm_count(int device);
+/* number of CUDA kernels this library has launched in the process (launch accounting for bench.py) */
+long long foe_kernel_launch_count(void);
 
 /* ---- filter bank: FoEModel.filters (prior.py:75-78) + weights --------------------------------
  * filters: host float64 (n, m, m) in true-convolution orientation (what convolve_same takes,

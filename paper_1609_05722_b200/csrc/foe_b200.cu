@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -36,6 +37,7 @@ struct foe_bank {
 namespace {
 
 thread_local std::string g_err;
+std::atomic<long long> g_launches{0};  // kernels launched by this library (bench accounting)
 
 int fail(int code, const char *fmt, ...) {
     char buf[512];
@@ -683,6 +685,7 @@ int launch_pass_t(const PassArgs &a, cudaStream_t st) {
     dim3 grid(a.tiles_x * a.tiles_y, a.B);
     k_pass<M, TRIAL, SYM><<<grid, C::NT, smem, st>>>(a);
     FOE_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     return FOE_OK;
 }
 
@@ -753,6 +756,7 @@ thread_local PinnedFlags t_flags;
 extern "C" {
 
 int foe_abi_version(void) { return 1; }
+long long foe_kernel_launch_count(void) { return g_launches.load(); }
 const char *foe_last_error(void) { return g_err.c_str(); }
 
 int foe_device_sm_count(int device) {
@@ -810,6 +814,7 @@ int foe_bank_info(const foe_bank *bank, int *n, int *m, int *boundary) {
 
 int foe_anscombe_forward(const double *y, float *v, int64_t n, void *stream) {
     if (n <= 0) return FOE_OK;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     k_anscombe_fwd<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(y, v, n);
     FOE_CUDA(cudaGetLastError());
     return FOE_OK;
@@ -818,6 +823,7 @@ int foe_anscombe_forward(const double *y, float *v, int64_t n, void *stream) {
 int foe_direct_obs(const double *y, float *obs, double c, int64_t n, void *stream) {
     if (c < 0) return fail(FOE_E_INVALID, "zero_offset_c must be non-negative");
     if (n <= 0) return FOE_OK;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     k_direct_obs<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(y, obs, c, n);
     FOE_CUDA(cudaGetLastError());
     return FOE_OK;
@@ -826,6 +832,7 @@ int foe_direct_obs(const double *y, float *obs, double c, int64_t n, void *strea
 int foe_anscombe_inverse_exact_unbiased(const float *z, double *x, int64_t n, unsigned long long *counts,
                                         void *stream) {
     if (n <= 0) return FOE_OK;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     k_inverse_exact_unbiased<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(z, x, n, counts);
     FOE_CUDA(cudaGetLastError());
     return FOE_OK;
@@ -834,6 +841,7 @@ int foe_anscombe_inverse_exact_unbiased(const float *z, double *x, int64_t n, un
 int foe_prox_quadratic(const float *ut, const float *v, float *out, double t, int64_t n, void *stream) {
     if (t < 0) return fail(FOE_E_INVALID, "t must be >= 0, got %g", t);  // solver.py:94-95
     if (n <= 0) return FOE_OK;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     k_prox_quadratic<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(ut, v, out, (float)t, n);
     FOE_CUDA(cudaGetLastError());
     return FOE_OK;
@@ -842,6 +850,7 @@ int foe_prox_quadratic(const float *ut, const float *v, float *out, double t, in
 int foe_prox_idiv(const float *ut, const float *obs, float *out, double t, int64_t n, void *stream) {
     if (t < 0) return fail(FOE_E_INVALID, "t must be >= 0, got %g", t);  // solver.py:111-112
     if (n <= 0) return FOE_OK;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     k_prox_idiv<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(ut, obs, out, (float)t, n);
     FOE_CUDA(cudaGetLastError());
     return FOE_OK;
@@ -1025,6 +1034,7 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     cudaEventDestroy(ev[1]);
     {
         dim3 grid(std::max(1, std::min(148, (int)((size_t)H * W / 1024 + 1))), B);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
         k_gather_final<<<grid, 256, 0, st>>>(a.U, a.plane, a.ctl, u_out, (size_t)H * W, B);
         FOE_CUDA(cudaGetLastError());
     }

@@ -16,7 +16,7 @@ from tests.conftest import REPO
 def test_library_builds_and_exports_every_header_symbol():
     _lib.build()
     header = open(os.path.join(REPO, "include", "foe_b200.h")).read()
-    declared = set(re.findall(r"^(?:int|size_t|const char \*)\s*(foe_[a-z0-9_]+)\(", header, re.M))
+    declared = set(re.findall(r"^(?:int|size_t|long long|const char \*)\s*(foe_[a-z0-9_]+)\(", header, re.M))
     assert declared == set(_lib.EXPORTED_SYMBOLS)
     so = ctypes.CDLL(_lib.LIB_PATH)
     for name in declared:
