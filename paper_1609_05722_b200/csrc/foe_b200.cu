@@ -30,7 +30,7 @@
 #include <vector>
 
 struct foe_bank {
-    int n, m, boundary, device;
+    int n, m, boundary, device, zero_mean;
     float *d_kf, *d_alpha;
 };
 
@@ -70,7 +70,7 @@ struct ImgCtl {
 };
 
 struct PassArgs {
-    int B, H, W, n_filters, tiles_x, tiles_y, mode, no_decide;
+    int B, H, W, n_filters, tiles_x, tiles_y, mode, no_decide, zero_mean;
     size_t plane;  // B*H*W: distance between state slots
     const float *kf;     // (n, M*M) flipped taps (correlation orientation of the forward conv)
     const float *alpha;  // (n)
@@ -120,29 +120,6 @@ __device__ __forceinline__ int src_idx(int q, int n) {
     }
 }
 
-template <int M_>
-struct PassCfg {
-    static constexpr int M = M_;
-    static constexpr int R = M / 2;
-    static constexpr int RH = 48, RW = 48;  // region = owned tile + r ring
-    static constexpr int MY = 6;            // micro-tile: MY rows x 4 cols per thread
-    static constexpr int G = 3;             // filter groups per CTA
-    static constexpr int FG = 2;            // filters per group between barriers
-    static constexpr int NTX = RW / 4, NTY = RH / MY, NTG = NTX * NTY, NT = G * NTG;
-    static constexpr int CW = RW + 2 * R;  // staged columns
-    static constexpr int SH = RH + 2 * R;  // staged rows
-    // row pitch: multiple of 4 (float4) with MY*SW == 16 (mod 32) -> conflict-free LDS.128
-    static constexpr int pitch() {
-        int p = (CW + 3) & ~3;
-        while ((MY * p) % 32 != 16) p += 4;
-        return p;
-    }
-    static constexpr int SW = pitch();
-    static constexpr int PLANE = SH * SW;
-    static constexpr int TH = RH - 2 * R, TW = RW - 2 * R;  // max owned tile
-    static_assert(NTG % 32 == 0, "filter groups must be whole warps");
-    static_assert(TH >= 2 * R, "tile too small for the fold rule");
-};
 
 template <int W>
 __device__ __forceinline__ void load_row(const float *p, float (&r)[W]) {
@@ -243,308 +220,7 @@ __device__ __forceinline__ void block_reduce(double (&v)[kNumPartials], double (
     }
 }
 
-// ------------------------------------------------------------------------------------------------
-// the fused pass
-
-template <int M, bool TRIAL, bool SYM>
-__global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
-    using C = PassCfg<M>;
-    constexpr int R = C::R, SW = C::SW, CW = C::CW, SH = C::SH, MY = C::MY, NT = C::NT;
-    constexpr int WIN = 4 + 2 * R;
-
-    extern __shared__ __align__(16) float sm[];
-    __shared__ double red[NT / 32][kNumPartials];
-    __shared__ double s_sum[kNumPartials];
-    __shared__ int s_last;
-
-    const int tid = threadIdx.x;
-    const int b = blockIdx.y;
-    const int H = a.H, W = a.W, nf = a.n_filters;
-
-    int iu = 0, iup = 0, inew = 0, ig = 0, ignew = 0, branch = 0;
-    float tau32 = 0.f, t32 = 0.f, gam32 = 0.f;
-    if (a.mode != MODE_EVAL) {
-        const ImgCtl &c = a.ctl[b];
-        if (c.done && !a.no_decide) return;
-        iu = c.iu; iup = c.iup; inew = c.inew; ig = c.ig; ignew = c.ignew; branch = c.branch;
-        if (TRIAL) {
-            const double tau = a.step_num / c.L;  // SolverConfig.step_size, solver.py:64-65
-            tau32 = (float)tau;
-            t32 = (float)(tau * c.lam);
-            gam32 = (float)a.gamma;
-        }
-    }
-    const size_t HW = (size_t)H * W;
-    const size_t ioff = (size_t)b * HW;
-    const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
-    float *gout, *uout = nullptr;
-    if (a.mode == MODE_EVAL) {
-        uin = a.u_in + ioff;
-        gout = a.g_out + ioff;
-    } else {
-        uin = a.U + iu * a.plane + ioff;
-        if (TRIAL) {
-            upv = a.U + iup * a.plane + ioff;
-            gin = a.Gs + ig * a.plane + ioff;
-            obs = a.obs + ioff;
-            uout = a.U + inew * a.plane + ioff;
-            gout = a.Gs + ignew * a.plane + ioff;
-        } else {
-            gout = a.Gs + ig * a.plane + ioff;
-        }
-    }
-
-    const int t = blockIdx.x;
-    const int tyi = t / a.tiles_x, txi = t - tyi * a.tiles_x;
-    const int s0 = tile_start(tyi, a.tiles_y, C::TH, H, R), s1 = tile_start(tyi + 1, a.tiles_y, C::TH, H, R);
-    const int c0 = tile_start(txi, a.tiles_x, C::TW, W, R), c1 = tile_start(txi + 1, a.tiles_x, C::TW, W, R);
-    const int ry0 = s0 - R, rx0 = c0 - R;  // region origin; staged cell (i,j) <-> (ry0-R+i, rx0-R+j)
-
-    float *Un = sm;
-    float *Du = Un + C::PLANE;
-    float *Psi = TRIAL ? Du + C::PLANE : Du;
-    float *s_taps = Psi + C::G * C::FG * C::PLANE;
-    float *s_alpha = s_taps + nf * M * M;
-
-    for (int k = tid; k < nf * M * M; k += NT) s_taps[k] = a.kf[k];
-    for (int k = tid; k < nf; k += NT) s_alpha[k] = a.alpha[k];
-    // zero ring of every psi plane: psi_0 = 0 outside the region (and outside the image)
-    if constexpr (R > 0) {
-        constexpr int RING = SH * CW - C::RH * C::RW;
-        for (int k = tid; k < C::G * C::FG * RING; k += NT) {
-            const int pl = k / RING, e = k - pl * RING;
-            int i, j;
-            if (e < R * CW) { i = e / CW; j = e - i * CW; }
-            else if (e < 2 * R * CW) { const int e2 = e - R * CW; i = C::RH + R + e2 / CW; j = e2 % CW; }
-            else { const int e3 = e - 2 * R * CW; i = R + e3 / (2 * R); const int jj = e3 % (2 * R); j = jj < R ? jj : C::RW + jj; }
-            Psi[pl * C::PLANE + i * SW + j] = 0.0f;
-        }
-    }
-
-    // ---- prologue: stage u (EVAL/INIT) or the trial point u_new and du (TRIAL) -------------------
-    double acc[kNumPartials];
-#pragma unroll
-    for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
-    for (int k = tid; k < SH * CW; k += NT) {
-        const int i = k / CW, j = k - i * CW;
-        const int gy = ry0 - R + i, gx = rx0 - R + j;
-        const size_t o = (size_t)src_idx<SYM>(gy, H) * W + src_idx<SYM>(gx, W);
-        if (TRIAL) {
-            const float u = __ldg(uin + o), up = __ldg(upv + o), g = __ldg(gin + o), ob = __ldg(obs + o);
-            // u - tau g + gamma (u - u_prev)  (solver.py:146-149)
-            const float ut = (u - tau32 * g) + gam32 * (u - up);
-            const float un = (branch == FOE_QUADRATIC) ? prox_quad(ut, t32, ob) : prox_idv(ut, t32, ob);
-            const float du = un - u;
-            Un[i * SW + j] = un;
-            Du[i * SW + j] = du;
-            if (gy >= s0 && gy < s1 && gx >= c0 && gx < c1) {
-                acc[1] += (double)du * (double)du;  // vdot(du, du)  solver.py:152
-                acc[2] += (double)g * (double)du;   // vdot(g, du)   solver.py:153
-                acc[3] += (double)u * (double)u;    // |u|^2 for the stop test, solver.py:173
-                if (branch == FOE_QUADRATIC) {
-                    const double d = (double)un - (double)ob;
-                    acc[4] += d * d;
-                } else {
-                    acc[4] += (double)un;
-                    if (ob > 0.0f) {
-                        if (un > 0.0f) acc[5] += (double)ob * (double)logf(un);
-                        else acc[6] += 1.0;
-                    }
-                }
-            }
-        } else {
-            Un[i * SW + j] = __ldg(uin + o);
-        }
-    }
-    __syncthreads();
-
-    // ---- filter loop -----------------------------------------------------------------------------
-    const int grp = tid / C::NTG, lt = tid - grp * C::NTG;
-    const int tx = lt % C::NTX, ty = lt / C::NTX;
-    const int fpg = (nf + C::G - 1) / C::G;
-    const int fbeg = grp * fpg, fend = min(nf, fbeg + fpg);
-    const int ly0 = ty * MY, lx0 = tx * 4;  // region-local origin of this thread's micro-tile
-
-    bool own_r[MY], img_r[MY], own_c[4], img_c[4];
-#pragma unroll
-    for (int o = 0; o < MY; ++o) {
-        const int gy = ry0 + ly0 + o;
-        own_r[o] = gy >= s0 && gy < s1;
-        img_r[o] = gy >= 0 && gy < H;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const int gx = rx0 + lx0 + c;
-        own_c[c] = gx >= c0 && gx < c1;
-        img_c[c] = gx >= 0 && gx < W;
-    }
-
-    float gacc[MY][4];
-#pragma unroll
-    for (int o = 0; o < MY; ++o)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) gacc[o][c] = 0.0f;
-
-    const float *ubase = Un + ly0 * SW + lx0;
-    const float *dbase = Du + ly0 * SW + lx0;
-
-#pragma unroll 1
-    for (int fr = 0; fr < fpg; fr += C::FG) {
-#pragma unroll 1
-        for (int q = 0; q < C::FG; ++q) {
-            const int f = fbeg + fr + q;
-            if (fr + q >= fpg || f >= fend) continue;
-            float w[M * M];
-#pragma unroll
-            for (int k = 0; k < M * M; ++k) w[k] = s_taps[f * M * M + k];
-            const float al = s_alpha[f];
-            float z[MY][4], dz[MY][4];
-#pragma unroll
-            for (int o = 0; o < MY; ++o)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) { z[o][c] = 0.0f; dz[o][c] = 0.0f; }
-            // forward responses: z = K_f u_new (image.py:37-58), dz = K_f du
-#pragma unroll
-            for (int i = 0; i < MY + 2 * R; ++i) {
-                float ru[WIN], rd[WIN];
-                load_row<WIN>(ubase + i * SW, ru);
-                if (TRIAL) load_row<WIN>(dbase + i * SW, rd);
-#pragma unroll
-                for (int o = 0; o < MY; ++o) {
-                    const int aa = i - o;
-                    if (aa < 0 || aa >= M) continue;
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb) {
-                        const float wt = w[aa * M + bb];
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            z[o][c] = fmaf(wt, ru[c + bb], z[o][c]);
-                            if (TRIAL) dz[o][c] = fmaf(wt, rd[c + bb], dz[o][c]);
-                        }
-                    }
-                }
-            }
-            // pointwise: psi = a_f rho'(z) (prior.py:31-32), energy terms on owned pixels
-            float *ps = Psi + (grp * C::FG + q) * C::PLANE + (ly0 + R) * SW + lx0 + R;
-            double e = 0.0;
-#pragma unroll
-            for (int o = 0; o < MY; ++o) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const float zz = z[o][c];
-                    float psi = __fdividef(2.0f * al * zz, fmaf(zz, zz, 1.0f));
-                    if (SYM && !(img_r[o] && img_c[c])) psi = 0.0f;
-                    ps[o * SW + c] = psi;
-                    if (own_r[o] && own_c[c]) {
-                        if (TRIAL) {
-                            // F(u_new) - F(u) per response: log1p(dz (2 z_old + dz) / (1 + z_old^2))
-                            const float d = dz[o][c];
-                            const float zo = zz - d;
-                            const float x = d * fmaf(2.0f, zo, d) / fmaf(zo, zo, 1.0f);
-                            e += (double)log1pf(x);
-                        } else {
-                            e += (double)log1pf(zz * zz);  // potential order 0, prior.py:30
-                        }
-                    }
-                }
-            }
-            acc[0] += (double)al * e;
-        }
-        __syncthreads();
-        // adjoint: gacc += K_f^T psi_f  (correlation with the unflipped kernel, image.py:84-87)
-#pragma unroll 1
-        for (int q = 0; q < C::FG; ++q) {
-            const int f = fbeg + fr + q;
-            if (fr + q >= fpg || f >= fend) continue;
-            float w[M * M];
-#pragma unroll
-            for (int k = 0; k < M * M; ++k) w[k] = s_taps[f * M * M + (M * M - 1 - k)];
-            const float *pb = Psi + (grp * C::FG + q) * C::PLANE + ly0 * SW + lx0;
-#pragma unroll
-            for (int i = 0; i < MY + 2 * R; ++i) {
-                float rp[WIN];
-                load_row<WIN>(pb + i * SW, rp);
-#pragma unroll
-                for (int o = 0; o < MY; ++o) {
-                    const int aa = i - o;
-                    if (aa < 0 || aa >= M) continue;
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb) {
-                        const float wt = w[aa * M + bb];
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) gacc[o][c] = fmaf(wt, rp[c + bb], gacc[o][c]);
-                    }
-                }
-            }
-        }
-        __syncthreads();
-    }
-
-    // ---- combine filter groups, fold padded pixels (P^T, image.py:88-90), write ------------------
-    float *gb = Psi;  // G planes of RH x RW
-#pragma unroll
-    for (int o = 0; o < MY; ++o)
-        *reinterpret_cast<float4 *>(gb + grp * C::RH * C::RW + (ly0 + o) * C::RW + lx0) =
-            make_float4(gacc[o][0], gacc[o][1], gacc[o][2], gacc[o][3]);
-    __syncthreads();
-    auto gsum = [&](int ly, int lx) {
-        float s = gb[ly * C::RW + lx];
-#pragma unroll
-        for (int g2 = 1; g2 < C::G; ++g2) s += gb[g2 * C::RH * C::RW + ly * C::RW + lx];
-        return s;
-    };
-    const int oh = s1 - s0, ow = c1 - c0;
-    for (int k = tid; k < oh * ow; k += NT) {
-        const int yy = k / ow, xx = k - yy * ow;
-        const int gy = s0 + yy, gx = c0 + xx;
-        const int ly = gy - ry0, lx = gx - rx0;
-        float val = gsum(ly, lx);
-        if (SYM && R > 0) {
-            int my = -1, mx = -1;
-            if (gy < R) my = (-1 - gy) - ry0;
-            else if (gy >= H - R) my = (2 * H - 1 - gy) - ry0;
-            if (gx < R) mx = (-1 - gx) - rx0;
-            else if (gx >= W - R) mx = (2 * W - 1 - gx) - rx0;
-            if (my >= 0) val += gsum(my, lx);
-            if (mx >= 0) val += gsum(ly, mx);
-            if (my >= 0 && mx >= 0) val += gsum(my, mx);
-        }
-        const size_t o = (size_t)gy * W + gx;
-        gout[o] = val;
-        if (TRIAL) uout[o] = Un[(ly + R) * SW + lx + R];
-    }
-
-    // ---- per-tile partials, last CTA of the image reduces and decides ----------------------------
-    const int ntiles = a.tiles_x * a.tiles_y;
-    block_reduce<NT>(acc, red, s_sum);
-    if (tid < kNumPartials) {
-        a.partials[((size_t)b * ntiles + t) * kPartialStride + tid] = s_sum[tid];
-        __threadfence();
-    }
-    __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(a.tickets + b, 1u) == (unsigned)(ntiles - 1));
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    double tot[kNumPartials];
-#pragma unroll
-    for (int k = 0; k < kNumPartials; ++k) tot[k] = 0.0;
-    const double *pp = a.partials + (size_t)b * ntiles * kPartialStride;
-    for (int tt = tid; tt < ntiles; tt += NT)
-#pragma unroll
-        for (int k = 0; k < kNumPartials; ++k) tot[k] += __ldcg(pp + (size_t)tt * kPartialStride + k);
-    __syncthreads();
-    block_reduce<NT>(tot, red, s_sum);
-    __syncthreads();
-    if (tid == 0) {
-        a.tickets[b] = 0u;
-        if (a.mode == MODE_EVAL) {
-            a.energy_out[b] = s_sum[0];
-        } else if (!a.no_decide) {
-            decide(a, b, s_sum);
-        }
-    }
-}
+#include "foe_pass.cuh"
 
 // ------------------------------------------------------------------------------------------------
 // elementwise kernels
@@ -668,7 +344,7 @@ int grid_1d(int64_t n, int block = 256) {
 template <int M>
 size_t pass_smem_bytes(int nf, bool trial) {
     using C = PassCfg<M>;
-    return sizeof(float) * ((size_t)(trial ? 2 : 1) * C::PLANE + (size_t)C::G * C::FG * C::PLANE + (size_t)nf * M * M + nf);
+    return sizeof(float) * ((size_t)(trial ? 2 : 1) * C::PLANE + (size_t)C::NPSI * C::PLANE + (size_t)nf * C::TAPS + nf);
 }
 
 template <int M, bool TRIAL, bool SYM>
@@ -708,9 +384,9 @@ int launch_pass(int m, bool sym, const PassArgs &a, cudaStream_t st) {
 
 void tile_counts(int m, int H, int W, int *tx, int *ty) {
     const int r = m / 2;
-    const int T = 48 - 2 * r;  // PassCfg<M>::TH == TW for every M
-    *ty = (H + T - 1) / T;
-    *tx = (W + T - 1) / T;
+    const int TH = PassCfg<1>::RH - 2 * r, TW = PassCfg<1>::RW - 2 * r;  // PassCfg<M>::TH / TW
+    *ty = (H + TH - 1) / TH;
+    *tx = (W + TW - 1) / TW;
 }
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
@@ -776,14 +452,35 @@ int foe_bank_create(const double *filters, const double *weights, int n, int m, 
     for (int i = 0; i < n; ++i)
         if (!(weights[i] > 0)) return fail(FOE_E_INVALID, "expert weights must be strictly positive");
     std::vector<float> kf((size_t)n * m * m), al(n);
+    int zero_mean = m > 1;
     for (int i = 0; i < n; ++i) {
         al[i] = (float)weights[i];
+        double sum = 0.0, asum = 0.0;
         for (int a = 0; a < m; ++a)
-            for (int b = 0; b < m; ++b)  // cv2.filter2D correlates with the flipped kernel, image.py:49-50
-                kf[(size_t)i * m * m + a * m + b] = (float)filters[(size_t)i * m * m + (m - 1 - a) * m + (m - 1 - b)];
+            for (int b = 0; b < m; ++b) {  // cv2.filter2D correlates with the flipped kernel, image.py:49-50
+                const double v = filters[(size_t)i * m * m + (m - 1 - a) * m + (m - 1 - b)];
+                kf[(size_t)i * m * m + a * m + b] = (float)v;
+                sum += v;
+                asum += fabs(v);
+            }
+        if (!(fabs(sum) <= 1e-9 * asum)) zero_mean = 0;
+    }
+    if (zero_mean) {
+        // the fp32 taps of a zero-mean filter are made to sum to zero as well (adjust the largest tap
+        // by the exact fp32 residual), so shifting the input by a constant leaves K u unchanged
+        for (int i = 0; i < n; ++i) {
+            float *k = kf.data() + (size_t)i * m * m;
+            double s32 = 0.0;
+            int big = 0;
+            for (int e = 0; e < m * m; ++e) {
+                s32 += (double)k[e];
+                if (fabsf(k[e]) > fabsf(k[big])) big = e;
+            }
+            k[big] = (float)((double)k[big] - s32);
+        }
     }
     foe_bank *bk = new foe_bank();
-    bk->n = n; bk->m = m; bk->boundary = boundary;
+    bk->n = n; bk->m = m; bk->boundary = boundary; bk->zero_mean = zero_mean;
     cudaGetDevice(&bk->device);
     if (cudaMalloc(&bk->d_kf, kf.size() * sizeof(float)) != cudaSuccess ||
         cudaMalloc(&bk->d_alpha, al.size() * sizeof(float)) != cudaSuccess) {
@@ -909,7 +606,7 @@ int foe_energy_grad(const foe_bank *bank, const float *u, float *grad, double *e
     if (workspace_bytes < foe_eval_workspace_size(bank, B, H, W)) return fail(FOE_E_INVALID, "workspace too small");
     cudaStream_t st = (cudaStream_t)stream;
     PassArgs a{};
-    a.B = B; a.H = H; a.W = W; a.n_filters = bank->n;
+    a.B = B; a.H = H; a.W = W; a.n_filters = bank->n; a.zero_mean = bank->zero_mean;
     tile_counts(bank->m, H, W, &a.tiles_x, &a.tiles_y);
     a.mode = MODE_EVAL;
     a.kf = bank->d_kf; a.alpha = bank->d_alpha;
@@ -927,7 +624,7 @@ size_t foe_solve_workspace_size(const foe_bank *bank, int B, int H, int W, int t
 
 static void fill_solve_args(PassArgs &a, const foe_bank *bank, const foe_solver_cfg &cfg, int B, int H, int W,
                             int trace_cap, char *ws, const SolveLayout &L) {
-    a.B = B; a.H = H; a.W = W; a.n_filters = bank->n;
+    a.B = B; a.H = H; a.W = W; a.n_filters = bank->n; a.zero_mean = bank->zero_mean;
     tile_counts(bank->m, H, W, &a.tiles_x, &a.tiles_y);
     a.plane = (size_t)B * H * W;
     a.kf = bank->d_kf; a.alpha = bank->d_alpha;

@@ -1,0 +1,423 @@
+// foe_pass.cuh -- the fused FoE pass kernel (included by foe_b200.cu).
+//
+// One CTA = one tile of one image.  Region = owned tile + r ring (the pixels whose responses the
+// adjoint needs); staged cells = region + another r ring (the inputs of those responses).
+//
+// Thread layout: 3 filter groups x 6 warps.  A warp covers 8 micro-columns x 4 micro-rows of
+// 3x4-pixel micro-tiles, so each 8-lane LDS.128 phase reads 32 consecutive floats of one smem row
+// (bank-conflict free for any pitch).  Each group owns every 3rd filter slice of the bank and
+// double-buffered psi planes, so groups synchronise only among themselves (named barriers).
+//
+// Per filter and thread: forward z = K u_new and dz = K du on 12 pixels from a 5x8 (r=2) window
+// streamed from smem (600 FFMA), pointwise psi = 2a z/(1+z^2) and the energy change
+// a*log1p(dz(2z_o+dz)/(1+z_o^2)) evaluated as 2a*atanh(t), t = (z^2-z_o^2)/((1+z^2)+(1+z_o^2)),
+// then the adjoint K^T psi (300 FFMA).
+
+template <int M_>
+struct PassCfg {
+    static constexpr int M = M_;
+    static constexpr int R = M / 2;
+    static constexpr int RH = 36, RW = 64;  // region (owned tile + r ring)
+    static constexpr int MY = 3, MX = 4;    // micro-tile per thread
+    static constexpr int G = 3;             // filter groups per CTA
+    static constexpr int FG = 2;            // filters per group between group barriers
+    static constexpr int NTX = RW / MX, NTY = RH / MY, NTG = NTX * NTY, NT = G * NTG;
+    static constexpr int WARPS_G = NTG / 32;
+    static constexpr int CW = RW + 2 * R;       // staged columns
+    static constexpr int SH = RH + 2 * R;       // staged rows
+    static constexpr int SW = (CW + 3) & ~3;    // row pitch (float4 aligned)
+    static constexpr int PLANE = SH * SW;
+    static constexpr int NPSI = 2 * G * FG;     // double-buffered psi planes
+    static constexpr int TH = RH - 2 * R, TW = RW - 2 * R;  // max owned tile
+    static constexpr int TAPS = (M * M + 3) & ~3;           // per-filter tap stride (float4)
+    static_assert(NTX == 16 && NTY == 12, "warp layout assumes 16 x 12 micro-tiles per group");
+    static_assert(TH >= 2 * R, "tile too small for the fold rule");
+    static_assert(G * RH * RW <= NPSI * PLANE, "group partial-gradient buffer must fit the psi planes");
+};
+
+__device__ __forceinline__ float rcp_approx(float x) {  // MUFU.RCP, no denormal fix-up
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ void group_barrier(int grp, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(nthreads) : "memory");
+}
+
+// 2*atanh(t) == log1p(x) for t = x / (2 + x).  Series to t^9 for |t| <= 0.2 (rel. error < 1e-8);
+// MUFU-based logarithm of (1+t)/(1-t) otherwise (|result| >= 0.4, abs. error ~1e-7).
+__device__ __forceinline__ float two_atanh(float t) {
+    if (fabsf(t) <= 0.2f) {
+        const float s = t * t;
+        float p = fmaf(s, 1.0f / 9.0f, 1.0f / 7.0f);
+        p = fmaf(s, p, 1.0f / 5.0f);
+        p = fmaf(s, p, 1.0f / 3.0f);
+        p = fmaf(s, p, 1.0f);
+        return 2.0f * t * p;
+    }
+    return __logf((1.0f + t) * rcp_approx(1.0f - t));
+}
+
+template <int M, bool TRIAL, bool SYM>
+__global__ void __maxnreg__(112) k_pass(const PassArgs a) {
+    using C = PassCfg<M>;
+    constexpr int R = C::R, SW = C::SW, CW = C::CW, SH = C::SH, MY = C::MY, NT = C::NT;
+    constexpr int WIN = C::MX + 2 * R;  // window width per micro-tile row
+    constexpr int WR = MY + 2 * R;      // window rows
+
+    extern __shared__ __align__(16) float sm[];
+    __shared__ double red[NT / 32][kNumPartials];
+    __shared__ double s_sum[kNumPartials];
+    __shared__ int s_last;
+
+    const int tid = threadIdx.x;
+    const int b = blockIdx.y;
+    const int H = a.H, W = a.W, nf = a.n_filters;
+
+    int iu = 0, iup = 0, inew = 0, ig = 0, ignew = 0, branch = 0;
+    float tau32 = 0.f, t32 = 0.f, gam32 = 0.f;
+    if (a.mode != MODE_EVAL) {
+        const ImgCtl &c = a.ctl[b];
+        if (c.done && !a.no_decide) return;
+        iu = c.iu; iup = c.iup; inew = c.inew; ig = c.ig; ignew = c.ignew; branch = c.branch;
+        if (TRIAL) {
+            const double tau = a.step_num / c.L;  // SolverConfig.step_size, solver.py:64-65
+            tau32 = (float)tau;
+            t32 = (float)(tau * c.lam);
+            gam32 = (float)a.gamma;
+        }
+    }
+    const size_t HW = (size_t)H * W;
+    const size_t ioff = (size_t)b * HW;
+    const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
+    float *gout, *uout = nullptr;
+    if (a.mode == MODE_EVAL) {
+        uin = a.u_in + ioff;
+        gout = a.g_out + ioff;
+    } else {
+        uin = a.U + iu * a.plane + ioff;
+        if (TRIAL) {
+            upv = a.U + iup * a.plane + ioff;
+            gin = a.Gs + ig * a.plane + ioff;
+            obs = a.obs + ioff;
+            uout = a.U + inew * a.plane + ioff;
+            gout = a.Gs + ignew * a.plane + ioff;
+        } else {
+            gout = a.Gs + ig * a.plane + ioff;
+        }
+    }
+
+    const int t = blockIdx.x;
+    const int tyi = t / a.tiles_x, txi = t - tyi * a.tiles_x;
+    const int s0 = tile_start(tyi, a.tiles_y, C::TH, H, R), s1 = tile_start(tyi + 1, a.tiles_y, C::TH, H, R);
+    const int c0 = tile_start(txi, a.tiles_x, C::TW, W, R), c1 = tile_start(txi + 1, a.tiles_x, C::TW, W, R);
+    const int ry0 = s0 - R, rx0 = c0 - R;  // region origin; staged cell (i,j) <-> (ry0-R+i, rx0-R+j)
+
+    float *Un = sm;
+    float *Du = Un + C::PLANE;
+    float *Psi = TRIAL ? Du + C::PLANE : Du;
+    float *s_taps = Psi + C::NPSI * C::PLANE;
+    float *s_alpha = s_taps + nf * C::TAPS;
+
+    for (int k = tid; k < nf * C::TAPS; k += NT) {
+        const int f = k / C::TAPS, e = k - f * C::TAPS;
+        s_taps[k] = e < M * M ? a.kf[f * M * M + e] : 0.0f;
+    }
+    for (int k = tid; k < nf; k += NT) s_alpha[k] = a.alpha[k];
+    // zero ring of every psi plane: psi_0 = 0 outside the region (and the image)
+    if constexpr (R > 0) {
+        constexpr int RING = SH * CW - C::RH * C::RW;
+        for (int k = tid; k < C::NPSI * RING; k += NT) {
+            const int pl = k / RING, e = k - pl * RING;
+            int i, j;
+            if (e < R * CW) { i = e / CW; j = e - i * CW; }
+            else if (e < 2 * R * CW) { const int e2 = e - R * CW; i = C::RH + R + e2 / CW; j = e2 % CW; }
+            else { const int e3 = e - 2 * R * CW; i = R + e3 / (2 * R); const int jj = e3 % (2 * R); j = jj < R ? jj : C::RW + jj; }
+            Psi[pl * C::PLANE + i * SW + j] = 0.0f;
+        }
+    }
+
+    // Filters are zero-mean (DCT basis without DC, image.py:117-130), so K(u - c) == K u: staging
+    // u - c with c = the tile's anchor pixel keeps the fp32 products small (accuracy, not speed).
+    const float shift = a.zero_mean ? __ldg(uin + (size_t)s0 * W + c0) : 0.0f;
+
+    // ---- prologue: stage u (EVAL/INIT) or the trial point u_new and du (TRIAL) -------------------
+    double acc[kNumPartials];
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
+    for (int k = tid; k < SH * CW; k += NT) {
+        const int i = k / CW, j = k - i * CW;
+        const int gy = ry0 - R + i, gx = rx0 - R + j;
+        const size_t o = (size_t)src_idx<SYM>(gy, H) * W + src_idx<SYM>(gx, W);
+        const bool own = gy >= s0 && gy < s1 && gx >= c0 && gx < c1;
+        if (TRIAL) {
+            const float u = __ldg(uin + o), up = __ldg(upv + o), g = __ldg(gin + o), ob = __ldg(obs + o);
+            // u - tau g + gamma (u - u_prev)  (solver.py:146-149)
+            const float ut = (u - tau32 * g) + gam32 * (u - up);
+            const float un = (branch == FOE_QUADRATIC) ? prox_quad(ut, t32, ob) : prox_idv(ut, t32, ob);
+            const float du = un - u;
+            Un[i * SW + j] = un - shift;
+            Du[i * SW + j] = du;
+            if (own) {
+                uout[(size_t)gy * W + gx] = un;
+                acc[1] += (double)du * (double)du;  // vdot(du, du)  solver.py:152
+                acc[2] += (double)g * (double)du;   // vdot(g, du)   solver.py:153
+                acc[3] += (double)u * (double)u;    // |u|^2 for the stop test, solver.py:173
+                if (branch == FOE_QUADRATIC) {
+                    const double d = (double)un - (double)ob;
+                    acc[4] += d * d;
+                } else {
+                    acc[4] += (double)un;
+                    if (ob > 0.0f) {
+                        if (un > 0.0f) acc[5] += (double)ob * (double)logf(un);
+                        else acc[6] += 1.0;
+                    }
+                }
+            }
+        } else {
+            Un[i * SW + j] = __ldg(uin + o) - shift;
+        }
+    }
+    __syncthreads();
+
+    // ---- filter loop -----------------------------------------------------------------------------
+    const int grp = tid / C::NTG, lt = tid - grp * C::NTG;
+    const int wg = lt >> 5, lane = lt & 31;
+    const int tx = (wg & 1) * 8 + (lane & 7), ty = (wg >> 1) * 4 + (lane >> 3);
+    const int fpg = (nf + C::G - 1) / C::G;
+    const int fbeg = grp * fpg, fend = min(nf, fbeg + fpg);
+    const int ly0 = ty * MY, lx0 = tx * C::MX;  // region-local origin of this thread's micro-tile
+
+    // edge handling, hoisted out of the filter loop: which of this thread's pixels lie outside the
+    // image (psi_0 must be 0 there, symmetric rule) and which it owns (energy terms)
+    unsigned out_bits = 0u, own_bits = 0u;
+#pragma unroll
+    for (int o = 0; o < MY; ++o) {
+        const int gy = ry0 + ly0 + o;
+#pragma unroll
+        for (int c = 0; c < C::MX; ++c) {
+            const int gx = rx0 + lx0 + c;
+            if (SYM && !(gy >= 0 && gy < H && gx >= 0 && gx < W)) out_bits |= 1u << (o * C::MX + c);
+            if (gy >= s0 && gy < s1 && gx >= c0 && gx < c1) own_bits |= 1u << (o * C::MX + c);
+        }
+    }
+    float epx[MY][C::MX];  // per-pixel energy terms summed over this group's filters (fp32)
+#pragma unroll
+    for (int o = 0; o < MY; ++o)
+#pragma unroll
+        for (int c = 0; c < C::MX; ++c) epx[o][c] = 0.0f;
+
+    float gacc[MY][C::MX];
+#pragma unroll
+    for (int o = 0; o < MY; ++o)
+#pragma unroll
+        for (int c = 0; c < C::MX; ++c) gacc[o][c] = 0.0f;
+
+    const float *ubase = Un + ly0 * SW + lx0;
+    const float *dbase = Du + ly0 * SW + lx0;
+
+    int buf = 0;
+#pragma unroll 1
+    for (int fr = 0; fr < fpg; fr += C::FG, buf ^= 1) {
+#pragma unroll 1
+        for (int q = 0; q < C::FG; ++q) {
+            const int f = fbeg + fr + q;
+            if (fr + q >= fpg || f >= fend) continue;
+            float w[C::TAPS];
+#pragma unroll
+            for (int k = 0; k < C::TAPS; k += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(s_taps + f * C::TAPS + k);
+                w[k] = v.x; w[k + 1] = v.y; w[k + 2] = v.z; w[k + 3] = v.w;
+            }
+            const float al = s_alpha[f];
+            float z[MY][C::MX], dz[MY][C::MX];
+#pragma unroll
+            for (int o = 0; o < MY; ++o)
+#pragma unroll
+                for (int c = 0; c < C::MX; ++c) { z[o][c] = 0.0f; dz[o][c] = 0.0f; }
+            // forward responses: z = K_f u_new (image.py:37-58), dz = K_f du
+#pragma unroll
+            for (int i = 0; i < WR; ++i) {
+                float ru[WIN], rd[WIN];
+                load_row<WIN>(ubase + i * SW, ru);
+                if (TRIAL) load_row<WIN>(dbase + i * SW, rd);
+#pragma unroll
+                for (int o = 0; o < MY; ++o) {
+                    const int aa = i - o;
+                    if (aa < 0 || aa >= M) continue;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) {
+                        const float wt = w[aa * M + bb];
+#pragma unroll
+                        for (int c = 0; c < C::MX; ++c) {
+                            z[o][c] = fmaf(wt, ru[c + bb], z[o][c]);
+                            if (TRIAL) dz[o][c] = fmaf(wt, rd[c + bb], dz[o][c]);
+                        }
+                    }
+                }
+            }
+            // pointwise: psi = a rho'(z) (prior.py:31-32); energy terms
+            float *ps = Psi + ((buf * C::G + grp) * C::FG + q) * C::PLANE + (ly0 + R) * SW + lx0 + R;
+            const float a2 = 2.0f * al;
+            float tt[MY][C::MX];
+            float tmax = 0.0f;
+#pragma unroll
+            for (int o = 0; o < MY; ++o) {
+#pragma unroll
+                for (int c = 0; c < C::MX; ++c) {
+                    const float zz = z[o][c];
+                    const float q1 = fmaf(zz, zz, 1.0f);
+                    ps[o * SW + c] = (a2 * zz) * rcp_approx(q1);
+                    if (TRIAL) {
+                        // F(u_new) - F(u) per response: log((1+z^2)/(1+z_o^2)) = 2 atanh(t) with
+                        // t = (z^2 - z_o^2) / ((1+z^2) + (1+z_o^2)), z_o = z - dz
+                        const float d = dz[o][c];
+                        const float zo = zz - d;
+                        const float num = d * fmaf(2.0f, zo, d);
+                        const float den = fmaf(zo, zo, q1) + 1.0f;
+                        tt[o][c] = num * rcp_approx(den);
+                        tmax = fmaxf(tmax, fabsf(tt[o][c]));
+                    }
+                }
+            }
+            if (SYM && out_bits) {  // psi_0 = 0 outside the image (only threads on an image edge)
+#pragma unroll
+                for (int o = 0; o < MY; ++o)
+#pragma unroll
+                    for (int c = 0; c < C::MX; ++c)
+                        if (out_bits >> (o * C::MX + c) & 1u) ps[o * SW + c] = 0.0f;
+            }
+            if (TRIAL) {
+                if (__any_sync(0xffffffffu, tmax > 0.2f)) {
+#pragma unroll
+                    for (int o = 0; o < MY; ++o)
+#pragma unroll
+                        for (int c = 0; c < C::MX; ++c) epx[o][c] = fmaf(al, two_atanh(tt[o][c]), epx[o][c]);
+                } else {
+#pragma unroll
+                    for (int o = 0; o < MY; ++o)
+#pragma unroll
+                        for (int c = 0; c < C::MX; ++c) {
+                            const float t1 = tt[o][c], sq = t1 * t1;
+                            float pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
+                            pp = fmaf(sq, pp, 1.0f / 5.0f);
+                            pp = fmaf(sq, pp, 1.0f / 3.0f);
+                            pp = fmaf(sq, pp, 1.0f);
+                            epx[o][c] = fmaf(a2 * t1, pp, epx[o][c]);
+                        }
+                }
+            } else {
+#pragma unroll
+                for (int o = 0; o < MY; ++o)
+#pragma unroll
+                    for (int c = 0; c < C::MX; ++c) epx[o][c] = fmaf(al, log1pf(z[o][c] * z[o][c]), epx[o][c]);
+            }
+        }
+        group_barrier(grp, C::NTG);
+        // adjoint: gacc += K_f^T psi_f  (correlation with the unflipped kernel, image.py:84-87)
+#pragma unroll 1
+        for (int q = 0; q < C::FG; ++q) {
+            const int f = fbeg + fr + q;
+            if (fr + q >= fpg || f >= fend) continue;
+            float w[C::TAPS];
+#pragma unroll
+            for (int k = 0; k < C::TAPS; k += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(s_taps + f * C::TAPS + k);
+                w[k] = v.x; w[k + 1] = v.y; w[k + 2] = v.z; w[k + 3] = v.w;
+            }
+            const float *pb = Psi + ((buf * C::G + grp) * C::FG + q) * C::PLANE + ly0 * SW + lx0;
+#pragma unroll
+            for (int i = 0; i < WR; ++i) {
+                float rp[WIN];
+                load_row<WIN>(pb + i * SW, rp);
+#pragma unroll
+                for (int o = 0; o < MY; ++o) {
+                    const int aa = i - o;
+                    if (aa < 0 || aa >= M) continue;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) {
+                        const float wt = w[(M - 1 - aa) * M + (M - 1 - bb)];
+#pragma unroll
+                        for (int c = 0; c < C::MX; ++c) gacc[o][c] = fmaf(wt, rp[c + bb], gacc[o][c]);
+                    }
+                }
+            }
+        }
+        // no second barrier: the next round writes the other psi buffer, and its barrier orders
+        // this round's reads before the round after overwrites this buffer
+    }
+    {
+        double e = 0.0;  // owned pixels only, fp64 across pixels
+#pragma unroll
+        for (int o = 0; o < MY; ++o)
+#pragma unroll
+            for (int c = 0; c < C::MX; ++c)
+                if (own_bits >> (o * C::MX + c) & 1u) e += (double)epx[o][c];
+        acc[0] = e;
+    }
+    __syncthreads();
+
+    // ---- combine filter groups, fold padded pixels (P^T, image.py:88-90), write ------------------
+    float *gb = Psi;  // G planes of RH x RW
+#pragma unroll
+    for (int o = 0; o < MY; ++o)
+        *reinterpret_cast<float4 *>(gb + grp * C::RH * C::RW + (ly0 + o) * C::RW + lx0) =
+            make_float4(gacc[o][0], gacc[o][1], gacc[o][2], gacc[o][3]);
+    __syncthreads();
+    auto gsum = [&](int ly, int lx) {
+        float s = gb[ly * C::RW + lx];
+#pragma unroll
+        for (int g2 = 1; g2 < C::G; ++g2) s += gb[g2 * C::RH * C::RW + ly * C::RW + lx];
+        return s;
+    };
+    const int oh = s1 - s0, ow = c1 - c0;
+    for (int k = tid; k < oh * ow; k += NT) {
+        const int yy = k / ow, xx = k - yy * ow;
+        const int gy = s0 + yy, gx = c0 + xx;
+        const int ly = gy - ry0, lx = gx - rx0;
+        float val = gsum(ly, lx);
+        if (SYM && R > 0) {
+            int my = -1, mx = -1;
+            if (gy < R) my = (-1 - gy) - ry0;
+            else if (gy >= H - R) my = (2 * H - 1 - gy) - ry0;
+            if (gx < R) mx = (-1 - gx) - rx0;
+            else if (gx >= W - R) mx = (2 * W - 1 - gx) - rx0;
+            if (my >= 0) val += gsum(my, lx);
+            if (mx >= 0) val += gsum(ly, mx);
+            if (my >= 0 && mx >= 0) val += gsum(my, mx);
+        }
+        gout[(size_t)gy * W + gx] = val;
+    }
+
+    // ---- per-tile partials, last CTA of the image reduces and decides ----------------------------
+    const int ntiles = a.tiles_x * a.tiles_y;
+    block_reduce<NT>(acc, red, s_sum);
+    if (tid < kNumPartials) {
+        a.partials[((size_t)b * ntiles + t) * kPartialStride + tid] = s_sum[tid];
+        __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(a.tickets + b, 1u) == (unsigned)(ntiles - 1));
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double tot[kNumPartials];
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) tot[k] = 0.0;
+    const double *pp = a.partials + (size_t)b * ntiles * kPartialStride;
+    for (int tt = tid; tt < ntiles; tt += NT)
+#pragma unroll
+        for (int k = 0; k < kNumPartials; ++k) tot[k] += __ldcg(pp + (size_t)tt * kPartialStride + k);
+    __syncthreads();
+    block_reduce<NT>(tot, red, s_sum);
+    __syncthreads();
+    if (tid == 0) {
+        a.tickets[b] = 0u;
+        if (a.mode == MODE_EVAL) {
+            a.energy_out[b] = s_sum[0];
+        } else if (!a.no_decide) {
+            decide(a, b, s_sum);
+        }
+    }
+}
