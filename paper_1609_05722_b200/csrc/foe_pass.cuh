@@ -60,7 +60,7 @@ __device__ __forceinline__ float two_atanh(float t) {
 }
 
 template <int M, bool TRIAL, bool SYM>
-__global__ void __maxnreg__(112) k_pass(const PassArgs a) {
+__global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     using C = PassCfg<M>;
     constexpr int R = C::R, SW = C::SW, CW = C::CW, SH = C::SH, MY = C::MY, NT = C::NT;
     constexpr int WIN = C::MX + 2 * R;  // window width per micro-tile row
