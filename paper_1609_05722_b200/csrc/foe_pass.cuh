@@ -20,14 +20,14 @@ struct PassCfg {
     static constexpr int RH = 36, RW = 64;  // region (owned tile + r ring)
     static constexpr int MY = 3, MX = 4;    // micro-tile per thread
     static constexpr int G = 3;             // filter groups per CTA
-    static constexpr int FG = 2;            // filters per group between group barriers
+    static constexpr int NBUF = 4;          // psi buffers per group (pipelined mbarrier ring)
     static constexpr int NTX = RW / MX, NTY = RH / MY, NTG = NTX * NTY, NT = G * NTG;
     static constexpr int WARPS_G = NTG / 32;
     static constexpr int CW = RW + 2 * R;       // staged columns
     static constexpr int SH = RH + 2 * R;       // staged rows
     static constexpr int SW = (CW + 3) & ~3;    // row pitch (float4 aligned)
     static constexpr int PLANE = SH * SW;
-    static constexpr int NPSI = 2 * G * FG;     // double-buffered psi planes
+    static constexpr int NPSI = G * NBUF;       // psi planes
     static constexpr int TH = RH - 2 * R, TW = RW - 2 * R;  // max owned tile
     static constexpr int TAPS = (M * M + 3) & ~3;           // per-filter tap stride (float4)
     static_assert(NTX == 16 && NTY == 12, "warp layout assumes 16 x 12 micro-tiles per group");
@@ -41,8 +41,24 @@ __device__ __forceinline__ float rcp_approx(float x) {  // MUFU.RCP, no denormal
     return r;
 }
 
-__device__ __forceinline__ void group_barrier(int grp, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(nthreads) : "memory");
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.release.cta.shared::cta.b64 st, [%0]; }" ::"r"(a) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{ .reg .pred p;\n"
+        "WAIT_%=: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=; }" ::"r"(a),
+        "r"(parity)
+        : "memory");
 }
 
 // 2*atanh(t) == log1p(x) for t = x / (2 + x).  Series to t^9 for |t| <= 0.2 (rel. error < 1e-8);
@@ -70,6 +86,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     __shared__ double red[NT / 32][kNumPartials];
     __shared__ double s_sum[kNumPartials];
     __shared__ int s_last;
+    __shared__ unsigned long long s_mbar[C::G][C::NBUF];
 
     const int tid = threadIdx.x;
     const int b = blockIdx.y;
@@ -125,6 +142,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
         s_taps[k] = e < M * M ? a.kf[f * M * M + e] : 0.0f;
     }
     for (int k = tid; k < nf; k += NT) s_alpha[k] = a.alpha[k];
+    if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG);
     // zero ring of every psi plane: psi_0 = 0 outside the region (and the image)
     if constexpr (R > 0) {
         constexpr int RING = SH * CW - C::RH * C::RW;
@@ -179,7 +197,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
             Un[i * SW + j] = __ldg(uin + o) - shift;
         }
     }
-    __syncthreads();
+    __syncthreads();  // staged tile, taps and mbarrier init visible
 
     // ---- filter loop -----------------------------------------------------------------------------
     const int grp = tid / C::NTG, lt = tid - grp * C::NTG;
@@ -217,135 +235,139 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     const float *ubase = Un + ly0 * SW + lx0;
     const float *dbase = Du + ly0 * SW + lx0;
 
-    int buf = 0;
+    // software-pipelined over this group's filters: forward(k) -> arrive(k) -> wait(k-1) ->
+    // adjoint(k-1).  psi of round k lives in buffer k % NBUF; a warp waits only if a peer has not
+    // finished the previous round's forward.  NBUF = 4 keeps the buffer written by forward(k)
+    // clear of readers: its last reader, adjoint(k-4), precedes every thread's arrive(k-2), and a
+    // thread at forward(k) has already waited on round k-2.
 #pragma unroll 1
-    for (int fr = 0; fr < fpg; fr += C::FG, buf ^= 1) {
-#pragma unroll 1
-        for (int q = 0; q < C::FG; ++q) {
-            const int f = fbeg + fr + q;
-            if (fr + q >= fpg || f >= fend) continue;
-            float w[C::TAPS];
+    for (int k = 0; k <= fpg; ++k) {
+        if (k < fpg) {
+            const int f = fbeg + k;
+            const int kb = k % C::NBUF;
+            if (f < fend) {
+                float w[C::TAPS];
 #pragma unroll
-            for (int k = 0; k < C::TAPS; k += 4) {
-                const float4 v = *reinterpret_cast<const float4 *>(s_taps + f * C::TAPS + k);
-                w[k] = v.x; w[k + 1] = v.y; w[k + 2] = v.z; w[k + 3] = v.w;
-            }
-            const float al = s_alpha[f];
-            float z[MY][C::MX], dz[MY][C::MX];
-#pragma unroll
-            for (int o = 0; o < MY; ++o)
-#pragma unroll
-                for (int c = 0; c < C::MX; ++c) { z[o][c] = 0.0f; dz[o][c] = 0.0f; }
-            // forward responses: z = K_f u_new (image.py:37-58), dz = K_f du
-#pragma unroll
-            for (int i = 0; i < WR; ++i) {
-                float ru[WIN], rd[WIN];
-                load_row<WIN>(ubase + i * SW, ru);
-                if (TRIAL) load_row<WIN>(dbase + i * SW, rd);
-#pragma unroll
-                for (int o = 0; o < MY; ++o) {
-                    const int aa = i - o;
-                    if (aa < 0 || aa >= M) continue;
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb) {
-                        const float wt = w[aa * M + bb];
-#pragma unroll
-                        for (int c = 0; c < C::MX; ++c) {
-                            z[o][c] = fmaf(wt, ru[c + bb], z[o][c]);
-                            if (TRIAL) dz[o][c] = fmaf(wt, rd[c + bb], dz[o][c]);
-                        }
-                    }
+                for (int kk = 0; kk < C::TAPS; kk += 4) {
+                    const float4 v = *reinterpret_cast<const float4 *>(s_taps + f * C::TAPS + kk);
+                    w[kk] = v.x; w[kk + 1] = v.y; w[kk + 2] = v.z; w[kk + 3] = v.w;
                 }
-            }
-            // pointwise: psi = a rho'(z) (prior.py:31-32); energy terms
-            float *ps = Psi + ((buf * C::G + grp) * C::FG + q) * C::PLANE + (ly0 + R) * SW + lx0 + R;
-            const float a2 = 2.0f * al;
-            float tt[MY][C::MX];
-            float tmax = 0.0f;
-#pragma unroll
-            for (int o = 0; o < MY; ++o) {
-#pragma unroll
-                for (int c = 0; c < C::MX; ++c) {
-                    const float zz = z[o][c];
-                    const float q1 = fmaf(zz, zz, 1.0f);
-                    ps[o * SW + c] = (a2 * zz) * rcp_approx(q1);
-                    if (TRIAL) {
-                        // F(u_new) - F(u) per response: log((1+z^2)/(1+z_o^2)) = 2 atanh(t) with
-                        // t = (z^2 - z_o^2) / ((1+z^2) + (1+z_o^2)), z_o = z - dz
-                        const float d = dz[o][c];
-                        const float zo = zz - d;
-                        const float num = d * fmaf(2.0f, zo, d);
-                        const float den = fmaf(zo, zo, q1) + 1.0f;
-                        tt[o][c] = num * rcp_approx(den);
-                        tmax = fmaxf(tmax, fabsf(tt[o][c]));
-                    }
-                }
-            }
-            if (SYM && out_bits) {  // psi_0 = 0 outside the image (only threads on an image edge)
+                const float al = s_alpha[f];
+                float z[MY][C::MX], dz[MY][C::MX];
 #pragma unroll
                 for (int o = 0; o < MY; ++o)
 #pragma unroll
-                    for (int c = 0; c < C::MX; ++c)
-                        if (out_bits >> (o * C::MX + c) & 1u) ps[o * SW + c] = 0.0f;
-            }
-            if (TRIAL) {
-                if (__any_sync(0xffffffffu, tmax > 0.2f)) {
+                    for (int c = 0; c < C::MX; ++c) { z[o][c] = 0.0f; dz[o][c] = 0.0f; }
+                // forward responses: z = K_f u_new (image.py:37-58), dz = K_f du
+#pragma unroll
+                for (int i = 0; i < WR; ++i) {
+                    float ru[WIN], rd[WIN];
+                    load_row<WIN>(ubase + i * SW, ru);
+                    if (TRIAL) load_row<WIN>(dbase + i * SW, rd);
+#pragma unroll
+                    for (int o = 0; o < MY; ++o) {
+                        const int aa = i - o;
+                        if (aa < 0 || aa >= M) continue;
+#pragma unroll
+                        for (int bb = 0; bb < M; ++bb) {
+                            const float wt = w[aa * M + bb];
+#pragma unroll
+                            for (int c = 0; c < C::MX; ++c) {
+                                z[o][c] = fmaf(wt, ru[c + bb], z[o][c]);
+                                if (TRIAL) dz[o][c] = fmaf(wt, rd[c + bb], dz[o][c]);
+                            }
+                        }
+                    }
+                }
+                // pointwise: psi = a rho'(z) (prior.py:31-32); energy terms
+                float *ps = Psi + (grp * C::NBUF + kb) * C::PLANE + (ly0 + R) * SW + lx0 + R;
+                const float a2 = 2.0f * al;
+                float tt[MY][C::MX];
+                float tmax = 0.0f;
+#pragma unroll
+                for (int o = 0; o < MY; ++o) {
+#pragma unroll
+                    for (int c = 0; c < C::MX; ++c) {
+                        const float zz = z[o][c];
+                        const float q1 = fmaf(zz, zz, 1.0f);
+                        ps[o * SW + c] = (a2 * zz) * rcp_approx(q1);
+                        if (TRIAL) {
+                            // F(u_new) - F(u) per response: log((1+z^2)/(1+z_o^2)) = 2 atanh(t) with
+                            // t = (z^2 - z_o^2) / ((1+z^2) + (1+z_o^2)), z_o = z - dz
+                            const float d = dz[o][c];
+                            const float zo = zz - d;
+                            const float num = d * fmaf(2.0f, zo, d);
+                            const float den = fmaf(zo, zo, q1) + 1.0f;
+                            tt[o][c] = num * rcp_approx(den);
+                            tmax = fmaxf(tmax, fabsf(tt[o][c]));
+                        }
+                    }
+                }
+                if (SYM && out_bits) {  // psi_0 = 0 outside the image (only threads on an image edge)
 #pragma unroll
                     for (int o = 0; o < MY; ++o)
 #pragma unroll
-                        for (int c = 0; c < C::MX; ++c) epx[o][c] = fmaf(al, two_atanh(tt[o][c]), epx[o][c]);
+                        for (int c = 0; c < C::MX; ++c)
+                            if (out_bits >> (o * C::MX + c) & 1u) ps[o * SW + c] = 0.0f;
+                }
+                if (TRIAL) {
+                    if (__any_sync(0xffffffffu, tmax > 0.2f)) {
+#pragma unroll
+                        for (int o = 0; o < MY; ++o)
+#pragma unroll
+                            for (int c = 0; c < C::MX; ++c) epx[o][c] = fmaf(al, two_atanh(tt[o][c]), epx[o][c]);
+                    } else {
+#pragma unroll
+                        for (int o = 0; o < MY; ++o)
+#pragma unroll
+                            for (int c = 0; c < C::MX; ++c) {
+                                const float t1 = tt[o][c], sq = t1 * t1;
+                                float pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
+                                pp = fmaf(sq, pp, 1.0f / 5.0f);
+                                pp = fmaf(sq, pp, 1.0f / 3.0f);
+                                pp = fmaf(sq, pp, 1.0f);
+                                epx[o][c] = fmaf(a2 * t1, pp, epx[o][c]);
+                            }
+                    }
                 } else {
 #pragma unroll
                     for (int o = 0; o < MY; ++o)
 #pragma unroll
-                        for (int c = 0; c < C::MX; ++c) {
-                            const float t1 = tt[o][c], sq = t1 * t1;
-                            float pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
-                            pp = fmaf(sq, pp, 1.0f / 5.0f);
-                            pp = fmaf(sq, pp, 1.0f / 3.0f);
-                            pp = fmaf(sq, pp, 1.0f);
-                            epx[o][c] = fmaf(a2 * t1, pp, epx[o][c]);
-                        }
+                        for (int c = 0; c < C::MX; ++c) epx[o][c] = fmaf(al, log1pf(z[o][c] * z[o][c]), epx[o][c]);
                 }
-            } else {
-#pragma unroll
-                for (int o = 0; o < MY; ++o)
-#pragma unroll
-                    for (int c = 0; c < C::MX; ++c) epx[o][c] = fmaf(al, log1pf(z[o][c] * z[o][c]), epx[o][c]);
             }
+            mbar_arrive(&s_mbar[grp][kb]);
         }
-        group_barrier(grp, C::NTG);
-        // adjoint: gacc += K_f^T psi_f  (correlation with the unflipped kernel, image.py:84-87)
-#pragma unroll 1
-        for (int q = 0; q < C::FG; ++q) {
-            const int f = fbeg + fr + q;
-            if (fr + q >= fpg || f >= fend) continue;
-            float w[C::TAPS];
+        if (k > 0) {
+            const int f = fbeg + k - 1;
+            const int kb = (k - 1) % C::NBUF;
+            mbar_wait(&s_mbar[grp][kb], ((k - 1) / C::NBUF) & 1);
+            if (f < fend) {
+                float w[C::TAPS];
 #pragma unroll
-            for (int k = 0; k < C::TAPS; k += 4) {
-                const float4 v = *reinterpret_cast<const float4 *>(s_taps + f * C::TAPS + k);
-                w[k] = v.x; w[k + 1] = v.y; w[k + 2] = v.z; w[k + 3] = v.w;
-            }
-            const float *pb = Psi + ((buf * C::G + grp) * C::FG + q) * C::PLANE + ly0 * SW + lx0;
+                for (int kk = 0; kk < C::TAPS; kk += 4) {
+                    const float4 v = *reinterpret_cast<const float4 *>(s_taps + f * C::TAPS + kk);
+                    w[kk] = v.x; w[kk + 1] = v.y; w[kk + 2] = v.z; w[kk + 3] = v.w;
+                }
+                const float *pb = Psi + (grp * C::NBUF + kb) * C::PLANE + ly0 * SW + lx0;
 #pragma unroll
-            for (int i = 0; i < WR; ++i) {
-                float rp[WIN];
-                load_row<WIN>(pb + i * SW, rp);
+                for (int i = 0; i < WR; ++i) {
+                    float rp[WIN];
+                    load_row<WIN>(pb + i * SW, rp);
 #pragma unroll
-                for (int o = 0; o < MY; ++o) {
-                    const int aa = i - o;
-                    if (aa < 0 || aa >= M) continue;
+                    for (int o = 0; o < MY; ++o) {
+                        const int aa = i - o;
+                        if (aa < 0 || aa >= M) continue;
 #pragma unroll
-                    for (int bb = 0; bb < M; ++bb) {
-                        const float wt = w[(M - 1 - aa) * M + (M - 1 - bb)];
+                        for (int bb = 0; bb < M; ++bb) {
+                            const float wt = w[(M - 1 - aa) * M + (M - 1 - bb)];
 #pragma unroll
-                        for (int c = 0; c < C::MX; ++c) gacc[o][c] = fmaf(wt, rp[c + bb], gacc[o][c]);
+                            for (int c = 0; c < C::MX; ++c) gacc[o][c] = fmaf(wt, rp[c + bb], gacc[o][c]);
+                        }
                     }
                 }
             }
         }
-        // no second barrier: the next round writes the other psi buffer, and its barrier orders
-        // this round's reads before the round after overwrites this buffer
     }
     {
         double e = 0.0;  // owned pixels only, fp64 across pixels
