@@ -143,8 +143,11 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     }
     for (int k = tid; k < nf; k += NT) s_alpha[k] = a.alpha[k];
     if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG);
-    // zero ring of every psi plane: psi_0 = 0 outside the region (and the image)
-    if constexpr (R > 0) {
+    // psi_0 = 0 outside the image: the r ring of every psi plane is read only by outputs on the
+    // region border, which matter only where they are padded pixels folded back (symmetric rule,
+    // tiles on an image edge).  Elsewhere the ring feeds discarded outputs and stays unwritten.
+    const bool edge_tile = SYM && (s0 == 0 || c0 == 0 || s1 == H || c1 == W);
+    if (R > 0 && edge_tile) {
         constexpr int RING = SH * CW - C::RH * C::RW;
         for (int k = tid; k < C::NPSI * RING; k += NT) {
             const int pl = k / RING, e = k - pl * RING;
@@ -164,37 +167,68 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     double acc[kNumPartials];
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
-    for (int k = tid; k < SH * CW; k += NT) {
-        const int i = k / CW, j = k - i * CW;
-        const int gy = ry0 - R + i, gx = rx0 - R + j;
-        const size_t o = (size_t)src_idx<SYM>(gy, H) * W + src_idx<SYM>(gx, W);
-        const bool own = gy >= s0 && gy < s1 && gx >= c0 && gx < c1;
-        if (TRIAL) {
-            const float u = __ldg(uin + o), up = __ldg(upv + o), g = __ldg(gin + o), ob = __ldg(obs + o);
-            // u - tau g + gamma (u - u_prev)  (solver.py:146-149)
-            const float ut = (u - tau32 * g) + gam32 * (u - up);
-            const float un = (branch == FOE_QUADRATIC) ? prox_quad(ut, t32, ob) : prox_idv(ut, t32, ob);
-            const float du = un - u;
-            Un[i * SW + j] = un - shift;
-            Du[i * SW + j] = du;
-            if (own) {
-                uout[(size_t)gy * W + gx] = un;
-                acc[1] += (double)du * (double)du;  // vdot(du, du)  solver.py:152
-                acc[2] += (double)g * (double)du;   // vdot(g, du)   solver.py:153
-                acc[3] += (double)u * (double)u;    // |u|^2 for the stop test, solver.py:173
-                if (branch == FOE_QUADRATIC) {
-                    const double d = (double)un - (double)ob;
-                    acc[4] += d * d;
-                } else {
-                    acc[4] += (double)un;
-                    if (ob > 0.0f) {
-                        if (un > 0.0f) acc[5] += (double)ob * (double)logf(un);
-                        else acc[6] += 1.0;
+    constexpr int NCELL = SH * CW;
+    constexpr int CPT = (NCELL + NT - 1) / NT;  // staged cells per thread
+    if (TRIAL) {
+        // all global loads of this thread's cells first (4 x CPT in flight), then the arithmetic
+        float lu[CPT], lup[CPT], lg[CPT], lob[CPT];
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            const int k = tid + q * NT;
+            if (k < NCELL) {
+                const int i = k / CW, j = k - i * CW;
+                const size_t o = (size_t)src_idx<SYM>(ry0 - R + i, H) * W + src_idx<SYM>(rx0 - R + j, W);
+                lu[q] = __ldg(uin + o); lup[q] = __ldg(upv + o); lg[q] = __ldg(gin + o); lob[q] = __ldg(obs + o);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            const int k = tid + q * NT;
+            if (k < NCELL) {
+                const int i = k / CW, j = k - i * CW;
+                const int gy = ry0 - R + i, gx = rx0 - R + j;
+                const float u = lu[q], g = lg[q], ob = lob[q];
+                // u - tau g + gamma (u - u_prev)  (solver.py:146-149)
+                const float ut = (u - tau32 * g) + gam32 * (u - lup[q]);
+                const float un = (branch == FOE_QUADRATIC) ? prox_quad(ut, t32, ob) : prox_idv(ut, t32, ob);
+                const float du = un - u;
+                Un[i * SW + j] = un - shift;
+                Du[i * SW + j] = du;
+                if (gy >= s0 && gy < s1 && gx >= c0 && gx < c1) {
+                    uout[(size_t)gy * W + gx] = un;
+                    acc[1] += (double)du * (double)du;  // vdot(du, du)  solver.py:152
+                    acc[2] += (double)g * (double)du;   // vdot(g, du)   solver.py:153
+                    acc[3] += (double)u * (double)u;    // |u|^2 for the stop test, solver.py:173
+                    if (branch == FOE_QUADRATIC) {
+                        const double d = (double)un - (double)ob;
+                        acc[4] += d * d;
+                    } else {
+                        acc[4] += (double)un;
+                        if (ob > 0.0f) {
+                            if (un > 0.0f) acc[5] += (double)ob * (double)logf(un);
+                            else acc[6] += 1.0;
+                        }
                     }
                 }
             }
-        } else {
-            Un[i * SW + j] = __ldg(uin + o) - shift;
+        }
+    } else {
+        float lu[CPT];
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            const int k = tid + q * NT;
+            if (k < NCELL) {
+                const int i = k / CW, j = k - i * CW;
+                lu[q] = __ldg(uin + (size_t)src_idx<SYM>(ry0 - R + i, H) * W + src_idx<SYM>(rx0 - R + j, W));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            const int k = tid + q * NT;
+            if (k < NCELL) {
+                const int i = k / CW, j = k - i * CW;
+                Un[i * SW + j] = lu[q] - shift;
+            }
         }
     }
     __syncthreads();  // staged tile, taps and mbarrier init visible
@@ -393,23 +427,32 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
         for (int g2 = 1; g2 < C::G; ++g2) s += gb[g2 * C::RH * C::RW + ly * C::RW + lx];
         return s;
     };
-    const int oh = s1 - s0, ow = c1 - c0;
-    for (int k = tid; k < oh * ow; k += NT) {
-        const int yy = k / ow, xx = k - yy * ow;
-        const int gy = s0 + yy, gx = c0 + xx;
-        const int ly = gy - ry0, lx = gx - rx0;
-        float val = gsum(ly, lx);
-        if (SYM && R > 0) {
-            int my = -1, mx = -1;
-            if (gy < R) my = (-1 - gy) - ry0;
-            else if (gy >= H - R) my = (2 * H - 1 - gy) - ry0;
-            if (gx < R) mx = (-1 - gx) - rx0;
-            else if (gx >= W - R) mx = (2 * W - 1 - gx) - rx0;
-            if (my >= 0) val += gsum(my, lx);
-            if (mx >= 0) val += gsum(ly, mx);
-            if (my >= 0 && mx >= 0) val += gsum(my, mx);
+    // 2-D ownership walk: column = tid % RW, rows strided by NT / RW (no integer division)
+    static_assert(NT % C::RW == 0, "fold walk assumes whole region rows per pass");
+    {
+        const int xx = tid % C::RW;
+        const int gx = c0 + xx;
+        if (gx < c1) {
+            const int lx = gx - rx0;
+            int mx = -1;
+            if (SYM && R > 0) {
+                if (gx < R) mx = (-1 - gx) - rx0;
+                else if (gx >= W - R) mx = (2 * W - 1 - gx) - rx0;
+            }
+            for (int gy = s0 + tid / C::RW; gy < s1; gy += NT / C::RW) {
+                const int ly = gy - ry0;
+                float val = gsum(ly, lx);
+                if (SYM && R > 0) {
+                    int my = -1;
+                    if (gy < R) my = (-1 - gy) - ry0;
+                    else if (gy >= H - R) my = (2 * H - 1 - gy) - ry0;
+                    if (my >= 0) val += gsum(my, lx);
+                    if (mx >= 0) val += gsum(ly, mx);
+                    if (my >= 0 && mx >= 0) val += gsum(my, mx);
+                }
+                gout[(size_t)gy * W + gx] = val;
+            }
         }
-        gout[(size_t)gy * W + gx] = val;
     }
 
     // ---- per-tile partials, last CTA of the image reduces and decides ----------------------------
