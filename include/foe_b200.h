@@ -128,6 +128,55 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfg, int B, int H, int
 int foe_bench_trial_pass(const foe_bank *bank, int B, int H, int W, int trace_cap, int reps,
                          void *workspace, size_t workspace_bytes, void *stream);
 
+
+/* ---- row-band decomposition (BASELINE config 5; reference has none) -------
+ * A band owns global tile rows [ty0, ty1) of a B x H x W problem and keeps local rows
+ * [lrow0, lrow0 + Hl) = owned rows +- halo (halo = 2r).  Per pass each band runs foe_band_trial,
+ * the caller all-gathers the per-tile partials chunk [partials_offset, +partials_count) of
+ * `partials` into every band's array and swaps the halo send buffers with the neighbouring bands
+ * (dir 0 <-> band above, dir 1 <-> band below), then foe_band_commit takes the decision.  The
+ * reduction order equals the single-device path, so any band count gives bitwise-identical
+ * results.  Symmetric boundary only. */
+typedef struct foe_band_desc {
+    int B, H, W;          /* batch and GLOBAL image size */
+    int ty0, ty1;         /* global tile rows owned by the band */
+    int tiles_x, tiles_y; /* global tile grid */
+    int row0, row1;       /* owned global rows */
+    int lrow0, Hl;        /* local rows [lrow0, lrow0 + Hl) */
+    int halo;             /* rows exchanged with each neighbour per pass */
+} foe_band_desc;
+
+typedef struct foe_band_buffers {
+    double *partials;       /* device [tiles_y*tiles_x][B][8] fp64 */
+    size_t partials_offset; /* doubles: this band's chunk */
+    size_t partials_count;
+    size_t partials_total;
+    float *sendbuf, *recvbuf; /* device [2 dir][B][2 field][halo][W] */
+    size_t halo_count;        /* floats per direction */
+    int *n_active;            /* device live-image counter */
+} foe_band_buffers;
+
+/* tile grid / band geometry for filter side m (host-only, no device needed) */
+int foe_tile_grid(int m, int H, int W, int *tiles_x, int *tiles_y);
+int foe_band_geometry(int m, int B, int H, int W, int ty0, int ty1, foe_band_desc *out);
+int foe_band_describe(const foe_bank *bank, int B, int H, int W, int ty0, int ty1, foe_band_desc *out);
+size_t foe_band_workspace_size(const foe_bank *bank, const foe_band_desc *d, int trace_cap);
+int foe_band_buffers_get(const foe_bank *bank, const foe_band_desc *d, int trace_cap, void *workspace,
+                         foe_band_buffers *out);
+/* u0_local, obs_local: device (B, Hl, W) rows [lrow0, lrow0+Hl) of the start point / observation */
+int foe_band_begin(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_band_desc *d,
+                   const float *u0_local, const float *obs_local, const double *lam, const int *branch,
+                   const int *max_iters, int trace_cap, void *workspace, size_t workspace_bytes,
+                   void *stream);
+int foe_band_trial(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_band_desc *d, int trace_cap,
+                   void *workspace, size_t workspace_bytes, void *stream);
+int foe_band_commit(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_band_desc *d, int trace_cap,
+                    int init, void *workspace, size_t workspace_bytes, void *stream);
+/* u_owned: device (B, row1-row0, W) final iterate rows; status/trace as foe_solve */
+int foe_band_end(const foe_bank *bank, const foe_band_desc *d, int trace_cap, void *workspace,
+                 size_t workspace_bytes, float *u_owned, foe_image_status *status, double *trace,
+                 void *stream);
+
 #ifdef __cplusplus
 }
 #endif

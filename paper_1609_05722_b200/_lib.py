@@ -124,5 +124,6 @@ EXPORTED_SYMBOLS = [
     "foe_bank_info", "foe_anscombe_forward", "foe_direct_obs", "foe_anscombe_inverse_exact_unbiased",
     "foe_prox_quadratic", "foe_prox_idiv", "foe_convolve_same", "foe_convolve_adjoint",
     "foe_eval_workspace_size", "foe_energy_grad", "foe_solve_workspace_size", "foe_solve",
-    "foe_bench_trial_pass",
+    "foe_bench_trial_pass", "foe_tile_grid", "foe_band_geometry", "foe_band_describe", "foe_band_workspace_size",
+    "foe_band_buffers_get", "foe_band_begin", "foe_band_trial", "foe_band_commit", "foe_band_end",
 ]

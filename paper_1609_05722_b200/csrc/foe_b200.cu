@@ -71,6 +71,12 @@ struct ImgCtl {
 
 struct PassArgs {
     int B, H, W, n_filters, tiles_x, tiles_y, mode, no_decide, zero_mean;
+    // row-band decomposition (single device: ty0 = 0, lrow0 = 0, Hl = H, band = 0)
+    int ty0;    // first global tile row of this launch (tiles_y is the global count)
+    int tiles_yl;  // tile rows in this launch
+    int lrow0;  // global row stored in local row 0
+    int Hl;     // local rows per image (plane stride = Hl * W)
+    int band;   // 1: write partials only, decisions by k_decide after the all-gather
     size_t plane;  // B*H*W: distance between state slots
     const float *kf;     // (n, M*M) flipped taps (correlation orientation of the forward conv)
     const float *alpha;  // (n)
@@ -220,6 +226,23 @@ __device__ __forceinline__ void block_reduce(double (&v)[kNumPartials], double (
     }
 }
 
+// fixed-order sum of one image's tile partials (layout [tile][B][8]) into s_sum, by a whole CTA of
+// NT threads: thread k sums tiles k, k+NT, ... then a fixed tree.  Shared by the last-CTA path and
+// k_decide, so a band-decomposed solve reduces in exactly the single-device order.
+template <int NT>
+__device__ void reduce_tiles(const double *partials, int ntiles, int B, int b, double (*red)[kNumPartials],
+                             double *s_sum) {
+    double tot[kNumPartials];
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) tot[k] = 0.0;
+    for (int tt = threadIdx.x; tt < ntiles; tt += NT)
+#pragma unroll
+        for (int k = 0; k < kNumPartials; ++k) tot[k] += __ldcg(partials + ((size_t)tt * B + b) * kPartialStride + k);
+    __syncthreads();
+    block_reduce<NT>(tot, red, s_sum);
+    __syncthreads();
+}
+
 #include "foe_pass.cuh"
 
 // ------------------------------------------------------------------------------------------------
@@ -333,6 +356,73 @@ __global__ void k_gather_final(const float *__restrict__ U, size_t plane, const 
         dst[i] = src[i];
 }
 
+
+// ------------------------------------------------------------------------------------------------
+// row-band decomposition (BASELINE config 5): decisions after the partials all-gather, halo rows
+
+// one CTA per image: the same fixed-order reduction as the last-CTA path, then the decision
+__global__ void __launch_bounds__(PassCfg<5>::NT) k_decide(const PassArgs a) {
+    constexpr int NT = PassCfg<5>::NT;
+    __shared__ double red[NT / 32][kNumPartials];
+    __shared__ double s_sum[kNumPartials];
+    const int b = blockIdx.x;
+    if (a.ctl[b].done) return;
+    reduce_tiles<NT>(a.partials, a.tiles_x * a.tiles_y, a.B, b, red, s_sum);
+    if (threadIdx.x == 0) decide(a, b, s_sum);
+}
+
+// boundary rows -> send buffer [dir][B][field][halo][W]; dir 0 = first owned rows (to the band
+// above), dir 1 = last owned rows (to the band below); field 0 = u, 1 = grad.  init: the gradient of
+// the start point (u halos come with the input); otherwise the trial slots.
+__global__ void k_band_pack(const PassArgs a, float *send, int halo, int row0, int row1, int init) {
+    const int b = blockIdx.y;
+    const ImgCtl &c = a.ctl[b];
+    const float *U = a.U + (init ? c.iu : c.inew) * a.plane + (size_t)b * a.Hl * a.W;
+    const float *G = a.Gs + (init ? c.ig : c.ignew) * a.plane + (size_t)b * a.Hl * a.W;
+    const size_t per = (size_t)halo * a.W;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < 2 * per; i += (size_t)gridDim.x * blockDim.x) {
+        const int dir = (int)(i / per);
+        const size_t e = i - dir * per;
+        const int row = (dir == 0 ? row0 : row1 - halo) + (int)(e / a.W);
+        const size_t src = (size_t)(row - a.lrow0) * a.W + e % a.W;
+        float *dst = send + ((size_t)dir * a.B + b) * 2 * per;
+        dst[e] = U[src];
+        dst[per + e] = G[src];
+    }
+}
+
+// receive buffer [dir][B][field][halo][W] -> halo rows; dir 0 came from the band above (rows
+// [row0-halo, row0)), dir 1 from the band below (rows [row1, row1+halo)).
+__global__ void k_band_unpack(const PassArgs a, const float *recv, int halo, int row0, int row1, int init) {
+    const int b = blockIdx.y;
+    const ImgCtl &c = a.ctl[b];
+    float *U = a.U + (init ? c.iu : c.inew) * a.plane + (size_t)b * a.Hl * a.W;
+    float *G = a.Gs + (init ? c.ig : c.ignew) * a.plane + (size_t)b * a.Hl * a.W;
+    const size_t per = (size_t)halo * a.W;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < 2 * per; i += (size_t)gridDim.x * blockDim.x) {
+        const int dir = (int)(i / per);
+        if (dir == 0 && row0 == 0) continue;
+        if (dir == 1 && row1 == a.H) continue;
+        const size_t e = i - dir * per;
+        const int row = (dir == 0 ? row0 - halo : row1) + (int)(e / a.W);
+        const size_t dst = (size_t)(row - a.lrow0) * a.W + e % a.W;
+        const float *src = recv + ((size_t)dir * a.B + b) * 2 * per;
+        if (!init) U[dst] = src[e];
+        G[dst] = src[per + e];
+    }
+}
+
+// gather the owned rows of the final iterate
+__global__ void k_gather_band(const float *__restrict__ U, size_t plane, const ImgCtl *__restrict__ ctl,
+                              float *__restrict__ out, int Hl, int W, int row0, int row1, int lrow0) {
+    const int b = blockIdx.y;
+    const float *src = U + (size_t)ctl[b].iu * plane + (size_t)b * Hl * W + (size_t)(row0 - lrow0) * W;
+    float *dst = out + (size_t)b * (row1 - row0) * W;
+    const size_t n = (size_t)(row1 - row0) * W;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
 // ------------------------------------------------------------------------------------------------
 // host side
 
@@ -358,7 +448,7 @@ int launch_pass_t(const PassArgs &a, cudaStream_t st) {
         FOE_CUDA(cudaFuncSetAttribute(k_pass<M, TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured |= 1ull << (dev & 63);
     }
-    dim3 grid(a.tiles_x * a.tiles_y, a.B);
+    dim3 grid(a.tiles_x * a.tiles_yl, a.B);
     k_pass<M, TRIAL, SYM><<<grid, C::NT, smem, st>>>(a);
     FOE_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -392,13 +482,16 @@ void tile_counts(int m, int H, int W, int *tx, int *ty) {
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct SolveLayout {
-    size_t U, G, O, ctl, partials, tickets, trace, n_active, total;
+    size_t U, G, O, ctl, partials, tickets, trace, n_active, send, recv, total;
+    size_t halo_floats;  // per direction
 };
 
-SolveLayout solve_layout(int m, int B, int H, int W, int trace_cap) {
+// Hl = local rows per image (H unless a row band), halo = rows exchanged per side (0 unless banded)
+SolveLayout solve_layout(int m, int B, int H, int W, int trace_cap, int Hl = -1, int halo = 0) {
+    if (Hl < 0) Hl = H;
     int tx, ty;
     tile_counts(m, H, W, &tx, &ty);
-    const size_t plane = (size_t)B * H * W * sizeof(float);
+    const size_t plane = (size_t)B * Hl * W * sizeof(float);
     SolveLayout L;
     size_t off = 0;
     L.U = off; off = align_up(off + 3 * plane);
@@ -409,6 +502,9 @@ SolveLayout solve_layout(int m, int B, int H, int W, int trace_cap) {
     L.tickets = off; off = align_up(off + sizeof(unsigned) * B);
     L.trace = off; off = align_up(off + sizeof(double) * 6 * (size_t)B * trace_cap);
     L.n_active = off; off = align_up(off + sizeof(int) * 4);
+    L.halo_floats = (size_t)B * 2 * halo * W;
+    L.send = off; off = align_up(off + sizeof(float) * 2 * L.halo_floats);
+    L.recv = off; off = align_up(off + sizeof(float) * 2 * L.halo_floats);
     L.total = off;
     return L;
 }
@@ -608,6 +704,7 @@ int foe_energy_grad(const foe_bank *bank, const float *u, float *grad, double *e
     PassArgs a{};
     a.B = B; a.H = H; a.W = W; a.n_filters = bank->n; a.zero_mean = bank->zero_mean;
     tile_counts(bank->m, H, W, &a.tiles_x, &a.tiles_y);
+    a.tiles_yl = a.tiles_y; a.ty0 = 0; a.lrow0 = 0; a.Hl = H; a.band = 0;
     a.mode = MODE_EVAL;
     a.kf = bank->d_kf; a.alpha = bank->d_alpha;
     a.u_in = u; a.g_out = grad; a.energy_out = energy;
@@ -623,10 +720,15 @@ size_t foe_solve_workspace_size(const foe_bank *bank, int B, int H, int W, int t
 }
 
 static void fill_solve_args(PassArgs &a, const foe_bank *bank, const foe_solver_cfg &cfg, int B, int H, int W,
-                            int trace_cap, char *ws, const SolveLayout &L) {
+                            int trace_cap, char *ws, const SolveLayout &L, const foe_band_desc *band = nullptr) {
     a.B = B; a.H = H; a.W = W; a.n_filters = bank->n; a.zero_mean = bank->zero_mean;
     tile_counts(bank->m, H, W, &a.tiles_x, &a.tiles_y);
-    a.plane = (size_t)B * H * W;
+    if (band) {
+        a.ty0 = band->ty0; a.tiles_yl = band->ty1 - band->ty0; a.lrow0 = band->lrow0; a.Hl = band->Hl; a.band = 1;
+    } else {
+        a.ty0 = 0; a.tiles_yl = a.tiles_y; a.lrow0 = 0; a.Hl = H; a.band = 0;
+    }
+    a.plane = (size_t)B * a.Hl * W;
     a.kf = bank->d_kf; a.alpha = bank->d_alpha;
     a.U = (float *)(ws + L.U);
     a.Gs = (float *)(ws + L.G);
@@ -763,6 +865,164 @@ int foe_bench_trial_pass(const foe_bank *bank, int B, int H, int W, int trace_ca
     for (int k = 0; k < reps; ++k)
         if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, (cudaStream_t)stream))) return rc;
     return FOE_OK;
+}
+
+
+int foe_tile_grid(int m, int H, int W, int *tiles_x, int *tiles_y) {
+    if (m < 1 || m % 2 != 1 || m > 7) return fail(FOE_E_INVALID, "bad filter size %d", m);
+    int tx, ty;
+    tile_counts(m, H, W, &tx, &ty);
+    if (tiles_x) *tiles_x = tx;
+    if (tiles_y) *tiles_y = ty;
+    return FOE_OK;
+}
+
+int foe_band_describe(const foe_bank *bank, int B, int H, int W, int ty0, int ty1, foe_band_desc *d) {
+    int rc = check_dims(bank, B, H, W);
+    if (rc) return rc;
+    if (bank->boundary != FOE_SYMMETRIC)
+        return fail(FOE_E_UNSUPPORTED, "row bands support the symmetric boundary only");
+    return foe_band_geometry(bank->m, B, H, W, ty0, ty1, d);
+}
+
+int foe_band_geometry(int m, int B, int H, int W, int ty0, int ty1, foe_band_desc *d) {
+    if (!d || m < 1 || m % 2 != 1 || m > 7 || B < 1 || H < m || W < m) return fail(FOE_E_INVALID, "bad geometry");
+    int tx, ty;
+    tile_counts(m, H, W, &tx, &ty);
+    if (ty0 < 0 || ty1 > ty || ty0 >= ty1) return fail(FOE_E_INVALID, "tile rows [%d, %d) outside [0, %d)", ty0, ty1, ty);
+    const int r = m / 2, T = PassCfg<1>::RH - 2 * r;
+    d->B = B; d->H = H; d->W = W; d->ty0 = ty0; d->ty1 = ty1; d->tiles_x = tx; d->tiles_y = ty;
+    d->row0 = tile_start(ty0, ty, T, H, r);
+    d->row1 = tile_start(ty1, ty, T, H, r);
+    d->halo = 2 * r;  // the trial point is formed on the region + r ring = owned rows +- 2r
+    if (ty0 > 0 && d->row1 - d->row0 < d->halo) return fail(FOE_E_INVALID, "band thinner than its halo");
+    d->lrow0 = std::max(0, d->row0 - d->halo);
+    d->Hl = std::min(H, d->row1 + d->halo) - d->lrow0;
+    return FOE_OK;
+}
+
+size_t foe_band_workspace_size(const foe_bank *bank, const foe_band_desc *d, int trace_cap) {
+    if (!bank || !d) return 0;
+    return solve_layout(bank->m, d->B, d->H, d->W, trace_cap, d->Hl, d->halo).total;
+}
+
+int foe_band_buffers_get(const foe_bank *bank, const foe_band_desc *d, int trace_cap, void *workspace,
+                         foe_band_buffers *out) {
+    if (!bank || !d || !out) return fail(FOE_E_INVALID, "null argument");
+    const SolveLayout L = solve_layout(bank->m, d->B, d->H, d->W, trace_cap, d->Hl, d->halo);
+    char *ws = (char *)workspace;
+    out->partials = (double *)(ws + L.partials);
+    out->partials_offset = (size_t)d->ty0 * d->tiles_x * d->B * kPartialStride;
+    out->partials_count = (size_t)(d->ty1 - d->ty0) * d->tiles_x * d->B * kPartialStride;
+    out->partials_total = (size_t)d->tiles_y * d->tiles_x * d->B * kPartialStride;
+    out->sendbuf = (float *)(ws + L.send);
+    out->recvbuf = (float *)(ws + L.recv);
+    out->halo_count = L.halo_floats;
+    out->n_active = (int *)(ws + L.n_active);
+    return FOE_OK;
+}
+
+static int band_args(const foe_bank *bank, const foe_band_desc *d, int trace_cap, void *workspace,
+                     size_t workspace_bytes, PassArgs &a, SolveLayout &L, const foe_solver_cfg *cfgp = nullptr) {
+    if (!bank || !d || !workspace) return fail(FOE_E_INVALID, "null argument");
+    L = solve_layout(bank->m, d->B, d->H, d->W, trace_cap, d->Hl, d->halo);
+    if (workspace_bytes < L.total) return fail(FOE_E_INVALID, "band workspace too small");
+    static const foe_solver_cfg def{0.8, 1.0, 1.2, 1.05, 1e-6, 1e15};  // only for cfg-free calls
+    memset(&a, 0, sizeof(a));
+    fill_solve_args(a, bank, cfgp ? *cfgp : def, d->B, d->H, d->W, trace_cap, (char *)workspace, L, d);
+    return FOE_OK;
+}
+
+int foe_band_begin(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_band_desc *d, const float *u0_local,
+                   const float *obs_local, const double *lam, const int *branch, const int *max_iters, int trace_cap,
+                   void *workspace, size_t workspace_bytes, void *stream) {
+    if (!cfg || !u0_local || !obs_local || !lam || !branch || !max_iters) return fail(FOE_E_INVALID, "null argument");
+    PassArgs a;
+    SolveLayout L;
+    int rc = band_args(bank, d, trace_cap, workspace, workspace_bytes, a, L, cfg);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int B = d->B;
+    std::vector<ImgCtl> hc(B);
+    for (int b = 0; b < B; ++b) {
+        if (max_iters[b] < 1 || max_iters[b] > trace_cap) return fail(FOE_E_INVALID, "bad max_iters");
+        if (!(lam[b] > 0)) return fail(FOE_E_INVALID, "lambda must be positive");
+        ImgCtl &c = hc[b];
+        memset(&c, 0, sizeof(c));
+        c.L = cfg->lipschitz_init; c.lam = lam[b]; c.max_iters = max_iters[b]; c.branch = branch[b]; c.failed_at = -1;
+        c.iu = 0; c.iup = 2; c.inew = 1; c.ig = 0; c.ignew = 1;
+    }
+    const size_t local = (size_t)B * d->Hl * d->W;
+    FOE_CUDA(cudaMemcpyAsync(a.ctl, hc.data(), sizeof(ImgCtl) * B, cudaMemcpyHostToDevice, st));
+    FOE_CUDA(cudaMemcpyAsync(a.n_active, &B, sizeof(int), cudaMemcpyHostToDevice, st));
+    FOE_CUDA(cudaMemcpyAsync(a.U, u0_local, sizeof(float) * local, cudaMemcpyDeviceToDevice, st));
+    FOE_CUDA(cudaMemcpyAsync(a.U + 2 * a.plane, u0_local, sizeof(float) * local, cudaMemcpyDeviceToDevice, st));
+    FOE_CUDA(cudaMemcpyAsync((void *)a.obs, obs_local, sizeof(float) * local, cudaMemcpyDeviceToDevice, st));
+    a.mode = MODE_INIT;
+    if ((rc = launch_pass(bank->m, true, a, st))) return rc;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_band_pack<<<dim3(32, B), 256, 0, st>>>(a, (float *)((char *)workspace + L.send), d->halo, d->row0, d->row1, 1);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_band_trial(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_band_desc *d, int trace_cap,
+                   void *workspace, size_t workspace_bytes, void *stream) {
+    PassArgs a;
+    SolveLayout L;
+    int rc = band_args(bank, d, trace_cap, workspace, workspace_bytes, a, L, cfg);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    a.mode = MODE_TRIAL;
+    if ((rc = launch_pass(bank->m, true, a, st))) return rc;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_band_pack<<<dim3(32, d->B), 256, 0, st>>>(a, (float *)((char *)workspace + L.send), d->halo, d->row0, d->row1, 0);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_band_commit(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_band_desc *d, int trace_cap, int init,
+                    void *workspace, size_t workspace_bytes, void *stream) {
+    PassArgs a;
+    SolveLayout L;
+    int rc = band_args(bank, d, trace_cap, workspace, workspace_bytes, a, L, cfg);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    a.mode = init ? MODE_INIT : MODE_TRIAL;
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    k_band_unpack<<<dim3(32, d->B), 256, 0, st>>>(a, (const float *)((char *)workspace + L.recv), d->halo, d->row0,
+                                                 d->row1, init);
+    FOE_CUDA(cudaGetLastError());
+    k_decide<<<d->B, PassCfg<5>::NT, 0, st>>>(a);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_band_end(const foe_bank *bank, const foe_band_desc *d, int trace_cap, void *workspace, size_t workspace_bytes,
+                 float *u_owned, foe_image_status *status, double *trace, void *stream) {
+    PassArgs a;
+    SolveLayout L;
+    int rc = band_args(bank, d, trace_cap, workspace, workspace_bytes, a, L);
+    if (rc) return rc;
+    if (!u_owned || !status || !trace) return fail(FOE_E_INVALID, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int B = d->B;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_gather_band<<<dim3(64, B), 256, 0, st>>>(a.U, a.plane, a.ctl, u_owned, d->Hl, d->W, d->row0, d->row1, d->lrow0);
+    FOE_CUDA(cudaGetLastError());
+    std::vector<ImgCtl> hc(B);
+    FOE_CUDA(cudaMemcpyAsync(hc.data(), a.ctl, sizeof(ImgCtl) * B, cudaMemcpyDeviceToHost, st));
+    FOE_CUDA(cudaMemcpyAsync(trace, a.trace, sizeof(double) * 6 * (size_t)B * trace_cap, cudaMemcpyDeviceToHost, st));
+    FOE_CUDA(cudaStreamSynchronize(st));
+    int any_fail = 0;
+    for (int b = 0; b < B; ++b) {
+        status[b].status = hc[b].status;
+        status[b].n_iters = hc[b].n;
+        status[b].n_trials = hc[b].trials;
+        status[b].failed_at = hc[b].status ? hc[b].failed_at : -1;
+        any_fail |= hc[b].status != 0;
+    }
+    return any_fail ? fail(FOE_E_NUMERICAL, "numerical failure in at least one image") : FOE_OK;
 }
 
 }  // extern "C"

@@ -105,8 +105,10 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
             gam32 = (float)a.gamma;
         }
     }
-    const size_t HW = (size_t)H * W;
-    const size_t ioff = (size_t)b * HW;
+    // local buffers hold global rows [lrow0, lrow0 + Hl) of each image (the whole image unless this
+    // launch is one row band of a decomposed image)
+    const int lrow0 = a.lrow0;
+    const size_t ioff = (size_t)b * a.Hl * W;
     const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
     float *gout, *uout = nullptr;
     if (a.mode == MODE_EVAL) {
@@ -125,8 +127,9 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
         }
     }
 
-    const int t = blockIdx.x;
-    const int tyi = t / a.tiles_x, txi = t - tyi * a.tiles_x;
+    const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
+    const int tyi = a.ty0 + tyl;              // global tile row
+    const int t = tyi * a.tiles_x + txi;      // global tile index (partials layout [tile][B][8])
     const int s0 = tile_start(tyi, a.tiles_y, C::TH, H, R), s1 = tile_start(tyi + 1, a.tiles_y, C::TH, H, R);
     const int c0 = tile_start(txi, a.tiles_x, C::TW, W, R), c1 = tile_start(txi + 1, a.tiles_x, C::TW, W, R);
     const int ry0 = s0 - R, rx0 = c0 - R;  // region origin; staged cell (i,j) <-> (ry0-R+i, rx0-R+j)
@@ -147,21 +150,24 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     // region border, which matter only where they are padded pixels folded back (symmetric rule,
     // tiles on an image edge).  Elsewhere the ring feeds discarded outputs and stays unwritten.
     const bool edge_tile = SYM && (s0 == 0 || c0 == 0 || s1 == H || c1 == W);
-    if (R > 0 && edge_tile) {
-        constexpr int RING = SH * CW - C::RH * C::RW;
-        for (int k = tid; k < C::NPSI * RING; k += NT) {
-            const int pl = k / RING, e = k - pl * RING;
-            int i, j;
-            if (e < R * CW) { i = e / CW; j = e - i * CW; }
-            else if (e < 2 * R * CW) { const int e2 = e - R * CW; i = C::RH + R + e2 / CW; j = e2 % CW; }
-            else { const int e3 = e - 2 * R * CW; i = R + e3 / (2 * R); const int jj = e3 % (2 * R); j = jj < R ? jj : C::RW + jj; }
-            Psi[pl * C::PLANE + i * SW + j] = 0.0f;
+    if constexpr (R > 0) {
+        if (edge_tile) {
+            constexpr int RING = SH * CW - C::RH * C::RW;
+            for (int k = tid; k < C::NPSI * RING; k += NT) {
+                const int pl = k / RING, e = k - pl * RING;
+                int i, j;
+                if (e < R * CW) { i = e / CW; j = e - i * CW; }
+                else if (e < 2 * R * CW) { const int e2 = e - R * CW; i = C::RH + R + e2 / CW; j = e2 % CW; }
+                else { const int e3 = e - 2 * R * CW; i = R + e3 / (2 * R); const int jj = e3 % (2 * R); j = jj < R ? jj : C::RW + jj; }
+                Psi[pl * C::PLANE + i * SW + j] = 0.0f;
+            }
         }
     }
 
+
     // Filters are zero-mean (DCT basis without DC, image.py:117-130), so K(u - c) == K u: staging
     // u - c with c = the tile's anchor pixel keeps the fp32 products small (accuracy, not speed).
-    const float shift = a.zero_mean ? __ldg(uin + (size_t)s0 * W + c0) : 0.0f;
+    const float shift = a.zero_mean ? __ldg(uin + (size_t)(s0 - lrow0) * W + c0) : 0.0f;
 
     // ---- prologue: stage u (EVAL/INIT) or the trial point u_new and du (TRIAL) -------------------
     double acc[kNumPartials];
@@ -177,7 +183,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
             const int k = tid + q * NT;
             if (k < NCELL) {
                 const int i = k / CW, j = k - i * CW;
-                const size_t o = (size_t)src_idx<SYM>(ry0 - R + i, H) * W + src_idx<SYM>(rx0 - R + j, W);
+                const size_t o = (size_t)(src_idx<SYM>(ry0 - R + i, H) - lrow0) * W + src_idx<SYM>(rx0 - R + j, W);
                 lu[q] = __ldg(uin + o); lup[q] = __ldg(upv + o); lg[q] = __ldg(gin + o); lob[q] = __ldg(obs + o);
             }
         }
@@ -195,7 +201,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
                 Un[i * SW + j] = un - shift;
                 Du[i * SW + j] = du;
                 if (gy >= s0 && gy < s1 && gx >= c0 && gx < c1) {
-                    uout[(size_t)gy * W + gx] = un;
+                    uout[(size_t)(gy - lrow0) * W + gx] = un;
                     acc[1] += (double)du * (double)du;  // vdot(du, du)  solver.py:152
                     acc[2] += (double)g * (double)du;   // vdot(g, du)   solver.py:153
                     acc[3] += (double)u * (double)u;    // |u|^2 for the stop test, solver.py:173
@@ -219,7 +225,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
             const int k = tid + q * NT;
             if (k < NCELL) {
                 const int i = k / CW, j = k - i * CW;
-                lu[q] = __ldg(uin + (size_t)src_idx<SYM>(ry0 - R + i, H) * W + src_idx<SYM>(rx0 - R + j, W));
+                lu[q] = __ldg(uin + (size_t)(src_idx<SYM>(ry0 - R + i, H) - lrow0) * W + src_idx<SYM>(rx0 - R + j, W));
             }
         }
 #pragma unroll
@@ -450,33 +456,25 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
                     if (mx >= 0) val += gsum(ly, mx);
                     if (my >= 0 && mx >= 0) val += gsum(my, mx);
                 }
-                gout[(size_t)gy * W + gx] = val;
+                gout[(size_t)(gy - lrow0) * W + gx] = val;
             }
         }
     }
 
     // ---- per-tile partials, last CTA of the image reduces and decides ----------------------------
-    const int ntiles = a.tiles_x * a.tiles_y;
     block_reduce<NT>(acc, red, s_sum);
     if (tid < kNumPartials) {
-        a.partials[((size_t)b * ntiles + t) * kPartialStride + tid] = s_sum[tid];
+        a.partials[((size_t)t * a.B + b) * kPartialStride + tid] = s_sum[tid];
         __threadfence();
     }
+    if (a.band) return;  // band mode: partials are all-gathered and decided by k_decide
+    const int nlaunch = a.tiles_x * a.tiles_y;
     __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(a.tickets + b, 1u) == (unsigned)(ntiles - 1));
+    if (tid == 0) s_last = (atomicAdd(a.tickets + b, 1u) == (unsigned)(nlaunch - 1));
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    double tot[kNumPartials];
-#pragma unroll
-    for (int k = 0; k < kNumPartials; ++k) tot[k] = 0.0;
-    const double *pp = a.partials + (size_t)b * ntiles * kPartialStride;
-    for (int tt = tid; tt < ntiles; tt += NT)
-#pragma unroll
-        for (int k = 0; k < kNumPartials; ++k) tot[k] += __ldcg(pp + (size_t)tt * kPartialStride + k);
-    __syncthreads();
-    block_reduce<NT>(tot, red, s_sum);
-    __syncthreads();
+    reduce_tiles<NT>(a.partials, a.tiles_x * a.tiles_y, a.B, b, red, s_sum);
     if (tid == 0) {
         a.tickets[b] = 0u;
         if (a.mode == MODE_EVAL) {

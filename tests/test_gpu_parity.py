@@ -254,3 +254,23 @@ def test_numerical_failure_raises_with_trace():
     with pytest.raises(fp.NumericalFailure) as ei:
         fp.denoise(req, fp.SolverConfig(lipschitz_init=1.0, max_lipschitz=1.5))
     assert ei.value.trace is not None
+
+
+@pytest.mark.parametrize("n_bands,H,W,iters", [(2, 200, 130, 40), (3, 200, 130, 40), (4, 1000, 333, 12),
+                                               (4, 8192, 8192, 3)])
+def test_row_bands_equal_single_device_bitwise(n_bands, H, W, iters):
+    """Config-5 decomposition through the halo/all-gather path (bands in-process on one GPU):
+    bitwise identical to the single-device solve, for any band count."""
+    import torch
+    from paper_1609_05722_b200 import bands
+    from paper_1609_05722_b200.anscombe import forward_device
+    model = fp.load_packaged_model("foe_a")
+    _, y = make_counts(H, W, 7, 2.0)
+    v = forward_device(torch.from_numpy(y).cuda())
+    cfg = fp.SolverConfig(rel_tol=0.0)
+    lam = fp.select_lambda(2.0, "transform", force_branch="quadratic")
+    single = fp.solve_device(model, v, v, lam, "quadratic", iters, cfg)
+    u, traces, status = bands.solve_image_bands(model, v, v, lam, "quadratic", iters, n_bands, cfg)
+    assert status == [0]
+    assert traces[0].L == single.traces[0].L and traces[0].F == single.traces[0].F
+    assert torch.equal(u[0], single.u)
