@@ -133,6 +133,86 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_scaling_config(args, rank, local_rank, world):
+    """Configs 4 (batch sharding) and 5 (row bands): strong scaling, device-timed, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1609_05722_b200 as fp
+    from paper_1609_05722_b200 import bands
+    from paper_1609_05722_b200.anscombe import forward_device, inverse_exact_unbiased_device
+    from paper_1609_05722_b200.synth import make_counts
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    model = fp.load_packaged_model("foe_a")
+    cfg0 = fp.SolverConfig(rel_tol=0.0)
+    stream = torch.cuda.current_stream()
+    if args.config == 4:
+        sl = bands.shard_batch(args.batch, rank, world)
+        seeds = list(range(args.batch))[sl]
+        peaks = [[0.5, 1.0, 2.0, 4.0][s % 4] for s in seeds]
+        ys = torch.from_numpy(np.stack([make_counts(H, W, s, p)[1] for s, p in zip(seeds, peaks)])).cuda()
+
+        def step():
+            img, traces, _, _ = fp.denoise_batch(ys, peaks, model, "transform", force_branch="quadratic",
+                                                 solver=cfg0, return_device=True)
+            return sum(len(t) for t in traces) * H * W
+        workload = f"cfg4: {args.batch} x 512x512, peaks cycling 0.5/1/2/4, quadratic, foe_a, 150 iters, " \
+                   f"batch-sharded over {world} ranks (no collective)"
+        dtag = "dp"
+    else:
+        HH = WW = 8192
+        _, ty = bands.tile_grid(5, HH, WW)
+        t0, t1 = bands.partition_tile_rows(ty, world)[rank]
+        lam = fp.select_lambda(2.0, "transform", force_branch="quadratic")
+        band = bands.Band(model, 1, HH, WW, t0, t1, 150, cfg0)
+        l0, l1 = band.local_rows
+        _, y = make_counts(HH, WW, 0, 2.0)
+        v_local = forward_device(torch.from_numpy(np.ascontiguousarray(y[l0:l1])).cuda())[None]
+        ex = bands.DistExchange() if world > 1 else bands.LocalExchange()
+
+        def step():
+            res = bands.solve_bands([band], ex, [v_local], [v_local], lam, "quadratic", 150)
+            inverse_exact_unbiased_device(res[0][0])
+            return len(res[0][1][0]) * HH * WW / world
+        workload = f"cfg5: 8192x8192, peak 2, quadratic, foe_a, 150 iters, {world} row band(s), 4-row halo " \
+                   f"+ per-pass partials all-gather"
+        dtag = "bands"
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms, px_it = 0.0, 0.0
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            px_it += step()
+            e1.record(stream)
+            e1.synchronize()
+            total_ms += e0.elapsed_time(e1)
+    t = torch.tensor([total_ms, px_it], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.barrier()
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        total_ms, px_it = float(tmax[0]), float(t[1])
+    value = px_it / (total_ms * 1e-3) / 1e6
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": value, "unit": "Mpixel*iter/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+                          "data": "synthetic", "config": {"workload": workload, "parallelism": f"{dtag}{world}"},
+                          "clocks": clk.summary()}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -143,12 +223,19 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pass-reps", type=int, default=100)
+    ap.add_argument("--config", type=int, default=2, choices=[2, 4, 5],
+                    help="2: 512^2 single image (headline); 4: 256 x 512^2 batch sharded over ranks; "
+                         "5: one 8192^2 image split into row bands over ranks")
+    ap.add_argument("--batch", type=int, default=256, help="config 4: total images (strong scaling)")
     args = ap.parse_args()
     rank, local_rank, world = dist_env()
     args.warmup = max(args.warmup, 0)
 
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.config in (4, 5):
+        run_scaling_config(args, rank, local_rank, world)
         return
 
     import torch
