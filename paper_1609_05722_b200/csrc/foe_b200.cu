@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -77,6 +78,7 @@ struct PassArgs {
     int lrow0;  // global row stored in local row 0
     int Hl;     // local rows per image (plane stride = Hl * W)
     int band;   // 1: write partials only, decisions by k_decide after the all-gather
+    unsigned *grid_bar;  // resident solver: [0] arrival count, [1] generation
     size_t plane;  // B*H*W: distance between state slots
     const float *kf;     // (n, M*M) flipped taps (correlation orientation of the forward conv)
     const float *alpha;  // (n)
@@ -157,19 +159,21 @@ __device__ __forceinline__ float prox_idv(float ut, float t, float ob) {
 // ------------------------------------------------------------------------------------------------
 // decision (the body of the backtracking loop, solver.py:147-174), run by one thread per image
 
-__device__ void finish_image(const PassArgs &a, ImgCtl &c) {
+__device__ void finish_image(const PassArgs &a, ImgCtl &c, bool primary) {
     c.done = 1;
-    atomicSub(a.n_active, 1);
+    if (primary) atomicSub(a.n_active, 1);
 }
 
-__device__ void decide(const PassArgs &a, int b, const double *s) {
-    ImgCtl &c = a.ctl[b];
-    if (a.mode == MODE_INIT) {
+// Apply one pass's summed partials s[0..6] to image b's control block c.  `primary` = this copy of
+// the control block is the authoritative one (writes the trace row and the live counter); the
+// resident solver runs the same function on a private copy in every CTA.
+__device__ void decide_ctl(const PassArgs &a, int b, const double *s, ImgCtl &c, bool primary, int mode) {
+    if (mode == MODE_INIT) {
         c.f_u = s[0];
         if (!isfinite(s[0])) {  // solver.py:142-144
             c.status = FOE_SOLVE_NONFINITE;
             c.failed_at = c.n;
-            finish_image(a, c);
+            finish_image(a, c, primary);
         }
         return;
     }
@@ -181,12 +185,14 @@ __device__ void decide(const PassArgs &a, int b, const double *s) {
     const double tol = 1e-12 * (fabs(c.f_u) + fabs(f_new) + fabs(gd) + 0.5 * L * sq);
     c.trials++;
     if (isfinite(f_new) && slack <= tol) {  // solver.py:156
-        double Gv;
-        if (c.branch == FOE_QUADRATIC) Gv = 0.5 * c.lam * s[4];  // pipeline.py:200
-        else Gv = (s[6] > 0.0) ? INFINITY : c.lam * (s[4] - s[5]);  // pipeline.py:141-149
+        if (primary) {
+            double Gv;
+            if (c.branch == FOE_QUADRATIC) Gv = 0.5 * c.lam * s[4];  // pipeline.py:200
+            else Gv = (s[6] > 0.0) ? INFINITY : c.lam * (s[4] - s[5]);  // pipeline.py:141-149
+            double *row = a.trace + ((size_t)b * a.trace_cap + c.n) * 6;  // solver.py:162-169
+            row[0] = f_new; row[1] = Gv; row[2] = L; row[3] = sqrt(sq); row[4] = slack; row[5] = tol;
+        }
         const double step = sqrt(sq);
-        double *row = a.trace + ((size_t)b * a.trace_cap + c.n) * 6;  // solver.py:162-169
-        row[0] = f_new; row[1] = Gv; row[2] = L; row[3] = step; row[4] = slack; row[5] = tol;
         const int old_up = c.iup;  // u_prev, u = u, u_new (solver.py:171)
         c.iup = c.iu; c.iu = c.inew; c.inew = old_up;
         const int og = c.ig; c.ig = c.ignew; c.ignew = og;
@@ -194,16 +200,18 @@ __device__ void decide(const PassArgs &a, int b, const double *s) {
         c.L = L / a.relax;  // solver.py:172
         c.n++;
         const double un = sqrt(un2);
-        if (step < a.rel_tol * fmax(un, 1e-300) || c.n >= c.max_iters) finish_image(a, c);  // :173-174
+        if (step < a.rel_tol * fmax(un, 1e-300) || c.n >= c.max_iters) finish_image(a, c, primary);  // :173-174
     } else {
         c.L = L * a.eta;  // solver.py:158-160
         if (c.L > a.max_L) {
             c.status = FOE_SOLVE_STALLED;
             c.failed_at = c.n;
-            finish_image(a, c);
+            finish_image(a, c, primary);
         }
     }
 }
+
+__device__ void decide(const PassArgs &a, int b, const double *s) { decide_ctl(a, b, s, a.ctl[b], true, a.mode); }
 
 // fixed-order block reduction of kNumPartials doubles (deterministic)
 template <int NT>
@@ -432,9 +440,8 @@ int grid_1d(int64_t n, int block = 256) {
 }
 
 template <int M>
-size_t pass_smem_bytes(int nf, bool trial) {
-    using C = PassCfg<M>;
-    return sizeof(float) * ((size_t)(trial ? 2 : 1) * C::PLANE + (size_t)C::NPSI * C::PLANE + (size_t)nf * C::TAPS + nf);
+size_t pass_smem_bytes(int nf, bool trial, bool resident = false) {
+    return sizeof(float) * smem_floats<M>(nf, trial, resident);
 }
 
 template <int M, bool TRIAL, bool SYM>
@@ -472,6 +479,37 @@ int launch_pass(int m, bool sym, const PassArgs &a, cudaStream_t st) {
     return sym ? launch_pass_m<false, true>(m, a, st) : launch_pass_m<false, false>(m, a, st);
 }
 
+// resident (single cooperative launch) solve: returns FOE_OK if launched, 1 if not applicable
+template <int M, bool SYM>
+int launch_resident_t(const PassArgs &a, cudaStream_t st) {
+    using C = PassCfg<M>;
+    const size_t smem = pass_smem_bytes<M>(a.n_filters, true, true);
+    if (smem > 232448) return 1;
+    int dev = 0, nsm = 0, nb = 0, coop = 0;
+    FOE_CUDA(cudaGetDevice(&dev));
+    FOE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    FOE_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    if (!coop) return 1;
+    FOE_CUDA(cudaFuncSetAttribute(k_solve_resident<M, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    FOE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_solve_resident<M, SYM>, C::NT, smem));
+    if ((long)nb * nsm < (long)a.tiles_x * a.tiles_y * a.B) return 1;
+    dim3 grid(a.tiles_x * a.tiles_y, a.B);
+    void *args[] = {(void *)&a};
+    FOE_CUDA(cudaLaunchCooperativeKernel((const void *)k_solve_resident<M, SYM>, grid, dim3(C::NT), args, smem, st));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return FOE_OK;
+}
+
+int launch_resident(int m, bool sym, const PassArgs &a, cudaStream_t st) {
+    switch (m) {
+        case 1: return sym ? launch_resident_t<1, true>(a, st) : launch_resident_t<1, false>(a, st);
+        case 3: return sym ? launch_resident_t<3, true>(a, st) : launch_resident_t<3, false>(a, st);
+        case 5: return sym ? launch_resident_t<5, true>(a, st) : launch_resident_t<5, false>(a, st);
+        case 7: return sym ? launch_resident_t<7, true>(a, st) : launch_resident_t<7, false>(a, st);
+        default: return 1;
+    }
+}
+
 void tile_counts(int m, int H, int W, int *tx, int *ty) {
     const int r = m / 2;
     const int TH = PassCfg<1>::RH - 2 * r, TW = PassCfg<1>::RW - 2 * r;  // PassCfg<M>::TH / TW
@@ -482,7 +520,7 @@ void tile_counts(int m, int H, int W, int *tx, int *ty) {
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct SolveLayout {
-    size_t U, G, O, ctl, partials, tickets, trace, n_active, send, recv, total;
+    size_t U, G, O, ctl, partials, tickets, trace, n_active, send, recv, grid_bar, total;
     size_t halo_floats;  // per direction
 };
 
@@ -498,13 +536,15 @@ SolveLayout solve_layout(int m, int B, int H, int W, int trace_cap, int Hl = -1,
     L.G = off; off = align_up(off + 2 * plane);
     L.O = off; off = align_up(off + plane);
     L.ctl = off; off = align_up(off + sizeof(ImgCtl) * B);
-    L.partials = off; off = align_up(off + sizeof(double) * kPartialStride * (size_t)B * tx * ty);
+    // partials double-buffered by pass parity (the resident solver reads pass k while writing k+1)
+    L.partials = off; off = align_up(off + 2 * sizeof(double) * kPartialStride * (size_t)B * tx * ty);
     L.tickets = off; off = align_up(off + sizeof(unsigned) * B);
     L.trace = off; off = align_up(off + sizeof(double) * 6 * (size_t)B * trace_cap);
     L.n_active = off; off = align_up(off + sizeof(int) * 4);
     L.halo_floats = (size_t)B * 2 * halo * W;
     L.send = off; off = align_up(off + sizeof(float) * 2 * L.halo_floats);
     L.recv = off; off = align_up(off + sizeof(float) * 2 * L.halo_floats);
+    L.grid_bar = off; off = align_up(off + sizeof(unsigned) * 2);
     L.total = off;
     return L;
 }
@@ -739,6 +779,7 @@ static void fill_solve_args(PassArgs &a, const foe_bank *bank, const foe_solver_
     a.trace = (double *)(ws + L.trace);
     a.trace_cap = trace_cap;
     a.n_active = (int *)(ws + L.n_active);
+    a.grid_bar = (unsigned *)(ws + L.grid_bar);
     a.gamma = cfg.gamma;
     a.step_num = 1.99 * (1.0 - cfg.gamma);  // solver.py:64-65
     a.eta = cfg.backtrack_factor;
@@ -796,6 +837,16 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     FOE_CUDA(cudaMemcpyAsync(a.U + 2 * a.plane, u0, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
     FOE_CUDA(cudaMemcpyAsync((float *)(ws + L.O), obs, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
 
+    const char *env = getenv("FOE_RESIDENT");
+    const bool try_resident = B <= kResidentMaxB && !(env && env[0] == '0');
+    bool resident = false;
+    if (try_resident) {
+        FOE_CUDA(cudaMemsetAsync(a.grid_bar, 0, sizeof(unsigned) * 2, st));
+        rc = launch_resident(bank->m, bank->boundary == FOE_SYMMETRIC, a, st);
+        if (rc < 0) return rc;
+        resident = rc == FOE_OK;
+    }
+    if (!resident) {
     // iteration 0 needs F(u0) and grad F(u0)
     a.mode = MODE_INIT;
     if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, st))) return rc;
@@ -831,6 +882,7 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     }
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
+    }  // per-launch path
     {
         dim3 grid(std::max(1, std::min(148, (int)((size_t)H * W / 1024 + 1))), B);
         g_launches.fetch_add(1, std::memory_order_relaxed);

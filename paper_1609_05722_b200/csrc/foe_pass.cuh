@@ -1,17 +1,25 @@
-// foe_pass.cuh -- the fused FoE pass kernel (included by foe_b200.cu).
+// foe_pass.cuh -- the fused FoE pass (included by foe_b200.cu).
 //
 // One CTA = one tile of one image.  Region = owned tile + r ring (the pixels whose responses the
 // adjoint needs); staged cells = region + another r ring (the inputs of those responses).
 //
 // Thread layout: 3 filter groups x 6 warps.  A warp covers 8 micro-columns x 4 micro-rows of
 // 3x4-pixel micro-tiles, so each 8-lane LDS.128 phase reads 32 consecutive floats of one smem row
-// (bank-conflict free for any pitch).  Each group owns every 3rd filter slice of the bank and
-// double-buffered psi planes, so groups synchronise only among themselves (named barriers).
+// (bank-conflict free for any pitch).  Each group owns a third of the filter bank and a ring of
+// psi buffers, synchronised with split-phase mbarriers.
 //
 // Per filter and thread: forward z = K u_new and dz = K du on 12 pixels from a 5x8 (r=2) window
 // streamed from smem (600 FFMA), pointwise psi = 2a z/(1+z^2) and the energy change
 // a*log1p(dz(2z_o+dz)/(1+z_o^2)) evaluated as 2a*atanh(t), t = (z^2-z_o^2)/((1+z^2)+(1+z_o^2)),
 // then the adjoint K^T psi (300 FFMA).
+//
+// Two drivers share the tile code:
+//  * k_pass: one launch per trial pass (any batch size, row bands); the last CTA of an image
+//    reduces the tile partials and decides.
+//  * k_solve_resident: the whole solve in one cooperative launch when every (image, tile) has its
+//    own SM.  Each CTA keeps its tile's u, u_prev, grad, obs in shared memory across passes (only
+//    the 2r halo comes from global memory), passes are separated by a grid barrier, and every CTA
+//    reduces the partials and takes the (identical) decision itself.
 
 template <int M_>
 struct PassCfg {
@@ -22,18 +30,23 @@ struct PassCfg {
     static constexpr int G = 3;             // filter groups per CTA
     static constexpr int NBUF = 4;          // psi buffers per group (pipelined mbarrier ring)
     static constexpr int NTX = RW / MX, NTY = RH / MY, NTG = NTX * NTY, NT = G * NTG;
-    static constexpr int WARPS_G = NTG / 32;
     static constexpr int CW = RW + 2 * R;       // staged columns
     static constexpr int SH = RH + 2 * R;       // staged rows
     static constexpr int SW = (CW + 3) & ~3;    // row pitch (float4 aligned)
     static constexpr int PLANE = SH * SW;
     static constexpr int NPSI = G * NBUF;       // psi planes
     static constexpr int TH = RH - 2 * R, TW = RW - 2 * R;  // max owned tile
+    static constexpr int TOWN = TH * TW;                    // resident state plane (owned pixels)
     static constexpr int TAPS = (M * M + 3) & ~3;           // per-filter tap stride (float4)
+    static constexpr int NCELL = SH * CW;
+    static constexpr int CPT = (NCELL + NT - 1) / NT;       // staged cells per thread
     static_assert(NTX == 16 && NTY == 12, "warp layout assumes 16 x 12 micro-tiles per group");
     static_assert(TH >= 2 * R, "tile too small for the fold rule");
     static_assert(G * RH * RW <= NPSI * PLANE, "group partial-gradient buffer must fit the psi planes");
+    static_assert(NT % RW == 0, "fold walk assumes whole region rows per pass");
 };
+
+constexpr int kResidentMaxB = 8;  // images per resident solve (control blocks kept in smem)
 
 __device__ __forceinline__ float rcp_approx(float x) {  // MUFU.RCP, no denormal fix-up
     float r;
@@ -75,171 +88,195 @@ __device__ __forceinline__ float two_atanh(float t) {
     return __logf((1.0f + t) * rcp_approx(1.0f - t));
 }
 
-template <int M, bool TRIAL, bool SYM>
-__global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
+// ------------------------------------------------------------------------------------------------
+// tile geometry and shared-memory carve-up
+
+struct TileGeom {
+    int t;                 // global tile index (partials layout [tile][B][8])
+    int s0, s1, c0, c1;    // owned rows / cols
+    int ry0, rx0;          // region origin; staged cell (i,j) <-> (ry0-R+i, rx0-R+j)
+    bool edge;             // touches the image edge (symmetric rule needs the psi ring zeroed)
+};
+
+template <int M, bool SYM>
+__device__ __forceinline__ TileGeom tile_geom(const PassArgs &a, int tyl, int txi) {
     using C = PassCfg<M>;
-    constexpr int R = C::R, SW = C::SW, CW = C::CW, SH = C::SH, MY = C::MY, NT = C::NT;
-    constexpr int WIN = C::MX + 2 * R;  // window width per micro-tile row
-    constexpr int WR = MY + 2 * R;      // window rows
+    TileGeom g;
+    const int tyi = a.ty0 + tyl;
+    g.t = tyi * a.tiles_x + txi;
+    g.s0 = tile_start(tyi, a.tiles_y, C::TH, a.H, C::R);
+    g.s1 = tile_start(tyi + 1, a.tiles_y, C::TH, a.H, C::R);
+    g.c0 = tile_start(txi, a.tiles_x, C::TW, a.W, C::R);
+    g.c1 = tile_start(txi + 1, a.tiles_x, C::TW, a.W, C::R);
+    g.ry0 = g.s0 - C::R;
+    g.rx0 = g.c0 - C::R;
+    g.edge = SYM && (g.s0 == 0 || g.c0 == 0 || g.s1 == a.H || g.c1 == a.W);
+    return g;
+}
 
-    extern __shared__ __align__(16) float sm[];
-    __shared__ double red[NT / 32][kNumPartials];
-    __shared__ double s_sum[kNumPartials];
-    __shared__ int s_last;
-    __shared__ unsigned long long s_mbar[C::G][C::NBUF];
-
-    const int tid = threadIdx.x;
-    const int b = blockIdx.y;
-    const int H = a.H, W = a.W, nf = a.n_filters;
-
-    int iu = 0, iup = 0, inew = 0, ig = 0, ignew = 0, branch = 0;
-    float tau32 = 0.f, t32 = 0.f, gam32 = 0.f;
-    if (a.mode != MODE_EVAL) {
-        const ImgCtl &c = a.ctl[b];
-        if (c.done && !a.no_decide) return;
-        iu = c.iu; iup = c.iup; inew = c.inew; ig = c.ig; ignew = c.ignew; branch = c.branch;
-        if (TRIAL) {
-            const double tau = a.step_num / c.L;  // SolverConfig.step_size, solver.py:64-65
-            tau32 = (float)tau;
-            t32 = (float)(tau * c.lam);
-            gam32 = (float)a.gamma;
-        }
+template <int M>
+struct Smem {
+    float *Un, *Du, *Psi, *taps, *alpha;
+    float *Su, *Sg, *So;  // resident state: u slots [3][TOWN], grad slots [2][TOWN], obs [TOWN]
+    __device__ Smem(float *sm, int nf, bool trial_planes) {
+        using C = PassCfg<M>;
+        Un = sm;
+        Du = Un + C::PLANE;
+        Psi = trial_planes ? Du + C::PLANE : Du;
+        taps = Psi + C::NPSI * C::PLANE;
+        alpha = taps + nf * C::TAPS;
+        Su = alpha + ((nf + 3) & ~3);
+        Sg = Su + 3 * C::TOWN;
+        So = Sg + 2 * C::TOWN;
     }
-    // local buffers hold global rows [lrow0, lrow0 + Hl) of each image (the whole image unless this
-    // launch is one row band of a decomposed image)
-    const int lrow0 = a.lrow0;
-    const size_t ioff = (size_t)b * a.Hl * W;
-    const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
-    float *gout, *uout = nullptr;
-    if (a.mode == MODE_EVAL) {
-        uin = a.u_in + ioff;
-        gout = a.g_out + ioff;
-    } else {
-        uin = a.U + iu * a.plane + ioff;
-        if (TRIAL) {
-            upv = a.U + iup * a.plane + ioff;
-            gin = a.Gs + ig * a.plane + ioff;
-            obs = a.obs + ioff;
-            uout = a.U + inew * a.plane + ioff;
-            gout = a.Gs + ignew * a.plane + ioff;
-        } else {
-            gout = a.Gs + ig * a.plane + ioff;
-        }
-    }
+};
 
-    const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
-    const int tyi = a.ty0 + tyl;              // global tile row
-    const int t = tyi * a.tiles_x + txi;      // global tile index (partials layout [tile][B][8])
-    const int s0 = tile_start(tyi, a.tiles_y, C::TH, H, R), s1 = tile_start(tyi + 1, a.tiles_y, C::TH, H, R);
-    const int c0 = tile_start(txi, a.tiles_x, C::TW, W, R), c1 = tile_start(txi + 1, a.tiles_x, C::TW, W, R);
-    const int ry0 = s0 - R, rx0 = c0 - R;  // region origin; staged cell (i,j) <-> (ry0-R+i, rx0-R+j)
+template <int M>
+__host__ __device__ constexpr size_t smem_floats(int nf, bool trial, bool resident) {
+    using C = PassCfg<M>;
+    return (size_t)(trial ? 2 : 1) * C::PLANE + (size_t)C::NPSI * C::PLANE + (size_t)nf * C::TAPS +
+           (size_t)((nf + 3) & ~3) + (resident ? (size_t)6 * C::TOWN : 0);
+}
 
-    float *Un = sm;
-    float *Du = Un + C::PLANE;
-    float *Psi = TRIAL ? Du + C::PLANE : Du;
-    float *s_taps = Psi + C::NPSI * C::PLANE;
-    float *s_alpha = s_taps + nf * C::TAPS;
-
-    for (int k = tid; k < nf * C::TAPS; k += NT) {
+template <int M>
+__device__ void stage_bank(const PassArgs &a, const Smem<M> &S) {
+    using C = PassCfg<M>;
+    const int nf = a.n_filters;
+    for (int k = threadIdx.x; k < nf * C::TAPS; k += C::NT) {
         const int f = k / C::TAPS, e = k - f * C::TAPS;
-        s_taps[k] = e < M * M ? a.kf[f * M * M + e] : 0.0f;
+        S.taps[k] = e < M * M ? a.kf[f * M * M + e] : 0.0f;
     }
-    for (int k = tid; k < nf; k += NT) s_alpha[k] = a.alpha[k];
-    if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG);
-    // psi_0 = 0 outside the image: the r ring of every psi plane is read only by outputs on the
-    // region border, which matter only where they are padded pixels folded back (symmetric rule,
-    // tiles on an image edge).  Elsewhere the ring feeds discarded outputs and stays unwritten.
-    const bool edge_tile = SYM && (s0 == 0 || c0 == 0 || s1 == H || c1 == W);
+    for (int k = threadIdx.x; k < nf; k += C::NT) S.alpha[k] = a.alpha[k];
+}
+
+// psi_0 = 0 outside the image: the r ring of every psi plane is read only by outputs on the region
+// border, which matter only where they are padded pixels folded back (symmetric rule, tiles on an
+// image edge).  Elsewhere the ring feeds discarded outputs and stays unwritten.
+template <int M>
+__device__ void zero_psi_ring(const Smem<M> &S) {
+    using C = PassCfg<M>;
+    constexpr int R = C::R, CW = C::CW, SH = C::SH;
     if constexpr (R > 0) {
-        if (edge_tile) {
-            constexpr int RING = SH * CW - C::RH * C::RW;
-            for (int k = tid; k < C::NPSI * RING; k += NT) {
-                const int pl = k / RING, e = k - pl * RING;
-                int i, j;
-                if (e < R * CW) { i = e / CW; j = e - i * CW; }
-                else if (e < 2 * R * CW) { const int e2 = e - R * CW; i = C::RH + R + e2 / CW; j = e2 % CW; }
-                else { const int e3 = e - 2 * R * CW; i = R + e3 / (2 * R); const int jj = e3 % (2 * R); j = jj < R ? jj : C::RW + jj; }
-                Psi[pl * C::PLANE + i * SW + j] = 0.0f;
-            }
+        constexpr int RING = SH * CW - C::RH * C::RW;
+        for (int k = threadIdx.x; k < C::NPSI * RING; k += C::NT) {
+            const int pl = k / RING, e = k - pl * RING;
+            int i, j;
+            if (e < R * CW) { i = e / CW; j = e - i * CW; }
+            else if (e < 2 * R * CW) { const int e2 = e - R * CW; i = C::RH + R + e2 / CW; j = e2 % CW; }
+            else { const int e3 = e - 2 * R * CW; i = R + e3 / (2 * R); const int jj = e3 % (2 * R); j = jj < R ? jj : C::RW + jj; }
+            S.Psi[pl * C::PLANE + i * C::SW + j] = 0.0f;
         }
     }
+}
 
+// per-image trial parameters of one pass
+struct TrialParams {
+    int iu, iup, inew, ig, ignew, branch;
+    float tau, t, gam;
+};
 
-    // Filters are zero-mean (DCT basis without DC, image.py:117-130), so K(u - c) == K u: staging
-    // u - c with c = the tile's anchor pixel keeps the fp32 products small (accuracy, not speed).
-    const float shift = a.zero_mean ? __ldg(uin + (size_t)(s0 - lrow0) * W + c0) : 0.0f;
+__device__ __forceinline__ TrialParams trial_params(const PassArgs &a, const ImgCtl &c) {
+    TrialParams p;
+    p.iu = c.iu; p.iup = c.iup; p.inew = c.inew; p.ig = c.ig; p.ignew = c.ignew; p.branch = c.branch;
+    const double tau = a.step_num / c.L;  // SolverConfig.step_size, solver.py:64-65
+    p.tau = (float)tau;
+    p.t = (float)(tau * c.lam);
+    p.gam = (float)a.gamma;
+    return p;
+}
 
-    // ---- prologue: stage u (EVAL/INIT) or the trial point u_new and du (TRIAL) -------------------
-    double acc[kNumPartials];
+// ------------------------------------------------------------------------------------------------
+// prologue: stage u (EVAL/INIT) or the trial point u_new and du (TRIAL) into Un/Du
+//   global inputs are image-offset pointers to local buffers holding rows [lrow0, lrow0 + Hl);
+//   RES: the owned pixels come from the resident smem state, only the halo from global (L2)
+
+template <int M, bool TRIAL, bool SYM, bool RES>
+__device__ void stage(const PassArgs &a, const TileGeom &g, const Smem<M> &S, const TrialParams &p, const float *uin,
+                      const float *upv, const float *gin, const float *obs, float *uout, float shift,
+                      double (&acc)[kNumPartials]) {
+    using C = PassCfg<M>;
+    constexpr int R = C::R, CW = C::CW, SW = C::SW, NT = C::NT, CPT = C::CPT, NCELL = C::NCELL;
+    const int H = a.H, W = a.W, lrow0 = a.lrow0, tid = threadIdx.x;
+    const int ow = g.c1 - g.c0;
+    // load phase: every global read of this thread's cells in flight before any use
+    float lu[CPT], lup[CPT], lg[CPT], lob[CPT];
 #pragma unroll
-    for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
-    constexpr int NCELL = SH * CW;
-    constexpr int CPT = (NCELL + NT - 1) / NT;  // staged cells per thread
-    if (TRIAL) {
-        // all global loads of this thread's cells first (4 x CPT in flight), then the arithmetic
-        float lu[CPT], lup[CPT], lg[CPT], lob[CPT];
-#pragma unroll
-        for (int q = 0; q < CPT; ++q) {
-            const int k = tid + q * NT;
-            if (k < NCELL) {
-                const int i = k / CW, j = k - i * CW;
-                const size_t o = (size_t)(src_idx<SYM>(ry0 - R + i, H) - lrow0) * W + src_idx<SYM>(rx0 - R + j, W);
-                lu[q] = __ldg(uin + o); lup[q] = __ldg(upv + o); lg[q] = __ldg(gin + o); lob[q] = __ldg(obs + o);
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < CPT; ++q) {
-            const int k = tid + q * NT;
-            if (k < NCELL) {
-                const int i = k / CW, j = k - i * CW;
-                const int gy = ry0 - R + i, gx = rx0 - R + j;
-                const float u = lu[q], g = lg[q], ob = lob[q];
-                // u - tau g + gamma (u - u_prev)  (solver.py:146-149)
-                const float ut = (u - tau32 * g) + gam32 * (u - lup[q]);
-                const float un = (branch == FOE_QUADRATIC) ? prox_quad(ut, t32, ob) : prox_idv(ut, t32, ob);
-                const float du = un - u;
-                Un[i * SW + j] = un - shift;
-                Du[i * SW + j] = du;
-                if (gy >= s0 && gy < s1 && gx >= c0 && gx < c1) {
-                    uout[(size_t)(gy - lrow0) * W + gx] = un;
-                    acc[1] += (double)du * (double)du;  // vdot(du, du)  solver.py:152
-                    acc[2] += (double)g * (double)du;   // vdot(g, du)   solver.py:153
-                    acc[3] += (double)u * (double)u;    // |u|^2 for the stop test, solver.py:173
-                    if (branch == FOE_QUADRATIC) {
-                        const double d = (double)un - (double)ob;
-                        acc[4] += d * d;
-                    } else {
-                        acc[4] += (double)un;
-                        if (ob > 0.0f) {
-                            if (un > 0.0f) acc[5] += (double)ob * (double)logf(un);
-                            else acc[6] += 1.0;
-                        }
-                    }
+    for (int q = 0; q < CPT; ++q) {
+        const int k = tid + q * NT;
+        if (k < NCELL) {
+            const int i = k / CW, j = k - i * CW;
+            const int sy = src_idx<SYM>(g.ry0 - R + i, H), sx = src_idx<SYM>(g.rx0 - R + j, W);
+            if (RES && sy >= g.s0 && sy < g.s1 && sx >= g.c0 && sx < g.c1) {
+                const int ri = (sy - g.s0) * ow + (sx - g.c0);
+                lu[q] = S.Su[p.iu * C::TOWN + ri];
+                if (TRIAL) {
+                    lup[q] = S.Su[p.iup * C::TOWN + ri];
+                    lg[q] = S.Sg[p.ig * C::TOWN + ri];
+                    lob[q] = S.So[ri];
+                }
+            } else {
+                const size_t o = (size_t)(sy - lrow0) * W + sx;
+                if (RES) {  // written by other CTAs during this kernel: bypass L1
+                    lu[q] = __ldcg(uin + o);
+                    if (TRIAL) { lup[q] = __ldcg(upv + o); lg[q] = __ldcg(gin + o); lob[q] = __ldg(obs + o); }
+                } else {
+                    lu[q] = __ldg(uin + o);
+                    if (TRIAL) { lup[q] = __ldg(upv + o); lg[q] = __ldg(gin + o); lob[q] = __ldg(obs + o); }
                 }
             }
         }
-    } else {
-        float lu[CPT];
+    }
 #pragma unroll
-        for (int q = 0; q < CPT; ++q) {
-            const int k = tid + q * NT;
-            if (k < NCELL) {
-                const int i = k / CW, j = k - i * CW;
-                lu[q] = __ldg(uin + (size_t)(src_idx<SYM>(ry0 - R + i, H) - lrow0) * W + src_idx<SYM>(rx0 - R + j, W));
-            }
+    for (int q = 0; q < CPT; ++q) {
+        const int k = tid + q * NT;
+        if (k >= NCELL) continue;
+        const int i = k / CW, j = k - i * CW;
+        if (!TRIAL) {
+            S.Un[i * SW + j] = lu[q] - shift;
+            continue;
         }
-#pragma unroll
-        for (int q = 0; q < CPT; ++q) {
-            const int k = tid + q * NT;
-            if (k < NCELL) {
-                const int i = k / CW, j = k - i * CW;
-                Un[i * SW + j] = lu[q] - shift;
+        const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
+        const float u = lu[q], gg = lg[q], ob = lob[q];
+        // u - tau g + gamma (u - u_prev)  (solver.py:146-149)
+        const float ut = (u - p.tau * gg) + p.gam * (u - lup[q]);
+        const float un = (p.branch == FOE_QUADRATIC) ? prox_quad(ut, p.t, ob) : prox_idv(ut, p.t, ob);
+        const float du = un - u;
+        S.Un[i * SW + j] = un - shift;
+        S.Du[i * SW + j] = du;
+        if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) {
+            uout[(size_t)(gy - lrow0) * W + gx] = un;
+            if (RES) S.Su[p.inew * C::TOWN + (gy - g.s0) * ow + (gx - g.c0)] = un;
+            acc[1] += (double)du * (double)du;  // vdot(du, du)  solver.py:152
+            acc[2] += (double)gg * (double)du;  // vdot(g, du)   solver.py:153
+            acc[3] += (double)u * (double)u;    // |u|^2 for the stop test, solver.py:173
+            if (p.branch == FOE_QUADRATIC) {
+                const double d = (double)un - (double)ob;
+                acc[4] += d * d;
+            } else {
+                acc[4] += (double)un;
+                if (ob > 0.0f) {
+                    if (un > 0.0f) acc[5] += (double)ob * (double)logf(un);
+                    else acc[6] += 1.0;
+                }
             }
         }
     }
-    __syncthreads();  // staged tile, taps and mbarrier init visible
+}
 
-    // ---- filter loop -----------------------------------------------------------------------------
+// ------------------------------------------------------------------------------------------------
+// filter loop: per filter forward responses, pointwise, adjoint; returns this thread's owned
+// energy terms (fp64) and leaves the group's partial gradient in gacc.  `phase` carries the
+// mbarrier parities of the NBUF slots across calls (the resident solver reuses the barriers).
+
+template <int M, bool TRIAL, bool SYM>
+__device__ double filter_loop(const PassArgs &a, const TileGeom &g, const Smem<M> &S,
+                              unsigned long long (*mbar)[PassCfg<M>::NBUF], unsigned &phase,
+                              float (&gacc)[PassCfg<M>::MY][PassCfg<M>::MX]) {
+    using C = PassCfg<M>;
+    constexpr int R = C::R, SW = C::SW, MY = C::MY;
+    constexpr int WIN = C::MX + 2 * R;  // window width per micro-tile row
+    constexpr int WR = MY + 2 * R;      // window rows
+    const int H = a.H, W = a.W, nf = a.n_filters, tid = threadIdx.x;
     const int grp = tid / C::NTG, lt = tid - grp * C::NTG;
     const int wg = lt >> 5, lane = lt & 31;
     const int tx = (wg & 1) * 8 + (lane & 7), ty = (wg >> 1) * 4 + (lane >> 3);
@@ -252,28 +289,22 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     unsigned out_bits = 0u, own_bits = 0u;
 #pragma unroll
     for (int o = 0; o < MY; ++o) {
-        const int gy = ry0 + ly0 + o;
+        const int gy = g.ry0 + ly0 + o;
 #pragma unroll
         for (int c = 0; c < C::MX; ++c) {
-            const int gx = rx0 + lx0 + c;
+            const int gx = g.rx0 + lx0 + c;
             if (SYM && !(gy >= 0 && gy < H && gx >= 0 && gx < W)) out_bits |= 1u << (o * C::MX + c);
-            if (gy >= s0 && gy < s1 && gx >= c0 && gx < c1) own_bits |= 1u << (o * C::MX + c);
+            if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) own_bits |= 1u << (o * C::MX + c);
         }
     }
     float epx[MY][C::MX];  // per-pixel energy terms summed over this group's filters (fp32)
 #pragma unroll
     for (int o = 0; o < MY; ++o)
 #pragma unroll
-        for (int c = 0; c < C::MX; ++c) epx[o][c] = 0.0f;
+        for (int c = 0; c < C::MX; ++c) { epx[o][c] = 0.0f; gacc[o][c] = 0.0f; }
 
-    float gacc[MY][C::MX];
-#pragma unroll
-    for (int o = 0; o < MY; ++o)
-#pragma unroll
-        for (int c = 0; c < C::MX; ++c) gacc[o][c] = 0.0f;
-
-    const float *ubase = Un + ly0 * SW + lx0;
-    const float *dbase = Du + ly0 * SW + lx0;
+    const float *ubase = S.Un + ly0 * SW + lx0;
+    const float *dbase = S.Du + ly0 * SW + lx0;
 
     // software-pipelined over this group's filters: forward(k) -> arrive(k) -> wait(k-1) ->
     // adjoint(k-1).  psi of round k lives in buffer k % NBUF; a warp waits only if a peer has not
@@ -289,10 +320,10 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
                 float w[C::TAPS];
 #pragma unroll
                 for (int kk = 0; kk < C::TAPS; kk += 4) {
-                    const float4 v = *reinterpret_cast<const float4 *>(s_taps + f * C::TAPS + kk);
+                    const float4 v = *reinterpret_cast<const float4 *>(S.taps + f * C::TAPS + kk);
                     w[kk] = v.x; w[kk + 1] = v.y; w[kk + 2] = v.z; w[kk + 3] = v.w;
                 }
-                const float al = s_alpha[f];
+                const float al = S.alpha[f];
                 float z[MY][C::MX], dz[MY][C::MX];
 #pragma unroll
                 for (int o = 0; o < MY; ++o)
@@ -320,7 +351,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
                     }
                 }
                 // pointwise: psi = a rho'(z) (prior.py:31-32); energy terms
-                float *ps = Psi + (grp * C::NBUF + kb) * C::PLANE + (ly0 + R) * SW + lx0 + R;
+                float *ps = S.Psi + (grp * C::NBUF + kb) * C::PLANE + (ly0 + R) * SW + lx0 + R;
                 const float a2 = 2.0f * al;
                 float tt[MY][C::MX];
                 float tmax = 0.0f;
@@ -376,20 +407,22 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
                         for (int c = 0; c < C::MX; ++c) epx[o][c] = fmaf(al, log1pf(z[o][c] * z[o][c]), epx[o][c]);
                 }
             }
-            mbar_arrive(&s_mbar[grp][kb]);
+            mbar_arrive(&mbar[grp][kb]);
         }
         if (k > 0) {
             const int f = fbeg + k - 1;
             const int kb = (k - 1) % C::NBUF;
-            mbar_wait(&s_mbar[grp][kb], ((k - 1) / C::NBUF) & 1);
+            mbar_wait(&mbar[grp][kb], (phase >> kb) & 1u);
+            phase ^= 1u << kb;
             if (f < fend) {
                 float w[C::TAPS];
 #pragma unroll
                 for (int kk = 0; kk < C::TAPS; kk += 4) {
-                    const float4 v = *reinterpret_cast<const float4 *>(s_taps + f * C::TAPS + kk);
+                    const float4 v = *reinterpret_cast<const float4 *>(S.taps + f * C::TAPS + kk);
                     w[kk] = v.x; w[kk + 1] = v.y; w[kk + 2] = v.z; w[kk + 3] = v.w;
                 }
-                const float *pb = Psi + (grp * C::NBUF + kb) * C::PLANE + ly0 * SW + lx0;
+                const float *pb = S.Psi + (grp * C::NBUF + kb) * C::PLANE + ly0 * SW + lx0;
+                // adjoint: gacc += K_f^T psi_f  (correlation with the unflipped kernel, image.py:84-87)
 #pragma unroll
                 for (int i = 0; i < WR; ++i) {
                     float rp[WIN];
@@ -409,19 +442,29 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
             }
         }
     }
-    {
-        double e = 0.0;  // owned pixels only, fp64 across pixels
+    double e = 0.0;  // owned pixels only, fp64 across pixels
 #pragma unroll
-        for (int o = 0; o < MY; ++o)
+    for (int o = 0; o < MY; ++o)
 #pragma unroll
-            for (int c = 0; c < C::MX; ++c)
-                if (own_bits >> (o * C::MX + c) & 1u) e += (double)epx[o][c];
-        acc[0] = e;
-    }
-    __syncthreads();
+        for (int c = 0; c < C::MX; ++c)
+            if (own_bits >> (o * C::MX + c) & 1u) e += (double)epx[o][c];
+    return e;
+}
 
-    // ---- combine filter groups, fold padded pixels (P^T, image.py:88-90), write ------------------
-    float *gb = Psi;  // G planes of RH x RW
+// combine the group partial gradients, fold padded pixels onto their mirror sources (P^T,
+// image.py:88-90) and write the owned gradient (global, and resident smem slot if Sgo != null)
+template <int M, bool SYM>
+__device__ void fold_and_write(const PassArgs &a, const TileGeom &g, const Smem<M> &S,
+                               const float (&gacc)[PassCfg<M>::MY][PassCfg<M>::MX], float *gout, float *Sgo) {
+    using C = PassCfg<M>;
+    constexpr int R = C::R, NT = C::NT, MY = C::MY;
+    const int tid = threadIdx.x, H = a.H, W = a.W;
+    const int grp = tid / C::NTG, lt = tid - grp * C::NTG;
+    const int wg = lt >> 5, lane = lt & 31;
+    const int tx = (wg & 1) * 8 + (lane & 7), ty = (wg >> 1) * 4 + (lane >> 3);
+    const int ly0 = ty * MY, lx0 = tx * C::MX;
+    __syncthreads();  // all groups done with their psi planes
+    float *gb = S.Psi;  // G planes of RH x RW
 #pragma unroll
     for (int o = 0; o < MY; ++o)
         *reinterpret_cast<float4 *>(gb + grp * C::RH * C::RW + (ly0 + o) * C::RW + lx0) =
@@ -434,37 +477,98 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
         return s;
     };
     // 2-D ownership walk: column = tid % RW, rows strided by NT / RW (no integer division)
-    static_assert(NT % C::RW == 0, "fold walk assumes whole region rows per pass");
-    {
-        const int xx = tid % C::RW;
-        const int gx = c0 + xx;
-        if (gx < c1) {
-            const int lx = gx - rx0;
-            int mx = -1;
+    const int xx = tid % C::RW;
+    const int gx = g.c0 + xx;
+    const int ow = g.c1 - g.c0;
+    if (gx < g.c1) {
+        const int lx = gx - g.rx0;
+        int mx = -1;
+        if (SYM && R > 0) {
+            if (gx < R) mx = (-1 - gx) - g.rx0;
+            else if (gx >= W - R) mx = (2 * W - 1 - gx) - g.rx0;
+        }
+        for (int gy = g.s0 + tid / C::RW; gy < g.s1; gy += NT / C::RW) {
+            const int ly = gy - g.ry0;
+            float val = gsum(ly, lx);
             if (SYM && R > 0) {
-                if (gx < R) mx = (-1 - gx) - rx0;
-                else if (gx >= W - R) mx = (2 * W - 1 - gx) - rx0;
+                int my = -1;
+                if (gy < R) my = (-1 - gy) - g.ry0;
+                else if (gy >= H - R) my = (2 * H - 1 - gy) - g.ry0;
+                if (my >= 0) val += gsum(my, lx);
+                if (mx >= 0) val += gsum(ly, mx);
+                if (my >= 0 && mx >= 0) val += gsum(my, mx);
             }
-            for (int gy = s0 + tid / C::RW; gy < s1; gy += NT / C::RW) {
-                const int ly = gy - ry0;
-                float val = gsum(ly, lx);
-                if (SYM && R > 0) {
-                    int my = -1;
-                    if (gy < R) my = (-1 - gy) - ry0;
-                    else if (gy >= H - R) my = (2 * H - 1 - gy) - ry0;
-                    if (my >= 0) val += gsum(my, lx);
-                    if (mx >= 0) val += gsum(ly, mx);
-                    if (my >= 0 && mx >= 0) val += gsum(my, mx);
-                }
-                gout[(size_t)(gy - lrow0) * W + gx] = val;
-            }
+            gout[(size_t)(gy - a.lrow0) * W + gx] = val;
+            if (Sgo) Sgo[(gy - g.s0) * ow + xx] = val;
         }
     }
+}
 
-    // ---- per-tile partials, last CTA of the image reduces and decides ----------------------------
+// ------------------------------------------------------------------------------------------------
+// k_pass: one trial (or eval/init) pass per launch
+
+template <int M, bool TRIAL, bool SYM>
+__global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
+    using C = PassCfg<M>;
+    constexpr int NT = C::NT;
+    extern __shared__ __align__(16) float sm[];
+    __shared__ double red[NT / 32][kNumPartials];
+    __shared__ double s_sum[kNumPartials];
+    __shared__ int s_last;
+    __shared__ unsigned long long s_mbar[C::G][C::NBUF];
+
+    const int tid = threadIdx.x;
+    const int b = blockIdx.y;
+    TrialParams p{};
+    if (a.mode != MODE_EVAL) {
+        const ImgCtl &c = a.ctl[b];
+        if (c.done && !a.no_decide) return;
+        p = trial_params(a, c);
+    }
+    // local buffers hold global rows [lrow0, lrow0 + Hl) of each image (the whole image unless this
+    // launch is one row band of a decomposed image)
+    const size_t ioff = (size_t)b * a.Hl * a.W;
+    const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
+    float *gout, *uout = nullptr;
+    if (a.mode == MODE_EVAL) {
+        uin = a.u_in + ioff;
+        gout = a.g_out + ioff;
+    } else {
+        uin = a.U + p.iu * a.plane + ioff;
+        if (TRIAL) {
+            upv = a.U + p.iup * a.plane + ioff;
+            gin = a.Gs + p.ig * a.plane + ioff;
+            obs = a.obs + ioff;
+            uout = a.U + p.inew * a.plane + ioff;
+            gout = a.Gs + p.ignew * a.plane + ioff;
+        } else {
+            gout = a.Gs + p.ig * a.plane + ioff;
+        }
+    }
+    const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
+    const TileGeom g = tile_geom<M, SYM>(a, tyl, txi);
+    const Smem<M> S(sm, a.n_filters, TRIAL);
+    stage_bank<M>(a, S);
+    if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG);
+    if (g.edge) zero_psi_ring<M>(S);
+    // Filters are zero-mean (DCT basis without DC, image.py:117-130), so K(u - c) == K u: staging
+    // u - c with c = the tile's anchor pixel keeps the fp32 products small (accuracy, not speed).
+    const float shift = a.zero_mean ? __ldg(uin + (size_t)(g.s0 - a.lrow0) * a.W + g.c0) : 0.0f;
+    double acc[kNumPartials];
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
+    stage<M, TRIAL, SYM, false>(a, g, S, p, uin, upv, gin, obs, uout, shift, acc);
+    __syncthreads();  // staged tile, taps and mbarrier init visible
+
+    float gacc[C::MY][C::MX];
+    unsigned phase = 0u;
+    acc[0] = filter_loop<M, TRIAL, SYM>(a, g, S, s_mbar, phase, gacc);
+    fold_and_write<M, SYM>(a, g, S, gacc, gout, nullptr);
+
+    // per-tile partials, last CTA of the image reduces and decides
     block_reduce<NT>(acc, red, s_sum);
     if (tid < kNumPartials) {
-        a.partials[((size_t)t * a.B + b) * kPartialStride + tid] = s_sum[tid];
+        a.partials[((size_t)g.t * a.B + b) * kPartialStride + tid] = s_sum[tid];
         __threadfence();
     }
     if (a.band) return;  // band mode: partials are all-gathered and decided by k_decide
@@ -483,4 +587,122 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
             decide(a, b, s_sum);
         }
     }
+}
+
+// ------------------------------------------------------------------------------------------------
+// k_solve_resident: the whole device-resident solve in one cooperative launch
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// generation barrier across the (co-resident) grid; bounded spin -> trap on a hang
+__device__ void grid_barrier(unsigned *bar, unsigned nblocks, unsigned &gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            unsigned long long spins = 0;
+            while (ld_acquire_gpu(bar + 1) == gen) {
+                __nanosleep(64);
+                if (++spins > (1ull << 28)) __trap();  // ~> 20 s: a co-residency bug, not a slow pass
+            }
+        }
+        __threadfence();
+    }
+    ++gen;
+    __syncthreads();
+}
+
+template <int M, bool SYM>
+__global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_solve_resident(const PassArgs a) {
+    using C = PassCfg<M>;
+    constexpr int NT = C::NT;
+    extern __shared__ __align__(16) float sm[];
+    __shared__ double red[NT / 32][kNumPartials];
+    __shared__ double s_sum[kNumPartials];
+    __shared__ unsigned long long s_mbar[C::G][C::NBUF];
+    __shared__ ImgCtl s_ctl[kResidentMaxB];
+
+    const int tid = threadIdx.x;
+    const int b = blockIdx.y;
+    const int B = a.B;
+    const bool primary = blockIdx.x == 0 && blockIdx.y == 0;
+    const unsigned nblocks = gridDim.x * gridDim.y;
+    const int ntiles = a.tiles_x * a.tiles_y;
+    unsigned gen = 0;
+    if (tid == 0) gen = ld_acquire_gpu(a.grid_bar + 1);
+
+    const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
+    const TileGeom g = tile_geom<M, SYM>(a, tyl, txi);
+    const Smem<M> S(sm, a.n_filters, true);
+    stage_bank<M>(a, S);
+    if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG);
+    if (tid < B) s_ctl[tid] = a.ctl[tid];
+    if (g.edge) zero_psi_ring<M>(S);
+    const size_t ioff = (size_t)b * a.Hl * a.W;
+    const int ow = g.c1 - g.c0, oh = g.s1 - g.s0;
+    __syncthreads();
+    {   // resident state: u_prev = u = u0 (slots iu, iup), obs
+        const ImgCtl &c = s_ctl[b];
+        for (int k = tid; k < oh * ow; k += NT) {
+            const int yy = k / ow, xx = k - yy * ow;
+            const size_t o = (size_t)(g.s0 + yy - a.lrow0) * a.W + g.c0 + xx;
+            const float u0 = a.U[c.iu * a.plane + ioff + o];
+            S.Su[c.iu * C::TOWN + k] = u0;
+            S.Su[c.iup * C::TOWN + k] = u0;
+            S.So[k] = a.obs[ioff + o];
+        }
+    }
+    __syncthreads();
+    unsigned phase = 0u;
+
+    for (int pass = 0;; ++pass) {
+        const bool init = pass == 0;
+        double *parts = a.partials + (size_t)(pass & 1) * ntiles * B * kPartialStride;  // double-buffered
+        const ImgCtl c = s_ctl[b];
+        if (!c.done) {
+            const TrialParams p = trial_params(a, c);
+            // zero-mean shift anchor = current u at the tile's first owned pixel (as in k_pass)
+            const float shift = a.zero_mean ? S.Su[p.iu * C::TOWN] : 0.0f;
+            double acc[kNumPartials];
+#pragma unroll
+            for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
+            float gacc[C::MY][C::MX];
+            if (init) {
+                stage<M, false, SYM, true>(a, g, S, p, a.U + p.iu * a.plane + ioff, nullptr, nullptr, nullptr,
+                                           nullptr, shift, acc);
+                __syncthreads();
+                acc[0] = filter_loop<M, false, SYM>(a, g, S, s_mbar, phase, gacc);
+                fold_and_write<M, SYM>(a, g, S, gacc, a.Gs + p.ig * a.plane + ioff, S.Sg + p.ig * C::TOWN);
+            } else {
+                stage<M, true, SYM, true>(a, g, S, p, a.U + p.iu * a.plane + ioff, a.U + p.iup * a.plane + ioff,
+                                          a.Gs + p.ig * a.plane + ioff, a.obs + ioff,
+                                          a.U + p.inew * a.plane + ioff, shift, acc);
+                __syncthreads();
+                acc[0] = filter_loop<M, true, SYM>(a, g, S, s_mbar, phase, gacc);
+                fold_and_write<M, SYM>(a, g, S, gacc, a.Gs + p.ignew * a.plane + ioff, S.Sg + p.ignew * C::TOWN);
+            }
+            block_reduce<NT>(acc, red, s_sum);
+            if (tid < kNumPartials) parts[((size_t)g.t * B + b) * kPartialStride + tid] = s_sum[tid];
+        }
+        grid_barrier(a.grid_bar, nblocks, gen);
+        // every CTA reduces every live image's partials in the fixed order and decides identically
+        bool all_done = true;
+        for (int bb = 0; bb < B; ++bb) {
+            if (s_ctl[bb].done) continue;
+            reduce_tiles<NT>(parts, ntiles, B, bb, red, s_sum);
+            if (tid == 0) decide_ctl(a, bb, s_sum, s_ctl[bb], primary, init ? MODE_INIT : MODE_TRIAL);
+            __syncthreads();
+            all_done &= s_ctl[bb].done != 0;
+        }
+        if (all_done) break;
+    }
+    if (primary && tid < B) a.ctl[tid] = s_ctl[tid];
 }
