@@ -484,13 +484,15 @@ template <int M, bool SYM>
 int launch_resident_t(const PassArgs &a, cudaStream_t st) {
     using C = PassCfg<M>;
     const size_t smem = pass_smem_bytes<M>(a.n_filters, true, true);
-    if (smem > 232448) return 1;
-    int dev = 0, nsm = 0, nb = 0, coop = 0;
+    int dev = 0, nsm = 0, nb = 0, coop = 0, optin = 0;
     FOE_CUDA(cudaGetDevice(&dev));
     FOE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     FOE_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    if (!coop) return 1;
-    FOE_CUDA(cudaFuncSetAttribute(k_solve_resident<M, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+    FOE_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    FOE_CUDA(cudaFuncGetAttributes(&fa, k_solve_resident<M, SYM>));
+    if (!coop || smem + fa.sharedSizeBytes > (size_t)optin) return 1;
+    FOE_CUDA(cudaFuncSetAttribute(k_solve_resident<M, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     FOE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_solve_resident<M, SYM>, C::NT, smem));
     if ((long)nb * nsm < (long)a.tiles_x * a.tiles_y * a.B) return 1;
     dim3 grid(a.tiles_x * a.tiles_y, a.B);
