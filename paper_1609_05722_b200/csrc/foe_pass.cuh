@@ -645,7 +645,6 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_solve_resident(const Pass
     stage_bank<M>(a, S);
     if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG);
     if (tid < B) s_ctl[tid] = a.ctl[tid];
-    if (g.edge) zero_psi_ring<M>(S);
     const size_t ioff = (size_t)b * a.Hl * a.W;
     const int ow = g.c1 - g.c0, oh = g.s1 - g.s0;
     __syncthreads();
@@ -671,6 +670,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_solve_resident(const Pass
             const TrialParams p = trial_params(a, c);
             // zero-mean shift anchor = current u at the tile's first owned pixel (as in k_pass)
             const float shift = a.zero_mean ? S.Su[p.iu * C::TOWN] : 0.0f;
+            if (g.edge) zero_psi_ring<M>(S);  // the previous pass's gradient combine reused the planes
             double acc[kNumPartials];
 #pragma unroll
             for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
