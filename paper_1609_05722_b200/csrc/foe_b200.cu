@@ -839,8 +839,10 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     FOE_CUDA(cudaMemcpyAsync(a.U + 2 * a.plane, u0, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
     FOE_CUDA(cudaMemcpyAsync((float *)(ws + L.O), obs, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
 
+    // the resident single-launch solver is opt-in (FOE_RESIDENT=1): measured no faster than the
+    // per-pass launches on B200 (grid barrier + redundant decisions cost what the launches did)
     const char *env = getenv("FOE_RESIDENT");
-    const bool try_resident = B <= kResidentMaxB && !(env && env[0] == '0');
+    const bool try_resident = B <= kResidentMaxB && env && env[0] == '1';
     bool resident = false;
     if (try_resident) {
         FOE_CUDA(cudaMemsetAsync(a.grid_bar, 0, sizeof(unsigned) * 2, st));
