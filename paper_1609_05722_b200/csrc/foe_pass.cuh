@@ -26,8 +26,8 @@ struct PassCfg {
     static constexpr int M = M_;
     static constexpr int R = M / 2;
     static constexpr int RH = 36, RW = 64;  // region (owned tile + r ring)
-    static constexpr int MY = 6, MX = 4;    // micro-tile per thread
-    static constexpr int G = 4;             // filter groups per CTA (one warp of each on every SMSP)
+    static constexpr int MY = 3, MX = 4;    // micro-tile per thread
+    static constexpr int G = 2;             // filter groups per CTA (6 warps each: 3 warps per SMSP)
     static constexpr int NBUF = 3;          // psi buffers per group (pipelined mbarrier ring)
     static constexpr int NTX = RW / MX, NTY = RH / MY, NTG = NTX * NTY, NT = G * NTG;
     static constexpr int CW = RW + 2 * R;       // staged columns
@@ -40,7 +40,7 @@ struct PassCfg {
     static constexpr int TAPS = (M * M + 3) & ~3;           // per-filter tap stride (float4)
     static constexpr int NCELL = SH * CW;
     static constexpr int CPT = (NCELL + NT - 1) / NT;       // staged cells per thread
-    static_assert(NTX == 16 && NTY == 6, "warp layout assumes 16 x 6 micro-tiles per group (3 warps)");
+    static_assert(NTX == 16 && NTY == 12, "warp layout assumes 16 x 12 micro-tiles per group (6 warps)");
     static_assert(TH >= 2 * R, "tile too small for the fold rule");
     static_assert(G * RH * RW <= NPSI * PLANE, "group partial-gradient buffer must fit the psi planes");
     static_assert(NT % RW == 0, "fold walk assumes whole region rows per pass");
@@ -279,7 +279,7 @@ __device__ double filter_loop(const PassArgs &a, const TileGeom &g, const Smem<M
     const int H = a.H, W = a.W, nf = a.n_filters, tid = threadIdx.x;
     const int grp = tid / C::NTG, lt = tid - grp * C::NTG;
     const int wg = lt >> 5, lane = lt & 31;
-    const int tx = lane & 15, ty = wg * 2 + (lane >> 4);
+    const int tx = (wg & 1) * 8 + (lane & 7), ty = (wg >> 1) * 4 + (lane >> 3);
     const int fpg = (nf + C::G - 1) / C::G;
     const int fbeg = grp * fpg, fend = min(nf, fbeg + fpg);
     const int ly0 = ty * MY, lx0 = tx * C::MX;  // region-local origin of this thread's micro-tile
@@ -461,7 +461,7 @@ __device__ void fold_and_write(const PassArgs &a, const TileGeom &g, const Smem<
     const int tid = threadIdx.x, H = a.H, W = a.W;
     const int grp = tid / C::NTG, lt = tid - grp * C::NTG;
     const int wg = lt >> 5, lane = lt & 31;
-    const int tx = lane & 15, ty = wg * 2 + (lane >> 4);
+    const int tx = (wg & 1) * 8 + (lane & 7), ty = (wg >> 1) * 4 + (lane >> 3);
     const int ly0 = ty * MY, lx0 = tx * C::MX;
     __syncthreads();  // all groups done with their psi planes
     float *gb = S.Psi;  // G planes of RH x RW
