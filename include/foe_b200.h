@@ -95,6 +95,13 @@ int foe_prox_quadratic(const float *u_tilde, const float *v, float *out, double 
 int foe_prox_idiv(const float *u_tilde, const float *obs, float *out, double t, int64_t n,
                   void *stream);
 
+/* transform_binned (pipeline.py:214-235): bin3 (noise.py:55-71) -- factor x factor block sums with
+ * bottom/right replicate padding -> yb (ceil(H/f), ceil(W/f)); unbin_bilinear (noise.py:98-113) --
+ * divide by f^2, corner-aligned bilinear upsampling to the padded size, crop to (H, W).  fp64. */
+int foe_bin(const double *y, double *yb, int H, int W, int factor, void *stream);
+int foe_unbin_bilinear(const double *xb, double *out, int h, int w, int H, int W, int factor,
+                       void *stream);
+
 /* ---- operators ---------------------------------------------------------------------------------
  * convolve_same (image.py:37-58) / convolve_adjoint (image.py:68-83) with filter `index` of the
  * bank, B images of H x W.  Reference-operator surface for tests; the solve uses the fused pass. */
@@ -127,6 +134,10 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfg, int B, int H, int
  * the last foe_solve in `workspace` without changing it (decisions suppressed). */
 int foe_bench_trial_pass(const foe_bank *bank, int B, int H, int W, int trace_cap, int reps,
                          void *workspace, size_t workspace_bytes, void *stream);
+/* diagnostics: one such pass recording per-CTA %globaltimer [start, end-of-compute, exit] (ns) into
+ * device `times` (3 x CTAs) */
+int foe_debug_pass_times(const foe_bank *bank, int B, int H, int W, int trace_cap, void *workspace,
+                         size_t workspace_bytes, unsigned long long *times, void *stream);
 
 
 /* ---- row-band decomposition (BASELINE config 5; reference has none) -------

@@ -286,13 +286,56 @@ def select_lambda(peak, variant, table, force_branch=None) -> float:
     return float(np.exp(np.interp(np.log(p), np.log(peaks), np.log(lams))))
 
 
+def bin3(img, factor=BIN_FACTOR):
+    """noise.py:55-71: factor x factor block sums, bottom/right edge-replicate padding."""
+    img = np.asarray(img, dtype=np.float64)
+    if factor == 1:
+        return img.copy()
+    h, w = img.shape
+    img = np.pad(img, ((0, (-h) % factor), (0, (-w) % factor)), mode="edge")
+    return img.reshape(img.shape[0] // factor, factor, img.shape[1] // factor, factor).sum(axis=(1, 3))
+
+
+def unbin_bilinear(img, target_shape, factor=BIN_FACTOR):
+    """noise.py:74-113: divide by factor^2, corner-aligned bilinear upsampling, crop."""
+    img = np.asarray(img, dtype=np.float64)
+    H, W = target_shape
+    if factor == 1 and img.shape == (H, W):
+        return img.copy()
+    Hp, Wp = -(-H // factor) * factor, -(-W // factor) * factor
+    src = img / float(factor ** 2)
+    h, w = src.shape
+    out = np.empty((Hp, Wp))
+    for Y in range(Hp):
+        row = Y * (h - 1.0) / (Hp - 1.0) if (h > 1 and Hp > 1) else 0.0
+        i0 = min(int(row), h - 2) if h > 1 else 0
+        di = row - i0 if h > 1 else 0.0
+        i1 = min(i0 + 1, h - 1)
+        for X in range(Wp):
+            col = X * (w - 1.0) / (Wp - 1.0) if (w > 1 and Wp > 1) else 0.0
+            j0 = min(int(col), w - 2) if w > 1 else 0
+            dj = col - j0 if w > 1 else 0.0
+            j1 = min(j0 + 1, w - 1)
+            top = src[i0, j0] + (src[i0, j1] - src[i0, j0]) * dj
+            bot = src[i1, j0] + (src[i1, j1] - src[i1, j0]) * dj
+            out[Y, X] = top + (bot - top) * di
+    return out[:H, :W]
+
+
 def denoise(noisy, peak, model: OracleModel, variant, table, lam="auto", zero_offset_c=0.1,
-            force_branch=None, rel_tol=1e-6, max_iters=None):
+            force_branch=None, rel_tol=1e-6, max_iters=None, bin_factor=BIN_FACTOR):
     """denoise_transform / denoise_direct (pipeline.py:152-211) on the C oracle.
 
     max_iters=None applies solver_budget (pipeline.py:83-87); an explicit value
     bypasses it (the truncated-oracle mode of SURVEY.md Appendix B)."""
     noisy = _c(noisy)
+    if variant == "transform_binned":  # pipeline.py:214-235
+        f = int(bin_factor)
+        inner = denoise(bin3(noisy, f), float(f ** 2) * peak, model, "transform", table, lam, zero_offset_c,
+                        force_branch, rel_tol, max_iters)
+        inner["image"] = unbin_bilinear(inner["image"], noisy.shape, f)
+        inner["peak_used"] = float(f ** 2) * peak
+        return inner
     lam_v = select_lambda(peak, variant, table, force_branch) if lam == "auto" else float(lam)
     iters = solver_budget(peak) if max_iters is None else int(max_iters)
     if variant == "direct":

@@ -94,6 +94,9 @@ def lib():
     L.foe_anscombe_inverse_exact_unbiased.argtypes = [_vp, _vp, _i64, _vp, _vp]
     L.foe_prox_quadratic.argtypes = [_vp, _vp, _vp, ctypes.c_double, _i64, _vp]
     L.foe_prox_idiv.argtypes = [_vp, _vp, _vp, ctypes.c_double, _i64, _vp]
+    L.foe_bin.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp]
+    L.foe_unbin_bilinear.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     _vp]
     L.foe_convolve_same.argtypes = [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp]
     L.foe_convolve_adjoint.argtypes = L.foe_convolve_same.argtypes
     L.foe_eval_workspace_size.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
@@ -106,6 +109,8 @@ def lib():
                             _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int, _vp, ctypes.c_size_t, _vp]
     L.foe_bench_trial_pass.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        _vp, ctypes.c_size_t, _vp]
+    L.foe_debug_pass_times.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                       ctypes.c_size_t, _vp, _vp]
     _lib = L
     return L
 
@@ -122,8 +127,8 @@ def check(rc: int, what: str = "") -> int:
 EXPORTED_SYMBOLS = [
     "foe_abi_version", "foe_last_error", "foe_device_sm_count", "foe_kernel_launch_count", "foe_bank_create", "foe_bank_destroy",
     "foe_bank_info", "foe_anscombe_forward", "foe_direct_obs", "foe_anscombe_inverse_exact_unbiased",
-    "foe_prox_quadratic", "foe_prox_idiv", "foe_convolve_same", "foe_convolve_adjoint",
+    "foe_prox_quadratic", "foe_prox_idiv", "foe_bin", "foe_unbin_bilinear", "foe_convolve_same", "foe_convolve_adjoint",
     "foe_eval_workspace_size", "foe_energy_grad", "foe_solve_workspace_size", "foe_solve",
-    "foe_bench_trial_pass", "foe_tile_grid", "foe_band_geometry", "foe_band_describe", "foe_band_workspace_size",
+    "foe_bench_trial_pass", "foe_debug_pass_times", "foe_tile_grid", "foe_band_geometry", "foe_band_describe", "foe_band_workspace_size",
     "foe_band_buffers_get", "foe_band_begin", "foe_band_trial", "foe_band_commit", "foe_band_end",
 ]

@@ -79,6 +79,7 @@ struct PassArgs {
     int Hl;     // local rows per image (plane stride = Hl * W)
     int band;   // 1: write partials only, decisions by k_decide after the all-gather
     unsigned *grid_bar;  // resident solver: [0] arrival count, [1] generation
+    unsigned long long *dbg_times;  // optional per-CTA [start, end-of-compute, exit] %globaltimer (ns)
     size_t plane;  // B*H*W: distance between state slots
     const float *kf;     // (n, M*M) flipped taps (correlation orientation of the forward conv)
     const float *alpha;  // (n)
@@ -364,6 +365,51 @@ __global__ void k_gather_final(const float *__restrict__ U, size_t plane, const 
         dst[i] = src[i];
 }
 
+
+
+// ------------------------------------------------------------------------------------------------
+// transform_binned (pipeline.py:214-235): bin3 and unbin_bilinear (noise.py:55-113)
+
+// sum of factor x factor blocks, bottom/right replicate-padded (noise.py:55-71); exact for counts
+__global__ void k_bin(const double *__restrict__ y, double *__restrict__ yb, int H, int W, int f, int Hb, int Wb) {
+    const int64_t n = (int64_t)Hb * Wb;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / Wb), c = (int)(i - (int64_t)r * Wb);
+        double s = 0.0;
+        for (int a = 0; a < f; ++a) {
+            const double *row = y + (size_t)min(r * f + a, H - 1) * W;
+            for (int b = 0; b < f; ++b) s += row[min(c * f + b, W - 1)];
+        }
+        yb[i] = s;
+    }
+}
+
+// divide by factor^2, corner-aligned bilinear upsampling to the padded size, crop (noise.py:74-113)
+__global__ void k_unbin(const double *__restrict__ xb, double *__restrict__ out, int h, int w, int H, int W, int f) {
+    const int Hp = (H + f - 1) / f * f, Wp = (W + f - 1) / f * f;
+    const double inv = 1.0 / (double)(f * f);
+    const int64_t n = (int64_t)H * W;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int Y = (int)(i / W), X = (int)(i - (int64_t)Y * W);
+        int i0 = 0, j0 = 0;
+        double di = 0.0, dj = 0.0;
+        if (h > 1) {
+            const double row = Hp > 1 ? (double)Y * ((double)(h - 1) / (double)(Hp - 1)) : 0.0;
+            i0 = min((int)row, h - 2);
+            di = row - i0;
+        }
+        if (w > 1) {
+            const double col = Wp > 1 ? (double)X * ((double)(w - 1) / (double)(Wp - 1)) : 0.0;
+            j0 = min((int)col, w - 2);
+            dj = col - j0;
+        }
+        const int i1 = min(i0 + 1, h - 1), j1 = min(j0 + 1, w - 1);
+        const double tl = xb[(size_t)i0 * w + j0] * inv, tr = xb[(size_t)i0 * w + j1] * inv;
+        const double bl = xb[(size_t)i1 * w + j0] * inv, br = xb[(size_t)i1 * w + j1] * inv;
+        const double top = tl + (tr - tl) * dj, bot = bl + (br - bl) * dj;
+        out[i] = top + (bot - top) * di;
+    }
+}
 
 // ------------------------------------------------------------------------------------------------
 // row-band decomposition (BASELINE config 5): decisions after the partials all-gather, halo rows
@@ -907,6 +953,21 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     return any_fail ? fail(FOE_E_NUMERICAL, "numerical failure in at least one image") : FOE_OK;
 }
 
+int foe_debug_pass_times(const foe_bank *bank, int B, int H, int W, int trace_cap, void *workspace,
+                         size_t workspace_bytes, unsigned long long *times, void *stream) {
+    int rc = check_dims(bank, B, H, W);
+    if (rc) return rc;
+    const SolveLayout L = solve_layout(bank->m, B, H, W, trace_cap);
+    if (workspace_bytes < L.total) return fail(FOE_E_INVALID, "workspace too small");
+    foe_solver_cfg cfg{0.8, 1.0, 1.2, 1.05, 1e-6, 1e15};
+    PassArgs a{};
+    fill_solve_args(a, bank, cfg, B, H, W, trace_cap, (char *)workspace, L);
+    a.mode = MODE_TRIAL;
+    a.no_decide = 1;
+    a.dbg_times = times;
+    return launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, (cudaStream_t)stream);
+}
+
 int foe_bench_trial_pass(const foe_bank *bank, int B, int H, int W, int trace_cap, int reps, void *workspace,
                          size_t workspace_bytes, void *stream) {
     int rc = check_dims(bank, B, H, W);
@@ -1079,6 +1140,24 @@ int foe_band_end(const foe_bank *bank, const foe_band_desc *d, int trace_cap, vo
         any_fail |= hc[b].status != 0;
     }
     return any_fail ? fail(FOE_E_NUMERICAL, "numerical failure in at least one image") : FOE_OK;
+}
+
+
+int foe_bin(const double *y, double *yb, int H, int W, int factor, void *stream) {
+    if (factor < 1 || H < 1 || W < 1) return fail(FOE_E_INVALID, "bad bin arguments");
+    const int Hb = (H + factor - 1) / factor, Wb = (W + factor - 1) / factor;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_bin<<<grid_1d((int64_t)Hb * Wb), 256, 0, (cudaStream_t)stream>>>(y, yb, H, W, factor, Hb, Wb);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_unbin_bilinear(const double *xb, double *out, int h, int w, int H, int W, int factor, void *stream) {
+    if (factor < 1 || h < 1 || w < 1 || H < h || W < w) return fail(FOE_E_INVALID, "bad unbin arguments");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_unbin<<<grid_1d((int64_t)H * W), 256, 0, (cudaStream_t)stream>>>(xb, out, h, w, H, W, factor);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
 }
 
 }  // extern "C"

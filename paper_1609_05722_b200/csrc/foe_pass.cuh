@@ -48,6 +48,12 @@ struct PassCfg {
 
 constexpr int kResidentMaxB = 8;  // images per resident solve (control blocks kept in smem)
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {  // MUFU.RCP, no denormal fix-up
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -519,6 +525,8 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
 
     const int tid = threadIdx.x;
     const int b = blockIdx.y;
+    const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3] = globaltimer_ns();
     TrialParams p{};
     if (a.mode != MODE_EVAL) {
         const ImgCtl &c = a.ctl[b];
@@ -565,6 +573,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     acc[0] = filter_loop<M, TRIAL, SYM>(a, g, S, s_mbar, phase, gacc);
     fold_and_write<M, SYM>(a, g, S, gacc, gout, nullptr);
 
+    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 1] = globaltimer_ns();
     // per-tile partials, last CTA of the image reduces and decides
     block_reduce<NT>(acc, red, s_sum);
     if (tid < kNumPartials) {
@@ -576,6 +585,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     __syncthreads();
     if (tid == 0) s_last = (atomicAdd(a.tickets + b, 1u) == (unsigned)(nlaunch - 1));
     __syncthreads();
+    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
     if (!s_last) return;
     __threadfence();
     reduce_tiles<NT>(a.partials, a.tiles_x * a.tiles_y, a.B, b, red, s_sum);

@@ -148,6 +148,29 @@ def main():
         print(name, r.branch, r.lam, len(r.trace))
     np.savez_compressed(os.path.join(HERE, "denoise_small.npz"), **out)
 
+    # --- transform_binned (pipeline.py:214-235, noise.py:55-113) -----------------------------------
+    out = {}
+    for name, H, W, seed, peak, fb, bf in [("b_p05", 61, 50, 3, 0.5, None, 3), ("b_p02_quad", 49, 47, 8, 0.2, "quadratic", 3),
+                                           ("b_f1", 30, 31, 9, 1.0, None, 1), ("b_f2", 41, 37, 10, 0.4, None, 2)]:
+        x, y = make_counts(H, W, seed, peak)
+        req = pipeline.DenoiseRequest(noisy=y, peak=peak, model=foe_a, variant="transform_binned", force_branch=fb,
+                                      bin_factor=bf)
+        r = pipeline.denoise(req, cfg)
+        from foepoisson import noise
+        out[f"{name}_noisy"] = y
+        out[f"{name}_clean"] = x
+        out[f"{name}_binned"] = noise.bin3(y, bf)
+        out[f"{name}_image"] = r.image
+        out[f"{name}_trace"] = trace_arrays(r.trace)
+        out[f"{name}_meta"] = np.array([peak, r.lam, H, W, seed, bf, r.peak_used])
+        out[f"{name}_branch"] = np.array(r.branch)
+        up = noise.unbin_bilinear(r.transformed, (H, W), bf)
+        out[f"{name}_unbin_of_transformed"] = up
+        print(name, r.branch, r.lam, len(r.trace), r.peak_used)
+    np.savez_compressed(os.path.join(HERE, "binned.npz"), **out)
+
+    if os.environ.get("GOLDEN_SKIP_CFG1"):
+        return
     # --- BASELINE config 1 at full size (256^2, peak 4, quadratic forced, foe_a) ----------------
     x, y = make_counts(256, 256, 0, 4.0)
     req = pipeline.DenoiseRequest(noisy=y, peak=4.0, model=foe_a, variant="transform", force_branch="quadratic")

@@ -295,3 +295,17 @@ def test_resident_solver_equals_per_pass_launches_bitwise(monkeypatch, shape, pe
     np.testing.assert_array_equal(a.image, b.image)
     assert a.trace.L == b.trace.L and a.trace.F == b.trace.F and a.trace.G == b.trace.G
     assert a.trace.n_trials == b.trace.n_trials
+
+
+def test_transform_binned_vs_reference_golden(golden):
+    """transform_binned on the device (bin3 / unbin kernels around the solve) vs the reference output."""
+    g = golden("binned")
+    model = fp.load_packaged_model("foe_a")
+    for name, fbr in (("b_p05", None), ("b_p02_quad", "quadratic"), ("b_f1", None), ("b_f2", None)):
+        meta = g[f"{name}_meta"]
+        peak = meta[0]
+        r = fp.denoise(fp.DenoiseRequest(noisy=g[f"{name}_noisy"], peak=peak, model=model, variant="transform_binned",
+                                         force_branch=fbr, bin_factor=int(meta[5])), fp.SolverConfig(rel_tol=0.0))
+        assert r.branch == str(g[f"{name}_branch"]) and r.peak_used == meta[6]
+        assert r.image.shape == g[f"{name}_image"].shape
+        _check_solve(r.image, g[f"{name}_image"], peak, g[f"{name}_clean"], name)

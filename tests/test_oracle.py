@@ -113,3 +113,20 @@ def test_cfg1_full_size_matches_reference(golden):
     res = orc.denoise(y, 4.0, fa, "transform", table, force_branch="quadratic", rel_tol=0.0)
     np.testing.assert_allclose(res["trace"].L, g["trace"][:, 2], rtol=1e-13)
     assert np.max(np.abs(res["image"] - g["image"])) <= 1e-5 * 4.0   # golden stored as float32
+
+
+def test_binned_matches_reference(golden):
+    """transform_binned (pipeline.py:214-235) incl. bin3/unbin_bilinear (noise.py:55-113)."""
+    g = golden("binned")
+    table = orc.load_lambda_table(os.path.join(ASSETS, "lambda_table.json"))
+    fa = orc.read_foe(os.path.join(ASSETS, "foe_a.foe"))
+    for name, fbr in (("b_p05", None), ("b_p02_quad", "quadratic"), ("b_f1", None), ("b_f2", None)):
+        meta = g[f"{name}_meta"]
+        np.testing.assert_array_equal(orc.bin3(g[f"{name}_noisy"], int(meta[5])), g[f"{name}_binned"])
+        res = orc.denoise(g[f"{name}_noisy"], meta[0], fa, "transform_binned", table, force_branch=fbr,
+                          rel_tol=0.0, bin_factor=int(meta[5]))
+        assert res["branch"] == str(g[f"{name}_branch"]) and res["peak_used"] == meta[6]
+        np.testing.assert_allclose(res["trace"].L, g[f"{name}_trace"][:, 2], rtol=1e-13)
+        np.testing.assert_allclose(res["image"], g[f"{name}_image"], rtol=0, atol=1e-8 * meta[0])
+        np.testing.assert_allclose(orc.unbin_bilinear(res["transformed"], g[f"{name}_noisy"].shape, int(meta[5])),
+                                   g[f"{name}_unbin_of_transformed"], rtol=1e-13, atol=1e-13)

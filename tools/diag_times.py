@@ -1,0 +1,36 @@
+"""Per-CTA timing of one fused trial pass (512^2 cfg2 state after a solve): start skew, compute, tail."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1609_05722_b200 as fp  # noqa: E402
+from paper_1609_05722_b200 import _lib  # noqa: E402
+from paper_1609_05722_b200.anscombe import forward_device  # noqa: E402
+from paper_1609_05722_b200.synth import make_counts  # noqa: E402
+
+H = W = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+model = fp.load_packaged_model("foe_a")
+_, y = make_counts(H, W, 0, 1.0)
+v = forward_device(torch.from_numpy(y).cuda())
+res = fp.solve_device(model, v, v, 0.6075, "quadratic", 150, fp.SolverConfig(rel_tol=0.0))
+L = _lib.lib()
+ws = res._workspace
+ncta = (-(-H // 32)) * (-(-W // 60))
+t = torch.zeros(ncta * 3, dtype=torch.int64, device="cuda")
+for _ in range(3):
+    _lib.check(L.foe_debug_pass_times(res._bank.handle, 1, H, W, res._cap, ws.data_ptr(), ws.numel(), t.data_ptr(),
+                                      torch.cuda.current_stream().cuda_stream))
+torch.cuda.synchronize()
+a = t.cpu().numpy().reshape(ncta, 3).astype(np.float64)
+a -= a[:, 0].min()
+start, comp, end = a[:, 0] / 1e3, a[:, 1] / 1e3, a[:, 2] / 1e3
+dur = comp - start
+print(f"CTAs {ncta}: start skew max {start.max():.2f} us; compute dur min/med/max {dur.min():.2f}/"
+      f"{np.median(dur):.2f}/{dur.max():.2f} us; last compute end {comp.max():.2f}; last exit {end.max():.2f} us")
+ty, tx = -(-H // 32), -(-W // 60)
+grid = dur.reshape(ty, tx)
+np.set_printoptions(precision=1, suppress=True, linewidth=200)
+print(grid)
