@@ -134,6 +134,9 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfg, int B, int H, int
  * the last foe_solve in `workspace` without changing it (decisions suppressed). */
 int foe_bench_trial_pass(const foe_bank *bank, int B, int H, int W, int trace_cap, int reps,
                          void *workspace, size_t workspace_bytes, void *stream);
+/* diagnostics: the tcgen05 / TMEM primitives of the tensor-core pass on one 128 x 32 x 32 product,
+ * D = A . B^T in 3xTF32 (A: 128 x 32, B: 32 x 32 row-major fp32 device arrays) */
+int foe_tc_selftest(const float *A, const float *B, float *D, void *stream);
 /* diagnostics: one such pass recording per-CTA %globaltimer [start, end-of-compute, exit] (ns) into
  * device `times` (3 x CTAs) */
 int foe_debug_pass_times(const foe_bank *bank, int B, int H, int W, int trace_cap, void *workspace,

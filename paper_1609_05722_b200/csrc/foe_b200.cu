@@ -253,6 +253,7 @@ __device__ void reduce_tiles(const double *partials, int ntiles, int B, int b, d
 }
 
 #include "foe_pass.cuh"
+#include "foe_tc.cuh"
 
 // ------------------------------------------------------------------------------------------------
 // elementwise kernels
@@ -1156,6 +1157,14 @@ int foe_unbin_bilinear(const double *xb, double *out, int h, int w, int H, int W
     if (factor < 1 || h < 1 || w < 1 || H < h || W < w) return fail(FOE_E_INVALID, "bad unbin arguments");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     k_unbin<<<grid_1d((int64_t)H * W), 256, 0, (cudaStream_t)stream>>>(xb, out, h, w, H, W, factor);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+
+int foe_tc_selftest(const float *A, const float *B, float *D, void *stream) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_tc_selftest<<<1, 128, 0, (cudaStream_t)stream>>>(A, B, D);
     FOE_CUDA(cudaGetLastError());
     return FOE_OK;
 }

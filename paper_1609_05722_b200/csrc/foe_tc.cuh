@@ -1,0 +1,167 @@
+// foe_tc.cuh -- tcgen05 / TMEM primitives for the tensor-core FoE pass (included by foe_b200.cu).
+//
+// Operand conventions used by the implicit-GEMM pass:
+//  * A (M = 128 pixels x K) lives in TMEM: lane = pixel, one fp32/tf32 element per column.  Written
+//    by the owning thread with tcgen05.st (32x32b), no shared-memory staging (the "TS" MMA form).
+//  * B (N x K, K-major) lives in shared memory in the SWIZZLE_NONE canonical layout: core matrices
+//    of 8 rows x 16 bytes, 8-row groups SBO bytes apart, 16-byte K chunks LBO bytes apart.
+//  * D (128 x N fp32) in TMEM, read back with tcgen05.ld 32x32b (thread = pixel, register = column).
+//  * fp32 accuracy from tf32 units: x = hi + lo with hi = x truncated to tf32, lo = x - hi (exact);
+//    A.B ~= A_hi.B_hi + A_lo.B_hi + A_hi.B_lo (3xTF32, the A_lo.B_lo term is below fp32 rounding).
+
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// tcgen05.alloc by one full warp; the allocated base address is written to *slot (shared memory)
+__device__ __forceinline__ void tmem_alloc(uint32_t *slot, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t base, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(ncols) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 32 consecutive columns of this warp's 32 lanes: thread t <-> lane (32*(warp%4) + t)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+        "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+        "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
+          "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15]), "=f"(v[16]),
+          "=f"(v[17]), "=f"(v[18]), "=f"(v[19]), "=f"(v[20]), "=f"(v[21]), "=f"(v[22]), "=f"(v[23]), "=f"(v[24]),
+          "=f"(v[25]), "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_NONE (sm_100 "version 1" format)
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1u << 46;  // version
+    // base_offset 0, lbo_mode 0, layout_type 0 (SWIZZLE_NONE)
+    return d;
+}
+
+// instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]^T   (one K = 8 slice)
+__device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+        : "memory");
+}
+
+// arrive on an mbarrier when all previously issued tcgen05.mma of this thread have completed
+__device__ __forceinline__ void umma_commit(unsigned long long *mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+                 : "memory");
+}
+
+// B operand (N rows x K cols, K-major) element offset in floats within the SWIZZLE_NONE layout with
+// SBO = 128 B (8-row groups contiguous) and LBO = (N/8) * 128 B (next 16-byte K chunk)
+template <int N>
+__device__ __forceinline__ int bsw_offset(int n, int k) {
+    return (n & 7) * 4 + (k & 3) + (n >> 3) * 32 + (k >> 2) * (N / 8) * 32;
+}
+
+// 3xTF32 product of one 128 x K (TMEM) by N x K (smem) pair, K = 8 * nk; a_hi/a_lo are TMEM column
+// bases of the split A, b_hi/b_lo shared addresses of the split B.  Issued by one thread.
+template <int N>
+__device__ __forceinline__ void umma_3xtf32(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi, uint32_t b_lo,
+                                            int nk, bool accumulate) {
+    constexpr uint32_t LBO = (N / 8) * 128, SBO = 128;
+    const uint32_t idesc = idesc_tf32(128, N);
+    for (int j = 0; j < nk; ++j) {
+        const uint64_t dh = umma_desc_kmajor(b_hi + 2 * j * LBO, LBO, SBO);
+        const uint64_t dl = umma_desc_kmajor(b_lo + 2 * j * LBO, LBO, SBO);
+        umma_tf32_ts(d_tmem, a_hi + 8 * j, dh, idesc, (accumulate || j > 0) ? 1u : 0u);
+        umma_tf32_ts(d_tmem, a_lo + 8 * j, dh, idesc, 1u);
+        umma_tf32_ts(d_tmem, a_hi + 8 * j, dl, idesc, 1u);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// self-test: D (128 x 32) = A (128 x 32) . B (32 x 32)^T through the exact primitives of the pass
+
+__global__ void __launch_bounds__(128) k_tc_selftest(const float *__restrict__ A, const float *__restrict__ B,
+                                                     float *__restrict__ D) {
+    __shared__ __align__(128) float sB[2][32 * 32];
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) tmem_alloc(&s_tmem, 128);
+    if (tid == 0) mbar_init(&s_mbar, 1);
+    for (int e = tid; e < 32 * 32; e += 128) {
+        const int n = e / 32, k = e % 32;
+        const float x = B[e];
+        const float h = tf32_hi(x);
+        sB[0][bsw_offset<32>(n, k)] = h;
+        sB[1][bsw_offset<32>(n, k)] = x - h;
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = s_tmem;
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    {
+        float hi[32], lo[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const float x = A[tid * 32 + k];
+            hi[k] = tf32_hi(x);
+            lo[k] = x - hi[k];
+        }
+        tmem_st32(tbase + lane_base + 0, hi);   // A_hi: columns [0, 32)
+        tmem_st32(tbase + lane_base + 32, lo);  // A_lo: columns [32, 64)
+    }
+    tc_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+        tc_fence_after();
+        umma_3xtf32<32>(tbase + 64, tbase + 0, tbase + 32, smem_u32(sB[0]), smem_u32(sB[1]), 4, false);
+        umma_commit(&s_mbar);
+    }
+    mbar_wait(&s_mbar, 0);
+    tc_fence_after();
+    float d[32];
+    tmem_ld32(tbase + lane_base + 64, d);
+    tc_wait_ld();
+#pragma unroll
+    for (int n = 0; n < 32; ++n) D[tid * 32 + n] = d[n];
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tbase, 128);
+}

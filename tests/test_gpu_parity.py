@@ -309,3 +309,21 @@ def test_transform_binned_vs_reference_golden(golden):
         assert r.branch == str(g[f"{name}_branch"]) and r.peak_used == meta[6]
         assert r.image.shape == g[f"{name}_image"].shape
         _check_solve(r.image, g[f"{name}_image"], peak, g[f"{name}_clean"], name)
+
+
+def test_tcgen05_primitives_selftest():
+    """TMEM alloc / tcgen05.st / TS-form MMA with the hand-built K-major descriptor / commit / tcgen05.ld:
+    3xTF32 product matches fp64 to ~fp32 accuracy."""
+    import torch
+    from paper_1609_05722_b200 import _lib
+    rng = np.random.default_rng(3)
+    A = rng.normal(size=(128, 32)).astype(np.float32)
+    B = rng.normal(size=(32, 32)).astype(np.float32)
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    Dd = torch.zeros((128, 32), dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().foe_tc_selftest(Ad.data_ptr(), Bd.data_ptr(), Dd.data_ptr(),
+                                          torch.cuda.current_stream().cuda_stream))
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    got = Dd.cpu().numpy()
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err < 1e-6, err
