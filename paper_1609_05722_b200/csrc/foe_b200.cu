@@ -60,6 +60,7 @@ constexpr int kMaxTaps = 4096;
 constexpr int kMaxFilters = 512;
 constexpr int kNumPartials = 7;  // dF|F, sq, gd, |u|^2, G_a, G_b, G_bad
 constexpr int kPartialStride = 8;
+constexpr bool kTcDefault = false;  // tensor-core pass on by default once validated
 
 enum PassMode { MODE_EVAL = 0, MODE_INIT = 1, MODE_TRIAL = 2 };
 
@@ -254,6 +255,7 @@ __device__ void reduce_tiles(const double *partials, int ntiles, int B, int b, d
 
 #include "foe_pass.cuh"
 #include "foe_tc.cuh"
+#include "foe_pass_tc.cuh"
 
 // ------------------------------------------------------------------------------------------------
 // elementwise kernels
@@ -520,8 +522,38 @@ int launch_pass_m(int m, const PassArgs &a, cudaStream_t st) {
     }
 }
 
+// tensor-core pass (k_pass_tc): 5x5 banks with <= 32 filters; FOE_TC=0 forces the FFMA pass
+bool use_tc(int m, int nf) {
+    const char *e = getenv("FOE_TC");
+    const int env = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 1 : 2;
+    return env != 0 && m == 5 && nf <= 32 && (env == 1 || kTcDefault);
+}
+
+template <bool TRIAL, bool SYM>
+int launch_pass_tc_t(const PassArgs &a, cudaStream_t st) {
+    using T = TcCfg<32>;
+    // >= 116 KB keeps one CTA per SM: the 512 TMEM columns it allocates are the whole SM's
+    const size_t smem = std::max<size_t>(sizeof(float) * tc_smem_floats<32>(), 116 * 1024);
+    static unsigned long long configured = 0;
+    int dev = 0;
+    FOE_CUDA(cudaGetDevice(&dev));
+    if (!(configured >> (dev & 63) & 1ull)) {
+        FOE_CUDA(cudaFuncSetAttribute(k_pass_tc<TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured |= 1ull << (dev & 63);
+    }
+    dim3 grid(a.tiles_x * a.tiles_yl, a.B);
+    k_pass_tc<TRIAL, SYM><<<grid, T::NT, smem, st>>>(a);
+    FOE_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return FOE_OK;
+}
+
 int launch_pass(int m, bool sym, const PassArgs &a, cudaStream_t st) {
     const bool trial = a.mode == MODE_TRIAL;
+    if (use_tc(m, a.n_filters)) {
+        if (trial) return sym ? launch_pass_tc_t<true, true>(a, st) : launch_pass_tc_t<true, false>(a, st);
+        return sym ? launch_pass_tc_t<false, true>(a, st) : launch_pass_tc_t<false, false>(a, st);
+    }
     if (trial) return sym ? launch_pass_m<true, true>(m, a, st) : launch_pass_m<true, false>(m, a, st);
     return sym ? launch_pass_m<false, true>(m, a, st) : launch_pass_m<false, false>(m, a, st);
 }

@@ -1,0 +1,344 @@
+// foe_pass_tc.cuh -- tensor-core (tcgen05, 3xTF32) variant of the fused FoE pass for 5x5 banks
+// with at most 32 filters (included by foe_b200.cu after foe_pass.cuh / foe_tc.cuh).
+//
+// Same tile geometry, prologue, fold and reductions as k_pass; the two convolutions become
+// implicit GEMMs on the tensor cores, one 128-pixel block (two region rows) at a time:
+//   forward   Z  = A_u  . Kf^T    A_u[p][t] = u_new(p + off_t)  (im2col, K = 25 -> 32), N = filters
+//             dZ = A_du . Kf^T    (the same for du, for the energy change)
+//   adjoint   Y  = Psi  . Kt^T    Psi[p][f] = z/(1+z^2), Kt[t][f] = 2 a_f k_f[t], N = taps
+//             g(q) = sum_t Y(q + off_t)[t]       (25-term shifted sum on the CUDA cores)
+// A operands are written by their pixel's thread straight into TMEM (tcgen05.st), B operands sit in
+// shared memory, D accumulators in TMEM.  fp32 accuracy from tf32 units via the 3xTF32 split.
+// Two warpgroups alternate blocks so one builds operands / evaluates the pointwise terms while the
+// other's MMAs run.
+
+template <int NF_MAX>
+struct TcCfg {
+    using P = PassCfg<5>;
+    static constexpr int R = 2, M = 5, KT = 25;
+    static constexpr int RH = P::RH, RW = P::RW, SH = P::SH, SW = P::SW, PLANE = P::PLANE;
+    static constexpr int NBLK = RH * RW / 128;       // 128-pixel blocks (two region rows each)
+    static constexpr int NWG = 2, NT = 128 * NWG;    // warpgroups x 128 threads
+    static constexpr int YROWS = 8, YW = RW + 4;     // Y ring: 8 region rows, 2 zero columns each side
+    static constexpr int BSZ = 32 * 32;              // one 32 x 32 B operand (floats)
+    // TMEM columns per warpgroup: A_u hi/lo, A_du hi/lo (reused for Psi hi/lo), D_z (reused for
+    // D_y), D_dz
+    static constexpr int C_AUH = 0, C_AUL = 32, C_ADH = 64, C_ADL = 96, C_DZ = 128, C_DDZ = 160, C_WG = 256;
+    static_assert(RW == 64 && NBLK * 128 == RH * RW, "blocks of two 64-pixel region rows");
+    static_assert(NF_MAX <= 32, "one N = 32 MMA covers the bank");
+};
+
+template <int NF_MAX>
+__host__ __device__ constexpr size_t tc_smem_floats() {
+    using T = TcCfg<NF_MAX>;
+    // Un, Du staged planes; Kf hi/lo, Kt hi/lo; Y ring; region gradient
+    return 2 * (size_t)T::PLANE + 4 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + (size_t)T::RH * T::RW;
+}
+
+template <bool TRIAL, bool SYM>
+__global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) {
+    using T = TcCfg<32>;
+    using C = PassCfg<5>;
+    constexpr int NT = T::NT, R = T::R, SW = T::SW;
+    extern __shared__ __align__(128) float sm[];
+    __shared__ double red[NT / 32][kNumPartials];
+    __shared__ double s_sum[kNumPartials];
+    __shared__ int s_last;
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) unsigned long long s_mma[T::NWG];       // MMA completion, per warpgroup
+    __shared__ __align__(8) unsigned long long s_ready[T::NBLK];    // Y of block j in the ring
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int wg = tid >> 7, wt = tid & 127;  // warpgroup, thread in warpgroup (= TMEM lane)
+    const int b = blockIdx.y;
+    const int nf = a.n_filters;
+    TrialParams p{};
+    if (a.mode != MODE_EVAL) {
+        const ImgCtl &c = a.ctl[b];
+        if (c.done && !a.no_decide) return;
+        p = trial_params(a, c);
+    }
+    const size_t ioff = (size_t)b * a.Hl * a.W;
+    const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
+    float *gout, *uout = nullptr;
+    if (a.mode == MODE_EVAL) {
+        uin = a.u_in + ioff;
+        gout = a.g_out + ioff;
+    } else {
+        uin = a.U + p.iu * a.plane + ioff;
+        if (TRIAL) {
+            upv = a.U + p.iup * a.plane + ioff;
+            gin = a.Gs + p.ig * a.plane + ioff;
+            obs = a.obs + ioff;
+            uout = a.U + p.inew * a.plane + ioff;
+            gout = a.Gs + p.ignew * a.plane + ioff;
+        } else {
+            gout = a.Gs + p.ig * a.plane + ioff;
+        }
+    }
+    const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
+    const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
+
+    float *Un = sm;
+    float *Du = Un + T::PLANE;
+    float *Kf = Du + T::PLANE;     // [hi | lo], forward B (N = filters, K = taps)
+    float *Kt = Kf + 2 * T::BSZ;   // [hi | lo], adjoint B (N = taps, K = filters)
+    float *Yr = Kt + 2 * T::BSZ;   // Y ring [tap][ring row][YW]
+    float *Gr = Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold)
+
+    if (warp == 0) tmem_alloc(&s_tmem, 512);
+    if (tid < T::NWG) mbar_init(&s_mma[tid], 1);
+    if (tid < T::NBLK) mbar_init(&s_ready[tid], 128);
+    // B operands: Kf[f][t] = kf_f[t] (convolution orientation), Kt[t][f] = 2 a_f k_f[t] with the
+    // unflipped k_f[t] = kf_f[24 - t]; zero padding to 32 x 32; split into tf32 hi + fp32 lo
+    for (int e = tid; e < 32 * 32; e += NT) {
+        const int n = e >> 5, k = e & 31;
+        const float vf = (n < nf && k < T::KT) ? a.kf[n * T::KT + k] : 0.0f;
+        const float vt = (k < nf && n < T::KT) ? 2.0f * a.alpha[k] * a.kf[k * T::KT + (T::KT - 1 - n)] : 0.0f;
+        const float hf = tf32_hi(vf), ht = tf32_hi(vt);
+        Kf[bsw_offset<32>(n, k)] = hf;
+        Kf[T::BSZ + bsw_offset<32>(n, k)] = vf - hf;
+        Kt[bsw_offset<32>(n, k)] = ht;
+        Kt[T::BSZ + bsw_offset<32>(n, k)] = vt - ht;
+    }
+    // zero columns of the Y ring (padded positions outside the region)
+    for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {
+        const int col = e & 3, rr = e >> 2;
+        Yr[rr * T::YW + (col < 2 ? col : T::YW - 4 + col)] = 0.0f;
+    }
+    const float shift = a.zero_mean ? __ldg(uin + (size_t)(g.s0 - a.lrow0) * a.W + g.c0) : 0.0f;
+    double acc[kNumPartials];
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
+    // prologue: stage u_new - shift and du for the region + r ring (cells strided by NT here)
+    for (int k = tid; k < C::NCELL; k += NT) {
+        const int i = k / C::CW, j = k - i * C::CW;
+        const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
+        const size_t o = (size_t)(src_idx<SYM>(gy, a.H) - a.lrow0) * a.W + src_idx<SYM>(gx, a.W);
+        if (!TRIAL) {
+            Un[i * SW + j] = __ldg(uin + o) - shift;
+            continue;
+        }
+        const float u = __ldg(uin + o), up = __ldg(upv + o), gg = __ldg(gin + o), ob = __ldg(obs + o);
+        const float ut = (u - p.tau * gg) + p.gam * (u - up);  // solver.py:146-149
+        const float un = (p.branch == FOE_QUADRATIC) ? prox_quad(ut, p.t, ob) : prox_idv(ut, p.t, ob);
+        const float du = un - u;
+        Un[i * SW + j] = un - shift;
+        Du[i * SW + j] = du;
+        if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) {
+            uout[(size_t)(gy - a.lrow0) * a.W + gx] = un;
+            acc[1] += (double)du * (double)du;
+            acc[2] += (double)gg * (double)du;
+            acc[3] += (double)u * (double)u;
+            if (p.branch == FOE_QUADRATIC) {
+                const double d = (double)un - (double)ob;
+                acc[4] += d * d;
+            } else {
+                acc[4] += (double)un;
+                if (ob > 0.0f) {
+                    if (un > 0.0f) acc[5] += (double)ob * (double)logf(un);
+                    else acc[6] += 1.0;
+                }
+            }
+        }
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    const uint32_t tbase = s_tmem + (uint32_t)(wg * T::C_WG);
+    const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+    const uint32_t kf_hi = smem_u32(Kf), kf_lo = smem_u32(Kf + T::BSZ);
+    const uint32_t kt_hi = smem_u32(Kt), kt_lo = smem_u32(Kt + T::BSZ);
+    unsigned mma_phase = 0u;
+    double e_own = 0.0;
+
+    for (int blk = wg; blk < T::NBLK; blk += T::NWG) {
+        const int lr = 2 * blk + (wt >> 6), lc = wt & 63;  // this thread's pixel (region-local)
+        const int gy = g.ry0 + lr, gx = g.rx0 + lc;
+        const bool in_img = !SYM || (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W);
+        const bool owned = gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1;
+        // ---- im2col of u_new (and du) into TMEM: A[p][t] = staged(lr + a, lc + b), t = 5a + b ----
+        {
+            float hi[32], lo[32];
+            const float *src = Un + lr * SW + lc;
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+                const float x = t < T::KT ? src[(t / 5) * SW + (t % 5)] : 0.0f;
+                hi[t] = tf32_hi(x);
+                lo[t] = x - hi[t];
+            }
+            tmem_st32(tbase + lane_off + T::C_AUH, hi);
+            tmem_st32(tbase + lane_off + T::C_AUL, lo);
+            if (TRIAL) {
+                const float *sd = Du + lr * SW + lc;
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    const float x = t < T::KT ? sd[(t / 5) * SW + (t % 5)] : 0.0f;
+                    hi[t] = tf32_hi(x);
+                    lo[t] = x - hi[t];
+                }
+                tmem_st32(tbase + lane_off + T::C_ADH, hi);
+                tmem_st32(tbase + lane_off + T::C_ADL, lo);
+            }
+        }
+        tc_wait_st();
+        tc_fence_before();
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+        if (wt == 0) {
+            tc_fence_after();
+            umma_3xtf32<32>(tbase + T::C_DZ, tbase + T::C_AUH, tbase + T::C_AUL, kf_hi, kf_lo, 4, false);
+            if (TRIAL) umma_3xtf32<32>(tbase + T::C_DDZ, tbase + T::C_ADH, tbase + T::C_ADL, kf_hi, kf_lo, 4, false);
+            umma_commit(&s_mma[wg]);
+        }
+        mbar_wait(&s_mma[wg], mma_phase);
+        mma_phase ^= 1u;
+        tc_fence_after();
+        // ---- pointwise: psi' = z/(1+z^2) (2a_f is in Kt), energy terms ----
+        {
+            float z[32], dz[32];
+            tmem_ld32(tbase + lane_off + T::C_DZ, z);
+            if (TRIAL) tmem_ld32(tbase + lane_off + T::C_DDZ, dz);
+            tc_wait_ld();
+            float e = 0.0f, hi[32], lo[32];
+#pragma unroll
+            for (int f = 0; f < 32; ++f) {
+                if (f < nf) {
+                    const float zz = z[f];
+                    const float q1 = fmaf(zz, zz, 1.0f);
+                    const float ps = in_img ? zz * rcp_approx(q1) : 0.0f;
+                    hi[f] = tf32_hi(ps);
+                    lo[f] = ps - hi[f];
+                    const float al = __ldg(a.alpha + f);
+                    if (TRIAL) {
+                        const float d = dz[f];
+                        const float zo = zz - d;
+                        const float num = d * fmaf(2.0f, zo, d);
+                        const float den = fmaf(zo, zo, q1) + 1.0f;
+                        e = fmaf(al, two_atanh(num * rcp_approx(den)), e);
+                    } else {
+                        e = fmaf(al, log1pf(zz * zz), e);
+                    }
+                } else {
+                    hi[f] = 0.0f;
+                    lo[f] = 0.0f;
+                }
+            }
+            if (owned) e_own += (double)e;
+            tmem_st32(tbase + lane_off + T::C_AUH, hi);
+            tmem_st32(tbase + lane_off + T::C_AUL, lo);
+        }
+        tc_wait_st();
+        tc_fence_before();
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+        if (wt == 0) {
+            tc_fence_after();
+            umma_3xtf32<32>(tbase + T::C_DZ, tbase + T::C_AUH, tbase + T::C_AUL, kt_hi, kt_lo, 4, false);
+            umma_commit(&s_mma[wg]);
+        }
+        mbar_wait(&s_mma[wg], mma_phase);
+        mma_phase ^= 1u;
+        tc_fence_after();
+        // ---- Y rows of this block into the ring ----
+        {
+            float y[32];
+            tmem_ld32(tbase + lane_off + T::C_DZ, y);
+            tc_wait_ld();
+            float *yrow = Yr + (lr % T::YROWS) * T::YW + 2 + lc;
+#pragma unroll
+            for (int t = 0; t < T::KT; ++t) yrow[t * T::YROWS * T::YW] = y[t];
+        }
+        tc_fence_before();
+        mbar_arrive(&s_ready[blk]);
+        // ---- shifted sums for the previous block's rows: g(q) = sum_t Y(q + off_t)[t] ----
+        const int gb = blk - 1;
+        if (gb >= 0) {
+            mbar_wait(&s_ready[gb], 0);
+            if (blk >= 2) mbar_wait(&s_ready[blk - 2], 0);
+            const int r = 2 * gb + (wt >> 6), c = wt & 63;
+            float s = 0.0f;
+#pragma unroll
+            for (int aa = 0; aa < 5; ++aa) {
+                const int rr = r + aa - R;
+                if (rr < 0 || rr >= T::RH) continue;
+                const float *yp = Yr + (rr % T::YROWS) * T::YW + 2 + c - R;
+#pragma unroll
+                for (int bb = 0; bb < 5; ++bb) s += yp[(aa * 5 + bb) * T::YROWS * T::YW + bb];
+            }
+            Gr[r * T::RW + c] = s;
+        }
+    }
+    // the last block's rows (needs no later Y)
+    {
+        constexpr int last = T::NBLK - 1;
+        if (wg == (last % T::NWG)) {
+            mbar_wait(&s_ready[last - 1], 0);
+            const int r = 2 * last + (wt >> 6), c = wt & 63;
+            float s = 0.0f;
+#pragma unroll
+            for (int aa = 0; aa < 5; ++aa) {
+                const int rr = r + aa - R;
+                if (rr < 0 || rr >= T::RH) continue;
+                const float *yp = Yr + (rr % T::YROWS) * T::YW + 2 + c - R;
+#pragma unroll
+                for (int bb = 0; bb < 5; ++bb) s += yp[(aa * 5 + bb) * T::YROWS * T::YW + bb];
+            }
+            Gr[r * T::RW + c] = s;
+        }
+    }
+    acc[0] = e_own;
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(s_tmem, 512);
+
+    // ---- fold padded pixels (symmetric rule) and write the owned gradient ----
+    {
+        const int xx = tid % T::RW;
+        const int gx = g.c0 + xx;
+        if (gx < g.c1) {
+            const int lx = gx - g.rx0;
+            int mx = -1;
+            if (SYM) {
+                if (gx < R) mx = (-1 - gx) - g.rx0;
+                else if (gx >= a.W - R) mx = (2 * a.W - 1 - gx) - g.rx0;
+            }
+            for (int gy = g.s0 + tid / T::RW; gy < g.s1; gy += NT / T::RW) {
+                const int ly = gy - g.ry0;
+                float val = Gr[ly * T::RW + lx];
+                if (SYM) {
+                    int my = -1;
+                    if (gy < R) my = (-1 - gy) - g.ry0;
+                    else if (gy >= a.H - R) my = (2 * a.H - 1 - gy) - g.ry0;
+                    if (my >= 0) val += Gr[my * T::RW + lx];
+                    if (mx >= 0) val += Gr[ly * T::RW + mx];
+                    if (my >= 0 && mx >= 0) val += Gr[my * T::RW + mx];
+                }
+                gout[(size_t)(gy - a.lrow0) * a.W + gx] = val;
+            }
+        }
+    }
+
+    // ---- per-tile partials, last CTA of the image reduces and decides (as k_pass) ----
+    block_reduce<NT>(acc, red, s_sum);
+    if (tid < kNumPartials) {
+        a.partials[((size_t)g.t * a.B + b) * kPartialStride + tid] = s_sum[tid];
+        __threadfence();
+    }
+    if (a.band) return;
+    const int nlaunch = a.tiles_x * a.tiles_y;
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(a.tickets + b, 1u) == (unsigned)(nlaunch - 1));
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    reduce_tiles<NT>(a.partials, a.tiles_x * a.tiles_y, a.B, b, red, s_sum);
+    if (tid == 0) {
+        a.tickets[b] = 0u;
+        if (a.mode == MODE_EVAL) {
+            a.energy_out[b] = s_sum[0];
+        } else if (!a.no_decide) {
+            decide(a, b, s_sum);
+        }
+    }
+}

@@ -327,3 +327,46 @@ def test_tcgen05_primitives_selftest():
     got = Dd.cpu().numpy()
     err = np.abs(got - ref).max() / np.abs(ref).max()
     assert err < 1e-6, err
+
+
+@pytest.mark.parametrize("shape,boundary", [((47, 45), "symmetric"), ((130, 97), "symmetric"), ((512, 512), "symmetric"),
+                                            ((200, 136), "periodic"), ((7, 9), "symmetric")])
+def test_tensor_core_gradient_vs_oracle(monkeypatch, shape, boundary):
+    """k_pass_tc (tcgen05 implicit GEMMs, 3xTF32): fused energy / gradient vs the C oracle."""
+    monkeypatch.setenv("FOE_TC", "1")
+    rng = np.random.default_rng(hash((shape, boundary)) % 2 ** 32)
+    if boundary == "symmetric":
+        model = fp.load_packaged_model("foe_a")
+        u = orc.anscombe_forward(make_counts(*shape, 4, 2.0)[1])
+    else:
+        basis = fp.dct_basis(5)
+        model = fp.FoEModel(basis=basis, betas=rng.normal(scale=0.7, size=(20, basis.n_atoms)),
+                            weights=rng.uniform(0.5, 2, 20), domain_tag="anscombe", boundary=boundary)
+        u = rng.normal(scale=3, size=shape) + 5
+    u = u.astype(np.float32).astype(np.float64)
+    om = oracle_model(model)
+    ref_g, ref_e = orc.foe_gradient(u, om), orc.foe_energy(u, om)
+    assert rel_l2(fp.foe_gradient(u, model), ref_g) <= 1e-5
+    assert abs(fp.foe_energy(u, model) - ref_e) <= 1e-6 * abs(ref_e)
+
+
+@pytest.mark.parametrize("branch", ["quadratic", None])
+def test_tensor_core_solve_cfg2_vs_oracle(monkeypatch, branch):
+    """Config 2 (512^2, peak 1) through the tensor-core pass: parity gates vs the oracle."""
+    monkeypatch.setenv("FOE_TC", "1")
+    model = fp.load_packaged_model("foe_a")
+    x, y = make_counts(512, 512, 0, 1.0)
+    ref = orc.denoise(y, 1.0, oracle_model(model), "transform", TABLE, force_branch=branch, rel_tol=0.0)
+    r = fp.denoise(fp.DenoiseRequest(noisy=y, peak=1.0, model=model, variant="transform", force_branch=branch),
+                   fp.SolverConfig(rel_tol=0.0))
+    assert len(r.trace) == 150
+    _check_solve(r.image, ref["image"], 1.0, x, f"tc cfg2 {branch}")
+
+
+def test_tensor_core_cfg1_vs_reference_golden(monkeypatch, golden):
+    monkeypatch.setenv("FOE_TC", "1")
+    g = golden("cfg1_256")
+    x, y = make_counts(256, 256, 0, 4.0)
+    r = fp.denoise(fp.DenoiseRequest(noisy=y, peak=4.0, model=fp.load_packaged_model("foe_a"),
+                                     variant="transform", force_branch="quadratic"), fp.SolverConfig(rel_tol=0.0))
+    _check_solve(r.image, g["image"].astype(np.float64), 4.0, x, "tc cfg1")
