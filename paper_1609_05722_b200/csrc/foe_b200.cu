@@ -529,20 +529,20 @@ bool use_tc(int m, int nf) {
     return env != 0 && m == 5 && nf <= 32 && (env == 1 || kTcDefault);
 }
 
-template <bool TRIAL, bool SYM>
+template <int NF, bool TRIAL, bool SYM>
 int launch_pass_tc_t(const PassArgs &a, cudaStream_t st) {
     using T = TcCfg<32>;
     // >= 116 KB keeps one CTA per SM: the 512 TMEM columns it allocates are the whole SM's
-    const size_t smem = std::max<size_t>(sizeof(float) * tc_smem_floats<32>(), 116 * 1024);
+    const size_t smem = std::max<size_t>(sizeof(float) * (tc_smem_floats<32>() + 32), 116 * 1024);
     static unsigned long long configured = 0;
     int dev = 0;
     FOE_CUDA(cudaGetDevice(&dev));
     if (!(configured >> (dev & 63) & 1ull)) {
-        FOE_CUDA(cudaFuncSetAttribute(k_pass_tc<TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FOE_CUDA(cudaFuncSetAttribute(k_pass_tc<NF, TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured |= 1ull << (dev & 63);
     }
     dim3 grid(a.tiles_x * a.tiles_yl, a.B);
-    k_pass_tc<TRIAL, SYM><<<grid, T::NT, smem, st>>>(a);
+    k_pass_tc<NF, TRIAL, SYM><<<grid, T::NT, smem, st>>>(a);
     FOE_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return FOE_OK;
@@ -551,8 +551,16 @@ int launch_pass_tc_t(const PassArgs &a, cudaStream_t st) {
 int launch_pass(int m, bool sym, const PassArgs &a, cudaStream_t st) {
     const bool trial = a.mode == MODE_TRIAL;
     if (use_tc(m, a.n_filters)) {
-        if (trial) return sym ? launch_pass_tc_t<true, true>(a, st) : launch_pass_tc_t<true, false>(a, st);
-        return sym ? launch_pass_tc_t<false, true>(a, st) : launch_pass_tc_t<false, false>(a, st);
+        switch ((a.n_filters + 7) / 8) {
+            case 1: return trial ? (sym ? launch_pass_tc_t<8, true, true>(a, st) : launch_pass_tc_t<8, true, false>(a, st))
+                                 : (sym ? launch_pass_tc_t<8, false, true>(a, st) : launch_pass_tc_t<8, false, false>(a, st));
+            case 2: return trial ? (sym ? launch_pass_tc_t<16, true, true>(a, st) : launch_pass_tc_t<16, true, false>(a, st))
+                                 : (sym ? launch_pass_tc_t<16, false, true>(a, st) : launch_pass_tc_t<16, false, false>(a, st));
+            case 3: return trial ? (sym ? launch_pass_tc_t<24, true, true>(a, st) : launch_pass_tc_t<24, true, false>(a, st))
+                                 : (sym ? launch_pass_tc_t<24, false, true>(a, st) : launch_pass_tc_t<24, false, false>(a, st));
+            default: return trial ? (sym ? launch_pass_tc_t<32, true, true>(a, st) : launch_pass_tc_t<32, true, false>(a, st))
+                                  : (sym ? launch_pass_tc_t<32, false, true>(a, st) : launch_pass_tc_t<32, false, false>(a, st));
+        }
     }
     if (trial) return sym ? launch_pass_m<true, true>(m, a, st) : launch_pass_m<true, false>(m, a, st);
     return sym ? launch_pass_m<false, true>(m, a, st) : launch_pass_m<false, false>(m, a, st);

@@ -35,8 +35,9 @@ __host__ __device__ constexpr size_t tc_smem_floats() {
     return 2 * (size_t)T::PLANE + 4 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + (size_t)T::RH * T::RW;
 }
 
-template <bool TRIAL, bool SYM>
+template <int NF, bool TRIAL, bool SYM>
 __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) {
+    static_assert(NF % 8 == 0 && NF <= 32, "filter count rounded up to a multiple of 8");
     using T = TcCfg<32>;
     using C = PassCfg<5>;
     constexpr int NT = T::NT, R = T::R, SW = T::SW;
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     float *Kt = Kf + 2 * T::BSZ;   // [hi | lo], adjoint B (N = taps, K = filters)
     float *Yr = Kt + 2 * T::BSZ;   // Y ring [tap][ring row][YW]
     float *Gr = Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold)
+    float *s_al = Gr + T::RH * T::RW;            // alpha_f, zero-padded to NF
 
     if (warp == 0) tmem_alloc(&s_tmem, 512);
     if (tid < T::NWG) mbar_init(&s_mma[tid], 1);
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         Kt[bsw_offset<32>(n, k)] = ht;
         Kt[T::BSZ + bsw_offset<32>(n, k)] = vt - ht;
     }
+    for (int e = tid; e < NF; e += NT) s_al[e] = e < nf ? a.alpha[e] : 0.0f;
     // zero columns of the Y ring (padded positions outside the region)
     for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {
         const int col = e & 3, rr = e >> 2;
@@ -110,34 +113,52 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     double acc[kNumPartials];
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
-    // prologue: stage u_new - shift and du for the region + r ring (cells strided by NT here)
-    for (int k = tid; k < C::NCELL; k += NT) {
-        const int i = k / C::CW, j = k - i * C::CW;
-        const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
-        const size_t o = (size_t)(src_idx<SYM>(gy, a.H) - a.lrow0) * a.W + src_idx<SYM>(gx, a.W);
-        if (!TRIAL) {
-            Un[i * SW + j] = __ldg(uin + o) - shift;
-            continue;
+    // prologue: stage u_new - shift and du for the region + r ring; all loads of a thread in flight
+    // before any use (cells strided by NT)
+    {
+        constexpr int CPT = (C::NCELL + NT - 1) / NT;
+        float lu[CPT], lup[CPT], lg[CPT], lob[CPT];
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            const int k = tid + q * NT;
+            if (k < C::NCELL) {
+                const int i = k / C::CW, j = k - i * C::CW;
+                const size_t o = (size_t)(src_idx<SYM>(g.ry0 - R + i, a.H) - a.lrow0) * a.W +
+                                 src_idx<SYM>(g.rx0 - R + j, a.W);
+                lu[q] = __ldg(uin + o);
+                if (TRIAL) { lup[q] = __ldg(upv + o); lg[q] = __ldg(gin + o); lob[q] = __ldg(obs + o); }
+            }
         }
-        const float u = __ldg(uin + o), up = __ldg(upv + o), gg = __ldg(gin + o), ob = __ldg(obs + o);
-        const float ut = (u - p.tau * gg) + p.gam * (u - up);  // solver.py:146-149
-        const float un = (p.branch == FOE_QUADRATIC) ? prox_quad(ut, p.t, ob) : prox_idv(ut, p.t, ob);
-        const float du = un - u;
-        Un[i * SW + j] = un - shift;
-        Du[i * SW + j] = du;
-        if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) {
-            uout[(size_t)(gy - a.lrow0) * a.W + gx] = un;
-            acc[1] += (double)du * (double)du;
-            acc[2] += (double)gg * (double)du;
-            acc[3] += (double)u * (double)u;
-            if (p.branch == FOE_QUADRATIC) {
-                const double d = (double)un - (double)ob;
-                acc[4] += d * d;
-            } else {
-                acc[4] += (double)un;
-                if (ob > 0.0f) {
-                    if (un > 0.0f) acc[5] += (double)ob * (double)logf(un);
-                    else acc[6] += 1.0;
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            const int k = tid + q * NT;
+            if (k >= C::NCELL) continue;
+            const int i = k / C::CW, j = k - i * C::CW;
+            if (!TRIAL) {
+                Un[i * SW + j] = lu[q] - shift;
+                continue;
+            }
+            const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
+            const float u = lu[q], gg = lg[q], ob = lob[q];
+            const float ut = (u - p.tau * gg) + p.gam * (u - lup[q]);  // solver.py:146-149
+            const float un = (p.branch == FOE_QUADRATIC) ? prox_quad(ut, p.t, ob) : prox_idv(ut, p.t, ob);
+            const float du = un - u;
+            Un[i * SW + j] = un - shift;
+            Du[i * SW + j] = du;
+            if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) {
+                uout[(size_t)(gy - a.lrow0) * a.W + gx] = un;
+                acc[1] += (double)du * (double)du;
+                acc[2] += (double)gg * (double)du;
+                acc[3] += (double)u * (double)u;
+                if (p.branch == FOE_QUADRATIC) {
+                    const double d = (double)un - (double)ob;
+                    acc[4] += d * d;
+                } else {
+                    acc[4] += (double)un;
+                    if (ob > 0.0f) {
+                        if (un > 0.0f) acc[5] += (double)ob * (double)logf(un);
+                        else acc[6] += 1.0;
+                    }
                 }
             }
         }
@@ -195,47 +216,79 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         mbar_wait(&s_mma[wg], mma_phase);
         mma_phase ^= 1u;
         tc_fence_after();
-        // ---- pointwise: psi' = z/(1+z^2) (2a_f is in Kt), energy terms ----
+        // ---- pointwise: psi' = z/(1+z^2) (2a_f is in Kt) -> Psi operand; then the energy terms
+        //      are evaluated while the adjoint MMAs run ----
         {
             float z[32], dz[32];
             tmem_ld32(tbase + lane_off + T::C_DZ, z);
             if (TRIAL) tmem_ld32(tbase + lane_off + T::C_DDZ, dz);
             tc_wait_ld();
-            float e = 0.0f, hi[32], lo[32];
+            float hi[32], lo[32];
 #pragma unroll
             for (int f = 0; f < 32; ++f) {
-                if (f < nf) {
+                if (f < NF) {
                     const float zz = z[f];
-                    const float q1 = fmaf(zz, zz, 1.0f);
-                    const float ps = in_img ? zz * rcp_approx(q1) : 0.0f;
+                    const float ps = in_img ? zz * rcp_approx(fmaf(zz, zz, 1.0f)) : 0.0f;
                     hi[f] = tf32_hi(ps);
                     lo[f] = ps - hi[f];
-                    const float al = __ldg(a.alpha + f);
-                    if (TRIAL) {
-                        const float d = dz[f];
-                        const float zo = zz - d;
-                        const float num = d * fmaf(2.0f, zo, d);
-                        const float den = fmaf(zo, zo, q1) + 1.0f;
-                        e = fmaf(al, two_atanh(num * rcp_approx(den)), e);
-                    } else {
-                        e = fmaf(al, log1pf(zz * zz), e);
-                    }
                 } else {
                     hi[f] = 0.0f;
                     lo[f] = 0.0f;
                 }
             }
-            if (owned) e_own += (double)e;
             tmem_st32(tbase + lane_off + T::C_AUH, hi);
             tmem_st32(tbase + lane_off + T::C_AUL, lo);
-        }
-        tc_wait_st();
-        tc_fence_before();
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
-        if (wt == 0) {
-            tc_fence_after();
-            umma_3xtf32<32>(tbase + T::C_DZ, tbase + T::C_AUH, tbase + T::C_AUL, kt_hi, kt_lo, 4, false);
-            umma_commit(&s_mma[wg]);
+            tc_wait_st();
+            tc_fence_before();
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+            if (wt == 0) {
+                tc_fence_after();
+                umma_3xtf32<32>(tbase + T::C_DZ, tbase + T::C_AUH, tbase + T::C_AUL, kt_hi, kt_lo, NF / 8, false);
+                umma_commit(&s_mma[wg]);
+            }
+            // energy terms (z, dz still in registers; D_z is being overwritten by Y, not read again)
+            float e0 = 0.0f, e1 = 0.0f, e2 = 0.0f, e3 = 0.0f;
+            if (TRIAL) {
+                float tt[NF];
+                float tmax = 0.0f;
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    const float zz = z[f], d = dz[f];
+                    const float zo = zz - d;
+                    const float num = d * fmaf(2.0f, zo, d);
+                    const float den = fmaf(zo, zo, fmaf(zz, zz, 2.0f));
+                    tt[f] = num * rcp_approx(den);
+                    tmax = fmaxf(tmax, fabsf(tt[f]));
+                }
+                if (__any_sync(0xffffffffu, tmax > 0.2f)) {
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) {
+                        const float term = s_al[f] * two_atanh(tt[f]);
+                        if ((f & 3) == 0) e0 += term; else if ((f & 3) == 1) e1 += term;
+                        else if ((f & 3) == 2) e2 += term; else e3 += term;
+                    }
+                } else {
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) {
+                        const float t1 = tt[f], sq = t1 * t1;
+                        float pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
+                        pp = fmaf(sq, pp, 1.0f / 5.0f);
+                        pp = fmaf(sq, pp, 1.0f / 3.0f);
+                        pp = fmaf(sq, pp, 1.0f);
+                        const float term = (2.0f * s_al[f]) * t1 * pp;
+                        if ((f & 3) == 0) e0 += term; else if ((f & 3) == 1) e1 += term;
+                        else if ((f & 3) == 2) e2 += term; else e3 += term;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    const float term = s_al[f] * log1pf(z[f] * z[f]);
+                    if ((f & 3) == 0) e0 += term; else if ((f & 3) == 1) e1 += term;
+                    else if ((f & 3) == 2) e2 += term; else e3 += term;
+                }
+            }
+            if (owned) e_own += (double)((e0 + e1) + (e2 + e3));
         }
         mbar_wait(&s_mma[wg], mma_phase);
         mma_phase ^= 1u;
