@@ -533,7 +533,7 @@ template <int NF, bool TRIAL, bool SYM>
 int launch_pass_tc_t(const PassArgs &a, cudaStream_t st) {
     using T = TcCfg<32>;
     // >= 116 KB keeps one CTA per SM: the 512 TMEM columns it allocates are the whole SM's
-    const size_t smem = std::max<size_t>(sizeof(float) * (tc_smem_floats<32>() + 32), 116 * 1024);
+    const size_t smem = std::max<size_t>(sizeof(float) * (tc_smem_floats<32>() + 64), 116 * 1024);
     static unsigned long long configured = 0;
     int dev = 0;
     FOE_CUDA(cudaGetDevice(&dev));

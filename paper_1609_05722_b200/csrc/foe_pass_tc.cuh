@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     float *Yr = Kt + 2 * T::BSZ;   // Y ring [tap][ring row][YW]
     float *Gr = Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold)
     float *s_al = Gr + T::RH * T::RW;            // alpha_f, zero-padded to NF
+    float *s_k24 = s_al + 32;                    // tap 24 of each filter (outside the K = 24 MMAs)
 
     if (warp == 0) tmem_alloc(&s_tmem, 512);
     if (tid < T::NWG) mbar_init(&s_mma[tid], 1);
@@ -103,7 +104,10 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         Kt[bsw_offset<32>(n, k)] = ht;
         Kt[T::BSZ + bsw_offset<32>(n, k)] = vt - ht;
     }
-    for (int e = tid; e < NF; e += NT) s_al[e] = e < nf ? a.alpha[e] : 0.0f;
+    for (int e = tid; e < NF; e += NT) {
+        s_al[e] = e < nf ? a.alpha[e] : 0.0f;
+        s_k24[e] = e < nf ? a.kf[e * T::KT + 24] : 0.0f;
+    }
     // zero columns of the Y ring (padded positions outside the region)
     for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {
         const int col = e & 3, rr = e >> 2;
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const float *src = Un + lr * SW + lc;
 #pragma unroll
             for (int t = 0; t < 32; ++t) {
-                const float x = t < T::KT ? src[(t / 5) * SW + (t % 5)] : 0.0f;
+                const float x = t < 24 ? src[(t / 5) * SW + (t % 5)] : 0.0f;
                 hi[t] = tf32_hi(x);
                 lo[t] = x - hi[t];
             }
@@ -196,7 +200,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
                 const float *sd = Du + lr * SW + lc;
 #pragma unroll
                 for (int t = 0; t < 32; ++t) {
-                    const float x = t < T::KT ? sd[(t / 5) * SW + (t % 5)] : 0.0f;
+                    const float x = t < 24 ? sd[(t / 5) * SW + (t % 5)] : 0.0f;
                     hi[t] = tf32_hi(x);
                     lo[t] = x - hi[t];
                 }
@@ -209,10 +213,31 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
         if (wt == 0) {
             tc_fence_after();
-            umma_3xtf32<32>(tbase + T::C_DZ, tbase + T::C_AUH, tbase + T::C_AUL, kf_hi, kf_lo, 4, false);
-            if (TRIAL) umma_3xtf32<32>(tbase + T::C_DDZ, tbase + T::C_ADH, tbase + T::C_ADL, kf_hi, kf_lo, 4, false);
+            umma_3xtf32<32>(tbase + T::C_DZ, tbase + T::C_AUH, tbase + T::C_AUL, kf_hi, kf_lo, 3, false);
+            if (TRIAL) umma_3xtf32<32>(tbase + T::C_DDZ, tbase + T::C_ADH, tbase + T::C_ADL, kf_hi, kf_lo, 3, false);
             umma_commit(&s_mma[wg]);
         }
+        // while the forward MMAs run: shifted sums of block blk-2 (its Y neighbours are blocks
+        // blk-3 (ours), blk-2 (ours), blk-1 (the other warpgroup))
+        if (blk >= 2) {
+            const int gb = blk - 2;
+            mbar_wait(&s_ready[gb + 1], 0);
+            if (gb >= 1) mbar_wait(&s_ready[gb - 1], 0);
+            const int r = 2 * gb + (wt >> 6), c = wt & 63;
+            float s = 0.0f;
+#pragma unroll
+            for (int aa = 0; aa < 5; ++aa) {
+                const int rr = r + aa - R;
+                if (rr < 0 || rr >= T::RH) continue;
+                const float *yp = Yr + (rr % T::YROWS) * T::YW + 2 + c - R;
+#pragma unroll
+                for (int bb = 0; bb < 5; ++bb) s += yp[(aa * 5 + bb) * T::YROWS * T::YW + bb];
+            }
+            Gr[r * T::RW + c] = s;
+        }
+        // tap 24 (a = b = 4) on the CUDA cores: the MMAs cover K = 24
+        const float u24 = Un[(lr + 4) * SW + lc + 4];
+        const float d24 = TRIAL ? Du[(lr + 4) * SW + lc + 4] : 0.0f;
         mbar_wait(&s_mma[wg], mma_phase);
         mma_phase ^= 1u;
         tc_fence_after();
@@ -223,6 +248,12 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             tmem_ld32(tbase + lane_off + T::C_DZ, z);
             if (TRIAL) tmem_ld32(tbase + lane_off + T::C_DDZ, dz);
             tc_wait_ld();
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const float k24 = s_k24[f];
+                z[f] = fmaf(k24, u24, z[f]);
+                if (TRIAL) dz[f] = fmaf(k24, d24, dz[f]);
+            }
             float hi[32], lo[32];
 #pragma unroll
             for (int f = 0; f < 32; ++f) {
@@ -304,41 +335,24 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         }
         tc_fence_before();
         mbar_arrive(&s_ready[blk]);
-        // ---- shifted sums for the previous block's rows: g(q) = sum_t Y(q + off_t)[t] ----
-        const int gb = blk - 1;
-        if (gb >= 0) {
-            mbar_wait(&s_ready[gb], 0);
-            if (blk >= 2) mbar_wait(&s_ready[blk - 2], 0);
-            const int r = 2 * gb + (wt >> 6), c = wt & 63;
-            float s = 0.0f;
-#pragma unroll
-            for (int aa = 0; aa < 5; ++aa) {
-                const int rr = r + aa - R;
-                if (rr < 0 || rr >= T::RH) continue;
-                const float *yp = Yr + (rr % T::YROWS) * T::YW + 2 + c - R;
-#pragma unroll
-                for (int bb = 0; bb < 5; ++bb) s += yp[(aa * 5 + bb) * T::YROWS * T::YW + bb];
-            }
-            Gr[r * T::RW + c] = s;
-        }
     }
-    // the last block's rows (needs no later Y)
-    {
-        constexpr int last = T::NBLK - 1;
-        if (wg == (last % T::NWG)) {
-            mbar_wait(&s_ready[last - 1], 0);
-            const int r = 2 * last + (wt >> 6), c = wt & 63;
-            float s = 0.0f;
+    // the last two blocks' rows: g(NBLK-2) by the warpgroup of block NBLK-1's partner, g(NBLK-1)
+    // by the other (the Y ring still holds blocks NBLK-4 .. NBLK-1)
+    for (int gb = T::NBLK - 2 + wg; gb < T::NBLK; gb += T::NWG) {
+        if (gb + 1 < T::NBLK) mbar_wait(&s_ready[gb + 1], 0);
+        mbar_wait(&s_ready[gb], 0);
+        if (gb >= 1) mbar_wait(&s_ready[gb - 1], 0);
+        const int r = 2 * gb + (wt >> 6), c = wt & 63;
+        float s = 0.0f;
 #pragma unroll
-            for (int aa = 0; aa < 5; ++aa) {
-                const int rr = r + aa - R;
-                if (rr < 0 || rr >= T::RH) continue;
-                const float *yp = Yr + (rr % T::YROWS) * T::YW + 2 + c - R;
+        for (int aa = 0; aa < 5; ++aa) {
+            const int rr = r + aa - R;
+            if (rr < 0 || rr >= T::RH) continue;
+            const float *yp = Yr + (rr % T::YROWS) * T::YW + 2 + c - R;
 #pragma unroll
-                for (int bb = 0; bb < 5; ++bb) s += yp[(aa * 5 + bb) * T::YROWS * T::YW + bb];
-            }
-            Gr[r * T::RW + c] = s;
+            for (int bb = 0; bb < 5; ++bb) s += yp[(aa * 5 + bb) * T::YROWS * T::YW + bb];
         }
+        Gr[r * T::RW + c] = s;
     }
     acc[0] = e_own;
     tc_fence_before();
