@@ -18,8 +18,9 @@ struct TcCfg {
     static constexpr int R = 2, M = 5, KT = 25;
     static constexpr int RH = P::RH, RW = P::RW, SH = P::SH, SW = P::SW, PLANE = P::PLANE;
     static constexpr int NBLK = RH * RW / 128;       // 128-pixel blocks (two region rows each)
-    static constexpr int NWG = 2, NT = 128 * NWG;    // warpgroups x 128 threads
-    static constexpr int YROWS = 8, YW = RW + 4;     // Y ring: 8 region rows, 2 zero columns each side
+    static constexpr int NWG = 2, WGT = 256, NT = WGT * NWG;  // 2 warpgroups of 8 warps: warps w and w+4
+                                                              // share a TMEM lane quarter (same pixels)
+    static constexpr int YROWS = 12, YW = RW + 4;    // Y ring: 6 blocks of 2 rows, 2 zero columns each side
     static constexpr int BSZ = 32 * 32;              // one 32 x 32 B operand (floats)
     // TMEM columns per warpgroup: A_u hi/lo, A_du hi/lo (reused for Psi hi/lo), D_z (reused for
     // D_y), D_dz
@@ -32,7 +33,7 @@ template <int NF_MAX>
 __host__ __device__ constexpr size_t tc_smem_floats() {
     using T = TcCfg<NF_MAX>;
     // Un, Du staged planes; Kf hi/lo, Kt hi/lo; Y ring; region gradient
-    return 2 * (size_t)T::PLANE + 4 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + (size_t)T::RH * T::RW;
+    return 2 * (size_t)T::PLANE + 4 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW;
 }
 
 template <int NF, bool TRIAL, bool SYM>
@@ -50,8 +51,11 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     __shared__ __align__(8) unsigned long long s_ready[T::NBLK];    // Y of block j in the ring
 
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int wg = tid >> 7, wt = tid & 127;  // warpgroup, thread in warpgroup (= TMEM lane)
+    const int wg = tid / T::WGT, wt = tid % T::WGT;  // warpgroup, thread in warpgroup
+    const int hf = wt >> 7, pl = wt & 127;           // half (filters / taps), pixel = TMEM lane
     const int b = blockIdx.y;
+    const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3] = globaltimer_ns();
     const int nf = a.n_filters;
     TrialParams p{};
     if (a.mode != MODE_EVAL) {
@@ -86,12 +90,12 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     float *Kt = Kf + 2 * T::BSZ;   // [hi | lo], adjoint B (N = taps, K = filters)
     float *Yr = Kt + 2 * T::BSZ;   // Y ring [tap][ring row][YW]
     float *Gr = Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold)
-    float *s_al = Gr + T::RH * T::RW;            // alpha_f, zero-padded to NF
+    float *s_al = Gr + 2 * T::RH * T::RW;        // alpha_f, zero-padded to NF (Gr: two tap halves)
     float *s_k24 = s_al + 32;                    // tap 24 of each filter (outside the K = 24 MMAs)
 
     if (warp == 0) tmem_alloc(&s_tmem, 512);
     if (tid < T::NWG) mbar_init(&s_mma[tid], 1);
-    if (tid < T::NBLK) mbar_init(&s_ready[tid], 128);
+    if (tid < T::NBLK) mbar_init(&s_ready[tid], T::WGT);
     // B operands: Kf[f][t] = kf_f[t] (convolution orientation), Kt[t][f] = 2 a_f k_f[t] with the
     // unflipped k_f[t] = kf_f[24 - t]; zero padding to 32 x 32; split into tf32 hi + fp32 lo
     for (int e = tid; e < 32 * 32; e += NT) {
@@ -171,6 +175,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 1] = globaltimer_ns();
 
     const uint32_t tbase = s_tmem + (uint32_t)(wg * T::C_WG);
     const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
@@ -178,185 +183,179 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     const uint32_t kt_hi = smem_u32(Kt), kt_lo = smem_u32(Kt + T::BSZ);
     unsigned mma_phase = 0u;
     double e_own = 0.0;
+    constexpr int FH = NF > 16 ? 16 : NF;  // filters per half (half 1 idles for NF <= 16)
 
+    // g(q) over one half of the taps: half 0 taps [0, 13), half 1 taps [13, 25)
+    auto shifted_sum = [&](int gb) {
+        const int r = 2 * gb + (pl >> 6), c = pl & 63;
+        float s = 0.0f;
+#pragma unroll
+        for (int t = 0; t < T::KT; ++t) {
+            if ((t < 13) != (hf == 0)) continue;
+            const int aa = t / 5, bb = t % 5;
+            const int rr = r + aa - R;
+            if (rr < 0 || rr >= T::RH) continue;
+            s += Yr[(t * T::YROWS + rr % T::YROWS) * T::YW + 2 + c - R + bb];
+        }
+        Gr[hf * T::RH * T::RW + r * T::RW + c] = s;
+    };
+
+    unsigned long long *ph = (a.dbg_times && blockIdx.x == 0 && blockIdx.y == 0 && wt == 0)
+                                 ? a.dbg_times + 3 * (size_t)gridDim.x * gridDim.y : nullptr;
     for (int blk = wg; blk < T::NBLK; blk += T::NWG) {
-        const int lr = 2 * blk + (wt >> 6), lc = wt & 63;  // this thread's pixel (region-local)
+        if (ph) ph[blk * 8 + 0] = globaltimer_ns();
+        const int lr = 2 * blk + (pl >> 6), lc = pl & 63;  // this thread's pixel (region-local)
         const int gy = g.ry0 + lr, gx = g.rx0 + lc;
         const bool in_img = !SYM || (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W);
         const bool owned = gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1;
-        // ---- im2col of u_new (and du) into TMEM: A[p][t] = staged(lr + a, lc + b), t = 5a + b ----
-        {
+        // ---- im2col into TMEM, taps 0..23 (K = 24): half 0 u_new, half 1 du ----
+        if (hf == 0 || TRIAL) {
             float hi[32], lo[32];
-            const float *src = Un + lr * SW + lc;
+            const float *src = (hf ? Du : Un) + lr * SW + lc;
 #pragma unroll
             for (int t = 0; t < 32; ++t) {
                 const float x = t < 24 ? src[(t / 5) * SW + (t % 5)] : 0.0f;
                 hi[t] = tf32_hi(x);
                 lo[t] = x - hi[t];
             }
-            tmem_st32(tbase + lane_off + T::C_AUH, hi);
-            tmem_st32(tbase + lane_off + T::C_AUL, lo);
-            if (TRIAL) {
-                const float *sd = Du + lr * SW + lc;
-#pragma unroll
-                for (int t = 0; t < 32; ++t) {
-                    const float x = t < 24 ? sd[(t / 5) * SW + (t % 5)] : 0.0f;
-                    hi[t] = tf32_hi(x);
-                    lo[t] = x - hi[t];
-                }
-                tmem_st32(tbase + lane_off + T::C_ADH, hi);
-                tmem_st32(tbase + lane_off + T::C_ADL, lo);
-            }
+            tmem_st32(tbase + lane_off + (hf ? T::C_ADH : T::C_AUH), hi);
+            tmem_st32(tbase + lane_off + (hf ? T::C_ADL : T::C_AUL), lo);
         }
+        if (ph) ph[blk * 8 + 1] = globaltimer_ns();
         tc_wait_st();
         tc_fence_before();
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + wg), "r"(T::WGT) : "memory");
+        if (ph) ph[blk * 8 + 2] = globaltimer_ns();
         if (wt == 0) {
             tc_fence_after();
             umma_3xtf32<32>(tbase + T::C_DZ, tbase + T::C_AUH, tbase + T::C_AUL, kf_hi, kf_lo, 3, false);
             if (TRIAL) umma_3xtf32<32>(tbase + T::C_DDZ, tbase + T::C_ADH, tbase + T::C_ADL, kf_hi, kf_lo, 3, false);
             umma_commit(&s_mma[wg]);
         }
-        // while the forward MMAs run: shifted sums of block blk-2 (its Y neighbours are blocks
-        // blk-3 (ours), blk-2 (ours), blk-1 (the other warpgroup))
-        if (blk >= 2) {
-            const int gb = blk - 2;
-            mbar_wait(&s_ready[gb + 1], 0);
-            if (gb >= 1) mbar_wait(&s_ready[gb - 1], 0);
-            const int r = 2 * gb + (wt >> 6), c = wt & 63;
-            float s = 0.0f;
-#pragma unroll
-            for (int aa = 0; aa < 5; ++aa) {
-                const int rr = r + aa - R;
-                if (rr < 0 || rr >= T::RH) continue;
-                const float *yp = Yr + (rr % T::YROWS) * T::YW + 2 + c - R;
-#pragma unroll
-                for (int bb = 0; bb < 5; ++bb) s += yp[(aa * 5 + bb) * T::YROWS * T::YW + bb];
-            }
-            Gr[r * T::RW + c] = s;
+        // while the forward MMAs run: shifted sums of block blk-3 (its Y neighbours finished an
+        // iteration ago; the 6-block ring keeps blk-4 .. blk+1 live)
+        if (blk >= 3) {
+            mbar_wait(&s_ready[blk - 3], 0);
+            shifted_sum(blk - 3);
         }
         // tap 24 (a = b = 4) on the CUDA cores: the MMAs cover K = 24
         const float u24 = Un[(lr + 4) * SW + lc + 4];
         const float d24 = TRIAL ? Du[(lr + 4) * SW + lc + 4] : 0.0f;
+        if (ph) ph[blk * 8 + 3] = globaltimer_ns();
         mbar_wait(&s_mma[wg], mma_phase);
         mma_phase ^= 1u;
         tc_fence_after();
-        // ---- pointwise: psi' = z/(1+z^2) (2a_f is in Kt) -> Psi operand; then the energy terms
-        //      are evaluated while the adjoint MMAs run ----
+        if (ph) ph[blk * 8 + 4] = globaltimer_ns();
+        // ---- pointwise on this half's filters [16 hf, 16 hf + 16): psi' -> Psi operand, then the
+        //      energy terms while the adjoint MMAs run ----
         {
-            float z[32], dz[32];
-            tmem_ld32(tbase + lane_off + T::C_DZ, z);
-            if (TRIAL) tmem_ld32(tbase + lane_off + T::C_DDZ, dz);
+            const int f0 = 16 * hf;
+            float z[16], dz[16];
+            tmem_ld16(tbase + lane_off + T::C_DZ + f0, z);
+            if (TRIAL) tmem_ld16(tbase + lane_off + T::C_DDZ + f0, dz);
             tc_wait_ld();
+            float hi[16], lo[16];
 #pragma unroll
-            for (int f = 0; f < NF; ++f) {
-                const float k24 = s_k24[f];
-                z[f] = fmaf(k24, u24, z[f]);
-                if (TRIAL) dz[f] = fmaf(k24, d24, dz[f]);
-            }
-            float hi[32], lo[32];
-#pragma unroll
-            for (int f = 0; f < 32; ++f) {
-                if (f < NF) {
-                    const float zz = z[f];
+            for (int i = 0; i < 16; ++i) {
+                const int f = f0 + i;
+                if (i < FH && f < NF) {
+                    const float k24 = s_k24[f];
+                    z[i] = fmaf(k24, u24, z[i]);
+                    if (TRIAL) dz[i] = fmaf(k24, d24, dz[i]);
+                    const float zz = z[i];
                     const float ps = in_img ? zz * rcp_approx(fmaf(zz, zz, 1.0f)) : 0.0f;
-                    hi[f] = tf32_hi(ps);
-                    lo[f] = ps - hi[f];
+                    hi[i] = tf32_hi(ps);
+                    lo[i] = ps - hi[i];
                 } else {
-                    hi[f] = 0.0f;
-                    lo[f] = 0.0f;
+                    hi[i] = 0.0f;
+                    lo[i] = 0.0f;
                 }
             }
-            tmem_st32(tbase + lane_off + T::C_AUH, hi);
-            tmem_st32(tbase + lane_off + T::C_AUL, lo);
+            tmem_st16(tbase + lane_off + T::C_AUH + f0, hi);
+            tmem_st16(tbase + lane_off + T::C_AUL + f0, lo);
             tc_wait_st();
             tc_fence_before();
-            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + wg), "r"(T::WGT) : "memory");
             if (wt == 0) {
                 tc_fence_after();
                 umma_3xtf32<32>(tbase + T::C_DZ, tbase + T::C_AUH, tbase + T::C_AUL, kt_hi, kt_lo, NF / 8, false);
                 umma_commit(&s_mma[wg]);
             }
-            // energy terms (z, dz still in registers; D_z is being overwritten by Y, not read again)
-            float e0 = 0.0f, e1 = 0.0f, e2 = 0.0f, e3 = 0.0f;
+            float e0 = 0.0f, e1 = 0.0f;
             if (TRIAL) {
-                float tt[NF];
+                float tt[16];
                 float tmax = 0.0f;
 #pragma unroll
-                for (int f = 0; f < NF; ++f) {
-                    const float zz = z[f], d = dz[f];
+                for (int i = 0; i < 16; ++i) {
+                    if (!(i < FH && f0 + i < NF)) { tt[i] = 0.0f; continue; }
+                    const float zz = z[i], d = dz[i];
                     const float zo = zz - d;
                     const float num = d * fmaf(2.0f, zo, d);
                     const float den = fmaf(zo, zo, fmaf(zz, zz, 2.0f));
-                    tt[f] = num * rcp_approx(den);
-                    tmax = fmaxf(tmax, fabsf(tt[f]));
+                    tt[i] = num * rcp_approx(den);
+                    tmax = fmaxf(tmax, fabsf(tt[i]));
                 }
                 if (__any_sync(0xffffffffu, tmax > 0.2f)) {
 #pragma unroll
-                    for (int f = 0; f < NF; ++f) {
-                        const float term = s_al[f] * two_atanh(tt[f]);
-                        if ((f & 3) == 0) e0 += term; else if ((f & 3) == 1) e1 += term;
-                        else if ((f & 3) == 2) e2 += term; else e3 += term;
+                    for (int i = 0; i < 16; ++i) {
+                        if (!(i < FH && f0 + i < NF)) continue;
+                        const float term = s_al[f0 + i] * two_atanh(tt[i]);
+                        if (i & 1) e1 += term; else e0 += term;
                     }
                 } else {
 #pragma unroll
-                    for (int f = 0; f < NF; ++f) {
-                        const float t1 = tt[f], sq = t1 * t1;
+                    for (int i = 0; i < 16; ++i) {
+                        if (!(i < FH && f0 + i < NF)) continue;
+                        const float t1 = tt[i], sq = t1 * t1;
                         float pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
                         pp = fmaf(sq, pp, 1.0f / 5.0f);
                         pp = fmaf(sq, pp, 1.0f / 3.0f);
                         pp = fmaf(sq, pp, 1.0f);
-                        const float term = (2.0f * s_al[f]) * t1 * pp;
-                        if ((f & 3) == 0) e0 += term; else if ((f & 3) == 1) e1 += term;
-                        else if ((f & 3) == 2) e2 += term; else e3 += term;
+                        const float term = (2.0f * s_al[f0 + i]) * t1 * pp;
+                        if (i & 1) e1 += term; else e0 += term;
                     }
                 }
             } else {
 #pragma unroll
-                for (int f = 0; f < NF; ++f) {
-                    const float term = s_al[f] * log1pf(z[f] * z[f]);
-                    if ((f & 3) == 0) e0 += term; else if ((f & 3) == 1) e1 += term;
-                    else if ((f & 3) == 2) e2 += term; else e3 += term;
+                for (int i = 0; i < 16; ++i) {
+                    if (!(i < FH && f0 + i < NF)) continue;
+                    const float term = s_al[f0 + i] * log1pf(z[i] * z[i]);
+                    if (i & 1) e1 += term; else e0 += term;
                 }
             }
-            if (owned) e_own += (double)((e0 + e1) + (e2 + e3));
+            if (owned) e_own += (double)(e0 + e1);
         }
+        if (ph) ph[blk * 8 + 5] = globaltimer_ns();
         mbar_wait(&s_mma[wg], mma_phase);
         mma_phase ^= 1u;
         tc_fence_after();
-        // ---- Y rows of this block into the ring ----
+        if (ph) ph[blk * 8 + 6] = globaltimer_ns();
+        // ---- Y rows of this block into the ring: half 0 taps 0..15, half 1 taps 16..24 ----
         {
-            float y[32];
-            tmem_ld32(tbase + lane_off + T::C_DZ, y);
+            float y[16];
+            tmem_ld16(tbase + lane_off + T::C_DZ + 16 * hf, y);
             tc_wait_ld();
             float *yrow = Yr + (lr % T::YROWS) * T::YW + 2 + lc;
 #pragma unroll
-            for (int t = 0; t < T::KT; ++t) yrow[t * T::YROWS * T::YW] = y[t];
+            for (int i = 0; i < 16; ++i) {
+                const int t = 16 * hf + i;
+                if (t < T::KT) yrow[t * T::YROWS * T::YW] = y[i];
+            }
         }
         tc_fence_before();
         mbar_arrive(&s_ready[blk]);
+        if (ph) ph[blk * 8 + 7] = globaltimer_ns();
     }
-    // the last two blocks' rows: g(NBLK-2) by the warpgroup of block NBLK-1's partner, g(NBLK-1)
-    // by the other (the Y ring still holds blocks NBLK-4 .. NBLK-1)
-    for (int gb = T::NBLK - 2 + wg; gb < T::NBLK; gb += T::NWG) {
-        if (gb + 1 < T::NBLK) mbar_wait(&s_ready[gb + 1], 0);
-        mbar_wait(&s_ready[gb], 0);
-        if (gb >= 1) mbar_wait(&s_ready[gb - 1], 0);
-        const int r = 2 * gb + (wt >> 6), c = wt & 63;
-        float s = 0.0f;
-#pragma unroll
-        for (int aa = 0; aa < 5; ++aa) {
-            const int rr = r + aa - R;
-            if (rr < 0 || rr >= T::RH) continue;
-            const float *yp = Yr + (rr % T::YROWS) * T::YW + 2 + c - R;
-#pragma unroll
-            for (int bb = 0; bb < 5; ++bb) s += yp[(aa * 5 + bb) * T::YROWS * T::YW + bb];
-        }
-        Gr[r * T::RW + c] = s;
+    // the last three blocks' rows (their later Y neighbours exist only now)
+    for (int gb = T::NBLK - 3 + wg; gb < T::NBLK; gb += T::NWG) {
+        for (int q = gb - 1; q <= gb + 1; ++q)
+            if (q >= 0 && q < T::NBLK) mbar_wait(&s_ready[q], 0);
+        shifted_sum(gb);
     }
     acc[0] = e_own;
     tc_fence_before();
     __syncthreads();
+    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
     if (warp == 0) tmem_dealloc(s_tmem, 512);
 
     // ---- fold padded pixels (symmetric rule) and write the owned gradient ----
@@ -372,14 +371,15 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             }
             for (int gy = g.s0 + tid / T::RW; gy < g.s1; gy += NT / T::RW) {
                 const int ly = gy - g.ry0;
-                float val = Gr[ly * T::RW + lx];
+                auto gsum2 = [&](int yy, int xx2) { return Gr[yy * T::RW + xx2] + Gr[T::RH * T::RW + yy * T::RW + xx2]; };
+                float val = gsum2(ly, lx);
                 if (SYM) {
                     int my = -1;
                     if (gy < R) my = (-1 - gy) - g.ry0;
                     else if (gy >= a.H - R) my = (2 * a.H - 1 - gy) - g.ry0;
-                    if (my >= 0) val += Gr[my * T::RW + lx];
-                    if (mx >= 0) val += Gr[ly * T::RW + mx];
-                    if (my >= 0 && mx >= 0) val += Gr[my * T::RW + mx];
+                    if (my >= 0) val += gsum2(my, lx);
+                    if (mx >= 0) val += gsum2(ly, mx);
+                    if (my >= 0 && mx >= 0) val += gsum2(my, mx);
                 }
                 gout[(size_t)(gy - a.lrow0) * a.W + gx] = val;
             }

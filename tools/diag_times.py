@@ -19,17 +19,25 @@ res = fp.solve_device(model, v, v, 0.6075, "quadratic", 150, fp.SolverConfig(rel
 L = _lib.lib()
 ws = res._workspace
 ncta = (-(-H // 32)) * (-(-W // 60))
-t = torch.zeros(ncta * 3, dtype=torch.int64, device="cuda")
+t = torch.zeros(ncta * 3 + 18 * 8, dtype=torch.int64, device="cuda")
 for _ in range(3):
     _lib.check(L.foe_debug_pass_times(res._bank.handle, 1, H, W, res._cap, ws.data_ptr(), ws.numel(), t.data_ptr(),
                                       torch.cuda.current_stream().cuda_stream))
 torch.cuda.synchronize()
-a = t.cpu().numpy().reshape(ncta, 3).astype(np.float64)
+full = t.cpu().numpy()
+a = full[:ncta * 3].reshape(ncta, 3).astype(np.float64)
+phs = full[ncta * 3:].reshape(18, 8).astype(np.float64)
+if phs.any():
+    phs -= full[0]
+    np.set_printoptions(precision=2, suppress=True, linewidth=200)
+    print("block phases (us from CTA start): start, im2col-done, bar, fwd-issued(+g), fwd-done, psi+energy, adj-done, Y-done")
+    print(phs / 1e3)
 a -= a[:, 0].min()
 start, comp, end = a[:, 0] / 1e3, a[:, 1] / 1e3, a[:, 2] / 1e3
 dur = comp - start
-print(f"CTAs {ncta}: start skew max {start.max():.2f} us; compute dur min/med/max {dur.min():.2f}/"
-      f"{np.median(dur):.2f}/{dur.max():.2f} us; last compute end {comp.max():.2f}; last exit {end.max():.2f} us")
+print(f"CTAs {ncta}: start skew max {start.max():.2f} us; phase1 (t1-t0) min/med/max {dur.min():.2f}/"
+      f"{np.median(dur):.2f}/{dur.max():.2f} us; phase2 (t2-t1) med {np.median(end - comp):.2f} max "
+      f"{(end - comp).max():.2f}; last t1 {comp.max():.2f}; last t2 {end.max():.2f} us")
 ty, tx = -(-H // 32), -(-W // 60)
 grid = dur.reshape(ty, tx)
 np.set_printoptions(precision=1, suppress=True, linewidth=200)
