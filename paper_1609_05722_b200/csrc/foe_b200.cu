@@ -60,7 +60,7 @@ constexpr int kMaxTaps = 4096;
 constexpr int kMaxFilters = 512;
 constexpr int kNumPartials = 7;  // dF|F, sq, gd, |u|^2, G_a, G_b, G_bad
 constexpr int kPartialStride = 8;
-constexpr bool kTcDefault = false;  // tensor-core pass on by default once validated
+constexpr bool kTcDefault = true;  // tensor-core pass for eligible banks unless FOE_TC=0
 
 enum PassMode { MODE_EVAL = 0, MODE_INIT = 1, MODE_TRIAL = 2 };
 
@@ -236,16 +236,20 @@ __device__ __forceinline__ void block_reduce(double (&v)[kNumPartials], double (
     }
 }
 
-// fixed-order sum of one image's tile partials (layout [tile][B][8]) into s_sum, by a whole CTA of
-// NT threads: thread k sums tiles k, k+NT, ... then a fixed tree.  Shared by the last-CTA path and
+// fixed-order sum of one image's tile partials (layout [tile][B][8]) into s_sum, by a whole CTA:
+// thread k < 384 sums tiles k, k+384, ... then a fixed tree.  Shared by the last-CTA path and
 // k_decide, so a band-decomposed solve reduces in exactly the single-device order.
+// The tile stride is a fixed 384 whatever the block size (threads beyond it add exact zeros), so
+// every kernel that decides -- k_pass, k_pass_tc, k_decide -- reduces in the same order.
+constexpr int kReduceNT = 384;
 template <int NT>
 __device__ void reduce_tiles(const double *partials, int ntiles, int B, int b, double (*red)[kNumPartials],
                              double *s_sum) {
+    static_assert(NT >= kReduceNT && NT % 32 == 0, "reducing block narrower than the fixed tile stride");
     double tot[kNumPartials];
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) tot[k] = 0.0;
-    for (int tt = threadIdx.x; tt < ntiles; tt += NT)
+    for (int tt = threadIdx.x; threadIdx.x < kReduceNT && tt < ntiles; tt += kReduceNT)
 #pragma unroll
         for (int k = 0; k < kNumPartials; ++k) tot[k] += __ldcg(partials + ((size_t)tt * B + b) * kPartialStride + k);
     __syncthreads();
@@ -1201,6 +1205,22 @@ int foe_unbin_bilinear(const double *xb, double *out, int h, int w, int H, int W
     return FOE_OK;
 }
 
+
+int foe_debug_tc_rate(int n, int ts, int nmma, long long *out_cycles, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n != 32 && n != 64 && n != 128) return fail(FOE_E_INVALID, "n must be 32, 64 or 128");
+    if (ts) {
+        if (n == 32) k_tc_rate<32, true><<<1, 128, 0, st>>>(nmma, out_cycles);
+        if (n == 64) k_tc_rate<64, true><<<1, 128, 0, st>>>(nmma, out_cycles);
+        if (n == 128) k_tc_rate<128, true><<<1, 128, 0, st>>>(nmma, out_cycles);
+    } else {
+        if (n == 32) k_tc_rate<32, false><<<1, 128, 0, st>>>(nmma, out_cycles);
+        if (n == 64) k_tc_rate<64, false><<<1, 128, 0, st>>>(nmma, out_cycles);
+        if (n == 128) k_tc_rate<128, false><<<1, 128, 0, st>>>(nmma, out_cycles);
+    }
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
 
 int foe_tc_selftest(const float *A, const float *B, float *D, void *stream) {
     g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -446,7 +446,10 @@ __device__ double filter_loop(const PassArgs &a, const TileGeom &g, const Smem<M
                 }
             }
         }
-        if (k < fpg) mbar_arrive(&mbar[grp][k % C::NBUF]);
+        if (k < fpg) {  // one arrival per warp once its lanes' psi stores are ordered (__syncwarp)
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&mbar[grp][k % C::NBUF]);
+        }
     }
     double e = 0.0;  // owned pixels only, fp64 across pixels
 #pragma unroll
@@ -557,7 +560,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     const TileGeom g = tile_geom<M, SYM>(a, tyl, txi);
     const Smem<M> S(sm, a.n_filters, TRIAL);
     stage_bank<M>(a, S);
-    if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG);
+    if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG / 32);
     if (g.edge) zero_psi_ring<M>(S);
     // Filters are zero-mean (DCT basis without DC, image.py:117-130), so K(u - c) == K u: staging
     // u - c with c = the tile's anchor pixel keeps the fp32 products small (accuracy, not speed).
@@ -653,7 +656,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_solve_resident(const Pass
     const TileGeom g = tile_geom<M, SYM>(a, tyl, txi);
     const Smem<M> S(sm, a.n_filters, true);
     stage_bank<M>(a, S);
-    if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG);
+    if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG / 32);
     if (tid < B) s_ctl[tid] = a.ctl[tid];
     const size_t ioff = (size_t)b * a.Hl * a.W;
     const int ow = g.c1 - g.c0, oh = g.s1 - g.s0;

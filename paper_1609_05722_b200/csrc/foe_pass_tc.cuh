@@ -1,30 +1,45 @@
 // foe_pass_tc.cuh -- tensor-core (tcgen05, 3xTF32) variant of the fused FoE pass for 5x5 banks
 // with at most 32 filters (included by foe_b200.cu after foe_pass.cuh / foe_tc.cuh).
 //
-// Same tile geometry, prologue, fold and reductions as k_pass; the two convolutions become
-// implicit GEMMs on the tensor cores, one 128-pixel block (two region rows) at a time:
-//   forward   Z  = A_u  . Kf^T    A_u[p][t] = u_new(p + off_t)  (im2col, K = 25 -> 32), N = filters
+// Same tile geometry, prologue, fold and reductions as k_pass; the two convolutions become implicit
+// GEMMs on the tensor cores, one 128-pixel block (two region rows) at a time:
+//   forward   Z  = A_u  . Kf^T    A_u[p][t] = u_new(p + off_t)  (im2col, K = 24 taps; tap 24 by FFMA)
 //             dZ = A_du . Kf^T    (the same for du, for the energy change)
-//   adjoint   Y  = Psi  . Kt^T    Psi[p][f] = z/(1+z^2), Kt[t][f] = 2 a_f k_f[t], N = taps
+//   adjoint   Y  = Psi  . Kt^T    Psi[p][f] = z/(1+z^2), Kt[t][f] = 2 a_f k_f[t]
 //             g(q) = sum_t Y(q + off_t)[t]       (25-term shifted sum on the CUDA cores)
 // A operands are written by their pixel's thread straight into TMEM (tcgen05.st), B operands sit in
-// shared memory, D accumulators in TMEM.  fp32 accuracy from tf32 units via the 3xTF32 split.
-// Two warpgroups alternate blocks so one builds operands / evaluates the pointwise terms while the
-// other's MMAs run.
+// shared memory, D accumulators in TMEM; fp32 accuracy from tf32 units via the 3xTF32 split.
+//
+// Warp-specialised pipeline over the 18 blocks of a tile; block j uses A stage j%2 (im2col operands)
+// and D region j%2 (its forward accumulators, Psi in place over them, its adjoint accumulator):
+//   im2col (warps 0-7)      warps 0-3 A_u, warps 4-7 A_du of block j (once forward(j-2) released the
+//                           stage) -> a_full[s]; warp 0 issues forward(j) once the D region is free
+//                           (d_free[s]) -> d_full[s]
+//   point set s (8 warps)   blocks j = s, s+2, ...: z, dz -> energy terms and Psi (written over z, dz)
+//                           -> p_full[s]; the set's first warp issues adjoint(j) -> y_full[s]; Y ->
+//                           d_free[s] -> shared ring -> ring_full[j]; then g(j-1) = shifted sum over
+//                           the warp's tap half once Y(j-2 .. j) are in the ring -> sum_done[j-1]
+// so the tensor core, the operand build, two blocks' pointwise work and the shifted sums overlap.
+// Within a point set, warps w and w+4 share a TMEM lane quarter (same 32 pixels) and split the
+// filters (forward side, NF/2 each) and taps (adjoint side, 16 + 9).  24 warps: 80 registers/thread.
 
 template <int NF_MAX>
 struct TcCfg {
     using P = PassCfg<5>;
     static constexpr int R = 2, M = 5, KT = 25;
     static constexpr int RH = P::RH, RW = P::RW, SH = P::SH, SW = P::SW, PLANE = P::PLANE;
-    static constexpr int NBLK = RH * RW / 128;       // 128-pixel blocks (two region rows each)
-    static constexpr int NWG = 2, WGT = 256, NT = WGT * NWG;  // 2 warpgroups of 8 warps: warps w and w+4
-                                                              // share a TMEM lane quarter (same pixels)
-    static constexpr int YROWS = 12, YW = RW + 4;    // Y ring: 6 blocks of 2 rows, 2 zero columns each side
-    static constexpr int BSZ = 32 * 32;              // one 32 x 32 B operand (floats)
-    // TMEM columns per warpgroup: A_u hi/lo, A_du hi/lo (reused for Psi hi/lo), D_z (reused for
-    // D_y), D_dz
-    static constexpr int C_AUH = 0, C_AUL = 32, C_ADH = 64, C_ADL = 96, C_DZ = 128, C_DDZ = 160, C_WG = 256;
+    static constexpr int NBLK = RH * RW / 128;  // 128-pixel blocks (two region rows each)
+    static constexpr int W_PT = 8, NWARPS = 24, NT = NWARPS * 32;
+    // named barriers, one per stage / set: A complete, Psi complete, D region free, forward done (relayed
+    // to the set), adjoint done (relayed to the set), A stage free (relayed to the im2col warps)
+    static constexpr int BAR_AFULL = 1, BAR_PFULL = 3, BAR_DFREE = 5, BAR_DFULL = 7, BAR_YFULL = 9, BAR_AFREE = 11;
+    static constexpr int RING = 4;                       // Y ring: 4 blocks = 8 region rows
+    static constexpr int YROWS = 2 * RING, YW = RW + 4;  // 2 zero columns each side
+    static constexpr int BSZ = 32 * 32;                  // one 32 x 32 B operand (floats)
+    // TMEM columns: A stage s at 128 s (A_u hi/lo, A_du hi/lo); D region s at 256 + 96 s (D_z -> Psi hi,
+    // D_dz -> Psi lo, D_y)
+    static constexpr int C_AUH = 0, C_AUL = 32, C_ADH = 64, C_ADL = 96, C_ASTAGE = 128;
+    static constexpr int C_D0 = 256, C_DZ = 0, C_DDZ = 32, C_DY = 64, C_DREGION = 96;
     static_assert(RW == 64 && NBLK * 128 == RH * RW, "blocks of two 64-pixel region rows");
     static_assert(NF_MAX <= 32, "one N = 32 MMA covers the bank");
 };
@@ -32,8 +47,23 @@ struct TcCfg {
 template <int NF_MAX>
 __host__ __device__ constexpr size_t tc_smem_floats() {
     using T = TcCfg<NF_MAX>;
-    // Un, Du staged planes; Kf hi/lo, Kt hi/lo; Y ring; region gradient
-    return 2 * (size_t)T::PLANE + 4 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW;
+    // Un, Du staged planes; Kf hi/lo, Kt hi/lo; Y ring; region gradient (two tap halves); alpha, tap 24, 2 alpha
+    return 2 * (size_t)T::PLANE + 4 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96;
+}
+
+// sum over taps [T0, T1) of Y(row r + a - R, column c + b - R)[a M + b] from the Y ring
+template <int T0, int T1, class T>
+__device__ __forceinline__ float tc_tap_sum(const float *Yr, int r, int c) {
+    float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll
+    for (int t = T0; t < T1; ++t) {
+        const int aa = t / 5, bb = t % 5;
+        const int rr = r + aa - T::R;
+        if (rr < 0 || rr >= T::RH) continue;
+        const float v = Yr[(t * T::YROWS + rr % T::YROWS) * T::YW + 2 + c - T::R + bb];
+        if (t & 1) s1 += v; else s0 += v;
+    }
+    return s0 + s1;
 }
 
 template <int NF, bool TRIAL, bool SYM>
@@ -41,22 +71,20 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     static_assert(NF % 8 == 0 && NF <= 32, "filter count rounded up to a multiple of 8");
     using T = TcCfg<32>;
     using C = PassCfg<5>;
-    constexpr int NT = T::NT, R = T::R, SW = T::SW;
+    constexpr int NT = T::NT, R = T::R, SW = T::SW, NBLK = T::NBLK;
     extern __shared__ __align__(128) float sm[];
     __shared__ double red[NT / 32][kNumPartials];
     __shared__ double s_sum[kNumPartials];
     __shared__ int s_last;
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) unsigned long long s_mma[T::NWG];       // MMA completion, per warpgroup
-    __shared__ __align__(8) unsigned long long s_ready[T::NBLK];    // Y of block j in the ring
+    __shared__ __align__(8) unsigned long long mb_dfull[2], mb_yfull[2];
+    __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK];
 
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int wg = tid / T::WGT, wt = tid % T::WGT;  // warpgroup, thread in warpgroup
-    const int hf = wt >> 7, pl = wt & 127;           // half (filters / taps), pixel = TMEM lane
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b = blockIdx.y;
+    const int nf = a.n_filters;
     const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3] = globaltimer_ns();
-    const int nf = a.n_filters;
     TrialParams p{};
     if (a.mode != MODE_EVAL) {
         const ImgCtl &c = a.ctl[b];
@@ -89,31 +117,40 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     float *Kf = Du + T::PLANE;     // [hi | lo], forward B (N = filters, K = taps)
     float *Kt = Kf + 2 * T::BSZ;   // [hi | lo], adjoint B (N = taps, K = filters)
     float *Yr = Kt + 2 * T::BSZ;   // Y ring [tap][ring row][YW]
-    float *Gr = Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold)
-    float *s_al = Gr + 2 * T::RH * T::RW;        // alpha_f, zero-padded to NF (Gr: two tap halves)
+    float *Gr = Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold), two tap halves
+    float *s_al = Gr + 2 * T::RH * T::RW;        // alpha_f, zero-padded
     float *s_k24 = s_al + 32;                    // tap 24 of each filter (outside the K = 24 MMAs)
+    float *s_al2 = s_k24 + 32;                   // 2 alpha_f
 
     if (warp == 0) tmem_alloc(&s_tmem, 512);
-    if (tid < T::NWG) mbar_init(&s_mma[tid], 1);
-    if (tid < T::NBLK) mbar_init(&s_ready[tid], T::WGT);
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&mb_dfull[s], 1);
+            mbar_init(&mb_yfull[s], 1);
+        }
+        for (int j = 0; j < NBLK; ++j) {
+            mbar_init(&mb_ring[j], 8);  // one arrival per warp of the point set
+            mbar_init(&mb_sum[j], 8);
+        }
+    }
     // B operands: Kf[f][t] = kf_f[t] (convolution orientation), Kt[t][f] = 2 a_f k_f[t] with the
-    // unflipped k_f[t] = kf_f[24 - t]; zero padding to 32 x 32; split into tf32 hi + fp32 lo
+    // unflipped k_f[t] = kf_f[24 - t]; zero padding to 32 x 32; split into tf32 hi + tf32 lo (both rounded to nearest)
     for (int e = tid; e < 32 * 32; e += NT) {
         const int n = e >> 5, k = e & 31;
         const float vf = (n < nf && k < T::KT) ? a.kf[n * T::KT + k] : 0.0f;
         const float vt = (k < nf && n < T::KT) ? 2.0f * a.alpha[k] * a.kf[k * T::KT + (T::KT - 1 - n)] : 0.0f;
-        const float hf = tf32_hi(vf), ht = tf32_hi(vt);
+        const float hf = tf32_rn(vf), ht = tf32_rn(vt);
         Kf[bsw_offset<32>(n, k)] = hf;
-        Kf[T::BSZ + bsw_offset<32>(n, k)] = vf - hf;
+        Kf[T::BSZ + bsw_offset<32>(n, k)] = tf32_rn(vf - hf);
         Kt[bsw_offset<32>(n, k)] = ht;
-        Kt[T::BSZ + bsw_offset<32>(n, k)] = vt - ht;
+        Kt[T::BSZ + bsw_offset<32>(n, k)] = tf32_rn(vt - ht);
     }
-    for (int e = tid; e < NF; e += NT) {
+    for (int e = tid; e < 32; e += NT) {
         s_al[e] = e < nf ? a.alpha[e] : 0.0f;
         s_k24[e] = e < nf ? a.kf[e * T::KT + 24] : 0.0f;
+        s_al2[e] = e < nf ? 2.0f * a.alpha[e] : 0.0f;
     }
-    // zero columns of the Y ring (padded positions outside the region)
-    for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {
+    for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {  // zero columns of the Y ring
         const int col = e & 3, rr = e >> 2;
         Yr[rr * T::YW + (col < 2 ? col : T::YW - 4 + col)] = 0.0f;
     }
@@ -121,8 +158,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     double acc[kNumPartials];
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
-    // prologue: stage u_new - shift and du for the region + r ring; all loads of a thread in flight
-    // before any use (cells strided by NT)
+    // ---- prologue: stage u_new - shift and du for the region + r ring (all loads in flight first) ----
     {
         constexpr int CPT = (C::NCELL + NT - 1) / NT;
         float lu[CPT], lup[CPT], lg[CPT], lob[CPT];
@@ -176,213 +212,262 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     __syncthreads();
     tc_fence_after();
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 1] = globaltimer_ns();
-
-    const uint32_t tbase = s_tmem + (uint32_t)(wg * T::C_WG);
-    const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
-    const uint32_t kf_hi = smem_u32(Kf), kf_lo = smem_u32(Kf + T::BSZ);
-    const uint32_t kt_hi = smem_u32(Kt), kt_lo = smem_u32(Kt + T::BSZ);
-    unsigned mma_phase = 0u;
-    double e_own = 0.0;
-    constexpr int FH = NF > 16 ? 16 : NF;  // filters per half (half 1 idles for NF <= 16)
-
-    // g(q) over one half of the taps: half 0 taps [0, 13), half 1 taps [13, 25)
-    auto shifted_sum = [&](int gb) {
-        const int r = 2 * gb + (pl >> 6), c = pl & 63;
-        float s = 0.0f;
-#pragma unroll
-        for (int t = 0; t < T::KT; ++t) {
-            if ((t < 13) != (hf == 0)) continue;
-            const int aa = t / 5, bb = t % 5;
-            const int rr = r + aa - R;
-            if (rr < 0 || rr >= T::RH) continue;
-            s += Yr[(t * T::YROWS + rr % T::YROWS) * T::YW + 2 + c - R + bb];
-        }
-        Gr[hf * T::RH * T::RW + r * T::RW + c] = s;
-    };
-
-    unsigned long long *ph = (a.dbg_times && blockIdx.x == 0 && blockIdx.y == 0 && wt == 0)
+    // the CTA owns all 512 columns (one CTA per SM), so the allocation starts at column 0: constant
+    // TMEM addresses keep the MMA operands in uniform registers
+    constexpr uint32_t tmem = 0u;
+    if (tid == 0 && s_tmem != 0u) __trap();
+    // per-block role stamps of CTA (0, 0) for the timing diagnostic: [block][im2col, fwd, point, sum]
+    unsigned long long *ph = (a.dbg_times && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0)
                                  ? a.dbg_times + 3 * (size_t)gridDim.x * gridDim.y : nullptr;
-    for (int blk = wg; blk < T::NBLK; blk += T::NWG) {
-        if (ph) ph[blk * 8 + 0] = globaltimer_ns();
-        const int lr = 2 * blk + (pl >> 6), lc = pl & 63;  // this thread's pixel (region-local)
-        const int gy = g.ry0 + lr, gx = g.rx0 + lc;
-        const bool in_img = !SYM || (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W);
-        const bool owned = gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1;
-        // ---- im2col into TMEM, taps 0..23 (K = 24): half 0 u_new, half 1 du ----
-        if (hf == 0 || TRIAL) {
-            float hi[32], lo[32];
-            const float *src = (hf ? Du : Un) + lr * SW + lc;
-#pragma unroll
-            for (int t = 0; t < 32; ++t) {
-                const float x = t < 24 ? src[(t / 5) * SW + (t % 5)] : 0.0f;
-                hi[t] = tf32_hi(x);
-                lo[t] = x - hi[t];
-            }
-            tmem_st32(tbase + lane_off + (hf ? T::C_ADH : T::C_AUH), hi);
-            tmem_st32(tbase + lane_off + (hf ? T::C_ADL : T::C_AUL), lo);
-        }
-        if (ph) ph[blk * 8 + 1] = globaltimer_ns();
-        tc_wait_st();
-        tc_fence_before();
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + wg), "r"(T::WGT) : "memory");
-        if (ph) ph[blk * 8 + 2] = globaltimer_ns();
-        if (wt == 0) {
-            tc_fence_after();
-            umma_3xtf32<32>(tbase + T::C_DZ, tbase + T::C_AUH, tbase + T::C_AUL, kf_hi, kf_lo, 3, false);
-            if (TRIAL) umma_3xtf32<32>(tbase + T::C_DDZ, tbase + T::C_ADH, tbase + T::C_ADL, kf_hi, kf_lo, 3, false);
-            umma_commit(&s_mma[wg]);
-        }
-        // while the forward MMAs run: shifted sums of block blk-3 (its Y neighbours finished an
-        // iteration ago; the 6-block ring keeps blk-4 .. blk+1 live)
-        if (blk >= 3) {
-            mbar_wait(&s_ready[blk - 3], 0);
-            shifted_sum(blk - 3);
-        }
-        // tap 24 (a = b = 4) on the CUDA cores: the MMAs cover K = 24
-        const float u24 = Un[(lr + 4) * SW + lc + 4];
-        const float d24 = TRIAL ? Du[(lr + 4) * SW + lc + 4] : 0.0f;
-        if (ph) ph[blk * 8 + 3] = globaltimer_ns();
-        mbar_wait(&s_mma[wg], mma_phase);
-        mma_phase ^= 1u;
-        tc_fence_after();
-        if (ph) ph[blk * 8 + 4] = globaltimer_ns();
-        // ---- pointwise on this half's filters [16 hf, 16 hf + 16): psi' -> Psi operand, then the
-        //      energy terms while the adjoint MMAs run ----
-        {
-            const int f0 = 16 * hf;
-            float z[16], dz[16];
-            tmem_ld16(tbase + lane_off + T::C_DZ + f0, z);
-            if (TRIAL) tmem_ld16(tbase + lane_off + T::C_DDZ + f0, dz);
-            tc_wait_ld();
-            float hi[16], lo[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int f = f0 + i;
-                if (i < FH && f < NF) {
-                    const float k24 = s_k24[f];
-                    z[i] = fmaf(k24, u24, z[i]);
-                    if (TRIAL) dz[i] = fmaf(k24, d24, dz[i]);
-                    const float zz = z[i];
-                    const float ps = in_img ? zz * rcp_approx(fmaf(zz, zz, 1.0f)) : 0.0f;
-                    hi[i] = tf32_hi(ps);
-                    lo[i] = ps - hi[i];
+    if (ph && tid == 0) ph[NBLK * 16] = clock64();  // loop start (cycles)
+
+    if (warp < T::W_PT) {
+        // ================= im2col: block j's A operands into stage j%2 =================
+        // warps 0-3 build A_u (warp 0 issues the forward MMAs), warps 4-7 A_du
+        const int pl = tid & 127, v = warp >> 2;  // pixel = TMEM lane; u / du
+        const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+        const uint32_t kf_hi = smem_u32(Kf), kf_lo = smem_u32(Kf + T::BSZ);
+        for (int j = 0; j < NBLK; ++j) {
+            const int s = j & 1;
+            if (j >= 2) {  // forward(j-2) consumed the stage: warp 0 polls the commit, relays to warps 1-7
+                if (warp == 0) {
+                    mbar_wait_sleep(&mb_dfull[s], ((j - 2) >> 1) & 1);
+                    named_arrive(T::BAR_AFREE + s, 256);
                 } else {
-                    hi[i] = 0.0f;
-                    lo[i] = 0.0f;
+                    named_sync(T::BAR_AFREE + s, 256);
                 }
             }
-            tmem_st16(tbase + lane_off + T::C_AUH + f0, hi);
-            tmem_st16(tbase + lane_off + T::C_AUL + f0, lo);
-            tc_wait_st();
-            tc_fence_before();
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + wg), "r"(T::WGT) : "memory");
-            if (wt == 0) {
-                tc_fence_after();
-                umma_3xtf32<32>(tbase + T::C_DZ, tbase + T::C_AUH, tbase + T::C_AUL, kt_hi, kt_lo, NF / 8, false);
-                umma_commit(&s_mma[wg]);
-            }
-            float e0 = 0.0f, e1 = 0.0f;
-            if (TRIAL) {
-                float tt[16];
-                float tmax = 0.0f;
+            tc_fence_after();
+            if (ph && warp == 0) ph[j * 16 + 5] = clock64();
+            const uint32_t st = tmem + s * T::C_ASTAGE + lane_off;
+            const int lr = 2 * j + (pl >> 6), lc = pl & 63;
+            if (v == 0 || TRIAL) {
+                const float *src = (v ? Du : Un) + lr * SW + lc;
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    if (!(i < FH && f0 + i < NF)) { tt[i] = 0.0f; continue; }
-                    const float zz = z[i], d = dz[i];
-                    const float zo = zz - d;
-                    const float num = d * fmaf(2.0f, zo, d);
-                    const float den = fmaf(zo, zo, fmaf(zz, zz, 2.0f));
-                    tt[i] = num * rcp_approx(den);
-                    tmax = fmaxf(tmax, fabsf(tt[i]));
-                }
-                if (__any_sync(0xffffffffu, tmax > 0.2f)) {
+                for (int h = 0; h < 2; ++h) {  // taps 16h .. 16h+15 (24..31 are the zero K padding)
+                    float hi[16], lo[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
-                        if (!(i < FH && f0 + i < NF)) continue;
-                        const float term = s_al[f0 + i] * two_atanh(tt[i]);
+                        const int t = 16 * h + i;
+                        const float x = t < 24 ? src[(t / 5) * SW + (t % 5)] : 0.0f;
+                        hi[i] = tf32_rn(x);
+                        lo[i] = tf32_rn(x - hi[i]);
+                    }
+                    tmem_st16(st + (v ? T::C_ADH : T::C_AUH) + 16 * h, hi);
+                    tmem_st16(st + (v ? T::C_ADL : T::C_AUL) + 16 * h, lo);
+                }
+                tc_wait_st();
+            }
+            tc_fence_before();
+            if (warp != 0) named_arrive(T::BAR_AFULL + s, 256);
+            if (warp == 0) {  // forward(j) once A is complete and block j-2 left the D region
+                const uint32_t sa = tmem + s * T::C_ASTAGE, sd = tmem + T::C_D0 + s * T::C_DREGION;
+                named_sync(T::BAR_AFULL + s, 256);
+                if (j >= 2) named_sync(T::BAR_DFREE + s, 288);
+                tc_fence_after();
+                if (ph) ph[j * 16 + 7] = clock64();
+                if (elect_one()) {
+                    umma_3xtf32<32>(sd + T::C_DZ, sa + T::C_AUH, sa + T::C_AUL, kf_hi, kf_lo, 3, false);
+                    if (TRIAL) umma_3xtf32<32>(sd + T::C_DDZ, sa + T::C_ADH, sa + T::C_ADL, kf_hi, kf_lo, 3, false);
+                    umma_commit(&mb_dfull[s]);
+                }
+                __syncwarp();
+                if (ph) ph[j * 16 + 0] = clock64();
+            }
+        }
+    } else {
+        // ================= pointwise: psi, energy terms, Y into the ring =================
+        const int q4 = warp & 3, hf = ((warp - T::W_PT) >> 2) & 1;  // lane quarter; filter / tap half
+        const int set = (warp - T::W_PT) >> 3;                        // blocks j = set (mod 2), stage set
+        const bool issuer = warp == T::W_PT + 8 * set;  // whole warp; one elected lane issues
+        const uint32_t kt_hi = smem_u32(Kt), kt_lo = smem_u32(Kt + T::BSZ);
+        const int pl = 32 * q4 + lane;
+        const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
+        constexpr int FH = NF / 2;  // filters per half, in chunks of 4
+        const int f0 = FH * hf;
+        double e_own = 0.0;
+        // g(q) over this warp's tap half (0..11 / 12..24) once Y(q-1 .. q+1) are in the ring
+        auto shifted_sum = [&](int q) {
+            if (ph && (warp - T::W_PT) % 8 == 0) ph[q * 16 + 8] = clock64();
+            for (int n = q - 1; n <= q + 1; ++n)
+                if (n >= 0 && n < NBLK) mbar_wait_sleep(&mb_ring[n], 0);
+            if (ph && (warp - T::W_PT) % 8 == 0) ph[q * 16 + 9] = clock64();
+            const int r = 2 * q + (pl >> 6), c = pl & 63;
+            const float gsum = hf ? tc_tap_sum<12, 25, T>(Yr, r, c) : tc_tap_sum<0, 12, T>(Yr, r, c);
+            if (ph && (warp - T::W_PT) % 8 == 0) { ph[q * 16 + 6] = clock64() + (long long)(gsum * 0.0f); }
+            Gr[hf * T::RH * T::RW + r * T::RW + c] = gsum;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&mb_sum[q]);
+            if (ph && (warp - T::W_PT) % 8 == 0) ph[q * 16 + 4] = clock64();
+        };
+        for (int j = set; j < NBLK; j += 2) {
+            const int s = set;
+            const uint32_t sd = tmem + T::C_D0 + s * T::C_DREGION + lane_off;
+            const int lr = 2 * j + (pl >> 6), lc = pl & 63;
+            const int gy = g.ry0 + lr, gx = g.rx0 + lc;
+            const bool in_img = !SYM || (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W);
+            const bool owned = gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1;
+            const float u24 = Un[(lr + 4) * SW + lc + 4];
+            const float d24 = TRIAL ? Du[(lr + 4) * SW + lc + 4] : 0.0f;
+            if (issuer) {  // the set's first warp polls the forward commit and relays it to the set
+                mbar_wait_sleep(&mb_dfull[s], (j >> 1) & 1);
+                named_arrive(T::BAR_DFULL + s, 256);
+            } else {
+                named_sync(T::BAR_DFULL + s, 256);
+            }
+            tc_fence_after();
+            const bool pst = ph && (warp - T::W_PT) % 8 == 0;
+            if (pst) { ph[j * 16 + 1] = clock64(); ph[j * 16 + 10] = clock64(); }
+            // this half's filters: all z / dz loads in flight at once; psi' (tf32 hi / lo, written over
+            // the z / dz columns as the adjoint's A operand, whose K covers filters < NF only) and the
+            // atanh arguments for every filter with full ILP; Psi is handed to the adjoint MMA before
+            // the energy series are evaluated
+            float z[FH], dz[FH];
+#pragma unroll
+            for (int c = 0; c < FH / 4; ++c) {
+                tmem_ld4(sd + T::C_DZ + f0 + 4 * c, *reinterpret_cast<float(*)[4]>(&z[4 * c]));
+                if (TRIAL) tmem_ld4(sd + T::C_DDZ + f0 + 4 * c, *reinterpret_cast<float(*)[4]>(&dz[4 * c]));
+            }
+            tc_wait_ld();
+            if (pst) ph[j * 16 + 11] = clock64();
+            float tmax = 0.0f;
+#pragma unroll
+            for (int i = 0; i < FH; ++i) {
+                const float k24 = s_k24[f0 + i];
+                const float zz = fmaf(k24, u24, z[i]);  // tap 24
+                float ps;
+                if (TRIAL) {
+                    const float d = fmaf(k24, d24, dz[i]);
+                    const float zo = zz - d;
+                    // one reciprocal for 1/(1+z^2) (psi') and 1/(2+z^2+zo^2) (the atanh argument)
+                    const float a1 = fmaf(zz, zz, 1.0f);
+                    const float b1 = fmaf(zo, zo, a1) + 1.0f;
+                    const float r = rcp_approx(a1 * b1);
+                    ps = zz * (r * b1);
+                    dz[i] = (d * fmaf(2.0f, zo, d)) * (r * a1);  // t = (z^2 - zo^2) / (2 + z^2 + zo^2)
+                    tmax = fmaxf(tmax, fabsf(dz[i]));
+                } else {
+                    ps = zz * rcp_approx(fmaf(zz, zz, 1.0f));
+                    dz[i] = zz;  // keep z for log1p(z^2)
+                }
+                z[i] = in_img ? ps : 0.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < FH / 4; ++c) {
+                float hi[4], lo[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    hi[i] = tf32_rn(z[4 * c + i]);
+                    lo[i] = tf32_rn(z[4 * c + i] - hi[i]);
+                }
+                tmem_st4(sd + T::C_DZ + f0 + 4 * c, hi);
+                tmem_st4(sd + T::C_DDZ + f0 + 4 * c, lo);
+            }
+            if (pst) ph[j * 16 + 12] = clock64();
+            tc_wait_st();
+            if (pst) ph[j * 16 + 13] = clock64();
+            tc_fence_before();
+            if (!issuer) named_arrive(T::BAR_PFULL + s, 256);
+            if (issuer) {  // adjoint(j) once both halves of all four lane quarters wrote Psi
+                const uint32_t sb = tmem + T::C_D0 + s * T::C_DREGION;
+                named_sync(T::BAR_PFULL + s, 256);
+                tc_fence_after();
+                if (pst) ph[j * 16 + 14] = clock64();
+                if (elect_one()) {
+                    umma_3xtf32<32>(sb + T::C_DY, sb + T::C_DZ, sb + T::C_DDZ, kt_hi, kt_lo, NF / 8, false);
+                    umma_commit(&mb_yfull[s]);
+                }
+                __syncwarp();
+                if (ph) ph[j * 16 + 2] = clock64();
+            }
+            // energy terms while the adjoint MMAs run
+            float e0 = 0.0f, e1 = 0.0f;
+            if (TRIAL) {
+                if (__any_sync(0xffffffffu, tmax > 0.2f)) {
+#pragma unroll
+                    for (int i = 0; i < FH; ++i) {
+                        const float term = s_al[f0 + i] * two_atanh(dz[i]);
                         if (i & 1) e1 += term; else e0 += term;
                     }
                 } else {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        if (!(i < FH && f0 + i < NF)) continue;
-                        const float t1 = tt[i], sq = t1 * t1;
+                    for (int i = 0; i < FH; ++i) {
+                        const float t1 = dz[i], sq = t1 * t1;
                         float pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
                         pp = fmaf(sq, pp, 1.0f / 5.0f);
                         pp = fmaf(sq, pp, 1.0f / 3.0f);
                         pp = fmaf(sq, pp, 1.0f);
-                        const float term = (2.0f * s_al[f0 + i]) * t1 * pp;
-                        if (i & 1) e1 += term; else e0 += term;
+                        const float w = s_al2[f0 + i] * t1;  // 2 alpha t
+                        if (i & 1) e1 = fmaf(w, pp, e1); else e0 = fmaf(w, pp, e0);
                     }
                 }
             } else {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    if (!(i < FH && f0 + i < NF)) continue;
-                    const float term = s_al[f0 + i] * log1pf(z[i] * z[i]);
+                for (int i = 0; i < FH; ++i) {
+                    const float term = s_al[f0 + i] * log1pf(dz[i] * dz[i]);
                     if (i & 1) e1 += term; else e0 += term;
                 }
             }
             if (owned) e_own += (double)(e0 + e1);
-        }
-        if (ph) ph[blk * 8 + 5] = globaltimer_ns();
-        mbar_wait(&s_mma[wg], mma_phase);
-        mma_phase ^= 1u;
-        tc_fence_after();
-        if (ph) ph[blk * 8 + 6] = globaltimer_ns();
-        // ---- Y rows of this block into the ring: half 0 taps 0..15, half 1 taps 16..24 ----
-        {
+            // Y of this block: half 0 taps 0..15, half 1 taps 16..24
+            if (issuer) {
+                mbar_wait_sleep(&mb_yfull[s], (j >> 1) & 1);
+                named_arrive(T::BAR_YFULL + s, 256);
+            } else {
+                named_sync(T::BAR_YFULL + s, 256);
+            }
+            tc_fence_after();
             float y[16];
-            tmem_ld16(tbase + lane_off + T::C_DZ + 16 * hf, y);
+            if (pst) ph[j * 16 + 15] = clock64();
+            tmem_ld16(sd + T::C_DY + 16 * hf, y);
             tc_wait_ld();
+            tc_fence_before();
+            if (j + 2 < NBLK) named_arrive(T::BAR_DFREE + s, 288);  // the D region is free for block j + 2
+            // the ring slot held Y(j-4): g(j-5), g(j-3) were summed by this set, g(j-4) by the other
+            if (j >= T::RING) mbar_wait_sleep(&mb_sum[j - T::RING], 0);
             float *yrow = Yr + (lr % T::YROWS) * T::YW + 2 + lc;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 const int t = 16 * hf + i;
                 if (t < T::KT) yrow[t * T::YROWS * T::YW] = y[i];
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&mb_ring[j]);
+            if (ph && (warp - T::W_PT) % 8 == 0) ph[j * 16 + 3] = clock64();
+            if (j >= 1) shifted_sum(j - 1);
         }
-        tc_fence_before();
-        mbar_arrive(&s_ready[blk]);
-        if (ph) ph[blk * 8 + 7] = globaltimer_ns();
+        if (set == ((NBLK - 1) & 1)) shifted_sum(NBLK - 1);
+        acc[0] = e_own;
     }
-    // the last three blocks' rows (their later Y neighbours exist only now)
-    for (int gb = T::NBLK - 3 + wg; gb < T::NBLK; gb += T::NWG) {
-        for (int q = gb - 1; q <= gb + 1; ++q)
-            if (q >= 0 && q < T::NBLK) mbar_wait(&s_ready[q], 0);
-        shifted_sum(gb);
-    }
-    acc[0] = e_own;
     tc_fence_before();
     __syncthreads();
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
-    if (warp == 0) tmem_dealloc(s_tmem, 512);
+    if (warp == 0) tmem_dealloc(tmem, 512);
 
     // ---- fold padded pixels (symmetric rule) and write the owned gradient ----
-    {
-        const int xx = tid % T::RW;
+    for (int k = tid; k < T::RW * 8; k += NT) {
+        const int xx = k % T::RW, rows0 = k / T::RW;
         const int gx = g.c0 + xx;
-        if (gx < g.c1) {
-            const int lx = gx - g.rx0;
-            int mx = -1;
+        if (gx >= g.c1) continue;
+        const int lx = gx - g.rx0;
+        int mx = -1;
+        if (SYM) {
+            if (gx < R) mx = (-1 - gx) - g.rx0;
+            else if (gx >= a.W - R) mx = (2 * a.W - 1 - gx) - g.rx0;
+        }
+        for (int gy = g.s0 + rows0; gy < g.s1; gy += 8) {
+            const int ly = gy - g.ry0;
+            auto gr = [&](int yy, int xx2) { return Gr[yy * T::RW + xx2] + Gr[T::RH * T::RW + yy * T::RW + xx2]; };
+            float val = gr(ly, lx);
             if (SYM) {
-                if (gx < R) mx = (-1 - gx) - g.rx0;
-                else if (gx >= a.W - R) mx = (2 * a.W - 1 - gx) - g.rx0;
+                int my = -1;
+                if (gy < R) my = (-1 - gy) - g.ry0;
+                else if (gy >= a.H - R) my = (2 * a.H - 1 - gy) - g.ry0;
+                if (my >= 0) val += gr(my, lx);
+                if (mx >= 0) val += gr(ly, mx);
+                if (my >= 0 && mx >= 0) val += gr(my, mx);
             }
-            for (int gy = g.s0 + tid / T::RW; gy < g.s1; gy += NT / T::RW) {
-                const int ly = gy - g.ry0;
-                auto gsum2 = [&](int yy, int xx2) { return Gr[yy * T::RW + xx2] + Gr[T::RH * T::RW + yy * T::RW + xx2]; };
-                float val = gsum2(ly, lx);
-                if (SYM) {
-                    int my = -1;
-                    if (gy < R) my = (-1 - gy) - g.ry0;
-                    else if (gy >= a.H - R) my = (2 * a.H - 1 - gy) - g.ry0;
-                    if (my >= 0) val += gsum2(my, lx);
-                    if (mx >= 0) val += gsum2(ly, mx);
-                    if (my >= 0 && mx >= 0) val += gsum2(my, mx);
-                }
-                gout[(size_t)(gy - a.lrow0) * a.W + gx] = val;
-            }
+            gout[(size_t)(gy - a.lrow0) * a.W + gx] = val;
         }
     }
 

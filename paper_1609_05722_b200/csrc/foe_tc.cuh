@@ -10,6 +10,11 @@
 //    A.B ~= A_hi.B_hi + A_lo.B_hi + A_hi.B_lo (3xTF32, the A_lo.B_lo term is below fp32 rounding).
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+// nearest tf32 (ties away from zero): the 3xTF32 split x = hi + lo with hi = rn(x), lo = rn(x - hi)
+// leaves |lo| <= 2^-11 |x| and a lo error <= 2^-22 |x| (the MMA truncates fp32 inputs to tf32)
+__device__ __forceinline__ float tf32_rn(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -72,6 +77,71 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
           "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
         : "r"(taddr)
         : "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const float (&v)[4]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3])
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                 : "r"(taddr)
+                 : "memory");
+}
+
+// mbarrier wait: a non-blocking probe, then probes with a short nanosleep backoff so waiting warps
+// leave the issue slots to the working ones
+__device__ __forceinline__ bool mbar_test(unsigned long long *bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    uint32_t ok;
+    asm volatile(
+        "{ .reg .pred p;\n"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    return ok != 0u;
+}
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long *bar, unsigned parity) {
+    while (!mbar_test(bar, parity)) __nanosleep(64);
+}
+
+// hardware named barriers: producers arrive without blocking, the consumer warp blocks in sync
+// (no issue slots spent waiting); every participant passes the same thread count
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// one lane of a converged warp (tcgen05.mma / commit are single-thread instructions; issuing them
+// from converged code keeps their operands in uniform registers)
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{ .reg .pred p;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, p; }"
+        : "=r"(pred));
+    return pred != 0u;
 }
 
 // UMMA shared-memory descriptor, K-major, SWIZZLE_NONE (sm_100 "version 1" format)
@@ -184,3 +254,56 @@ __global__ void __launch_bounds__(128) k_tc_selftest(const float *__restrict__ A
     __syncthreads();
     if (warp == 0) tmem_dealloc(tbase, 128);
 }
+
+// ------------------------------------------------------------------------------------------------
+// MMA issue/throughput probe: one thread issues nmma accumulating kind::tf32 MMAs (M = 128, N, K = 8)
+// with A in TMEM (ts = true) or shared memory, then waits for their commit; clock64 cycles -> out[0]
+
+__device__ __forceinline__ void umma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+template <int N, bool TS>
+__global__ void __launch_bounds__(128) k_tc_rate(int nmma, long long *out) {
+    __shared__ __align__(128) float sA[128 * 8];
+    __shared__ __align__(128) float sB[N * 8];
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) tmem_alloc(&s_tmem, 512);
+    if (tid == 0) mbar_init(&s_mbar, 1);
+    for (int e = tid; e < 128 * 8; e += 128) sA[e] = 0.0f;
+    for (int e = tid; e < N * 8; e += 128) sB[e] = 0.0f;
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t t0 = s_tmem;
+    if (warp == 0) {
+        const uint64_t bd = umma_desc_kmajor(smem_u32(sB), (N / 8) * 128, 128);
+        const uint64_t ad = umma_desc_kmajor(smem_u32(sA), (128 / 8) * 128, 128);
+        const uint32_t idesc = idesc_tf32(128, N);
+        const long long c0 = clock64();
+        if (elect_one()) {
+            for (int i = 0; i < nmma; ++i) {
+                if (TS) umma_tf32_ts(t0 + 256, t0, bd, idesc, i > 0);
+                else umma_tf32_ss(t0 + 256, ad, bd, idesc, i > 0);
+            }
+            umma_commit(&s_mbar);
+        }
+        __syncwarp();
+        mbar_wait(&s_mbar, 0);
+        const long long c1 = clock64();
+        if (tid == 0) out[0] = c1 - c0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(t0, 512);
+}
+

@@ -118,12 +118,14 @@ def test_fused_gradient_shapes_and_boundaries(shape, m, boundary):
     assert abs(fp.foe_energy(u, model) - ref_e) <= 1e-6 * abs(ref_e)
 
 
-def test_gradient_along_oracle_iterates():
+@pytest.mark.parametrize("kernel", ["ffma", "tc"])
+def test_gradient_along_oracle_iterates(monkeypatch, kernel):
     """Per-iteration gradient check (north_star, rel-L2 <= 1e-5): at oracle iterates u_k of a 256^2 foe_a solve.
 
     The device state is fp32, so the oracle gradient is taken at the same fp32-representable
     iterate; rounding u_k itself to fp32 moves the reference gradient by up to ~9e-6 near
     convergence (input quantisation, reported separately and not charged to the operator)."""
+    monkeypatch.setenv("FOE_TC", "1" if kernel == "tc" else "0")
     model = fp.load_packaged_model("foe_a")
     om = oracle_model(model)
     _, y = make_counts(256, 256, 0, 4.0)
@@ -288,6 +290,7 @@ def test_resident_solver_equals_per_pass_launches_bitwise(monkeypatch, shape, pe
     _, y = make_counts(*shape, 11, peak)
     req = fp.DenoiseRequest(noisy=y, peak=peak, model=model, variant=variant)
     cfg = fp.SolverConfig(rel_tol=0.0)
+    monkeypatch.setenv("FOE_TC", "0")  # the resident solver is the FFMA formulation
     monkeypatch.setenv("FOE_RESIDENT", "0")
     a = fp.denoise(req, cfg)
     monkeypatch.setenv("FOE_RESIDENT", "1")
@@ -329,11 +332,13 @@ def test_tcgen05_primitives_selftest():
     assert err < 1e-6, err
 
 
+@pytest.mark.parametrize("kernel", ["ffma", "tc"])
 @pytest.mark.parametrize("shape,boundary", [((47, 45), "symmetric"), ((130, 97), "symmetric"), ((512, 512), "symmetric"),
                                             ((200, 136), "periodic"), ((7, 9), "symmetric")])
-def test_tensor_core_gradient_vs_oracle(monkeypatch, shape, boundary):
-    """k_pass_tc (tcgen05 implicit GEMMs, 3xTF32): fused energy / gradient vs the C oracle."""
-    monkeypatch.setenv("FOE_TC", "1")
+def test_pass_kernel_gradient_vs_oracle(monkeypatch, shape, boundary, kernel):
+    """Both pass kernels -- k_pass (FFMA) and k_pass_tc (tcgen05 implicit GEMMs, 3xTF32) -- fused
+    energy / gradient vs the C oracle."""
+    monkeypatch.setenv("FOE_TC", "1" if kernel == "tc" else "0")
     rng = np.random.default_rng(hash((shape, boundary)) % 2 ** 32)
     if boundary == "symmetric":
         model = fp.load_packaged_model("foe_a")
@@ -350,23 +355,26 @@ def test_tensor_core_gradient_vs_oracle(monkeypatch, shape, boundary):
     assert abs(fp.foe_energy(u, model) - ref_e) <= 1e-6 * abs(ref_e)
 
 
+@pytest.mark.parametrize("kernel", ["ffma", "tc"])
 @pytest.mark.parametrize("branch", ["quadratic", None])
-def test_tensor_core_solve_cfg2_vs_oracle(monkeypatch, branch):
-    """Config 2 (512^2, peak 1) through the tensor-core pass: parity gates vs the oracle."""
-    monkeypatch.setenv("FOE_TC", "1")
+def test_pass_kernel_solve_cfg2_vs_oracle(monkeypatch, branch, kernel):
+    """Config 2 (512^2, peak 1) through each pass kernel: parity gates vs the oracle."""
+    monkeypatch.setenv("FOE_TC", "1" if kernel == "tc" else "0")
     model = fp.load_packaged_model("foe_a")
     x, y = make_counts(512, 512, 0, 1.0)
     ref = orc.denoise(y, 1.0, oracle_model(model), "transform", TABLE, force_branch=branch, rel_tol=0.0)
     r = fp.denoise(fp.DenoiseRequest(noisy=y, peak=1.0, model=model, variant="transform", force_branch=branch),
                    fp.SolverConfig(rel_tol=0.0))
     assert len(r.trace) == 150
-    _check_solve(r.image, ref["image"], 1.0, x, f"tc cfg2 {branch}")
+    _check_solve(r.image, ref["image"], 1.0, x, f"{kernel} cfg2 {branch}")
 
 
-def test_tensor_core_cfg1_vs_reference_golden(monkeypatch, golden):
-    monkeypatch.setenv("FOE_TC", "1")
+@pytest.mark.parametrize("kernel", ["ffma", "tc"])
+def test_pass_kernel_cfg1_vs_reference_golden(monkeypatch, golden, kernel):
+    """Config 1 through each pass kernel vs the reference's own output."""
+    monkeypatch.setenv("FOE_TC", "1" if kernel == "tc" else "0")
     g = golden("cfg1_256")
     x, y = make_counts(256, 256, 0, 4.0)
     r = fp.denoise(fp.DenoiseRequest(noisy=y, peak=4.0, model=fp.load_packaged_model("foe_a"),
                                      variant="transform", force_branch="quadratic"), fp.SolverConfig(rel_tol=0.0))
-    _check_solve(r.image, g["image"].astype(np.float64), 4.0, x, "tc cfg1")
+    _check_solve(r.image, g["image"].astype(np.float64), 4.0, x, f"{kernel} cfg1")

@@ -19,19 +19,26 @@ res = fp.solve_device(model, v, v, 0.6075, "quadratic", 150, fp.SolverConfig(rel
 L = _lib.lib()
 ws = res._workspace
 ncta = (-(-H // 32)) * (-(-W // 60))
-t = torch.zeros(ncta * 3 + 18 * 8, dtype=torch.int64, device="cuda")
+t = torch.zeros(ncta * 3 + 18 * 16 + 16, dtype=torch.int64, device="cuda")
 for _ in range(3):
     _lib.check(L.foe_debug_pass_times(res._bank.handle, 1, H, W, res._cap, ws.data_ptr(), ws.numel(), t.data_ptr(),
                                       torch.cuda.current_stream().cuda_stream))
 torch.cuda.synchronize()
 full = t.cpu().numpy()
 a = full[:ncta * 3].reshape(ncta, 3).astype(np.float64)
-phs = full[ncta * 3:].reshape(18, 8).astype(np.float64)
+phs = full[ncta * 3:ncta * 3 + 18 * 16].reshape(18, 16).astype(np.float64)
+loop0 = float(full[ncta * 3 + 18 * 16])
 if phs.any():
-    phs -= full[0]
-    np.set_printoptions(precision=2, suppress=True, linewidth=200)
-    print("block phases (us from CTA start): start, im2col-done, bar, fwd-issued(+g), fwd-done, psi+energy, adj-done, Y-done")
-    print(phs / 1e3)
+    np.set_printoptions(precision=0, suppress=True, linewidth=200)
+    cols = [0, 1, 2, 3, 4, 5, 6, 7, 8, 9]
+    print("block stamps (cycles from loop start), TC pass: fwd-issued, fwd-seen (point), adj-issued, Y-in-ring, "
+          "g-done, im2col-start, sum-loads-done, d_free-seen, sum-start, ring-seen")
+    tab = phs[:, cols] - loop0
+    tab[phs[:, cols] == 0] = -1
+    print(tab.astype(np.int64))
+    cyc = phs[:, 10:16]
+    print("point set cycles from fwd-seen: wait_ld, compute+st issued, wait_st, p_full seen (issuer), y_full seen")
+    print(np.stack([cyc[:, k] - cyc[:, 0] for k in range(1, 6)], axis=1).astype(np.int64))
 a -= a[:, 0].min()
 start, comp, end = a[:, 0] / 1e3, a[:, 1] / 1e3, a[:, 2] / 1e3
 dur = comp - start

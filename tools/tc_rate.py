@@ -1,0 +1,23 @@
+"""tcgen05 kind::tf32 MMA throughput probe (M = 128, K = 8): cycles per MMA for A in TMEM / smem."""
+import ctypes
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1609_05722_b200 import _lib  # noqa: E402
+
+L = _lib.lib()
+L.foe_debug_tc_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+out = torch.zeros(1, dtype=torch.int64, device="cuda")
+for ts in (1, 0):
+    for n in (32, 64, 128):
+        res = []
+        for nm in (1, 9, 27, 108):
+            for _ in range(2):
+                _lib.check(L.foe_debug_tc_rate(n, ts, nm, out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+            torch.cuda.synchronize()
+            res.append((nm, int(out.item())))
+        per = (res[-1][1] - res[1][1]) / (res[-1][0] - res[1][0])
+        print(f"{'TS' if ts else 'SS'} N={n}: " + ", ".join(f"{nm}->{c}" for nm, c in res) + f"  => {per:.1f} cycles/MMA")
