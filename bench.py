@@ -35,7 +35,9 @@ sys.path.insert(0, REPO)
 H = W = 512
 PEAK = 1.0
 N_FILT, K = 24, 5
-ALG_FLOP_PER_PX_IT = 4 * N_FILT * K * K  # forward + adjoint
+ALG_FLOP_PER_PX_IT = 4 * N_FILT * K * K
+_PEAKS_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")
+PEAKS = json.load(open(_PEAKS_PATH)) if os.path.exists(_PEAKS_PATH) else {}  # forward + adjoint
 METRIC = "Mpixel·iter/s of FoE solver (fp32, % FP32 peak); 512² denoise ms"
 CONFIG = {"workload": "cfg2: 512x512 synthetic, peak 1, transform/quadratic, foe_a 24x5x5, 150 iters",
           "model": "foe_a (24 filters 5x5, dct5, symmetric)", "image": "512x512", "peak": PEAK,
@@ -312,6 +314,17 @@ def main():
     fp32_peak_tflops = sm_count * 128 * 2 * peak_clock * 1e6 / 1e12
     alg_flop_pass = ALG_FLOP_PER_PX_IT * H * W
     achieved = alg_flop_pass / (pass_ms * 1e-3) / 1e12
+    use_tc = bool(L.foe_pass_uses_tensor_cores(K, N_FILT))
+    tensor = None
+    if use_tc:
+        # executed tcgen05 work of one trial pass: per 128-pixel block 2 x 9 forward (u, du) + 9 adjoint
+        # kind::tf32 MMAs of 128 x 32 x 8 (3xTF32, K = 24 taps / 24 filters), 18 blocks per 32 x 60 tile
+        ctas = -(-H // 32) * -(-W // 60)
+        mma_flop = ctas * 18 * 27 * 2 * 128 * 32 * 8
+        tf32_peak = PEAKS.get("bf16_tflops", 2 * 1125.0) / 2
+        tensor = {"executed_tflops": mma_flop / (pass_ms * 1e-3) / 1e12, "mma_flop_per_launch": mma_flop,
+                  "peak_tf32_tflops": tf32_peak, "frac": mma_flop / (pass_ms * 1e-3) / 1e12 / tf32_peak,
+                  "peak_source": "dense tf32 = 1/2 of MEASURED_PEAKS.json bf16_tflops (burst)"}
     solve_frac = value * 1e6 * ALG_FLOP_PER_PX_IT / (world * fp32_peak_tflops * 1e12)
 
     # end to end through the public API with host buffers (H2D counts, D2H image + transformed)
@@ -346,10 +359,13 @@ def main():
                 "algorithmic_fp32_frac": solve_frac,
                 "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
                              "frac": achieved / fp32_peak_tflops, "traffic": None,
-                             "kernel": "k_pass<5,TRIAL,SYM> (fused trial pass)", "pass_ms": pass_ms,
+                             "kernel": ("k_pass_tc<24,TRIAL,SYM> (fused trial pass, tcgen05 3xTF32 implicit GEMMs)"
+                                        if use_tc else "k_pass<5,TRIAL,SYM> (fused trial pass, FFMA)"),
+                             "pass_ms": pass_ms, "tensor": tensor,
                              "flop_per_launch": alg_flop_pass,
                              "peak_source": f"{sm_count} SMs x 128 FP32 lanes x 2 x {peak_clock} MHz (nominal; "
-                                            "MEASURED_PEAKS.json has no FP32 figure)"},
+                                            "MEASURED_PEAKS.json has no FP32 figure); achieved = algorithmic "
+                                            "fp32 flops (forward + adjoint, 2400 per pixel) / pass time"},
                 "e2e": {"value": e2e_value, "unit": "Mpixel*iter/s", "ms_per_denoise": float(e2e_t.item()),
                         "h2d_bytes_per_step": int(y.nbytes), "d2h_bytes_per_step": int(2 * y.nbytes)},
                 "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,

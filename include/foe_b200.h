@@ -134,6 +134,14 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfg, int B, int H, int
  * the last foe_solve in `workspace` without changing it (decisions suppressed). */
 int foe_bench_trial_pass(const foe_bank *bank, int B, int H, int W, int trace_cap, int reps,
                          void *workspace, size_t workspace_bytes, void *stream);
+/* which fused pass a bank of m x m filters, nf of them, runs on: 1 = k_pass_tc (tcgen05 3xTF32
+ * implicit GEMMs; 5 x 5 banks of <= 32 filters, default), 0 = k_pass (FFMA).  The environment
+ * variable FOE_TC=0 forces the FFMA pass, FOE_TC=1 the tensor-core pass where eligible. */
+int foe_pass_uses_tensor_cores(int m, int nf);
+/* diagnostics: cycles (clock64, into device out_cycles[0]) for one thread to issue `nmma`
+ * accumulating kind::tf32 MMAs of M = 128, N = n (32 / 64 / 128), K = 8, A in TMEM (ts = 1) or
+ * shared memory (ts = 0), and observe their commit */
+int foe_debug_tc_rate(int n, int ts, int nmma, long long *out_cycles, void *stream);
 /* diagnostics: the tcgen05 / TMEM primitives of the tensor-core pass on one 128 x 32 x 32 product,
  * D = A . B^T in 3xTF32 (A: 128 x 32, B: 32 x 32 row-major fp32 device arrays) */
 int foe_tc_selftest(const float *A, const float *B, float *D, void *stream);

@@ -110,6 +110,8 @@ def lib():
     L.foe_bench_trial_pass.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        _vp, ctypes.c_size_t, _vp]
     L.foe_tc_selftest.argtypes = [_vp, _vp, _vp, _vp]
+    L.foe_pass_uses_tensor_cores.argtypes = [ctypes.c_int, ctypes.c_int]
+    L.foe_debug_tc_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
     L.foe_debug_pass_times.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
                                        ctypes.c_size_t, _vp, _vp]
     _lib = L
@@ -130,6 +132,7 @@ EXPORTED_SYMBOLS = [
     "foe_bank_info", "foe_anscombe_forward", "foe_direct_obs", "foe_anscombe_inverse_exact_unbiased",
     "foe_prox_quadratic", "foe_prox_idiv", "foe_bin", "foe_unbin_bilinear", "foe_convolve_same", "foe_convolve_adjoint",
     "foe_eval_workspace_size", "foe_energy_grad", "foe_solve_workspace_size", "foe_solve",
-    "foe_bench_trial_pass", "foe_debug_pass_times", "foe_tc_selftest", "foe_tile_grid", "foe_band_geometry", "foe_band_describe", "foe_band_workspace_size",
+    "foe_bench_trial_pass", "foe_debug_pass_times", "foe_tc_selftest", "foe_pass_uses_tensor_cores",
+    "foe_debug_tc_rate", "foe_tile_grid", "foe_band_geometry", "foe_band_describe", "foe_band_workspace_size",
     "foe_band_buffers_get", "foe_band_begin", "foe_band_trial", "foe_band_commit", "foe_band_end",
 ]

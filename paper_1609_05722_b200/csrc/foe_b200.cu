@@ -545,9 +545,21 @@ int launch_pass_tc_t(const PassArgs &a, cudaStream_t st) {
         FOE_CUDA(cudaFuncSetAttribute(k_pass_tc<NF, TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured |= 1ull << (dev & 63);
     }
-    dim3 grid(a.tiles_x * a.tiles_yl, a.B);
-    k_pass_tc<NF, TRIAL, SYM><<<grid, T::NT, smem, st>>>(a);
-    FOE_CUDA(cudaGetLastError());
+    // programmatic dependent launch: this pass's CTAs may start (TMEM, barriers, B operands) while the
+    // previous kernel in the stream drains; the kernel waits (griddepcontrol.wait) before reading its
+    // state.  FOE_PDL=0 launches with plain stream order.
+    static const bool pdl = !(getenv("FOE_PDL") && getenv("FOE_PDL")[0] == '0');
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.tiles_x * a.tiles_yl, a.B);
+    cfg.blockDim = dim3(T::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    FOE_CUDA(cudaLaunchKernelEx(&cfg, k_pass_tc<NF, TRIAL, SYM>, a));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return FOE_OK;
 }
@@ -1205,6 +1217,8 @@ int foe_unbin_bilinear(const double *xb, double *out, int h, int w, int H, int W
     return FOE_OK;
 }
 
+
+int foe_pass_uses_tensor_cores(int m, int nf) { return use_tc(m, nf) ? 1 : 0; }
 
 int foe_debug_tc_rate(int n, int ts, int nmma, long long *out_cycles, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;

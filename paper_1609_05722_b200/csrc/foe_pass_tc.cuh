@@ -85,30 +85,9 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     const int nf = a.n_filters;
     const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3] = globaltimer_ns();
-    TrialParams p{};
-    if (a.mode != MODE_EVAL) {
-        const ImgCtl &c = a.ctl[b];
-        if (c.done && !a.no_decide) return;
-        p = trial_params(a, c);
-    }
-    const size_t ioff = (size_t)b * a.Hl * a.W;
-    const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
-    float *gout, *uout = nullptr;
-    if (a.mode == MODE_EVAL) {
-        uin = a.u_in + ioff;
-        gout = a.g_out + ioff;
-    } else {
-        uin = a.U + p.iu * a.plane + ioff;
-        if (TRIAL) {
-            upv = a.U + p.iup * a.plane + ioff;
-            gin = a.Gs + p.ig * a.plane + ioff;
-            obs = a.obs + ioff;
-            uout = a.U + p.inew * a.plane + ioff;
-            gout = a.Gs + p.ignew * a.plane + ioff;
-        } else {
-            gout = a.Gs + p.ig * a.plane + ioff;
-        }
-    }
+    // programmatic dependent launch: the next pass may be scheduled as soon as every CTA of this one
+    // has started; everything up to griddep_wait() below depends only on the launch arguments
+    griddep_launch_dependents();
     const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
     const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
 
@@ -153,6 +132,35 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {  // zero columns of the Y ring
         const int col = e & 3, rr = e >> 2;
         Yr[rr * T::YW + (col < 2 ? col : T::YW - 4 + col)] = 0.0f;
+    }
+    griddep_wait();  // the previous pass (control block, iterates, gradients, partials) is complete
+    TrialParams p{};
+    if (a.mode != MODE_EVAL) {
+        const ImgCtl &c = a.ctl[b];
+        if (c.done && !a.no_decide) {  // image converged: release TMEM and leave
+            __syncthreads();
+            if (warp == 0) tmem_dealloc(s_tmem, 512);
+            return;
+        }
+        p = trial_params(a, c);
+    }
+    const size_t ioff = (size_t)b * a.Hl * a.W;
+    const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
+    float *gout, *uout = nullptr;
+    if (a.mode == MODE_EVAL) {
+        uin = a.u_in + ioff;
+        gout = a.g_out + ioff;
+    } else {
+        uin = a.U + p.iu * a.plane + ioff;
+        if (TRIAL) {
+            upv = a.U + p.iup * a.plane + ioff;
+            gin = a.Gs + p.ig * a.plane + ioff;
+            obs = a.obs + ioff;
+            uout = a.U + p.inew * a.plane + ioff;
+            gout = a.Gs + p.ignew * a.plane + ioff;
+        } else {
+            gout = a.Gs + p.ig * a.plane + ioff;
+        }
     }
     const float shift = a.zero_mean ? __ldg(uin + (size_t)(g.s0 - a.lrow0) * a.W + g.c0) : 0.0f;
     double acc[kNumPartials];

@@ -1,5 +1,4 @@
 """tcgen05 kind::tf32 MMA throughput probe (M = 128, K = 8): cycles per MMA for A in TMEM / smem."""
-import ctypes
 import os
 import sys
 
@@ -9,7 +8,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1609_05722_b200 import _lib  # noqa: E402
 
 L = _lib.lib()
-L.foe_debug_tc_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
 out = torch.zeros(1, dtype=torch.int64, device="cuda")
 for ts in (1, 0):
     for n in (32, 64, 128):
