@@ -497,6 +497,25 @@ size_t pass_smem_bytes(int nf, bool trial, bool resident = false) {
     return sizeof(float) * smem_floats<M>(nf, trial, resident);
 }
 
+// programmatic dependent launch of a pass kernel: its CTAs may start (bank staging, TMEM, barriers)
+// while the previous kernel in the stream drains; the kernel waits (griddepcontrol.wait) before
+// reading the state that kernel wrote.  FOE_PDL=0 launches in plain stream order.
+template <class K>
+cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const PassArgs &a) {
+    static const bool pdl = !(getenv("FOE_PDL") && getenv("FOE_PDL")[0] == '0');
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 template <int M, bool TRIAL, bool SYM>
 int launch_pass_t(const PassArgs &a, cudaStream_t st) {
     using C = PassCfg<M>;
@@ -508,9 +527,7 @@ int launch_pass_t(const PassArgs &a, cudaStream_t st) {
         FOE_CUDA(cudaFuncSetAttribute(k_pass<M, TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured |= 1ull << (dev & 63);
     }
-    dim3 grid(a.tiles_x * a.tiles_yl, a.B);
-    k_pass<M, TRIAL, SYM><<<grid, C::NT, smem, st>>>(a);
-    FOE_CUDA(cudaGetLastError());
+    FOE_CUDA(launch_pdl(k_pass<M, TRIAL, SYM>, dim3(a.tiles_x * a.tiles_yl, a.B), dim3(C::NT), smem, st, a));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return FOE_OK;
 }
@@ -545,21 +562,7 @@ int launch_pass_tc_t(const PassArgs &a, cudaStream_t st) {
         FOE_CUDA(cudaFuncSetAttribute(k_pass_tc<NF, TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured |= 1ull << (dev & 63);
     }
-    // programmatic dependent launch: this pass's CTAs may start (TMEM, barriers, B operands) while the
-    // previous kernel in the stream drains; the kernel waits (griddepcontrol.wait) before reading its
-    // state.  FOE_PDL=0 launches with plain stream order.
-    static const bool pdl = !(getenv("FOE_PDL") && getenv("FOE_PDL")[0] == '0');
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(a.tiles_x * a.tiles_yl, a.B);
-    cfg.blockDim = dim3(T::NT);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    FOE_CUDA(cudaLaunchKernelEx(&cfg, k_pass_tc<NF, TRIAL, SYM>, a));
+    FOE_CUDA(launch_pdl(k_pass_tc<NF, TRIAL, SYM>, dim3(a.tiles_x * a.tiles_yl, a.B), dim3(T::NT), smem, st, a));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return FOE_OK;
 }

@@ -60,6 +60,10 @@ __device__ __forceinline__ float rcp_approx(float x) {  // MUFU.RCP, no denormal
     return r;
 }
 
+// programmatic dependent launch (the launch carries cudaLaunchAttributeProgrammaticStreamSerialization)
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
@@ -530,6 +534,16 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     const int b = blockIdx.y;
     const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3] = globaltimer_ns();
+    // programmatic dependent launch: the next pass may be scheduled once every CTA of this one has
+    // started; the bank staging below depends only on the launch arguments
+    griddep_launch_dependents();
+    const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
+    const TileGeom g = tile_geom<M, SYM>(a, tyl, txi);
+    const Smem<M> S(sm, a.n_filters, TRIAL);
+    stage_bank<M>(a, S);
+    if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG / 32);
+    if (g.edge) zero_psi_ring<M>(S);
+    griddep_wait();  // the previous pass (control block, iterates, gradients, partials) is complete
     TrialParams p{};
     if (a.mode != MODE_EVAL) {
         const ImgCtl &c = a.ctl[b];
@@ -556,12 +570,6 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
             gout = a.Gs + p.ig * a.plane + ioff;
         }
     }
-    const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
-    const TileGeom g = tile_geom<M, SYM>(a, tyl, txi);
-    const Smem<M> S(sm, a.n_filters, TRIAL);
-    stage_bank<M>(a, S);
-    if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG / 32);
-    if (g.edge) zero_psi_ring<M>(S);
     // Filters are zero-mean (DCT basis without DC, image.py:117-130), so K(u - c) == K u: staging
     // u - c with c = the tile's anchor pixel keeps the fp32 products small (accuracy, not speed).
     const float shift = a.zero_mean ? __ldg(uin + (size_t)(g.s0 - a.lrow0) * a.W + g.c0) : 0.0f;

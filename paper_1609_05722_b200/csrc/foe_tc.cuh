@@ -132,10 +132,6 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// programmatic dependent launch (the launch carries cudaLaunchAttributeProgrammaticStreamSerialization)
-__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
 // one lane of a converged warp (tcgen05.mma / commit are single-thread instructions; issuing them
 // from converged code keeps their operands in uniform registers)
 __device__ __forceinline__ bool elect_one() {
