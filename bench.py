@@ -329,16 +329,19 @@ def main():
 
     # end to end through the public API with host buffers (H2D counts, D2H image + transformed)
     e2e_ms = []
-    for i in range(max(1, min(args.steps, 5)) + 1):
+    n_e2e_warm = 3  # first calls grow the allocator cache and the pinned staging buffers
+    for i in range(max(1, min(args.steps, 5)) + n_e2e_warm):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         r = fp.denoise(fp.DenoiseRequest(noisy=y, peak=PEAK, model=model, variant="transform",
                                           force_branch="quadratic"), cfg)
         dt = time.perf_counter() - t0
-        if i:
+        if i >= n_e2e_warm:
             e2e_ms.append(dt * 1e3)
+    if os.environ.get("BENCH_DEBUG_E2E"):
+        print("e2e samples (ms):", [round(t, 3) for t in e2e_ms], file=sys.stderr)
     e2e_iters = len(r.trace)
-    e2e_t = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
+    e2e_t = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = world * H * W * e2e_iters / (float(e2e_t.item()) * 1e-3) / 1e6
@@ -367,7 +370,8 @@ def main():
                                             "MEASURED_PEAKS.json has no FP32 figure); achieved = algorithmic "
                                             "fp32 flops (forward + adjoint, 2400 per pixel) / pass time"},
                 "e2e": {"value": e2e_value, "unit": "Mpixel*iter/s", "ms_per_denoise": float(e2e_t.item()),
-                        "h2d_bytes_per_step": int(y.nbytes), "d2h_bytes_per_step": int(2 * y.nbytes)},
+                        "h2d_bytes_per_step": int(y.nbytes),
+                        "d2h_bytes_per_step": int(H * W * (8 + 4))},  # image (f64) + transformed (f32)
                 "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
                 "clocks": clk.summary(),
                 "cpu_baseline": cpu}
