@@ -94,6 +94,29 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def measure_ffma_peak(L, dev, index):
+    """FP32 FFMA TFLOP/s of this GPU from the library's probe kernel (best of 5, CUDA events), and
+    the median SM clock NVML saw while it ran."""
+    import ctypes
+
+    import torch
+    from paper_1609_05722_b200 import _lib
+    scratch = torch.zeros(1, dtype=torch.float32, device=dev)
+    flop = ctypes.c_double(0.0)
+    stream = torch.cuda.current_stream()
+    best = 0.0
+    with ClockSampler(index) as clk:
+        for rep in range(6):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _lib.check(L.foe_measure_ffma_peak(4096, scratch.data_ptr(), ctypes.byref(flop), stream.cuda_stream))
+            e1.record(stream)
+            e1.synchronize()
+            if rep:
+                best = max(best, flop.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best, clk.summary()["sm_mhz"]
+
+
 def cpu_oracle_rate(y, iters, threads=None):
     """Oracle port (fp64 C, OpenMP) on a truncated 512^2 solve: Mpixel*iter/s, seconds, cores."""
     from oracle import cpu as orc
@@ -311,7 +334,8 @@ def main():
     props = torch.cuda.get_device_properties(dev)
     sm_count = props.multi_processor_count
     peak_clock = clk.max_mhz or 1965.0
-    fp32_peak_tflops = sm_count * 128 * 2 * peak_clock * 1e6 / 1e12
+    fp32_nominal_tflops = sm_count * 128 * 2 * peak_clock * 1e6 / 1e12
+    fp32_peak_tflops, ffma_clk = measure_ffma_peak(L, dev, local_rank)
     alg_flop_pass = ALG_FLOP_PER_PX_IT * H * W
     achieved = alg_flop_pass / (pass_ms * 1e-3) / 1e12
     use_tc = bool(L.foe_pass_uses_tensor_cores(K, N_FILT))
@@ -366,9 +390,12 @@ def main():
                                         if use_tc else "k_pass<5,TRIAL,SYM> (fused trial pass, FFMA)"),
                              "pass_ms": pass_ms, "tensor": tensor,
                              "flop_per_launch": alg_flop_pass,
-                             "peak_source": f"{sm_count} SMs x 128 FP32 lanes x 2 x {peak_clock} MHz (nominal; "
-                                            "MEASURED_PEAKS.json has no FP32 figure); achieved = algorithmic "
-                                            "fp32 flops (forward + adjoint, 2400 per pixel) / pass time"},
+                             "peak_source": "measured: FFMA probe k_ffma_peak (independent FMA chains on every SM, "
+                                            f"CUDA events; SM clock {ffma_clk} MHz during the probe); nominal "
+                                            f"{sm_count} SMs x 128 lanes x 2 x {peak_clock} MHz = "
+                                            f"{fp32_nominal_tflops:.1f} TFLOP/s (MEASURED_PEAKS.json has no FP32 "
+                                            "figure); achieved = algorithmic fp32 flops (forward + adjoint, 2400 "
+                                            "per pixel) / pass time"},
                 "e2e": {"value": e2e_value, "unit": "Mpixel*iter/s", "ms_per_denoise": float(e2e_t.item()),
                         "h2d_bytes_per_step": int(y.nbytes),
                         "d2h_bytes_per_step": int(H * W * (8 + 4))},  # image (f64) + transformed (f32)

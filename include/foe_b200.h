@@ -134,6 +134,10 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfg, int B, int H, int
  * the last foe_solve in `workspace` without changing it (decisions suppressed). */
 int foe_bench_trial_pass(const foe_bank *bank, int B, int H, int W, int trace_cap, int reps,
                          void *workspace, size_t workspace_bytes, void *stream);
+/* FP32 FFMA throughput probe for the roofline denominator: launches a kernel of independent FMA
+ * chains on every SM; *flop_out receives the FLOPs it executes (time it with events on `stream`).
+ * `scratch` is one device float. */
+int foe_measure_ffma_peak(int iters, float *scratch, double *flop_out, void *stream);
 /* which fused pass a bank of m x m filters, nf of them, runs on: 1 = k_pass_tc (tcgen05 3xTF32
  * implicit GEMMs; 5 x 5 banks of <= 32 filters, default), 0 = k_pass (FFMA).  The environment
  * variable FOE_TC=0 forces the FFMA pass, FOE_TC=1 the tensor-core pass where eligible. */

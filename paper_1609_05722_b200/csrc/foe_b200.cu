@@ -673,6 +673,24 @@ thread_local PinnedFlags t_flags;
 
 }  // namespace
 
+// FP32 FFMA throughput probe: 8 independent FMA chains per thread, 4 warps per SMSP, enough CTAs for
+// every SM; the result feeds the roofline peak (MEASURED_PEAKS.json has no FP32 figure)
+__global__ void __launch_bounds__(512) k_ffma_peak(float *out, int iters, float a, float b) {
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3f + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = fmaf(x[i], a, b);
+    }
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == 1234.5f) out[0] = s;  // keeps the chains live
+}
+
 extern "C" {
 
 int foe_abi_version(void) { return 1; }
@@ -1220,6 +1238,18 @@ int foe_unbin_bilinear(const double *xb, double *out, int h, int w, int H, int W
     return FOE_OK;
 }
 
+
+
+int foe_measure_ffma_peak(int iters, float *scratch, double *flop_out, void *stream) {
+    int dev = 0, sms = 0;
+    FOE_CUDA(cudaGetDevice(&dev));
+    FOE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int blocks = sms * 4;
+    k_ffma_peak<<<blocks, 512, 0, (cudaStream_t)stream>>>(scratch, iters, 0.999f, 1e-4f);
+    FOE_CUDA(cudaGetLastError());
+    if (flop_out) *flop_out = 2.0 * 8 * 16 * (double)iters * 512 * blocks;
+    return FOE_OK;
+}
 
 int foe_pass_uses_tensor_cores(int m, int nf) { return use_tc(m, nf) ? 1 : 0; }
 
