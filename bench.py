@@ -94,6 +94,44 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def bench_fallback_bank(fp, _lib, L, y_dev, lam, cfg, stream, fp32_peak_tflops, H, W, steps=2):
+    """Config 2 with the 48 x 7 x 7 fallback bank: device-timed solves and the fused pass."""
+    import torch
+    from paper_1609_05722_b200.anscombe import forward_device
+    model = fp.load_packaged_model("foe_fallback48x7")
+    n, k = model.n_filters, model.basis.atoms.shape[-1]
+    v = forward_device(y_dev)
+    res = fp.solve_device(model, v, v, lam, "quadratic", cfg.max_iters, cfg)  # warm-up
+    ms, iters = 0.0, 0
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = fp.solve_device(model, forward_device(y_dev), v, lam, "quadratic", cfg.max_iters, cfg)
+        e1.record(stream)
+        e1.synchronize()
+        ms += e0.elapsed_time(e1)
+        iters += len(res.traces[0])
+    ws = res._workspace
+    reps = 20
+    _lib.check(L.foe_bench_trial_pass(res._bank.handle, 1, H, W, res._cap, 3, ws.data_ptr(), ws.numel(),
+                                      stream.cuda_stream))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    _lib.check(L.foe_bench_trial_pass(res._bank.handle, 1, H, W, res._cap, reps, ws.data_ptr(), ws.numel(),
+                                      stream.cuda_stream))
+    e1.record(stream)
+    e1.synchronize()
+    pass_ms = e0.elapsed_time(e1) / reps
+    flop_px_it = 4 * n * k * k
+    achieved = flop_px_it * H * W / (pass_ms * 1e-3) / 1e12
+    tc = bool(L.foe_pass_uses_tensor_cores(k, n))
+    return {"model": f"foe_fallback48x7 ({n} filters {k}x{k}, dct7, symmetric)", "ms_per_denoise": ms / steps,
+            "value": H * W * iters / (ms * 1e-3) / 1e6, "unit": "Mpixel*iter/s", "iterations": iters / steps,
+            "pass_ms": pass_ms, "alg_flop_per_px_it": flop_px_it,
+            "kernel": "k_pass_tc" if tc else f"k_pass<{k},TRIAL,SYM> (FFMA)",
+            "roofline_frac": achieved / fp32_peak_tflops, "achieved_tflops": achieved}
+
+
 def measure_ffma_peak(L, dev, index):
     """FP32 FFMA TFLOP/s of this GPU from the library's probe kernel (best of 5, CUDA events), and
     the median SM clock NVML saw while it ran."""
@@ -247,6 +285,7 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=8)
     ap.add_argument("--cpu-iters", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fallback", action="store_true", help="skip the 48x7x7 fallback-bank line")
     ap.add_argument("--pass-reps", type=int, default=100)
     ap.add_argument("--config", type=int, default=2, choices=[2, 4, 5],
                     help="2: 512^2 single image (headline); 4: 256 x 512^2 batch sharded over ranks; "
@@ -370,6 +409,12 @@ def main():
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = world * H * W * e2e_iters / (float(e2e_t.item()) * 1e-3) / 1e6
 
+    # the same workload with the BASELINE 48 x 7 x 7 fallback bank ("all configs
+    # repeat with the fallback bank"): 4 N k^2 = 9,408 algorithmic FLOP per pixel-iteration
+    fallback = None
+    if rank == 0 and not args.no_fallback:
+        fallback = bench_fallback_bank(fp, _lib, L, y_dev, lam, cfg, stream, fp32_peak_tflops, H, W)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, secs, cores = cpu_oracle_rate(y, args.cpu_iters)
@@ -401,6 +446,7 @@ def main():
                         "d2h_bytes_per_step": int(H * W * (8 + 4))},  # image (f64) + transformed (f32)
                 "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
                 "clocks": clk.summary(),
+                "fallback_48x7": fallback,
                 "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if world > 1:

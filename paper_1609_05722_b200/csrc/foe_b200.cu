@@ -673,6 +673,97 @@ thread_local PinnedFlags t_flags;
 
 }  // namespace
 
+// ------------------------------------------------------------------------------------------------
+// device-side solve loop: a CUDA graph whose conditional WHILE node runs [kGraphChunk trial passes ->
+// k_loop_cond] until no image is live, so the tail of a solve needs no host round trip.  n_active[1]
+// counts the passes the loop ran, n_active[2] flags the safety cap.
+
+constexpr int kGraphChunk = 8;
+
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, int *n_active, int cap) {
+    const int passes = (n_active[1] += kGraphChunk);
+    const bool live = n_active[0] > 0;
+    if (live && passes >= cap) n_active[2] = 1;
+    cudaGraphSetConditional(h, (live && passes < cap) ? 1u : 0u);
+}
+
+struct LoopGraph {
+    PassArgs key{};
+    int m = 0, sym = 0, cap = 0, tc = 0;  // tc: which pass kernel the graph captured
+    cudaGraphExec_t exec = nullptr;
+};
+
+struct LoopGraphCache {
+    std::vector<LoopGraph> entries;
+    cudaStream_t cap_stream = nullptr;
+    ~LoopGraphCache() {
+        for (auto &e : entries)
+            if (e.exec) cudaGraphExecDestroy(e.exec);
+        if (cap_stream) cudaStreamDestroy(cap_stream);
+    }
+};
+thread_local LoopGraphCache t_graphs;
+
+// the instantiated loop graph for these pass arguments (captured once, reused while the workspace,
+// shape and solver constants stay the same)
+int loop_graph(int m, bool sym, const PassArgs &a, int cap, cudaGraphExec_t *out) {
+    const int tc = use_tc(m, a.n_filters) ? 1 : 0;
+    for (auto &e : t_graphs.entries)
+        if (e.m == m && e.sym == (int)sym && e.cap == cap && e.tc == tc && !memcmp(&e.key, &a, sizeof(PassArgs))) {
+            *out = e.exec;
+            return FOE_OK;
+        }
+    if (getenv("FOE_GRAPH_DEBUG")) fprintf(stderr, "foe: capturing solve-loop graph (%zu cached)\n", t_graphs.entries.size());
+    if (!t_graphs.cap_stream) FOE_CUDA(cudaStreamCreateWithFlags(&t_graphs.cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    FOE_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    FOE_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    FOE_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaStream_t cs = t_graphs.cap_stream;
+    FOE_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    const long long before = g_launches.load();
+    int rc = FOE_OK;
+    for (int k = 0; k < kGraphChunk && rc == FOE_OK; ++k) rc = launch_pass(m, sym, a, cs);
+    if (rc == FOE_OK) k_loop_cond<<<1, 1, 0, cs>>>(h, a.n_active, cap);
+    cudaGraph_t captured = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cs, &captured);
+    g_launches.store(before);  // captured launches run (and are counted) per graph execution
+    if (rc != FOE_OK) {
+        cudaGraphDestroy(g);
+        return rc;
+    }
+    if (ce != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return fail(FOE_E_CUDA, "loop graph capture: %s", cudaGetErrorString(ce));
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) return fail(FOE_E_CUDA, "loop graph instantiate: %s", cudaGetErrorString(ie));
+    if (t_graphs.entries.size() >= 8) {
+        cudaGraphExecDestroy(t_graphs.entries.front().exec);
+        t_graphs.entries.erase(t_graphs.entries.begin());
+    }
+    LoopGraph e;
+    memcpy(&e.key, &a, sizeof(PassArgs));  // bytewise, padding included (the cache compares bytes)
+    e.m = m;
+    e.sym = sym;
+    e.cap = cap;
+    e.tc = tc;
+    e.exec = exec;
+    t_graphs.entries.push_back(e);
+    *out = exec;
+    return FOE_OK;
+}
+
 // FP32 FFMA throughput probe: 8 independent FMA chains per thread, 4 warps per SMSP, enough CTAs for
 // every SM; the result feeds the roofline peak (MEASURED_PEAKS.json has no FP32 figure)
 __global__ void __launch_bounds__(512) k_ffma_peak(float *out, int iters, float a, float b) {
@@ -958,7 +1049,10 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     const size_t HWB = (size_t)B * H * W;
     FOE_CUDA(cudaMemcpyAsync(a.ctl, hc.data(), sizeof(ImgCtl) * B, cudaMemcpyHostToDevice, st));
     FOE_CUDA(cudaMemsetAsync(a.tickets, 0, sizeof(unsigned) * B, st));
-    FOE_CUDA(cudaMemcpyAsync(a.n_active, &B, sizeof(int), cudaMemcpyHostToDevice, st));
+    {
+        const int live[4] = {B, 0, 0, 0};  // live images, loop-graph pass count, loop-graph cap flag
+        FOE_CUDA(cudaMemcpyAsync(a.n_active, live, sizeof(live), cudaMemcpyHostToDevice, st));
+    }
     FOE_CUDA(cudaMemcpyAsync(a.U, u0, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
     FOE_CUDA(cudaMemcpyAsync(a.U + 2 * a.plane, u0, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
     FOE_CUDA(cudaMemcpyAsync((float *)(ws + L.O), obs, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
@@ -967,7 +1061,7 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     // per-pass launches on B200 (grid barrier + redundant decisions cost what the launches did)
     const char *env = getenv("FOE_RESIDENT");
     const bool try_resident = B <= kResidentMaxB && env && env[0] == '1';
-    bool resident = false;
+    bool resident = false, graph_loop = false;
     if (try_resident) {
         FOE_CUDA(cudaMemsetAsync(a.grid_bar, 0, sizeof(unsigned) * 2, st));
         rc = launch_resident(bank->m, bank->boundary == FOE_SYMMETRIC, a, st);
@@ -979,6 +1073,19 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     a.mode = MODE_INIT;
     if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, st))) return rc;
 
+    static const bool use_graph = !(getenv("FOE_GRAPH") && getenv("FOE_GRAPH")[0] == '0');
+    if (use_graph) {
+        // every image needs >= 1 trial per accepted iteration: min_it passes straight away, then the
+        // device-side loop graph until no image is live
+        a.mode = MODE_TRIAL;
+        for (int k = 0; k < std::max(1, min_it); ++k)
+            if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, st))) return rc;
+        const int cap = max_it * 200 + 64;
+        cudaGraphExec_t exec = nullptr;
+        if ((rc = loop_graph(bank->m, bank->boundary == FOE_SYMMETRIC, a, cap, &exec))) return rc;
+        FOE_CUDA(cudaGraphLaunch(exec, st));
+        graph_loop = true;
+    } else {
     if (!t_flags.p) FOE_CUDA(cudaHostAlloc(&t_flags.p, 4 * sizeof(int), cudaHostAllocDefault));
     cudaEvent_t ev[2];
     FOE_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
@@ -1010,6 +1117,7 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     }
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
+    }  // host-polled loop
     }  // per-launch path
     {
         dim3 grid(std::max(1, std::min(148, (int)((size_t)H * W / 1024 + 1))), B);
@@ -1019,7 +1127,13 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     }
     FOE_CUDA(cudaMemcpyAsync(hc.data(), a.ctl, sizeof(ImgCtl) * B, cudaMemcpyDeviceToHost, st));
     FOE_CUDA(cudaMemcpyAsync(trace, a.trace, sizeof(double) * 6 * (size_t)B * trace_cap, cudaMemcpyDeviceToHost, st));
+    int loop_info[4] = {0, 0, 0, 0};
+    if (graph_loop) FOE_CUDA(cudaMemcpyAsync(loop_info, a.n_active, sizeof(loop_info), cudaMemcpyDeviceToHost, st));
     FOE_CUDA(cudaStreamSynchronize(st));
+    if (graph_loop) {
+        g_launches.fetch_add(loop_info[1] + loop_info[1] / kGraphChunk, std::memory_order_relaxed);
+        if (loop_info[2]) return fail(FOE_E_NUMERICAL, "solver did not terminate after %d passes", loop_info[1]);
+    }
     int any_fail = 0;
     for (int b = 0; b < B; ++b) {
         status[b].status = hc[b].status;
