@@ -47,8 +47,9 @@ struct TcCfg {
 template <int NF_MAX>
 __host__ __device__ constexpr size_t tc_smem_floats() {
     using T = TcCfg<NF_MAX>;
-    // Un, Du staged planes; Kf hi/lo, Kt hi/lo; Y ring; region gradient (two tap halves); alpha, tap 24, 2 alpha
-    return 2 * (size_t)T::PLANE + 4 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96;
+    // staged planes u hi/lo, du hi/lo; Kf hi/lo, Kt hi/lo; Y ring; region gradient (two tap halves); alpha,
+    // tap 24, 2 alpha
+    return 4 * (size_t)T::PLANE + 4 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96;
 }
 
 // sum over taps [T0, T1) of Y(row r + a - R, column c + b - R)[a M + b] from the Y ring
@@ -91,9 +92,12 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
     const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
 
-    float *Un = sm;
-    float *Du = Un + T::PLANE;
-    float *Kf = Du + T::PLANE;     // [hi | lo], forward B (N = filters, K = taps)
+    // staged planes, split once into tf32 hi + lo (both rounded to nearest): u_new - shift and du
+    float *Uh = sm;
+    float *Ul = Uh + T::PLANE;
+    float *Dh = Ul + T::PLANE;
+    float *Dl = Dh + T::PLANE;
+    float *Kf = Dl + T::PLANE;     // [hi | lo], forward B (N = filters, K = taps)
     float *Kt = Kf + 2 * T::BSZ;   // [hi | lo], adjoint B (N = taps, K = filters)
     float *Yr = Kt + 2 * T::BSZ;   // Y ring [tap][ring row][YW]
     float *Gr = Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold), two tap halves
@@ -187,7 +191,9 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             if (k >= C::NCELL) continue;
             const int i = k / C::CW, j = k - i * C::CW;
             if (!TRIAL) {
-                Un[i * SW + j] = lu[q] - shift;
+                const float x = lu[q] - shift, h = tf32_rn(x);
+                Uh[i * SW + j] = h;
+                Ul[i * SW + j] = tf32_rn(x - h);
                 continue;
             }
             const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
@@ -195,8 +201,11 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const float ut = (u - p.tau * gg) + p.gam * (u - lup[q]);  // solver.py:146-149
             const float un = (p.branch == FOE_QUADRATIC) ? prox_quad(ut, p.t, ob) : prox_idv(ut, p.t, ob);
             const float du = un - u;
-            Un[i * SW + j] = un - shift;
-            Du[i * SW + j] = du;
+            const float x = un - shift, h = tf32_rn(x), hd = tf32_rn(du);
+            Uh[i * SW + j] = h;
+            Ul[i * SW + j] = tf32_rn(x - h);
+            Dh[i * SW + j] = hd;
+            Dl[i * SW + j] = tf32_rn(du - hd);
             if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) {
                 uout[(size_t)(gy - a.lrow0) * a.W + gx] = un;
                 acc[1] += (double)du * (double)du;
@@ -250,16 +259,15 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const uint32_t st = tmem + s * T::C_ASTAGE + lane_off;
             const int lr = 2 * j + (pl >> 6), lc = pl & 63;
             if (v == 0 || TRIAL) {
-                const float *src = (v ? Du : Un) + lr * SW + lc;
+                const float *sh = (v ? Dh : Uh) + lr * SW + lc, *sl = (v ? Dl : Ul) + lr * SW + lc;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {  // taps 16h .. 16h+15 (24..31 are the zero K padding)
                     float hi[16], lo[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const int t = 16 * h + i;
-                        const float x = t < 24 ? src[(t / 5) * SW + (t % 5)] : 0.0f;
-                        hi[i] = tf32_rn(x);
-                        lo[i] = tf32_rn(x - hi[i]);
+                        hi[i] = t < 24 ? sh[(t / 5) * SW + (t % 5)] : 0.0f;
+                        lo[i] = t < 24 ? sl[(t / 5) * SW + (t % 5)] : 0.0f;
                     }
                     tmem_st16(st + (v ? T::C_ADH : T::C_AUH) + 16 * h, hi);
                     tmem_st16(st + (v ? T::C_ADL : T::C_AUL) + 16 * h, lo);
@@ -315,8 +323,9 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const int gy = g.ry0 + lr, gx = g.rx0 + lc;
             const bool in_img = !SYM || (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W);
             const bool owned = gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1;
-            const float u24 = Un[(lr + 4) * SW + lc + 4];
-            const float d24 = TRIAL ? Du[(lr + 4) * SW + lc + 4] : 0.0f;
+            // tap 24 by FFMA from hi + lo (2^-22 relative, as the tensor-core taps)
+            const float u24 = Uh[(lr + 4) * SW + lc + 4] + Ul[(lr + 4) * SW + lc + 4];
+            const float d24 = TRIAL ? Dh[(lr + 4) * SW + lc + 4] + Dl[(lr + 4) * SW + lc + 4] : 0.0f;
             if (issuer) {  // the set's first warp polls the forward commit and relays it to the set
                 mbar_wait_sleep(&mb_dfull[s], (j >> 1) & 1);
                 named_arrive(T::BAR_DFULL + s, 256);

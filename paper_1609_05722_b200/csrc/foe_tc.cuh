@@ -13,7 +13,9 @@ __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__flo
 // nearest tf32 (ties away from zero): the 3xTF32 split x = hi + lo with hi = rn(x), lo = rn(x - hi)
 // leaves |lo| <= 2^-11 |x| and a lo error <= 2^-22 |x| (the MMA truncates fp32 inputs to tf32)
 __device__ __forceinline__ float tf32_rn(float x) {
-    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
