@@ -134,6 +134,15 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfg, int B, int H, int
  * the last foe_solve in `workspace` without changing it (decisions suppressed). */
 int foe_bench_trial_pass(const foe_bank *bank, int B, int H, int W, int trace_cap, int reps,
                          void *workspace, size_t workspace_bytes, void *stream);
+/* ---- scoring (metrics.py:30-102) ------------------------------------
+ * Per image b of B (H x W fp64, row-major, device): psnr[b] and mssim[b] of x_hat against g after the
+ * reference's convention (both scaled by 255 / peak, data_range 255; 11 x 11 Gaussian window,
+ * sigma 1.5, valid-mode statistics, K1 = 0.01, K2 = 0.03).  fp64 arithmetic, fixed-order sums
+ * (deterministic).  H, W >= 11 (ValueError in the reference otherwise). */
+size_t foe_score_workspace_size(int B, int H, int W);
+int foe_score(const double *x_hat, const double *g, int B, int H, int W, double peak, double *psnr,
+              double *mssim, void *workspace, size_t workspace_bytes, void *stream);
+
 /* FP32 FFMA throughput probe for the roofline denominator: launches a kernel of independent FMA
  * chains on every SM; *flop_out receives the FLOPs it executes (time it with events on `stream`).
  * `scratch` is one device float. */

@@ -348,3 +348,47 @@ def denoise(noisy, peak, model: OracleModel, variant, table, lam="auto", zero_of
     u, tr = ipiano_foe(v, v, model, lam_v, branch, max_iters=iters, rel_tol=rel_tol)
     return {"image": anscombe_inverse_exact_unbiased(u), "branch": f"transform_{branch}", "lam": lam_v,
             "trace": tr, "transformed": u}
+
+
+# --- scoring (metrics.py:30-102) ---------------------------------------------------------------------
+
+SSIM_WINDOW, SSIM_SIGMA, SSIM_K1, SSIM_K2 = 11, 1.5, 0.01, 0.03
+
+
+def _ssim_window():
+    """metrics.py:41-45: normalised 1-D Gaussian (sigma 1.5), 2-D window = outer product."""
+    d = np.arange(SSIM_WINDOW) - (SSIM_WINDOW - 1) / 2
+    g = np.exp(-0.5 * (d / SSIM_SIGMA) ** 2)
+    g /= g.sum()
+    return np.outer(g, g)
+
+
+def _valid_filter(a, w):
+    """Valid-mode correlation with the (symmetric) window: sum_{a,b} w[a,b] x[i+a, j+b]."""
+    win = np.lib.stride_tricks.sliding_window_view(a, w.shape)
+    return np.einsum("ijab,ab->ij", win, w)
+
+
+def psnr(x_hat, g, data_range):
+    """metrics.py:30-38."""
+    mse = float(np.mean((np.asarray(x_hat, float) - np.asarray(g, float)) ** 2))
+    return float("inf") if mse == 0.0 else float(10.0 * np.log10(data_range ** 2 / mse))
+
+
+def mssim(x_hat, g, data_range):
+    """metrics.py:51-72: valid-mode local statistics, K1 = 0.01, K2 = 0.03."""
+    x, y = np.asarray(x_hat, float), np.asarray(g, float)
+    w = _ssim_window()
+    ux, uy = _valid_filter(x, w), _valid_filter(y, w)
+    vx = _valid_filter(x * x, w) - ux * ux
+    vy = _valid_filter(y * y, w) - uy * uy
+    vxy = _valid_filter(x * y, w) - ux * uy
+    c1, c2 = (SSIM_K1 * data_range) ** 2, (SSIM_K2 * data_range) ** 2
+    s = ((2 * ux * uy + c1) * (2 * vxy + c2)) / ((ux ** 2 + uy ** 2 + c1) * (vx + vy + c2))
+    return float(s.mean())
+
+
+def score_denoised(x_hat, g, peak):
+    """metrics.py:91-102: both mapped to [0, 255] by 255 / peak, data_range 255 -> (psnr, mssim)."""
+    scale = 255.0 / peak
+    return psnr(x_hat * scale, g * scale, 255.0), mssim(x_hat * scale, g * scale, 255.0)

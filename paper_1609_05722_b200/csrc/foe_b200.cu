@@ -19,6 +19,7 @@
 #include "foe_b200.h"
 
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #include <algorithm>
 #include <atomic>
@@ -764,6 +765,115 @@ int loop_graph(int m, bool sym, const PassArgs &a, int cap, cudaGraphExec_t *out
     return FOE_OK;
 }
 
+// ------------------------------------------------------------------------------------------------
+// scoring (metrics.py:30-102): PSNR and mean SSIM of x_hat against g after the [0, 255] convention
+// (both scaled by 255 / peak, data_range 255), fp64 throughout.  SSIM: 11 x 11 Gaussian window
+// (sigma 1.5, the outer product of the normalised 1-D window), valid-mode local statistics.  Per-CTA
+// fp64 partials are summed in a fixed order by k_score_final, so the result is deterministic.
+
+constexpr int kSsimW = 11, kSsimT = 32, kSsimIn = kSsimT + kSsimW - 1;
+__constant__ double c_ssim_g[kSsimW];
+
+__global__ void __launch_bounds__(256) k_ssim_tiles(const double *__restrict__ xh, const double *__restrict__ gt,
+                                                    int H, int W, double scale, double c1, double c2,
+                                                    double *__restrict__ part) {
+    extern __shared__ double ssm[];
+    double *X = ssm, *Y = X + kSsimIn * kSsimIn;          // scaled inputs of the tile
+    double *Hs = Y + kSsimIn * kSsimIn;                   // horizontal sums [5][kSsimIn][kSsimT]
+    const int b = blockIdx.z, tid = threadIdx.x;
+    const int Hv = H - kSsimW + 1, Wv = W - kSsimW + 1;
+    const int oy0 = blockIdx.y * kSsimT, ox0 = blockIdx.x * kSsimT;
+    const double *xb = xh + (size_t)b * H * W, *gb = gt + (size_t)b * H * W;
+    for (int e = tid; e < kSsimIn * kSsimIn; e += 256) {
+        const int r = e / kSsimIn, c = e - r * kSsimIn;
+        const int y = min(oy0 + r, H - 1), x = min(ox0 + c, W - 1);
+        X[e] = xb[(size_t)y * W + x] * scale;
+        Y[e] = gb[(size_t)y * W + x] * scale;
+    }
+    __syncthreads();
+    for (int e = tid; e < kSsimIn * kSsimT; e += 256) {
+        const int r = e / kSsimT, c = e - r * kSsimT;
+        double sx = 0, sy = 0, sxx = 0, syy = 0, sxy = 0;
+#pragma unroll
+        for (int k = 0; k < kSsimW; ++k) {
+            const double w = c_ssim_g[k], a = X[r * kSsimIn + c + k], d = Y[r * kSsimIn + c + k];
+            sx += w * a;
+            sy += w * d;
+            sxx += w * a * a;
+            syy += w * d * d;
+            sxy += w * a * d;
+        }
+        const int o = r * kSsimT + c, P = kSsimIn * kSsimT;
+        Hs[o] = sx;
+        Hs[P + o] = sy;
+        Hs[2 * P + o] = sxx;
+        Hs[3 * P + o] = syy;
+        Hs[4 * P + o] = sxy;
+    }
+    __syncthreads();
+    double acc = 0.0;
+    for (int e = tid; e < kSsimT * kSsimT; e += 256) {
+        const int r = e / kSsimT, c = e - r * kSsimT;
+        if (oy0 + r >= Hv || ox0 + c >= Wv) continue;
+        const int P = kSsimIn * kSsimT;
+        double ux = 0, uy = 0, mxx = 0, myy = 0, mxy = 0;
+#pragma unroll
+        for (int k = 0; k < kSsimW; ++k) {
+            const double w = c_ssim_g[k];
+            const int o = (r + k) * kSsimT + c;
+            ux += w * Hs[o];
+            uy += w * Hs[P + o];
+            mxx += w * Hs[2 * P + o];
+            myy += w * Hs[3 * P + o];
+            mxy += w * Hs[4 * P + o];
+        }
+        const double vx = mxx - ux * ux, vy = myy - uy * uy, vxy = mxy - ux * uy;
+        acc += ((2 * ux * uy + c1) * (2 * vxy + c2)) / ((ux * ux + uy * uy + c1) * (vx + vy + c2));
+    }
+    // fixed-order block sum
+    __shared__ double red[256];
+    red[tid] = acc;
+    __syncthreads();
+    for (int sft = 128; sft > 0; sft >>= 1) {
+        if (tid < sft) red[tid] += red[tid + sft];
+        __syncthreads();
+    }
+    if (tid == 0) part[((size_t)b * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(256) k_sqdiff(const double *__restrict__ xh, const double *__restrict__ gt,
+                                                int64_t n, double scale, double *__restrict__ part) {
+    const int b = blockIdx.y, tid = threadIdx.x;
+    const double *xb = xh + (size_t)b * n, *gb = gt + (size_t)b * n;
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * 256 + tid; i < n; i += (int64_t)gridDim.x * 256) {
+        const double d = xb[i] * scale - gb[i] * scale;
+        acc += d * d;
+    }
+    __shared__ double red[256];
+    red[tid] = acc;
+    __syncthreads();
+    for (int sft = 128; sft > 0; sft >>= 1) {
+        if (tid < sft) red[tid] += red[tid + sft];
+        __syncthreads();
+    }
+    if (tid == 0) part[(size_t)b * gridDim.x + blockIdx.x] = red[0];
+}
+
+// per image: PSNR from the squared-difference partials, mean SSIM from the tile partials
+__global__ void k_score_final(const double *__restrict__ sq_part, int n_sq, const double *__restrict__ ss_part,
+                              int n_ss, int64_t n_px, int64_t n_valid, double data_range, double *psnr,
+                              double *mssim) {
+    const int b = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    double sq = 0.0, ss = 0.0;
+    for (int i = 0; i < n_sq; ++i) sq += sq_part[(size_t)b * n_sq + i];
+    for (int i = 0; i < n_ss; ++i) ss += ss_part[(size_t)b * n_ss + i];
+    const double mse = sq / (double)n_px;
+    psnr[b] = mse == 0.0 ? CUDART_INF : 10.0 * log10(data_range * data_range / mse);
+    mssim[b] = ss / (double)n_valid;
+}
+
 // FP32 FFMA throughput probe: 8 independent FMA chains per thread, 4 warps per SMSP, enough CTAs for
 // every SM; the result feeds the roofline peak (MEASURED_PEAKS.json has no FP32 figure)
 __global__ void __launch_bounds__(512) k_ffma_peak(float *out, int iters, float a, float b) {
@@ -1362,6 +1472,47 @@ int foe_measure_ffma_peak(int iters, float *scratch, double *flop_out, void *str
     k_ffma_peak<<<blocks, 512, 0, (cudaStream_t)stream>>>(scratch, iters, 0.999f, 1e-4f);
     FOE_CUDA(cudaGetLastError());
     if (flop_out) *flop_out = 2.0 * 8 * 16 * (double)iters * 512 * blocks;
+    return FOE_OK;
+}
+
+size_t foe_score_workspace_size(int B, int H, int W) {
+    if (B < 1 || H < kSsimW || W < kSsimW) return 0;
+    const size_t tiles = (size_t)((W - kSsimW + 1 + kSsimT - 1) / kSsimT) * ((H - kSsimW + 1 + kSsimT - 1) / kSsimT);
+    return sizeof(double) * (size_t)B * (tiles + 256);
+}
+
+int foe_score(const double *x_hat, const double *g, int B, int H, int W, double peak, double *psnr,
+              double *mssim, void *workspace, size_t workspace_bytes, void *stream) {
+    if (B < 1 || H < kSsimW || W < kSsimW) return fail(FOE_E_INVALID, "images must be at least %d pixels per side", kSsimW);
+    if (!(peak > 0)) return fail(FOE_E_INVALID, "peak must be positive");
+    if (workspace_bytes < foe_score_workspace_size(B, H, W)) return fail(FOE_E_INVALID, "workspace too small");
+    static bool init = false;
+    if (!init) {  // metrics.py:41-45: normalised 1-D Gaussian, sigma 1.5; the 2-D window is its outer product
+        double gw[kSsimW], sum = 0.0;
+        for (int k = 0; k < kSsimW; ++k) {
+            const double d = k - (kSsimW - 1) / 2.0;
+            gw[k] = exp(-0.5 * (d / 1.5) * (d / 1.5));
+            sum += gw[k];
+        }
+        for (int k = 0; k < kSsimW; ++k) gw[k] /= sum;
+        FOE_CUDA(cudaMemcpyToSymbol(c_ssim_g, gw, sizeof(gw)));
+        FOE_CUDA(cudaFuncSetAttribute(k_ssim_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        init = true;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const double scale = 255.0 / peak, dr = 255.0;  // metrics.py:93-101 scoring convention
+    const int tx = (W - kSsimW + 1 + kSsimT - 1) / kSsimT, ty = (H - kSsimW + 1 + kSsimT - 1) / kSsimT;
+    double *ss_part = (double *)workspace, *sq_part = ss_part + (size_t)B * tx * ty;
+    const size_t smem = sizeof(double) * (2 * kSsimIn * kSsimIn + 5 * kSsimIn * kSsimT);
+    k_ssim_tiles<<<dim3(tx, ty, B), 256, smem, st>>>(x_hat, g, H, W, scale, (0.01 * dr) * (0.01 * dr),
+                                                     (0.03 * dr) * (0.03 * dr), ss_part);
+    FOE_CUDA(cudaGetLastError());
+    k_sqdiff<<<dim3(256, B), 256, 0, st>>>(x_hat, g, (int64_t)H * W, scale, sq_part);
+    FOE_CUDA(cudaGetLastError());
+    k_score_final<<<B, 32, 0, st>>>(sq_part, 256, ss_part, tx * ty, (int64_t)H * W,
+                                    (int64_t)(H - kSsimW + 1) * (W - kSsimW + 1), dr, psnr, mssim);
+    FOE_CUDA(cudaGetLastError());
+    g_launches.fetch_add(3, std::memory_order_relaxed);
     return FOE_OK;
 }
 

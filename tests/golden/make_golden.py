@@ -169,6 +169,39 @@ def main():
         print(name, r.branch, r.lam, len(r.trace), r.peak_used)
     np.savez_compressed(os.path.join(HERE, "binned.npz"), **out)
 
+    # --- scoring (metrics.py:30-102) and the evaluation grid (benchmark.py:32-122) ------------------
+    # benchmark.py imports data.py, which needs scikit-image (absent here) only for its image
+    # roster; the grid below passes its own loader, so a stub module satisfies the import
+    import types
+    if "skimage" not in sys.modules:
+        stub = types.ModuleType("skimage")
+        stub.data = types.ModuleType("skimage.data")
+        sys.modules["skimage"], sys.modules["skimage.data"] = stub, stub.data
+    from foepoisson import benchmark, metrics
+    out = {}
+    rng = np.random.default_rng(5)
+    for i, (H, W, peak) in enumerate([(11, 11, 1.0), (37, 53, 4.0), (64, 64, 0.5), (20, 90, 40.0)]):
+        g = rng.uniform(0, peak, size=(H, W))
+        xh = np.clip(g + rng.normal(scale=0.1 * peak, size=(H, W)), 0, None)
+        sc = metrics.score_denoised(xh, g, peak)
+        out[f"m{i}_xhat"], out[f"m{i}_g"] = xh, g
+        out[f"m{i}_ref"] = np.array([peak, sc.psnr_db, sc.mssim])
+    np.savez_compressed(os.path.join(HERE, "metrics.npz"), **out)
+    from paper_1609_05722_b200.evaluate import synthetic_eval_image
+    foe_s = fileio.load_packaged_model("foe_s")
+    spec = benchmark.BenchmarkSpec(images=("syn40x36s1", "syn33x47s2"), peaks=(0.5, 2.0, 8.0),
+                                   variants=("transform", "transform_binned", "direct"), transform_model=foe_a,
+                                   direct_model=foe_s, base_seed=7)
+    rows = benchmark.run_benchmark(spec, image_loader=synthetic_eval_image, workers=1)
+    out = {"rows_num": np.array([[r.peak, r.psnr_db, r.mssim, r.lam] for r in rows]),
+           "rows_key": np.array([f"{r.image}|{r.variant}|{r.branch}" for r in rows]),
+           "row_seeds": np.array([r.seed for r in rows], dtype=np.uint64),
+           "seeds": np.array([benchmark.job_seed(n, p, v, 7) for n in ("a", "syn40x36s1") for p in (0.5, 40.0)
+                              for v in ("transform", "direct")], dtype=np.uint64)}
+    np.savez_compressed(os.path.join(HERE, "bench_grid.npz"), **out)
+    for r in rows:
+        print("grid", r.image, r.peak, r.variant, r.branch, round(r.psnr_db, 4), round(r.mssim, 5))
+
     if os.environ.get("GOLDEN_SKIP_CFG1"):
         return
     # --- BASELINE config 1 at full size (256^2, peak 4, quadratic forced, foe_a) ----------------

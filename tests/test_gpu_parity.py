@@ -378,3 +378,50 @@ def test_pass_kernel_cfg1_vs_reference_golden(monkeypatch, golden, kernel):
     r = fp.denoise(fp.DenoiseRequest(noisy=y, peak=4.0, model=fp.load_packaged_model("foe_a"),
                                      variant="transform", force_branch="quadratic"), fp.SolverConfig(rel_tol=0.0))
     _check_solve(r.image, g["image"].astype(np.float64), 4.0, x, f"{kernel} cfg1")
+
+
+def test_device_scores_vs_reference_golden(golden):
+    """foe_score (PSNR / MSSIM, metrics.py:30-102) vs the reference's own scores."""
+    from paper_1609_05722_b200 import metrics
+    g = golden("metrics")
+    for i in range(4):
+        peak, ref_psnr, ref_mssim = g[f"m{i}_ref"]
+        r = metrics.score_denoised(g[f"m{i}_xhat"], g[f"m{i}_g"], peak)
+        assert abs(r.psnr_db - ref_psnr) <= 1e-10 * abs(ref_psnr), (i, r.psnr_db, ref_psnr)
+        assert abs(r.mssim - ref_mssim) <= 1e-12, (i, r.mssim, ref_mssim)
+    # batched scoring equals one call per image
+    x = np.stack([g["m2_xhat"], g["m2_g"] * 0.9])
+    y = np.stack([g["m2_g"], g["m2_g"]])
+    ps, ms = metrics.score_batch(x, y, 0.5)
+    assert ps[0] == metrics.score_batch(x[0], y[0], 0.5)[0][0] and ms[1] == metrics.score_batch(x[1], y[1], 0.5)[1][0]
+
+
+def test_evaluation_grid_vs_reference_golden(golden):
+    """benchmark.run_benchmark on a 2 images x 3 peaks x 3 variants grid: batched device solves give
+    the reference's rows (seeds, branches, lambdas exact; PSNR within the 0.01 dB gate)."""
+    from paper_1609_05722_b200 import evaluate as ev
+    g = golden("bench_grid")
+    spec = ev.BenchmarkSpec(images=("syn40x36s1", "syn33x47s2"), peaks=(0.5, 2.0, 8.0),
+                            variants=("transform", "transform_binned", "direct"),
+                            transform_model=fp.load_packaged_model("foe_a"),
+                            direct_model=fp.load_packaged_model("foe_s"), base_seed=7)
+    rows = ev.run_benchmark(spec)
+    assert [f"{r.image}|{r.variant}|{r.branch}" for r in rows] == list(g["rows_key"])
+    assert [r.seed for r in rows] == [int(s) for s in g["row_seeds"]]
+    num = g["rows_num"]
+    for r, (peak, psnr_ref, mssim_ref, lam_ref) in zip(rows, num):
+        assert r.peak == peak and r.lam == lam_ref
+        assert abs(r.psnr_db - psnr_ref) <= 0.01, (r, psnr_ref)
+        assert abs(r.mssim - mssim_ref) <= 1e-3, (r, mssim_ref)
+
+
+def test_cli_denoise_round_trip(tmp_path):
+    """python -m paper_1609_05722_b200 denoise (cli.py:63-85 shim) equals the API call."""
+    from paper_1609_05722_b200.__main__ import main
+    _, y = make_counts(40, 44, 5, 2.0)
+    np.save(tmp_path / "in.npy", y)
+    assert main(["denoise", str(tmp_path / "in.npy"), str(tmp_path / "out.npy"), "--peak", "2",
+                 "--trace", str(tmp_path / "t.csv")]) == 0
+    ref = fp.denoise(fp.DenoiseRequest(noisy=y, peak=2.0, model=fp.load_packaged_model("foe_a")))
+    np.testing.assert_array_equal(np.load(tmp_path / "out.npy"), ref.image)
+    assert (tmp_path / "t.csv").exists()
