@@ -422,6 +422,6 @@ def test_cli_denoise_round_trip(tmp_path):
     np.save(tmp_path / "in.npy", y)
     assert main(["denoise", str(tmp_path / "in.npy"), str(tmp_path / "out.npy"), "--peak", "2",
                  "--trace", str(tmp_path / "t.csv")]) == 0
-    ref = fp.denoise(fp.DenoiseRequest(noisy=y, peak=2.0, model=fp.load_packaged_model("foe_a")))
+    ref = fp.denoise(fp.DenoiseRequest(noisy=y, peak=2.0, model=fp.load_packaged_model("foe_a"), variant="transform"))
     np.testing.assert_array_equal(np.load(tmp_path / "out.npy"), ref.image)
     assert (tmp_path / "t.csv").exists()
