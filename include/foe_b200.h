@@ -162,6 +162,10 @@ int foe_tc_selftest(const float *A, const float *B, float *D, void *stream);
  * device `times` (3 x CTAs) */
 int foe_debug_pass_times(const foe_bank *bank, int B, int H, int W, int trace_cap, void *workspace,
                          size_t workspace_bytes, unsigned long long *times, void *stream);
+/* diagnostics: n_passes such passes back to back (stream order / PDL as in a solve), pass k recording
+ * into times + k * (3 x CTAs + 512) */
+int foe_debug_pass_times_seq(const foe_bank *bank, int B, int H, int W, int trace_cap, void *workspace,
+                             size_t workspace_bytes, unsigned long long *times, int n_passes, void *stream);
 
 
 /* ---- row-band decomposition (BASELINE config 5; reference has none) -------

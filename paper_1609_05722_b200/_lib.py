@@ -138,6 +138,6 @@ EXPORTED_SYMBOLS = [
     "foe_prox_quadratic", "foe_prox_idiv", "foe_bin", "foe_unbin_bilinear", "foe_convolve_same", "foe_convolve_adjoint",
     "foe_eval_workspace_size", "foe_energy_grad", "foe_solve_workspace_size", "foe_solve",
     "foe_bench_trial_pass", "foe_debug_pass_times", "foe_tc_selftest", "foe_pass_uses_tensor_cores",
-    "foe_debug_tc_rate", "foe_measure_ffma_peak", "foe_score_workspace_size", "foe_score", "foe_tile_grid", "foe_band_geometry", "foe_band_describe", "foe_band_workspace_size",
+    "foe_debug_tc_rate", "foe_measure_ffma_peak", "foe_debug_pass_times_seq", "foe_score_workspace_size", "foe_score", "foe_tile_grid", "foe_band_geometry", "foe_band_describe", "foe_band_workspace_size",
     "foe_band_buffers_get", "foe_band_begin", "foe_band_trial", "foe_band_commit", "foe_band_end",
 ]

@@ -1255,6 +1255,25 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     return any_fail ? fail(FOE_E_NUMERICAL, "numerical failure in at least one image") : FOE_OK;
 }
 
+int foe_debug_pass_times_seq(const foe_bank *bank, int B, int H, int W, int trace_cap, void *workspace,
+                             size_t workspace_bytes, unsigned long long *times, int n_passes, void *stream) {
+    int rc = check_dims(bank, B, H, W);
+    if (rc) return rc;
+    const SolveLayout L = solve_layout(bank->m, B, H, W, trace_cap);
+    if (workspace_bytes < L.total) return fail(FOE_E_INVALID, "workspace too small");
+    foe_solver_cfg cfg{0.8, 1.0, 1.2, 1.05, 1e-6, 1e15};
+    PassArgs a{};
+    fill_solve_args(a, bank, cfg, B, H, W, trace_cap, (char *)workspace, L);
+    a.mode = MODE_TRIAL;
+    a.no_decide = 1;
+    const size_t stride = 3 * (size_t)a.tiles_x * a.tiles_y * B + 512;
+    for (int k = 0; k < n_passes; ++k) {
+        a.dbg_times = times + k * stride;
+        if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, (cudaStream_t)stream))) return rc;
+    }
+    return FOE_OK;
+}
+
 int foe_debug_pass_times(const foe_bank *bank, int B, int H, int W, int trace_cap, void *workspace,
                          size_t workspace_bytes, unsigned long long *times, void *stream) {
     int rc = check_dims(bank, B, H, W);

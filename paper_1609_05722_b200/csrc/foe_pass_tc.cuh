@@ -10,16 +10,18 @@
 // A operands are written by their pixel's thread straight into TMEM (tcgen05.st), B operands sit in
 // shared memory, D accumulators in TMEM; fp32 accuracy from tf32 units via the 3xTF32 split.
 //
-// Warp-specialised pipeline over the 18 blocks of a tile; block j uses A stage j%2 (im2col operands)
-// and D region j%2 (its forward accumulators, Psi in place over them, its adjoint accumulator):
+// Warp-specialised pipeline over the 18 blocks of a tile; block j uses A stage j%2 (im2col operands,
+// 96 TMEM columns: u / du hi / lo, K = 24 each) and D region j%3 (its forward accumulators, Psi in
+// place over them, its adjoint accumulator; 3 x 96 columns):
 //   im2col (warps 0-7)      warps 0-3 A_u, warps 4-7 A_du of block j (once forward(j-2) released the
-//                           stage) -> a_full[s]; warp 0 issues forward(j) once the D region is free
-//                           (d_free[s]) -> d_full[s]
+//                           stage) -> a_full[s]; warp 0 issues forward(j) once block j-3 has left the
+//                           D region (d_free[j%3]) -> d_full[j%3]
 //   point set s (8 warps)   blocks j = s, s+2, ...: z, dz -> energy terms and Psi (written over z, dz)
-//                           -> p_full[s]; the set's first warp issues adjoint(j) -> y_full[s]; Y ->
-//                           d_free[s] -> shared ring -> ring_full[j]; then g(j-1) = shifted sum over
+//                           -> p_full[s]; the set's first warp issues adjoint(j) -> y_full[j%3]; Y ->
+//                           d_free[j%3] -> shared ring -> ring_full[j]; then g(j-1) = shifted sum over
 //                           the warp's tap half once Y(j-2 .. j) are in the ring -> sum_done[j-1]
-// so the tensor core, the operand build, two blocks' pointwise work and the shifted sums overlap.
+// so the tensor core, the operand build, two blocks' pointwise work and the shifted sums overlap; with
+// three D regions the region a set's next block needs was freed by the other set one block earlier.
 // Within a point set, warps w and w+4 share a TMEM lane quarter (same 32 pixels) and split the
 // filters (forward side, NF/2 each) and taps (adjoint side, 16 + 9).  24 warps: 80 registers/thread.
 
@@ -32,14 +34,14 @@ struct TcCfg {
     static constexpr int W_PT = 8, NWARPS = 24, NT = NWARPS * 32;
     // named barriers, one per stage / set: A complete, Psi complete, D region free, forward done (relayed
     // to the set), adjoint done (relayed to the set), A stage free (relayed to the im2col warps)
-    static constexpr int BAR_AFULL = 1, BAR_PFULL = 3, BAR_DFREE = 5, BAR_DFULL = 7, BAR_YFULL = 9, BAR_AFREE = 11;
+    static constexpr int BAR_AFULL = 1, BAR_PFULL = 3, BAR_DFULL = 5, BAR_YFULL = 7, BAR_AFREE = 9, BAR_DFREE = 11;
     static constexpr int RING = 4;                       // Y ring: 4 blocks = 8 region rows
     static constexpr int YROWS = 2 * RING, YW = RW + 4;  // 2 zero columns each side
     static constexpr int BSZ = 32 * 32;                  // one 32 x 32 B operand (floats)
     // TMEM columns: A stage s at 128 s (A_u hi/lo, A_du hi/lo); D region s at 256 + 96 s (D_z -> Psi hi,
     // D_dz -> Psi lo, D_y)
-    static constexpr int C_AUH = 0, C_AUL = 32, C_ADH = 64, C_ADL = 96, C_ASTAGE = 128;
-    static constexpr int C_D0 = 256, C_DZ = 0, C_DDZ = 32, C_DY = 64, C_DREGION = 96;
+    static constexpr int C_AUH = 0, C_AUL = 24, C_ADH = 48, C_ADL = 72, C_ASTAGE = 96;  // K = 24 columns each
+    static constexpr int C_D0 = 192, C_DZ = 0, C_DDZ = 32, C_DY = 64, C_DREGION = 96, NDREG = 3;
     static_assert(RW == 64 && NBLK * 128 == RH * RW, "blocks of two 64-pixel region rows");
     static_assert(NF_MAX <= 32, "one N = 32 MMA covers the bank");
 };
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     __shared__ double s_sum[kNumPartials];
     __shared__ int s_last;
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) unsigned long long mb_dfull[2], mb_yfull[2];
+    __shared__ __align__(8) unsigned long long mb_dfull[T::NDREG], mb_yfull[T::NDREG];
     __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -110,6 +112,10 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         for (int s = 0; s < 2; ++s) {
             mbar_init(&mb_dfull[s], 1);
             mbar_init(&mb_yfull[s], 1);
+            if (s == 1) {
+                mbar_init(&mb_dfull[2], 1);
+                mbar_init(&mb_yfull[2], 1);
+            }
         }
         for (int j = 0; j < NBLK; ++j) {
             mbar_init(&mb_ring[j], 8);  // one arrival per warp of the point set
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const int s = j & 1;
             if (j >= 2) {  // forward(j-2) consumed the stage: warp 0 polls the commit, relays to warps 1-7
                 if (warp == 0) {
-                    mbar_wait_sleep(&mb_dfull[s], ((j - 2) >> 1) & 1);
+                    mbar_wait_sleep(&mb_dfull[(j - 2) % T::NDREG], ((j - 2) / T::NDREG) & 1);
                     named_arrive(T::BAR_AFREE + s, 256);
                 } else {
                     named_sync(T::BAR_AFREE + s, 256);
@@ -260,32 +266,42 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const int lr = 2 * j + (pl >> 6), lc = pl & 63;
             if (v == 0 || TRIAL) {
                 const float *sh = (v ? Dh : Uh) + lr * SW + lc, *sl = (v ? Dl : Ul) + lr * SW + lc;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {  // taps 16h .. 16h+15 (24..31 are the zero K padding)
+                {  // taps 0..15
                     float hi[16], lo[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int t = 16 * h + i;
-                        hi[i] = t < 24 ? sh[(t / 5) * SW + (t % 5)] : 0.0f;
-                        lo[i] = t < 24 ? sl[(t / 5) * SW + (t % 5)] : 0.0f;
+                    for (int t = 0; t < 16; ++t) {
+                        hi[t] = sh[(t / 5) * SW + (t % 5)];
+                        lo[t] = sl[(t / 5) * SW + (t % 5)];
                     }
-                    tmem_st16(st + (v ? T::C_ADH : T::C_AUH) + 16 * h, hi);
-                    tmem_st16(st + (v ? T::C_ADL : T::C_AUL) + 16 * h, lo);
+                    tmem_st16(st + (v ? T::C_ADH : T::C_AUH), hi);
+                    tmem_st16(st + (v ? T::C_ADL : T::C_AUL), lo);
+                }
+                {  // taps 16..23 (tap 24 is done by FFMA)
+                    float hi[8], lo[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int t = 16 + i;
+                        hi[i] = sh[(t / 5) * SW + (t % 5)];
+                        lo[i] = sl[(t / 5) * SW + (t % 5)];
+                    }
+                    tmem_st8(st + (v ? T::C_ADH : T::C_AUH) + 16, hi);
+                    tmem_st8(st + (v ? T::C_ADL : T::C_AUL) + 16, lo);
                 }
                 tc_wait_st();
             }
             tc_fence_before();
             if (warp != 0) named_arrive(T::BAR_AFULL + s, 256);
-            if (warp == 0) {  // forward(j) once A is complete and block j-2 left the D region
-                const uint32_t sa = tmem + s * T::C_ASTAGE, sd = tmem + T::C_D0 + s * T::C_DREGION;
+            if (warp == 0) {  // forward(j) once A is complete and block j-3 left D region j%3
+                const int rg = j % T::NDREG;
+                const uint32_t sa = tmem + s * T::C_ASTAGE, sd = tmem + T::C_D0 + rg * T::C_DREGION;
                 named_sync(T::BAR_AFULL + s, 256);
-                if (j >= 2) named_sync(T::BAR_DFREE + s, 288);
+                if (j >= T::NDREG) named_sync(T::BAR_DFREE + rg, 288);
                 tc_fence_after();
                 if (ph) ph[j * 16 + 7] = clock64();
                 if (elect_one()) {
                     umma_3xtf32<32>(sd + T::C_DZ, sa + T::C_AUH, sa + T::C_AUL, kf_hi, kf_lo, 3, false);
                     if (TRIAL) umma_3xtf32<32>(sd + T::C_DDZ, sa + T::C_ADH, sa + T::C_ADL, kf_hi, kf_lo, 3, false);
-                    umma_commit(&mb_dfull[s]);
+                    umma_commit(&mb_dfull[rg]);
                 }
                 __syncwarp();
                 if (ph) ph[j * 16 + 0] = clock64();
@@ -317,8 +333,8 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             if (ph && (warp - T::W_PT) % 8 == 0) ph[q * 16 + 4] = clock64();
         };
         for (int j = set; j < NBLK; j += 2) {
-            const int s = set;
-            const uint32_t sd = tmem + T::C_D0 + s * T::C_DREGION + lane_off;
+            const int s = set, rg = j % T::NDREG;  // D region of this block
+            const uint32_t sd = tmem + T::C_D0 + rg * T::C_DREGION + lane_off;
             const int lr = 2 * j + (pl >> 6), lc = pl & 63;
             const int gy = g.ry0 + lr, gx = g.rx0 + lc;
             const bool in_img = !SYM || (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W);
@@ -327,7 +343,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const float u24 = Uh[(lr + 4) * SW + lc + 4] + Ul[(lr + 4) * SW + lc + 4];
             const float d24 = TRIAL ? Dh[(lr + 4) * SW + lc + 4] + Dl[(lr + 4) * SW + lc + 4] : 0.0f;
             if (issuer) {  // the set's first warp polls the forward commit and relays it to the set
-                mbar_wait_sleep(&mb_dfull[s], (j >> 1) & 1);
+                mbar_wait_sleep(&mb_dfull[rg], (j / T::NDREG) & 1);
                 named_arrive(T::BAR_DFULL + s, 256);
             } else {
                 named_sync(T::BAR_DFULL + s, 256);
@@ -386,13 +402,13 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             tc_fence_before();
             if (!issuer) named_arrive(T::BAR_PFULL + s, 256);
             if (issuer) {  // adjoint(j) once both halves of all four lane quarters wrote Psi
-                const uint32_t sb = tmem + T::C_D0 + s * T::C_DREGION;
+                const uint32_t sb = tmem + T::C_D0 + rg * T::C_DREGION;
                 named_sync(T::BAR_PFULL + s, 256);
                 tc_fence_after();
                 if (pst) ph[j * 16 + 14] = clock64();
                 if (elect_one()) {
                     umma_3xtf32<32>(sb + T::C_DY, sb + T::C_DZ, sb + T::C_DDZ, kt_hi, kt_lo, NF / 8, false);
-                    umma_commit(&mb_yfull[s]);
+                    umma_commit(&mb_yfull[rg]);
                 }
                 __syncwarp();
                 if (ph) ph[j * 16 + 2] = clock64();
@@ -428,7 +444,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             if (owned) e_own += (double)(e0 + e1);
             // Y of this block: half 0 taps 0..15, half 1 taps 16..24
             if (issuer) {
-                mbar_wait_sleep(&mb_yfull[s], (j >> 1) & 1);
+                mbar_wait_sleep(&mb_yfull[rg], (j / T::NDREG) & 1);
                 named_arrive(T::BAR_YFULL + s, 256);
             } else {
                 named_sync(T::BAR_YFULL + s, 256);
@@ -439,7 +455,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             tmem_ld16(sd + T::C_DY + 16 * hf, y);
             tc_wait_ld();
             tc_fence_before();
-            if (j + 2 < NBLK) named_arrive(T::BAR_DFREE + s, 288);  // the D region is free for block j + 2
+            if (j + T::NDREG < NBLK) named_arrive(T::BAR_DFREE + rg, 288);  // D region free for block j + 3
             // the ring slot held Y(j-4): g(j-5), g(j-3) were summed by this set, g(j-4) by the other
             if (j >= T::RING) mbar_wait_sleep(&mb_sum[j - T::RING], 0);
             float *yrow = Yr + (lr % T::YROWS) * T::YW + 2 + lc;
@@ -458,7 +474,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     }
     tc_fence_before();
     __syncthreads();
-    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
+    if (ph && tid == 0) ph[NBLK * 16 + 1] = clock64();  // loop end (cycles), CTA (0, 0)
     if (warp == 0) tmem_dealloc(tmem, 512);
 
     // ---- fold padded pixels (symmetric rule) and write the owned gradient ----
@@ -499,6 +515,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     __syncthreads();
     if (tid == 0) s_last = (atomicAdd(a.tickets + b, 1u) == (unsigned)(nlaunch - 1));
     __syncthreads();
+    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
     if (!s_last) return;
     __threadfence();
     reduce_tiles<NT>(a.partials, a.tiles_x * a.tiles_y, a.B, b, red, s_sum);
