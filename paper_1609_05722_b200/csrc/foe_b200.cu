@@ -621,7 +621,8 @@ int launch_resident(int m, bool sym, const PassArgs &a, cudaStream_t st) {
 
 void tile_counts(int m, int H, int W, int *tx, int *ty) {
     const int r = m / 2;
-    const int TH = PassCfg<1>::RH - 2 * r, TW = PassCfg<1>::RW - 2 * r;  // PassCfg<M>::TH / TW
+    const int RH = m == 7 ? PassCfg<7>::RH : PassCfg<1>::RH;  // region rows by filter size
+    const int TH = RH - 2 * r, TW = PassCfg<1>::RW - 2 * r;     // PassCfg<M>::TH / TW
     *ty = (H + TH - 1) / TH;
     *tx = (W + TW - 1) / TW;
 }
@@ -1328,7 +1329,7 @@ int foe_band_geometry(int m, int B, int H, int W, int ty0, int ty1, foe_band_des
     int tx, ty;
     tile_counts(m, H, W, &tx, &ty);
     if (ty0 < 0 || ty1 > ty || ty0 >= ty1) return fail(FOE_E_INVALID, "tile rows [%d, %d) outside [0, %d)", ty0, ty1, ty);
-    const int r = m / 2, T = PassCfg<1>::RH - 2 * r;
+    const int r = m / 2, T = (m == 7 ? PassCfg<7>::RH : PassCfg<1>::RH) - 2 * r;
     d->B = B; d->H = H; d->W = W; d->ty0 = ty0; d->ty1 = ty1; d->tiles_x = tx; d->tiles_y = ty;
     d->row0 = tile_start(ty0, ty, T, H, r);
     d->row1 = tile_start(ty1, ty, T, H, r);

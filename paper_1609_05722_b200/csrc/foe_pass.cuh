@@ -25,7 +25,9 @@ template <int M_>
 struct PassCfg {
     static constexpr int M = M_;
     static constexpr int R = M / 2;
-    static constexpr int RH = 36, RW = 64;  // region (owned tile + r ring)
+    // region (owned tile + r ring): 36 x 64 (6 warps per filter group); 7 x 7 banks use 48 rows (8 warps
+    // per group) so a 512^2 image is 13 x 9 = 117 tiles, one wave on 148 SMs instead of 162
+    static constexpr int RH = (M_ == 7) ? 48 : 36, RW = 64;
     static constexpr int MY = 3, MX = 4;    // micro-tile per thread
     static constexpr int G = 2;             // filter groups per CTA (6 warps each: 3 warps per SMSP)
     static constexpr int NBUF = 3;          // psi buffers per group (pipelined mbarrier ring)
@@ -40,7 +42,7 @@ struct PassCfg {
     static constexpr int TAPS = (M * M + 3) & ~3;           // per-filter tap stride (float4)
     static constexpr int NCELL = SH * CW;
     static constexpr int CPT = (NCELL + NT - 1) / NT;       // staged cells per thread
-    static_assert(NTX == 16 && NTY == 12, "warp layout assumes 16 x 12 micro-tiles per group (6 warps)");
+    static_assert(NTX == 16 && (NTY == 12 || NTY == 16), "warp layout: 16 x 12 or 16 x 16 micro-tiles per group");
     static_assert(TH >= 2 * R, "tile too small for the fold rule");
     static_assert(G * RH * RW <= NPSI * PLANE, "group partial-gradient buffer must fit the psi planes");
     static_assert(NT % RW == 0, "fold walk assumes whole region rows per pass");
