@@ -329,13 +329,16 @@ def main():
         x = inverse_exact_unbiased_device(res.u)
         return res, x
 
+    L = _lib.lib()
+    # the FFMA peak probe (~0.1 s of full-chip work) also brings an idle GPU up to its boost clock
+    # before the warm-up steps
+    fp32_peak_tflops, ffma_clk = measure_ffma_peak(L, dev, local_rank)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    L = _lib.lib()
     launches0 = L.foe_kernel_launch_count()
     total_ms, iters, trials = 0.0, 0, 0
     with ClockSampler(local_rank) as clk:
@@ -374,7 +377,6 @@ def main():
     sm_count = props.multi_processor_count
     peak_clock = clk.max_mhz or 1965.0
     fp32_nominal_tflops = sm_count * 128 * 2 * peak_clock * 1e6 / 1e12
-    fp32_peak_tflops, ffma_clk = measure_ffma_peak(L, dev, local_rank)
     alg_flop_pass = ALG_FLOP_PER_PX_IT * H * W
     achieved = alg_flop_pass / (pass_ms * 1e-3) / 1e12
     use_tc = bool(L.foe_pass_uses_tensor_cores(K, N_FILT))

@@ -144,6 +144,30 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         Yr[rr * T::YW + (col < 2 ? col : T::YW - 4 + col)] = 0.0f;
     }
     griddep_wait();  // the previous pass (control block, iterates, gradients, partials) is complete
+    constexpr int CPT = (C::NCELL + NT - 1) / NT;
+    const size_t ioff = (size_t)b * a.Hl * a.W;
+    // TRIAL: every candidate slot (3 iterate planes, 2 gradient planes) and the observation are loaded
+    // before the control block that names the slots is read, so the two L2 round trips overlap
+    float cu[TRIAL ? 3 : 1][CPT], cg[TRIAL ? 2 : 1][CPT], cob[CPT], canc[TRIAL ? 3 : 1];
+    if (TRIAL) {
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+            const int k = tid + q * NT;
+            if (k < C::NCELL) {
+                const int i = k / C::CW, j = k - i * C::CW;
+                const size_t o = ioff + (size_t)(src_idx<SYM>(g.ry0 - R + i, a.H) - a.lrow0) * a.W +
+                                 src_idx<SYM>(g.rx0 - R + j, a.W);
+#pragma unroll
+                for (int sl = 0; sl < 3; ++sl) cu[sl][q] = __ldg(a.U + sl * a.plane + o);
+#pragma unroll
+                for (int sl = 0; sl < 2; ++sl) cg[sl][q] = __ldg(a.Gs + sl * a.plane + o);
+                cob[q] = __ldg(a.obs + o);
+            }
+        }
+        const size_t oa = ioff + (size_t)(g.s0 - a.lrow0) * a.W + g.c0;
+#pragma unroll
+        for (int sl = 0; sl < 3; ++sl) canc[sl] = a.zero_mean ? __ldg(a.U + sl * a.plane + oa) : 0.0f;
+    }
     TrialParams p{};
     if (a.mode != MODE_EVAL) {
         const ImgCtl &c = a.ctl[b];
@@ -154,7 +178,6 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         }
         p = trial_params(a, c);
     }
-    const size_t ioff = (size_t)b * a.Hl * a.W;
     const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
     float *gout, *uout = nullptr;
     if (a.mode == MODE_EVAL) {
@@ -172,23 +195,27 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             gout = a.Gs + p.ig * a.plane + ioff;
         }
     }
-    const float shift = a.zero_mean ? __ldg(uin + (size_t)(g.s0 - a.lrow0) * a.W + g.c0) : 0.0f;
+    const float shift = TRIAL ? (p.iu == 0 ? canc[0] : p.iu == 1 ? canc[1] : canc[2])
+                              : a.zero_mean ? __ldg(uin + (size_t)(g.s0 - a.lrow0) * a.W + g.c0) : 0.0f;
     double acc[kNumPartials];
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
     // ---- prologue: stage u_new - shift and du for the region + r ring (all loads in flight first) ----
     {
-        constexpr int CPT = (C::NCELL + NT - 1) / NT;
         float lu[CPT], lup[CPT], lg[CPT], lob[CPT];
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
             const int k = tid + q * NT;
-            if (k < C::NCELL) {
+            if (TRIAL) {  // select the slots named by the control block
+                lu[q] = p.iu == 0 ? cu[0][q] : p.iu == 1 ? cu[1][q] : cu[2][q];
+                lup[q] = p.iup == 0 ? cu[0][q] : p.iup == 1 ? cu[1][q] : cu[2][q];
+                lg[q] = p.ig == 0 ? cg[0][q] : cg[1][q];
+                lob[q] = cob[q];
+            } else if (k < C::NCELL) {
                 const int i = k / C::CW, j = k - i * C::CW;
                 const size_t o = (size_t)(src_idx<SYM>(g.ry0 - R + i, a.H) - a.lrow0) * a.W +
                                  src_idx<SYM>(g.rx0 - R + j, a.W);
                 lu[q] = __ldg(uin + o);
-                if (TRIAL) { lup[q] = __ldg(upv + o); lg[q] = __ldg(gin + o); lob[q] = __ldg(obs + o); }
             }
         }
 #pragma unroll
