@@ -94,14 +94,15 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def bench_fallback_bank(fp, _lib, L, y_dev, lam, cfg, stream, fp32_peak_tflops, H, W, steps=2):
+def bench_fallback_bank(fp, _lib, L, y_dev, lam, cfg, stream, fp32_peak_tflops, H, W, steps=3):
     """Config 2 with the 48 x 7 x 7 fallback bank: device-timed solves and the fused pass."""
     import torch
     from paper_1609_05722_b200.anscombe import forward_device
     model = fp.load_packaged_model("foe_fallback48x7")
     n, k = model.n_filters, model.basis.atoms.shape[-1]
     v = forward_device(y_dev)
-    res = fp.solve_device(model, v, v, lam, "quadratic", cfg.max_iters, cfg)  # warm-up
+    for _ in range(2):  # warm-up (graph capture, allocator)
+        res = fp.solve_device(model, v, v, lam, "quadratic", cfg.max_iters, cfg)
     ms, iters = 0.0, 0
     for _ in range(steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -130,6 +131,18 @@ def bench_fallback_bank(fp, _lib, L, y_dev, lam, cfg, stream, fp32_peak_tflops, 
             "pass_ms": pass_ms, "alg_flop_per_px_it": flop_px_it,
             "kernel": "k_pass_tc" if tc else f"k_pass<{k},TRIAL,SYM> (FFMA)",
             "roofline_frac": achieved / fp32_peak_tflops, "achieved_tflops": achieved}
+
+
+def pass_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the pass kernel, from the committed
+    ncu --set full summary of the current kernel (profiles/roofline_traffic.json), else None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "roofline_traffic.json")
+    try:
+        with open(path) as fh:
+            rec = json.load(fh).get(kernel)
+        return None if rec is None else rec["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def measure_ffma_peak(L, dev, index):
@@ -282,8 +295,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-iters", type=int, default=8)
-    ap.add_argument("--cpu-iters", type=int, default=30)
+    ap.add_argument("--ref-iters", type=int, default=30)
+    ap.add_argument("--cpu-iters", type=int, default=150, help="cpu_baseline sample: the full 150-iteration solve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fallback", action="store_true", help="skip the 48x7x7 fallback-bank line")
     ap.add_argument("--pass-reps", type=int, default=100)
@@ -380,6 +393,7 @@ def main():
     alg_flop_pass = ALG_FLOP_PER_PX_IT * H * W
     achieved = alg_flop_pass / (pass_ms * 1e-3) / 1e12
     use_tc = bool(L.foe_pass_uses_tensor_cores(K, N_FILT))
+    traffic = pass_traffic("k_pass_tc<24, 1, 1>" if use_tc else "k_pass<5, 1, 1>")
     tensor = None
     if use_tc:
         # executed tcgen05 work of one trial pass: per 128-pixel block 2 x 9 forward (u, du) + 9 adjoint
@@ -432,7 +446,7 @@ def main():
                 "trials_per_step": trials / args.steps,
                 "algorithmic_fp32_frac": solve_frac,
                 "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
-                             "frac": achieved / fp32_peak_tflops, "traffic": None,
+                             "frac": achieved / fp32_peak_tflops, "traffic": traffic,
                              "kernel": ("k_pass_tc<24,TRIAL,SYM> (fused trial pass, tcgen05 3xTF32 implicit GEMMs)"
                                         if use_tc else "k_pass<5,TRIAL,SYM> (fused trial pass, FFMA)"),
                              "pass_ms": pass_ms, "tensor": tensor,
