@@ -134,6 +134,16 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfg, int B, int H, int
  * the last foe_solve in `workspace` without changing it (decisions suppressed). */
 int foe_bench_trial_pass(const foe_bank *bank, int B, int H, int W, int trace_cap, int reps,
                          void *workspace, size_t workspace_bytes, void *stream);
+/* ---- fp64 bank operators for the training side -------------------
+ * filters: n x m x m fp64 in the reference orientation (FoEModel.filters), device memory.
+ * foe_conv_bank64:    out[B][n][H][W] = convolve_same(x[b], filters[i])        (image.py:37-58)
+ * foe_adjoint_bank64: out[B][H][W] = sum_i convolve_adjoint(y[b][i], filters[i]) (image.py:68-83)
+ * boundary FOE_SYMMETRIC / FOE_PERIODIC; H, W >= m. */
+int foe_conv_bank64(const double *filters, int n, int m, int boundary, const double *x, double *out, int B, int H,
+                    int W, void *stream);
+int foe_adjoint_bank64(const double *filters, int n, int m, int boundary, const double *y, double *out, int B, int H,
+                       int W, void *stream);
+
 /* ---- scoring (metrics.py:30-102) ------------------------------------
  * Per image b of B (H x W fp64, row-major, device): psnr[b] and mssim[b] of x_hat against g after the
  * reference's convention (both scaled by 255 / peak, data_range 255; 11 x 11 Gaussian window,

@@ -875,6 +875,133 @@ __global__ void k_score_final(const double *__restrict__ sq_part, int n_sq, cons
     mssim[b] = ss / (double)n_valid;
 }
 
+// ------------------------------------------------------------------------------------------------
+// fp64 filter-bank operators for the training side (training.py runs in
+// fp64 with 1e-9 CG / stationarity tolerances, so these stay fp64):
+//   k_conv_bank64: out[b][i] = convolve_same(x[b], k_i)          (image.py:37-58, true convolution)
+//   k_adj_bank64:  out[b]    = sum_i convolve_adjoint(y[b][i], k_i)  (image.py:68-83, exact adjoint:
+//                  V^T psi on the padded domain with psi_0 = 0 outside the image, folded by P^T)
+// Filters in the reference orientation (model.filters), n x m x m fp64, device memory.  16 x 16
+// output tiles; the adjoint resolves P^-1(q) per output pixel (single reflection: H, W >= m).
+
+constexpr int kT64 = 16;
+
+template <int M, bool SYM>
+__global__ void __launch_bounds__(256) k_conv_bank64(const double *__restrict__ kf, int n, const double *__restrict__ x,
+                                                     double *__restrict__ out, int H, int W) {
+    constexpr int R = M / 2, S = kT64 + 2 * R, FC = 8;
+    __shared__ double xs[S * S];
+    __shared__ double ks[FC * M * M];
+    const int tid = threadIdx.x, nch = (n + FC - 1) / FC;
+    const int b = blockIdx.z / nch, f0 = (blockIdx.z % nch) * FC, nfc = min(FC, n - f0);
+    const int y0 = blockIdx.y * kT64, x0 = blockIdx.x * kT64;
+    const double *xb = x + (size_t)b * H * W;
+    for (int e = tid; e < S * S; e += 256) {
+        const int i = e / S, j = e - i * S;
+        xs[e] = xb[(size_t)src_idx<SYM>(y0 - R + i, H) * W + src_idx<SYM>(x0 - R + j, W)];
+    }
+    for (int e = tid; e < nfc * M * M; e += 256) ks[e] = kf[(size_t)f0 * M * M + e];
+    __syncthreads();
+    const int ty = tid / kT64, tx = tid % kT64, y = y0 + ty, xx = x0 + tx;
+    if (y >= H || xx >= W) return;
+    for (int fi = 0; fi < nfc; ++fi) {
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < M; ++a)
+#pragma unroll
+            for (int c = 0; c < M; ++c)  // z(p) = sum_{a,b} k[a,b] u_ext(p - (a - r, b - r))
+                acc += ks[fi * M * M + a * M + c] * xs[(ty + 2 * R - a) * S + (tx + 2 * R - c)];
+        out[(((size_t)b * n + f0 + fi) * H + y) * W + xx] = acc;
+    }
+}
+
+template <int M, bool SYM>
+__global__ void __launch_bounds__(256) k_adj_bank64(const double *__restrict__ kf, int n, const double *__restrict__ y,
+                                                    double *__restrict__ out, int H, int W) {
+    constexpr int R = M / 2, S = kT64 + 2 * R;
+    __shared__ double ps[S * S];
+    __shared__ double ks[M * M];
+    const int tid = threadIdx.x, b = blockIdx.z;
+    const int y0 = blockIdx.y * kT64, x0 = blockIdx.x * kT64;
+    const int ty = tid / kT64, tx = tid % kT64, qy = y0 + ty, qx = x0 + tx;
+    // P^-1(q): the padded positions Q in [-r, n + r) whose source pixel is q (image.py:61-66)
+    int Qy[3], Qx[3], nqy = 1, nqx = 1;
+    Qy[0] = qy;
+    Qx[0] = qx;
+    if (SYM) {
+        if (qy < R) Qy[nqy++] = -1 - qy;
+        if (qy >= H - R) Qy[nqy++] = 2 * H - 1 - qy;
+        if (qx < R) Qx[nqx++] = -1 - qx;
+        if (qx >= W - R) Qx[nqx++] = 2 * W - 1 - qx;
+    }
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) {
+        __syncthreads();
+        const double *yb = y + ((size_t)b * n + i) * H * W;
+        for (int e = tid; e < S * S; e += 256) {
+            const int gy = y0 - R + e / S, gx = x0 - R + e % S;
+            double v;
+            if (SYM) v = (gy >= 0 && gy < H && gx >= 0 && gx < W) ? yb[(size_t)gy * W + gx] : 0.0;  // psi_0
+            else v = yb[(size_t)src_idx<false>(gy, H) * W + src_idx<false>(gx, W)];  // circular adjoint
+            ps[e] = v;
+        }
+        for (int e = tid; e < M * M; e += 256) ks[e] = kf[(size_t)i * M * M + e];
+        __syncthreads();
+        if (qy >= H || qx >= W) continue;
+        for (int u = 0; u < nqy; ++u)
+            for (int v = 0; v < nqx; ++v) {
+                const int ly = Qy[u] - y0, lx = Qx[v] - x0;  // psi_0(Q + (a - r, b - r)) at ring index ly + a
+#pragma unroll
+                for (int a = 0; a < M; ++a) {
+                    const int iy = ly + a;
+                    if (iy < 0 || iy >= S) continue;  // outside the staged ring: outside the image
+#pragma unroll
+                    for (int c = 0; c < M; ++c) {
+                        const int ix = lx + c;
+                        if (ix < 0 || ix >= S) continue;
+                        acc += ks[a * M + c] * ps[iy * S + ix];
+                    }
+                }
+            }
+    }
+    if (qy < H && qx < W) out[((size_t)b * H + qy) * W + qx] = acc;
+}
+
+template <bool ADJ, int M>
+int launch_bank64(const double *kf, int n, int boundary, const double *in, double *out, int B, int H, int W,
+                  cudaStream_t st) {
+    const dim3 tiles((W + kT64 - 1) / kT64, (H + kT64 - 1) / kT64);
+    const bool sym = boundary == FOE_SYMMETRIC;
+    if (ADJ) {
+        const dim3 grid(tiles.x, tiles.y, B);
+        if (sym) k_adj_bank64<M, true><<<grid, 256, 0, st>>>(kf, n, in, out, H, W);
+        else k_adj_bank64<M, false><<<grid, 256, 0, st>>>(kf, n, in, out, H, W);
+    } else {
+        const dim3 grid(tiles.x, tiles.y, B * ((n + 7) / 8));
+        if (sym) k_conv_bank64<M, true><<<grid, 256, 0, st>>>(kf, n, in, out, H, W);
+        else k_conv_bank64<M, false><<<grid, 256, 0, st>>>(kf, n, in, out, H, W);
+    }
+    FOE_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return FOE_OK;
+}
+
+template <bool ADJ>
+int bank64(const double *kf, int n, int m, int boundary, const double *in, double *out, int B, int H, int W,
+           void *stream) {
+    if (n < 1 || B < 1 || (boundary != FOE_SYMMETRIC && boundary != FOE_PERIODIC))
+        return fail(FOE_E_INVALID, "bad bank arguments");
+    if (H < m || W < m) return fail(FOE_E_INVALID, "fp64 bank operators need H, W >= m (got %dx%d, m=%d)", H, W, m);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (m) {
+        case 1: return launch_bank64<ADJ, 1>(kf, n, boundary, in, out, B, H, W, st);
+        case 3: return launch_bank64<ADJ, 3>(kf, n, boundary, in, out, B, H, W, st);
+        case 5: return launch_bank64<ADJ, 5>(kf, n, boundary, in, out, B, H, W, st);
+        case 7: return launch_bank64<ADJ, 7>(kf, n, boundary, in, out, B, H, W, st);
+        default: return fail(FOE_E_UNSUPPORTED, "filter size %d not compiled (1,3,5,7)", m);
+    }
+}
+
 // FP32 FFMA throughput probe: 8 independent FMA chains per thread, 4 warps per SMSP, enough CTAs for
 // every SM; the result feeds the roofline peak (MEASURED_PEAKS.json has no FP32 figure)
 __global__ void __launch_bounds__(512) k_ffma_peak(float *out, int iters, float a, float b) {
@@ -1534,6 +1661,16 @@ int foe_score(const double *x_hat, const double *g, int B, int H, int W, double 
     FOE_CUDA(cudaGetLastError());
     g_launches.fetch_add(3, std::memory_order_relaxed);
     return FOE_OK;
+}
+
+int foe_conv_bank64(const double *filters, int n, int m, int boundary, const double *x, double *out, int B, int H,
+                    int W, void *stream) {
+    return bank64<false>(filters, n, m, boundary, x, out, B, H, W, stream);
+}
+
+int foe_adjoint_bank64(const double *filters, int n, int m, int boundary, const double *y, double *out, int B, int H,
+                       int W, void *stream) {
+    return bank64<true>(filters, n, m, boundary, y, out, B, H, W, stream);
 }
 
 int foe_pass_uses_tensor_cores(int m, int nf) { return use_tc(m, nf) ? 1 : 0; }

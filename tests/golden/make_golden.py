@@ -202,6 +202,37 @@ def main():
     for r in rows:
         print("grid", r.image, r.peak, r.variant, r.branch, round(r.psnr_db, 4), round(r.mssim, 5))
 
+    # --- training operators (training.py:132-356), small patches -----------------------------------
+    from foepoisson import training
+    from paper_1609_05722_b200.synth import synthetic_clean, sample_poisson
+    out = {}
+    rng = np.random.default_rng(11)
+    clean = 4.0 * synthetic_clean(24, 28, 5)
+    noisy = sample_poisson(clean, 5)
+    smp = training.TrainingSample.create(clean, noisy)
+    out["tr_clean"], out["tr_noisy"] = clean, noisy
+    foe_s = fileio.load_packaged_model("foe_s")
+    per = random_model(rng, 6, 5, domain_tag="anscombe", boundary="periodic")
+    out["tr_per_betas"], out["tr_per_weights"] = per.betas, per.weights
+    for tag, model, objective in (("a", foe_a, "anscombe_domain"), ("s", foe_s, "original_domain"),
+                                  ("p", per, "anscombe_domain")):
+        w = smp.transformed + rng.normal(scale=0.3, size=clean.shape) if objective == "anscombe_domain" \
+            else noisy + 0.5 + rng.uniform(0, 0.5, size=clean.shape)
+        pv = rng.normal(size=clean.shape)
+        out[f"tr_{tag}_w"], out[f"tr_{tag}_p"] = w, pv
+        out[f"tr_{tag}_hp"] = training.hessian_apply(w, model, objective, pv, smp, lam=1.3)
+        out[f"tr_{tag}_grad"] = training.total_gradient(w, model, smp, objective, lam=1.3)
+        out[f"tr_{tag}_stat"] = np.array(training.stationarity_residual(w, model, smp, objective, lam=1.3))
+    cfg_t = training.TrainConfig()
+    w_star = training.lower_solve(smp, foe_a, "anscombe_domain", cfg_t)
+    rhs = rng.normal(size=clean.shape)
+    q, info = training.solve_hessian_system(w_star, foe_a, "anscombe_domain", rhs, smp, 1.0, tol=1e-9, max_iters=600)
+    out["tr_cg_rhs"], out["tr_cg_q"], out["tr_cg_iters"] = rhs, q, np.array(info["iterations"])
+    d_beta, d_logw = training.param_gradients(w_star, foe_a, smp, "anscombe_domain", cfg_t)
+    out["tr_wstar"], out["tr_dbeta"], out["tr_dlogw"] = w_star, d_beta, d_logw
+    np.savez_compressed(os.path.join(HERE, "training.npz"), **out)
+    print("training", info["iterations"], float(np.abs(d_beta).max()), float(np.abs(d_logw).max()))
+
     if os.environ.get("GOLDEN_SKIP_CFG1"):
         return
     # --- BASELINE config 1 at full size (256^2, peak 4, quadratic forced, foe_a) ----------------

@@ -425,3 +425,71 @@ def test_cli_denoise_round_trip(tmp_path):
     ref = fp.denoise(fp.DenoiseRequest(noisy=y, peak=2.0, model=fp.load_packaged_model("foe_a"), variant="transform"))
     np.testing.assert_array_equal(np.load(tmp_path / "out.npy"), ref.image)
     assert (tmp_path / "t.csv").exists()
+
+
+def test_fp64_bank_operators_vs_golden(golden):
+    """foe_conv_bank64 / foe_adjoint_bank64 (training side, fp64) vs the reference's convolve_same /
+    convolve_adjoint at the reference tests' 1e-12 tolerance, m in {1,3,5,7} x both boundaries."""
+    import torch
+    from paper_1609_05722_b200 import training as tr
+    from paper_1609_05722_b200.image import BOUNDARY_CODES
+    g = golden("conv")
+    for key in [k[5:] for k in g if k.startswith("same_")]:
+        b = key.split("_")[-1]
+        k = tr._dev(g[f"k_{key}"])[None]
+        bank = type("B", (), {})()
+        bank.m, bank.boundary, bank.filters = k.shape[-1], BOUNDARY_CODES[b], k
+        z = tr._Bank64.conv(bank, tr._dev(g[f"x_{key}"]))[0, 0].cpu().numpy()
+        a = tr._Bank64.adjoint(bank, tr._dev(g[f"y_{key}"])[None, None])[0].cpu().numpy()
+        assert np.allclose(z, g[f"same_{key}"], rtol=1e-12, atol=1e-12), key
+        assert np.allclose(a, g[f"adj_{key}"], rtol=1e-12, atol=1e-12), key
+    # adjointness of the whole bank: <K x, y> = <x, K^T y>
+    model = fp.load_packaged_model("foe_a")
+    bank = tr._Bank64(model)
+    rng = np.random.default_rng(3)
+    x, y = rng.normal(size=(1, 37, 41)), rng.normal(size=(1, 24, 37, 41))
+    lhs = float(torch.sum(bank.conv(tr._dev(x)) * tr._dev(y)).item())
+    rhs = float(torch.sum(tr._dev(x) * bank.adjoint(tr._dev(y))).item())
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+
+
+def _training_case(g, tag):
+    from paper_1609_05722_b200 import training as tr
+    if tag == "a":
+        model, objective = fp.load_packaged_model("foe_a"), "anscombe_domain"
+    elif tag == "s":
+        model, objective = fp.load_packaged_model("foe_s"), "original_domain"
+    else:
+        model = fp.FoEModel(basis=fp.dct_basis(5), betas=g["tr_per_betas"], weights=g["tr_per_weights"],
+                            domain_tag="anscombe", boundary="periodic")
+        objective = "anscombe_domain"
+    smp = tr.TrainingSample.create(g["tr_clean"], g["tr_noisy"])
+    return model, objective, smp
+
+
+def test_training_operators_vs_reference_golden(golden):
+    """hessian_apply / total_gradient / stationarity_residual (training.py:132-174), fp64 on the
+    device, vs the reference on three cases (anscombe foe_a, original-domain foe_s, periodic bank)."""
+    from paper_1609_05722_b200 import training as tr
+    g = golden("training")
+    for tag in ("a", "s", "p"):
+        model, objective, smp = _training_case(g, tag)
+        w, p = g[f"tr_{tag}_w"], g[f"tr_{tag}_p"]
+        assert rel_l2(tr.hessian_apply(w, model, objective, p, smp, lam=1.3), g[f"tr_{tag}_hp"]) <= 1e-12, tag
+        assert rel_l2(tr.total_gradient(w, model, smp, objective, lam=1.3), g[f"tr_{tag}_grad"]) <= 1e-12, tag
+        st = tr.stationarity_residual(w, model, smp, objective, lam=1.3)
+        assert abs(st - float(g[f"tr_{tag}_stat"])) <= 1e-12 * abs(st), tag
+
+
+def test_hessian_cg_and_param_gradients_vs_reference_golden(golden):
+    """solve_hessian_system at the reference's minimiser and param_gradients (training.py:183-356)."""
+    from paper_1609_05722_b200 import training as tr
+    g = golden("training")
+    model, objective, smp = _training_case(g, "a")
+    w_star = g["tr_wstar"]
+    q, info = tr.solve_hessian_system(w_star, model, objective, g["tr_cg_rhs"], smp, 1.0, tol=1e-9, max_iters=600)
+    assert abs(info["iterations"] - int(g["tr_cg_iters"])) <= 3
+    assert rel_l2(q, g["tr_cg_q"]) <= 1e-8
+    d_beta, d_logw = tr.param_gradients(w_star, model, smp, objective, tr.TrainConfig())
+    assert rel_l2(d_beta, g["tr_dbeta"]) <= 1e-8
+    assert rel_l2(d_logw, g["tr_dlogw"]) <= 1e-8

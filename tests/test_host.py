@@ -120,3 +120,18 @@ def test_synthetic_generator_is_deterministic():
     assert a.min() >= 0 and a.max() <= 1 and a.std() > 0.05
     x, y = make_counts(64, 48, 3, 4.0)
     assert np.array_equal(y, np.rint(y)) and y.min() >= 0
+
+
+def test_training_host_validation():
+    """TrainingSample / TrainConfig / objective checks of the device training operators (host only)."""
+    import numpy as np
+    from paper_1609_05722_b200 import training as tr
+    clean = np.ones((4, 4))
+    s = tr.TrainingSample.create(clean, np.zeros((4, 4)))
+    assert np.allclose(s.transformed, 2 * np.sqrt(0.375))
+    with pytest.raises(ValueError):
+        tr.TrainingSample.create(clean, np.full((4, 4), 0.5))
+    with pytest.raises(ValueError):
+        tr.TrainConfig(objective="nope")
+    with pytest.raises(ValueError):
+        tr._check_domain(fp.load_packaged_model("foe_a"), "original_domain")
