@@ -18,6 +18,10 @@
 //    gradient), so every pass is one trial: ~1.37 passes per accepted iteration.
 #include "foe_b200.h"
 
+#ifndef FOE_STAMPS
+#define FOE_STAMPS 0  // per-block cycle stamps of the tensor-core pass (timing diagnostic builds only)
+#endif
+
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
