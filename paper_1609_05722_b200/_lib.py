@@ -15,6 +15,8 @@ REPO = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc", "foe_b200.cu")
 INCLUDE = os.path.join(REPO, "include")
 LIB_PATH = os.path.join(PKG, "libfoe_b200.so")
+# diagnostic builds (e.g. -DFOE_STAMPS=1, built by tools/build_diag.py) load through FOE_LIB
+LOAD_PATH = os.environ.get("FOE_LIB", LIB_PATH)
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
@@ -35,21 +37,21 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = LIB_PATH, defines: tuple = ()) -> str:
     """nvcc -gencode arch=compute_100a,code=sm_100a ... -> libfoe_b200.so (no GPU needed)."""
-    if not force and not needs_build():
+    if out == LIB_PATH and not force and not needs_build():
         return LIB_PATH
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I" + INCLUDE, "-o", LIB_PATH + ".tmp", SRC]
+    cmd = [nvcc, *NVCC_FLAGS, *("-D" + d for d in defines), "-I" + INCLUDE, "-o", out + ".tmp", SRC]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stderr[-4000:])
-    os.replace(LIB_PATH + ".tmp", LIB_PATH)
+    os.replace(out + ".tmp", out)
     if verbose:
         print(res.stderr)
-    return LIB_PATH
+    return out
 
 
 class FoeError(RuntimeError):
@@ -78,10 +80,10 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise FoeError(f"{LIB_PATH} is not built; run paper_1609_05722_b200._lib.build() "
+    if not os.path.exists(LOAD_PATH):
+        raise FoeError(f"{LOAD_PATH} is not built; run paper_1609_05722_b200._lib.build() "
                        "(or __graft_entry__.build()) -- there is no CPU fallback")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(LOAD_PATH)
     L.foe_last_error.restype = ctypes.c_char_p
     L.foe_abi_version.restype = ctypes.c_int
     L.foe_device_sm_count.argtypes = [ctypes.c_int]

@@ -34,7 +34,7 @@ struct TcCfg {
     static constexpr int W_PT = 8, NWARPS = 24, NT = NWARPS * 32;
     // named barriers, one per stage / set: A complete, Psi complete, D region free, forward done (relayed
     // to the set), adjoint done (relayed to the set), A stage free (relayed to the im2col warps)
-    static constexpr int BAR_AFULL = 1, BAR_PFULL = 3, BAR_DFULL = 5, BAR_YFULL = 7, BAR_AFREE = 9, BAR_DFREE = 11;
+    static constexpr int BAR_AFULL = 1, BAR_PFULL = 3, BAR_DFULL = 5, BAR_AFREE = 9, BAR_DFREE = 11;
     static constexpr int RING = 4;                       // Y ring: 4 blocks = 8 region rows
     static constexpr int YROWS = 2 * RING, YW = RW + 4;  // 2 zero columns each side
     static constexpr int BSZ = 32 * 32;                  // one 32 x 32 B operand (floats)
@@ -50,8 +50,9 @@ template <int NF_MAX>
 __host__ __device__ constexpr size_t tc_smem_floats() {
     using T = TcCfg<NF_MAX>;
     // staged planes u hi/lo, du hi/lo; Kf hi/lo, Kt hi/lo; Y ring; region gradient (two tap halves); alpha,
-    // tap 24, 2 alpha
-    return 4 * (size_t)T::PLANE + 4 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96;
+    // tap 24, 2 alpha; the prologue's fp64 partials of every thread (parked for the epilogue)
+    return 4 * (size_t)T::PLANE + 4 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96 +
+           2 * (size_t)(kNumPartials - 1) * T::NT;
 }
 
 // sum over taps [T0, T1) of Y(row r + a - R, column c + b - R)[a M + b] from the Y ring: one ring-row
@@ -97,6 +98,15 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     const int nf = a.n_filters;
     const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3] = globaltimer_ns();
+    // per-block / per-phase cycle stamps of CTA (0, 0) for the timing diagnostic (compiled in only with
+    // -DFOE_STAMPS=1: the predicated-off stamps cost ~3 % of the pass's issue slots)
+#if FOE_STAMPS
+    unsigned long long *ph = (a.dbg_times && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0 && lane == 0)
+                                 ? a.dbg_times + 3 * (size_t)gridDim.x * gridDim.y : nullptr;
+#else
+    constexpr unsigned long long *ph = nullptr;
+#endif
+    if (ph && tid == 0) ph[NBLK * 16 + 2] = clock64();  // kernel start (cycles)
     // programmatic dependent launch: the next pass may be scheduled as soon as every CTA of this one
     // has started; everything up to griddep_wait() below depends only on the launch arguments
     griddep_launch_dependents();
@@ -104,17 +114,17 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
 
     // staged planes, split once into tf32 hi + lo (both rounded to nearest): u_new - shift and du
-    float *Uh = sm;
-    float *Ul = Uh + T::PLANE;
-    float *Dh = Ul + T::PLANE;
-    float *Dl = Dh + T::PLANE;
-    float *Kf = Dl + T::PLANE;     // [hi | lo], forward B (N = filters, K = taps)
+    // (interleaved per cell as {u hi, u lo, du hi, du lo}: one 16-byte load per tap in the im2col)
+    float4 *S4 = reinterpret_cast<float4 *>(sm);
+    float *Kf = sm + 4 * T::PLANE;  // [hi | lo], forward B (N = filters, K = taps)
     float *Kt = Kf + 2 * T::BSZ;   // [hi | lo], adjoint B (N = taps, K = filters)
     float *Yr = Kt + 2 * T::BSZ;   // Y ring [tap][ring row][YW]
     float *Gr = Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold), two tap halves
     float *s_al = Gr + 2 * T::RH * T::RW;        // alpha_f, zero-padded
     float *s_k24 = s_al + 32;                    // tap 24 of each filter (outside the K = 24 MMAs)
     float *s_al2 = s_k24 + 32;                   // 2 alpha_f
+    // prologue partials 1..6 per thread, [k - 1][tid]: kept out of registers through the block loop
+    double *s_acc = reinterpret_cast<double *>(s_al2 + 32);
 
     if (warp == 0) tmem_alloc(&s_tmem, 512);
     if (tid == 0) {
@@ -127,8 +137,8 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             }
         }
         for (int j = 0; j < NBLK; ++j) {
-            mbar_init(&mb_ring[j], 8);  // one arrival per warp of the point set
-            mbar_init(&mb_sum[j], 8);
+            mbar_init(&mb_ring[j], 8);  // one arrival per warp of the draining point set
+            mbar_init(&mb_sum[j], 8);   // one arrival per warp of the summing point set
         }
     }
     // B operands: Kf[f][t] = kf_f[t] (convolution orientation), Kt[t][f] = 2 a_f k_f[t] with the
@@ -153,6 +163,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         Yr[rr * T::YW + (col < 2 ? col : T::YW - 4 + col)] = 0.0f;
     }
     griddep_wait();  // the previous pass (control block, iterates, gradients, partials) is complete
+    if (ph && tid == 0) ph[NBLK * 16 + 3] = clock64();  // dependency resolved
     constexpr int CPT = (C::NCELL + NT - 1) / NT;
     const size_t ioff = (size_t)b * a.Hl * a.W;
     // TRIAL: every candidate slot (3 iterate planes, 2 gradient planes) and the observation are loaded
@@ -234,8 +245,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const int i = k / C::CW, j = k - i * C::CW;
             if (!TRIAL) {
                 const float x = lu[q] - shift, h = tf32_rn(x);
-                Uh[i * SW + j] = h;
-                Ul[i * SW + j] = tf32_rn(x - h);
+                S4[i * SW + j] = make_float4(h, tf32_rn(x - h), 0.0f, 0.0f);
                 continue;
             }
             const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
@@ -244,10 +254,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const float un = (p.branch == FOE_QUADRATIC) ? prox_quad(ut, p.t, ob) : prox_idv(ut, p.t, ob);
             const float du = un - u;
             const float x = un - shift, h = tf32_rn(x), hd = tf32_rn(du);
-            Uh[i * SW + j] = h;
-            Ul[i * SW + j] = tf32_rn(x - h);
-            Dh[i * SW + j] = hd;
-            Dl[i * SW + j] = tf32_rn(du - hd);
+            S4[i * SW + j] = make_float4(h, tf32_rn(x - h), hd, tf32_rn(du - hd));
             if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) {
                 uout[(size_t)(gy - a.lrow0) * a.W + gx] = un;
                 acc[1] += (double)du * (double)du;
@@ -266,6 +273,8 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             }
         }
     }
+#pragma unroll
+    for (int k = 1; k < kNumPartials; ++k) s_acc[(k - 1) * NT + tid] = acc[k];
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -275,73 +284,65 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     // TMEM addresses keep the MMA operands in uniform registers
     constexpr uint32_t tmem = 0u;
     if (tid == 0 && s_tmem != 0u) __trap();
-    // per-block role stamps of CTA (0, 0) for the timing diagnostic: [block][im2col, fwd, point, sum]
-    // (compiled in only with -DFOE_STAMPS=1: the predicated-off stamps cost ~3 % of the pass's issue slots)
-#if FOE_STAMPS
-    unsigned long long *ph = (a.dbg_times && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0)
-                                 ? a.dbg_times + 3 * (size_t)gridDim.x * gridDim.y : nullptr;
-#else
-    constexpr unsigned long long *ph = nullptr;
-#endif
+    // per-block role stamps: [block][im2col, fwd, point, sum]
     if (ph && tid == 0) ph[NBLK * 16] = clock64();  // loop start (cycles)
 
     if (warp < T::W_PT) {
         // ================= im2col: block j's A operands into stage j%2 =================
-        // warps 0-3 build A_u (warp 0 issues the forward MMAs), warps 4-7 A_du
-        const int pl = tid & 127, v = warp >> 2;  // pixel = TMEM lane; u / du
+        // warps 0-3 and 4-7 split the taps (warp 0 issues the forward MMAs)
+        const int pl = tid & 127, v = warp >> 2;  // pixel = TMEM lane; tap split
         const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
-        const uint32_t kf_hi = smem_u32(Kf), kf_lo = smem_u32(Kf + T::BSZ);
+        BDescs<32, 3> kfd;
+        kfd.build(smem_u32(Kf), smem_u32(Kf + T::BSZ));
         for (int j = 0; j < NBLK; ++j) {
             const int s = j & 1;
-            if (j >= 2) {  // forward(j-2) consumed the stage: warp 0 polls the commit, relays to warps 1-7
-                if (warp == 0) {
-                    mbar_wait_sleep(&mb_dfull[(j - 2) % T::NDREG], ((j - 2) / T::NDREG) & 1);
-                    named_arrive(T::BAR_AFREE + s, 256);
-                } else {
-                    named_sync(T::BAR_AFREE + s, 256);
-                }
-            }
+            if (j >= 2 && warp != 0) named_sync(T::BAR_AFREE + s, 256);  // released by warp 0 (below)
             tc_fence_after();
             if (ph && warp == 0) ph[j * 16 + 5] = clock64();
             const uint32_t st = tmem + s * T::C_ASTAGE + lane_off;
             const int lr = 2 * j + (pl >> 6), lc = pl & 63;
-            if (v == 0 || TRIAL) {
-                const float *sh = (v ? Dh : Uh) + lr * SW + lc, *sl = (v ? Dl : Ul) + lr * SW + lc;
-                {  // taps 0..15
-                    float hi[16], lo[16];
+            {
+                // taps {0..7, 16..19} (warps 0-3) / {8..15, 20..23} (warps 4-7) of all four planes; tap 24
+                // is done by FFMA
+                const float4 *sp = S4 + lr * SW + lc;
 #pragma unroll
-                    for (int t = 0; t < 16; ++t) {
-                        hi[t] = sh[(t / 5) * SW + (t % 5)];
-                        lo[t] = sl[(t / 5) * SW + (t % 5)];
-                    }
-                    tmem_st16(st + (v ? T::C_ADH : T::C_AUH), hi);
-                    tmem_st16(st + (v ? T::C_ADL : T::C_AUL), lo);
-                }
-                {  // taps 16..23 (tap 24 is done by FFMA)
-                    float hi[8], lo[8];
+                for (int rd = 0; rd < 3; ++rd) {  // 4 taps per round: 16 live registers
+                    const int c0 = rd < 2 ? 8 * v + 4 * rd : 16 + 4 * v;
+                    float uh[4], ul[4], dh[4], dl[4];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int t = 16 + i;
-                        hi[i] = sh[(t / 5) * SW + (t % 5)];
-                        lo[i] = sl[(t / 5) * SW + (t % 5)];
+                    for (int i = 0; i < 4; ++i) {
+                        const int t = c0 + i;
+                        const float4 c = sp[(t / 5) * SW + (t % 5)];
+                        uh[i] = c.x; ul[i] = c.y; dh[i] = c.z; dl[i] = c.w;
                     }
-                    tmem_st8(st + (v ? T::C_ADH : T::C_AUH) + 16, hi);
-                    tmem_st8(st + (v ? T::C_ADL : T::C_AUL) + 16, lo);
+                    tmem_st4(st + T::C_AUH + c0, uh);
+                    tmem_st4(st + T::C_AUL + c0, ul);
+                    if (TRIAL) {
+                        tmem_st4(st + T::C_ADH + c0, dh);
+                        tmem_st4(st + T::C_ADL + c0, dl);
+                    }
                 }
                 tc_wait_st();
             }
             tc_fence_before();
             if (warp != 0) named_arrive(T::BAR_AFULL + s, 256);
-            if (warp == 0) {  // forward(j) once A is complete and block j-3 left D region j%3
+            if (warp == 0) {
+                // release stage (j+1)%2 for the next im2col as soon as forward(j-1) has read it, before
+                // forward(j) is issued: the im2col of block j+1 overlaps this warp's issue of block j
+                if (j >= 1 && j + 1 < NBLK) {
+                    mbar_wait_sleep(&mb_dfull[(j - 1) % T::NDREG], ((j - 1) / T::NDREG) & 1);
+                    named_arrive(T::BAR_AFREE + (s ^ 1), 256);
+                }
+                // forward(j) once A is complete and block j-3 left D region j%3
                 const int rg = j % T::NDREG;
                 const uint32_t sa = tmem + s * T::C_ASTAGE, sd = tmem + T::C_D0 + rg * T::C_DREGION;
                 named_sync(T::BAR_AFULL + s, 256);
-                if (j >= T::NDREG) named_sync(T::BAR_DFREE + rg, 288);
+                if (j >= T::NDREG) named_sync(T::BAR_DFREE + rg, 288);  // Y(j-3) drained by its point set
                 tc_fence_after();
                 if (ph) ph[j * 16 + 7] = clock64();
                 if (elect_one()) {
-                    umma_3xtf32<32>(sd + T::C_DZ, sa + T::C_AUH, sa + T::C_AUL, kf_hi, kf_lo, 3, false);
-                    if (TRIAL) umma_3xtf32<32>(sd + T::C_DDZ, sa + T::C_ADH, sa + T::C_ADL, kf_hi, kf_lo, 3, false);
+                    umma_3xtf32_pre<32, 3>(sd + T::C_DZ, sa + T::C_AUH, sa + T::C_AUL, kfd, 3);
+                    if (TRIAL) umma_3xtf32_pre<32, 3>(sd + T::C_DDZ, sa + T::C_ADH, sa + T::C_ADL, kfd, 3);
                     umma_commit(&mb_dfull[rg]);
                 }
                 __syncwarp();
@@ -349,53 +350,79 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             }
         }
     } else {
-        // ================= pointwise: psi, energy terms, Y into the ring =================
+        // ================= point sets: drain Y one block late, shifted sums, psi, energy terms =========
+        // set s handles blocks j = s (mod 2); at step j it first drains Y(j-2) -- its own previous block,
+        // whose adjoint ran while it evaluated that block's energy terms -- into the ring (freeing D region
+        // (j+1)%3 for forward(j+1)), sums g(j-3) over its tap half once Y(j-4 .. j-2) are in the ring, and
+        // then evaluates block j: psi' -> adjoint(j) issued, energy terms.  Steps j >= NBLK only drain/sum.
         const int q4 = warp & 3, hf = ((warp - T::W_PT) >> 2) & 1;  // lane quarter; filter / tap half
-        const int set = (warp - T::W_PT) >> 3;                        // blocks j = set (mod 2), stage set
+        const int set = (warp - T::W_PT) >> 3;                        // blocks j = set (mod 2)
         const bool issuer = warp == T::W_PT + 8 * set;  // whole warp; one elected lane issues
-        const uint32_t kt_hi = smem_u32(Kt), kt_lo = smem_u32(Kt + T::BSZ);
+        BDescs<32, NF / 8> ktd;
+        ktd.build(smem_u32(Kt), smem_u32(Kt + T::BSZ));
         const int pl = 32 * q4 + lane;
         const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
         constexpr int FH = NF / 2;  // filters per half, in chunks of 4
         const int f0 = FH * hf;
         double e_own = 0.0;
-        // g(q) over this warp's tap half (0..11 / 12..24) once Y(q-1 .. q+1) are in the ring
-        auto shifted_sum = [&](int q) {
-            if (ph && (warp - T::W_PT) % 8 == 0) ph[q * 16 + 8] = clock64();
-            for (int n = q - 1; n <= q + 1; ++n)
-                if (n >= 0 && n < NBLK) mbar_wait_sleep(&mb_ring[n], 0);
-            if (ph && (warp - T::W_PT) % 8 == 0) ph[q * 16 + 9] = clock64();
-            const int r = 2 * q + (pl >> 6), c = pl & 63;
-            float gsum;
-            if (q == 0 || q == NBLK - 1)
-                gsum = hf ? tc_tap_sum<12, 25, true, T>(Yr, r, c) : tc_tap_sum<0, 12, true, T>(Yr, r, c);
-            else
-                gsum = hf ? tc_tap_sum<12, 25, false, T>(Yr, r, c) : tc_tap_sum<0, 12, false, T>(Yr, r, c);
-            if (ph && (warp - T::W_PT) % 8 == 0) { ph[q * 16 + 6] = clock64() + (long long)(gsum * 0.0f); }
-            Gr[hf * T::RH * T::RW + r * T::RW + c] = gsum;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&mb_sum[q]);
-            if (ph && (warp - T::W_PT) % 8 == 0) ph[q * 16 + 4] = clock64();
-        };
-        for (int j = set; j < NBLK; j += 2) {
-            const int s = set, rg = j % T::NDREG;  // D region of this block
+        for (int j = set; j < NBLK + 3; j += 2) {
+            const int s = set, jd = j - 2, js = j - 3;  // block to drain, block to sum
+            const bool comp = j < NBLK, drain = jd >= 0 && jd < NBLK, sum = js >= 0 && js < NBLK;
+            const int rg = j % T::NDREG;  // D region of block j
+            if (issuer) {  // forward(j) and adjoint(j-2) complete: polled by the set's first warp, relayed
+                if (comp) mbar_wait_sleep(&mb_dfull[rg], (j / T::NDREG) & 1);
+                if (drain) mbar_wait_sleep(&mb_yfull[jd % T::NDREG], (jd / T::NDREG) & 1);
+                named_arrive(T::BAR_DFULL + s, 256);
+            } else {
+                named_sync(T::BAR_DFULL + s, 256);
+            }
+            tc_fence_after();
+            if (drain) {  // Y(jd): half 0 taps 0..15, half 1 taps 16..24, into ring slot jd % RING
+                float y[16];
+                tmem_ld16(tmem + T::C_D0 + (jd % T::NDREG) * T::C_DREGION + lane_off + T::C_DY + 16 * hf, y);
+                tc_wait_ld();
+                tc_fence_before();
+                if (jd + T::NDREG < NBLK) named_arrive(T::BAR_DFREE + jd % T::NDREG, 288);  // for forward(jd + 3)
+                // the slot held Y(jd - 4), read by g(jd - 5) .. g(jd - 3): g(jd - 5) and g(jd - 3) were summed
+                // by this set (steps j - 4, j - 2), g(jd - 4) by the other one
+                if (jd >= T::RING) mbar_wait_sleep(&mb_sum[jd - T::RING], 0);
+                const int lr = 2 * jd + (pl >> 6), lc = pl & 63;
+                float *yrow = Yr + (lr & (T::YROWS - 1)) * T::YW + 2 + lc;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int t = 16 * hf + i;
+                    if (t < T::KT) yrow[t * T::YROWS * T::YW] = y[i];
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&mb_ring[jd]);
+                if (ph && (warp - T::W_PT) % 8 == 0) ph[jd * 16 + 3] = clock64();
+            }
+            if (sum) {  // g(js) over this warp's tap half (0..11 / 12..24) once Y(js-1 .. js+1) are in the ring
+                for (int n = js - 1; n <= js + 1; ++n)
+                    if (n >= 0 && n < NBLK) mbar_wait_sleep(&mb_ring[n], 0);
+                const int r = 2 * js + (pl >> 6), c = pl & 63;
+                float gsum;
+                if (js == 0 || js == NBLK - 1)
+                    gsum = hf ? tc_tap_sum<12, 25, true, T>(Yr, r, c) : tc_tap_sum<0, 12, true, T>(Yr, r, c);
+                else
+                    gsum = hf ? tc_tap_sum<12, 25, false, T>(Yr, r, c) : tc_tap_sum<0, 12, false, T>(Yr, r, c);
+                Gr[hf * T::RH * T::RW + r * T::RW + c] = gsum;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&mb_sum[js]);
+                if (ph && (warp - T::W_PT) % 8 == 0) ph[js * 16 + 4] = clock64();
+            }
+            if (!comp) continue;
             const uint32_t sd = tmem + T::C_D0 + rg * T::C_DREGION + lane_off;
             const int lr = 2 * j + (pl >> 6), lc = pl & 63;
             const int gy = g.ry0 + lr, gx = g.rx0 + lc;
             const bool in_img = !SYM || (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W);
             const bool owned = gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1;
             // tap 24 by FFMA from hi + lo (2^-22 relative, as the tensor-core taps)
-            const float u24 = Uh[(lr + 4) * SW + lc + 4] + Ul[(lr + 4) * SW + lc + 4];
-            const float d24 = TRIAL ? Dh[(lr + 4) * SW + lc + 4] + Dl[(lr + 4) * SW + lc + 4] : 0.0f;
-            if (issuer) {  // the set's first warp polls the forward commit and relays it to the set
-                mbar_wait_sleep(&mb_dfull[rg], (j / T::NDREG) & 1);
-                named_arrive(T::BAR_DFULL + s, 256);
-            } else {
-                named_sync(T::BAR_DFULL + s, 256);
-            }
-            tc_fence_after();
+            const float4 c24 = S4[(lr + 4) * SW + lc + 4];
+            const float u24 = c24.x + c24.y;
+            const float d24 = TRIAL ? c24.z + c24.w : 0.0f;
             const bool pst = ph && (warp - T::W_PT) % 8 == 0;
-            if (pst) { ph[j * 16 + 1] = clock64(); ph[j * 16 + 10] = clock64(); }
+            if (pst) ph[j * 16 + 1] = clock64();
             // this half's filters: all z / dz loads in flight at once; psi' (tf32 hi / lo, written over
             // the z / dz columns as the adjoint's A operand, whose K covers filters < NF only) and the
             // atanh arguments for every filter with full ILP; Psi is handed to the adjoint MMA before
@@ -407,7 +434,6 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
                 if (TRIAL) tmem_ld4(sd + T::C_DDZ + f0 + 4 * c, *reinterpret_cast<float(*)[4]>(&dz[4 * c]));
             }
             tc_wait_ld();
-            if (pst) ph[j * 16 + 11] = clock64();
             float tmax = 0.0f;
 #pragma unroll
             for (int i = 0; i < FH; ++i) {
@@ -441,24 +467,21 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
                 tmem_st4(sd + T::C_DZ + f0 + 4 * c, hi);
                 tmem_st4(sd + T::C_DDZ + f0 + 4 * c, lo);
             }
-            if (pst) ph[j * 16 + 12] = clock64();
             tc_wait_st();
-            if (pst) ph[j * 16 + 13] = clock64();
             tc_fence_before();
             if (!issuer) named_arrive(T::BAR_PFULL + s, 256);
             if (issuer) {  // adjoint(j) once both halves of all four lane quarters wrote Psi
                 const uint32_t sb = tmem + T::C_D0 + rg * T::C_DREGION;
                 named_sync(T::BAR_PFULL + s, 256);
                 tc_fence_after();
-                if (pst) ph[j * 16 + 14] = clock64();
                 if (elect_one()) {
-                    umma_3xtf32<32>(sb + T::C_DY, sb + T::C_DZ, sb + T::C_DDZ, kt_hi, kt_lo, NF / 8, false);
+                    umma_3xtf32_pre<32, NF / 8>(sb + T::C_DY, sb + T::C_DZ, sb + T::C_DDZ, ktd, NF / 8);
                     umma_commit(&mb_yfull[rg]);
                 }
                 __syncwarp();
                 if (ph) ph[j * 16 + 2] = clock64();
             }
-            // energy terms while the adjoint MMAs run
+            // energy terms while the adjoint MMAs run (Y(j) is drained at step j + 2)
             float e0 = 0.0f, e1 = 0.0f;
             if (TRIAL) {
                 if (__any_sync(0xffffffffu, tmax > 0.2f)) {
@@ -487,40 +510,16 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
                 }
             }
             if (owned) e_own += (double)(e0 + e1);
-            // Y of this block: half 0 taps 0..15, half 1 taps 16..24
-            if (issuer) {
-                mbar_wait_sleep(&mb_yfull[rg], (j / T::NDREG) & 1);
-                named_arrive(T::BAR_YFULL + s, 256);
-            } else {
-                named_sync(T::BAR_YFULL + s, 256);
-            }
-            tc_fence_after();
-            float y[16];
-            if (pst) ph[j * 16 + 15] = clock64();
-            tmem_ld16(sd + T::C_DY + 16 * hf, y);
-            tc_wait_ld();
-            tc_fence_before();
-            if (j + T::NDREG < NBLK) named_arrive(T::BAR_DFREE + rg, 288);  // D region free for block j + 3
-            // the ring slot held Y(j-4): g(j-5), g(j-3) were summed by this set, g(j-4) by the other
-            if (j >= T::RING) mbar_wait_sleep(&mb_sum[j - T::RING], 0);
-            float *yrow = Yr + (lr % T::YROWS) * T::YW + 2 + lc;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int t = 16 * hf + i;
-                if (t < T::KT) yrow[t * T::YROWS * T::YW] = y[i];
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&mb_ring[j]);
-            if (ph && (warp - T::W_PT) % 8 == 0) ph[j * 16 + 3] = clock64();
-            if (j >= 1) shifted_sum(j - 1);
         }
-        if (set == ((NBLK - 1) & 1)) shifted_sum(NBLK - 1);
         acc[0] = e_own;
     }
+#pragma unroll
+    for (int k = 1; k < kNumPartials; ++k) acc[k] = s_acc[(k - 1) * NT + tid];
     tc_fence_before();
     __syncthreads();
     if (ph && tid == 0) ph[NBLK * 16 + 1] = clock64();  // loop end (cycles), CTA (0, 0)
-    if (warp == 0) tmem_dealloc(tmem, 512);
+    // TMEM is released at the very end: tcgen05.dealloc here stalled warp 0 (and with it the fold and the
+    // block reduction) for ~6,500 cycles
 
     // ---- fold padded pixels (symmetric rule) and write the owned gradient ----
     for (int k = tid; k < T::RW * 8; k += NT) {
@@ -545,22 +544,32 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
                 if (mx >= 0) val += gr(ly, mx);
                 if (my >= 0 && mx >= 0) val += gr(my, mx);
             }
+            if (ph && tid == 0 && gy == g.s0) ph[NBLK * 16 + 8] = clock64();  // first value folded
             gout[(size_t)(gy - a.lrow0) * a.W + gx] = val;
+            if (ph && tid == 0 && gy == g.s0) ph[NBLK * 16 + 9] = clock64();  // first store issued
         }
     }
 
+    if (ph && tid == 0) ph[NBLK * 16 + 4] = clock64();  // fold done
     // ---- per-tile partials, last CTA of the image reduces and decides (as k_pass) ----
     block_reduce<NT>(acc, red, s_sum);
+    if (ph && tid == 0) ph[NBLK * 16 + 5] = clock64();  // block reduction done
     if (tid < kNumPartials) {
         a.partials[((size_t)g.t * a.B + b) * kPartialStride + tid] = s_sum[tid];
         __threadfence();
     }
-    if (a.band) return;
+    if (a.band) {
+        if (warp == 0) tmem_dealloc(tmem, 512);
+        return;
+    }
     const int nlaunch = a.tiles_x * a.tiles_y;
     __syncthreads();
     if (tid == 0) s_last = (atomicAdd(a.tickets + b, 1u) == (unsigned)(nlaunch - 1));
     __syncthreads();
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
+    if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket taken
+    if (warp == 0) tmem_dealloc(tmem, 512);
+    if (ph && tid == 0) ph[NBLK * 16 + 7] = clock64();  // TMEM released
     if (!s_last) return;
     __threadfence();
     reduce_tiles<NT>(a.partials, a.tiles_x * a.tiles_y, a.B, b, red, s_sum);

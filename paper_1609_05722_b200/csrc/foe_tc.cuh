@@ -11,11 +11,11 @@
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 // nearest tf32 (ties away from zero): the 3xTF32 split x = hi + lo with hi = rn(x), lo = rn(x - hi)
-// leaves |lo| <= 2^-11 |x| and a lo error <= 2^-22 |x| (the MMA truncates fp32 inputs to tf32)
+// leaves |lo| <= 2^-11 |x| and a lo error <= 2^-22 |x| (the MMA truncates fp32 inputs to tf32).
+// Integer form of cvt.rna.tf32.f32 (which sm_100a emulates with an extra infinity test): identical
+// for every finite x, and every operand split here is finite.
 __device__ __forceinline__ float tf32_rn(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -199,6 +199,33 @@ __device__ __forceinline__ void umma_3xtf32(uint32_t d_tmem, uint32_t a_hi, uint
         umma_tf32_ts(d_tmem, a_hi + 8 * j, dh, idesc, (accumulate || j > 0) ? 1u : 0u);
         umma_tf32_ts(d_tmem, a_lo + 8 * j, dh, idesc, 1u);
         umma_tf32_ts(d_tmem, a_hi + 8 * j, dl, idesc, 1u);
+    }
+}
+
+// the same product with the B descriptors built once (db[2 j] = hi, db[2 j + 1] = lo of K step j):
+// the issuing thread then spends three instructions per K step
+template <int N, int NK>
+struct BDescs {
+    uint64_t d[2 * NK];
+    __device__ __forceinline__ void build(uint32_t b_hi, uint32_t b_lo) {
+        constexpr uint32_t LBO = (N / 8) * 128, SBO = 128;
+#pragma unroll
+        for (int j = 0; j < NK; ++j) {
+            d[2 * j] = umma_desc_kmajor(b_hi + 2 * j * LBO, LBO, SBO);
+            d[2 * j + 1] = umma_desc_kmajor(b_lo + 2 * j * LBO, LBO, SBO);
+        }
+    }
+};
+template <int N, int NK>
+__device__ __forceinline__ void umma_3xtf32_pre(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo, const BDescs<N, NK> &b,
+                                                int nk) {
+    constexpr uint32_t idesc = idesc_tf32(128, N);
+#pragma unroll
+    for (int j = 0; j < NK; ++j) {
+        if (j >= nk) break;
+        umma_tf32_ts(d_tmem, a_hi + 8 * j, b.d[2 * j], idesc, j > 0 ? 1u : 0u);
+        umma_tf32_ts(d_tmem, a_lo + 8 * j, b.d[2 * j], idesc, 1u);
+        umma_tf32_ts(d_tmem, a_hi + 8 * j, b.d[2 * j + 1], idesc, 1u);
     }
 }
 

@@ -28,6 +28,11 @@ full = t.cpu().numpy()
 a = full[:ncta * 3].reshape(ncta, 3).astype(np.float64)
 phs = full[ncta * 3:ncta * 3 + 18 * 16].reshape(18, 16).astype(np.float64)
 loop0 = float(full[ncta * 3 + 18 * 16])
+ext = full[ncta * 3 + 18 * 16: ncta * 3 + 18 * 16 + 10].astype(np.float64)
+if ext[2]:
+    names = ["loop start", "loop end", "kernel start", "griddep done", "fold done", "block reduce done", "ticket", "tmem released", "first fold value", "first fold store"]
+    print("CTA (0,0) phase stamps, cycles from kernel start:",
+          {n: int(ext[i] - ext[2]) for i, n in enumerate(names) if ext[i]})
 if phs.any():
     np.set_printoptions(precision=0, suppress=True, linewidth=200)
     cols = [0, 1, 2, 3, 4, 5, 6, 7, 8, 9]
