@@ -79,6 +79,29 @@ __device__ __forceinline__ float tc_tap_sum(const float *Yr, int r, int c) {
     return s0 + s1;
 }
 
+// im2col of one pixel's taps {8V..8V+7, 16+4V..16+4V+3} from the interleaved staged cells (u hi, u lo,
+// du hi, du lo) into A stage columns (TMEM lane = pixel), 4 taps per round
+template <int V, bool TRIAL, class T>
+__device__ __forceinline__ void tc_im2col(const float4 *sp, uint32_t st) {
+#pragma unroll
+    for (int rd = 0; rd < 3; ++rd) {
+        const int c0 = rd < 2 ? 8 * V + 4 * rd : 16 + 4 * V;
+        float uh[4], ul[4], dh[4], dl[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int t = c0 + i;
+            const float4 c = sp[(t / T::M) * T::SW + (t % T::M)];
+            uh[i] = c.x; ul[i] = c.y; dh[i] = c.z; dl[i] = c.w;
+        }
+        tmem_st4(st + T::C_AUH + c0, uh);
+        tmem_st4(st + T::C_AUL + c0, ul);
+        if (TRIAL) {
+            tmem_st4(st + T::C_ADH + c0, dh);
+            tmem_st4(st + T::C_ADL + c0, dl);
+        }
+    }
+}
+
 template <int NF, bool TRIAL, bool SYM>
 __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) {
     static_assert(NF % 8 == 0 && NF <= 32, "filter count rounded up to a multiple of 8");
@@ -301,29 +324,13 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             if (ph && warp == 0) ph[j * 16 + 5] = clock64();
             const uint32_t st = tmem + s * T::C_ASTAGE + lane_off;
             const int lr = 2 * j + (pl >> 6), lc = pl & 63;
-            {
-                // taps {0..7, 16..19} (warps 0-3) / {8..15, 20..23} (warps 4-7) of all four planes; tap 24
-                // is done by FFMA
-                const float4 *sp = S4 + lr * SW + lc;
-#pragma unroll
-                for (int rd = 0; rd < 3; ++rd) {  // 4 taps per round: 16 live registers
-                    const int c0 = rd < 2 ? 8 * v + 4 * rd : 16 + 4 * v;
-                    float uh[4], ul[4], dh[4], dl[4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int t = c0 + i;
-                        const float4 c = sp[(t / 5) * SW + (t % 5)];
-                        uh[i] = c.x; ul[i] = c.y; dh[i] = c.z; dl[i] = c.w;
-                    }
-                    tmem_st4(st + T::C_AUH + c0, uh);
-                    tmem_st4(st + T::C_AUL + c0, ul);
-                    if (TRIAL) {
-                        tmem_st4(st + T::C_ADH + c0, dh);
-                        tmem_st4(st + T::C_ADL + c0, dl);
-                    }
-                }
-                tc_wait_st();
-            }
+            // taps {0..7, 16..19} (warps 0-3) / {8..15, 20..23} (warps 4-7) of all four planes (compile-time
+            // tap offsets: one LDS.128 with an immediate offset per tap); tap 24 is done by FFMA
+            if (v == 0)
+                tc_im2col<0, TRIAL, T>(S4 + lr * SW + lc, st);
+            else
+                tc_im2col<1, TRIAL, T>(S4 + lr * SW + lc, st);
+            tc_wait_st();
             tc_fence_before();
             if (warp != 0) named_arrive(T::BAR_AFULL + s, 256);
             if (warp == 0) {
@@ -435,27 +442,34 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             }
             tc_wait_ld();
             float tmax = 0.0f;
+            // psi' (zero on padded cells outside the image: a warp-uniform test, edge tiles only)
+            auto point = [&](auto keep_all) {
 #pragma unroll
-            for (int i = 0; i < FH; ++i) {
-                const float k24 = s_k24[f0 + i];
-                const float zz = fmaf(k24, u24, z[i]);  // tap 24
-                float ps;
-                if (TRIAL) {
-                    const float d = fmaf(k24, d24, dz[i]);
-                    const float zo = zz - d;
-                    // one reciprocal for 1/(1+z^2) (psi') and 1/(2+z^2+zo^2) (the atanh argument)
-                    const float a1 = fmaf(zz, zz, 1.0f);
-                    const float b1 = fmaf(zo, zo, a1) + 1.0f;
-                    const float r = rcp_approx(a1 * b1);
-                    ps = zz * (r * b1);
-                    dz[i] = (d * fmaf(2.0f, zo, d)) * (r * a1);  // t = (z^2 - zo^2) / (2 + z^2 + zo^2)
-                    tmax = fmaxf(tmax, fabsf(dz[i]));
-                } else {
-                    ps = zz * rcp_approx(fmaf(zz, zz, 1.0f));
-                    dz[i] = zz;  // keep z for log1p(z^2)
+                for (int i = 0; i < FH; ++i) {
+                    const float k24 = s_k24[f0 + i];
+                    const float zz = fmaf(k24, u24, z[i]);  // tap 24
+                    float ps;
+                    if (TRIAL) {
+                        const float d = fmaf(k24, d24, dz[i]);
+                        const float zo = zz - d;
+                        // one reciprocal for 1/(1+z^2) (psi') and 1/(2+z^2+zo^2) (the atanh argument)
+                        const float a1 = fmaf(zz, zz, 1.0f);
+                        const float b1 = fmaf(zo, zo, a1) + 1.0f;
+                        const float r = rcp_approx(a1 * b1);
+                        ps = zz * (r * b1);
+                        dz[i] = (d * (zz + zo)) * (r * a1);  // t = (z^2 - zo^2) / (2 + z^2 + zo^2)
+                        tmax = fmaxf(tmax, fabsf(dz[i]));
+                    } else {
+                        ps = zz * rcp_approx(fmaf(zz, zz, 1.0f));
+                        dz[i] = zz;  // keep z for log1p(z^2)
+                    }
+                    z[i] = (decltype(keep_all)::value || in_img) ? ps : 0.0f;
                 }
-                z[i] = in_img ? ps : 0.0f;
-            }
+            };
+            if (__all_sync(0xffffffffu, in_img))
+                point(std::true_type{});
+            else
+                point(std::false_type{});
 #pragma unroll
             for (int c = 0; c < FH / 4; ++c) {
                 float hi[4], lo[4];
@@ -484,23 +498,47 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             // energy terms while the adjoint MMAs run (Y(j) is drained at step j + 2)
             float e0 = 0.0f, e1 = 0.0f;
             if (TRIAL) {
-                if (__any_sync(0xffffffffu, tmax > 0.2f)) {
+                // 2 a atanh(t) = 2 a (t + t^3/3 + ...): the series is cut where the next term is below fp32
+                // rounding for the warp's largest |t| (degree 9 up to 0.2, then 5, 3, 1); MUFU log beyond
+                const float wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));  // tmax >= 0
+                auto series = [&](auto deg) {
+                    constexpr int D = decltype(deg)::value;
+#pragma unroll
+                    for (int i = 0; i < FH; ++i) {
+                        const float t1 = dz[i], w = s_al2[f0 + i] * t1;  // 2 alpha t
+                        if (D == 1) {
+                            if (i & 1) e1 += w; else e0 += w;
+                            continue;
+                        }
+                        const float sq = t1 * t1;
+                        float pp;
+                        if (D == 9) {
+                            pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
+                            pp = fmaf(sq, pp, 1.0f / 5.0f);
+                            pp = fmaf(sq, pp, 1.0f / 3.0f);
+                        } else if (D == 5) {
+                            pp = fmaf(sq, 1.0f / 5.0f, 1.0f / 3.0f);
+                        } else {
+                            pp = 1.0f / 3.0f;
+                        }
+                        pp = fmaf(sq, pp, 1.0f);
+                        if (i & 1) e1 = fmaf(w, pp, e1); else e0 = fmaf(w, pp, e0);
+                    }
+                };
+                if (wmax > 0.2f) {
 #pragma unroll
                     for (int i = 0; i < FH; ++i) {
                         const float term = s_al[f0 + i] * two_atanh(dz[i]);
                         if (i & 1) e1 += term; else e0 += term;
                     }
+                } else if (wmax > 0.04f) {
+                    series(std::integral_constant<int, 9>{});
+                } else if (wmax > 0.004f) {
+                    series(std::integral_constant<int, 5>{});
+                } else if (wmax > 1e-4f) {
+                    series(std::integral_constant<int, 3>{});
                 } else {
-#pragma unroll
-                    for (int i = 0; i < FH; ++i) {
-                        const float t1 = dz[i], sq = t1 * t1;
-                        float pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
-                        pp = fmaf(sq, pp, 1.0f / 5.0f);
-                        pp = fmaf(sq, pp, 1.0f / 3.0f);
-                        pp = fmaf(sq, pp, 1.0f);
-                        const float w = s_al2[f0 + i] * t1;  // 2 alpha t
-                        if (i & 1) e1 = fmaf(w, pp, e1); else e0 = fmaf(w, pp, e0);
-                    }
+                    series(std::integral_constant<int, 1>{});
                 }
             } else {
 #pragma unroll
