@@ -3,7 +3,7 @@
 //
 // Same tile geometry, prologue, fold and reductions as k_pass; the two convolutions become implicit
 // GEMMs on the tensor cores, one 128-pixel block (two region rows) at a time:
-//   forward   Z  = A_u  . Kf^T    A_u[p][t] = u_new(p + off_t)  (im2col, K = 24 taps; tap 24 by FFMA)
+//   forward   Z  = A_u  . Kf^T    A_u[p][t] = u_new(p + off_t)  (im2col, K = 24 taps + one tap-24 step)
 //             dZ = A_du . Kf^T    (the same for du, for the energy change)
 //   adjoint   Y  = Psi  . Kt^T    Psi[p][f] = z/(1+z^2), Kt[t][f] = 2 a_f k_f[t]
 //             g(q) = sum_t Y(q + off_t)[t]       (25-term shifted sum on the CUDA cores)
@@ -40,8 +40,11 @@ struct TcCfg {
     static constexpr int BSZ = 32 * 32;                  // one 32 x 32 B operand (floats)
     // TMEM columns: A stage s at 128 s (A_u hi/lo, A_du hi/lo); D region s at 256 + 96 s (D_z -> Psi hi,
     // D_dz -> Psi lo, D_y)
-    static constexpr int C_AUH = 0, C_AUL = 24, C_ADH = 48, C_ADL = 72, C_ASTAGE = 96;  // K = 24 columns each
-    static constexpr int C_D0 = 192, C_DZ = 0, C_DDZ = 32, C_DY = 64, C_DREGION = 96, NDREG = 3;
+    // A stage: taps 0..23 of u hi / lo, du hi / lo (K = 24 each), then the tap-24 group {u hi, u lo, du hi,
+    // du lo, 0, 0, 0, 0} (one K = 8 step whose B operand selects the plane)
+    static constexpr int C_AUH = 0, C_AUL = 24, C_ADH = 48, C_ADL = 72, C_T24 = 96, C_ASTAGE = 104;
+    static constexpr int C_D0 = 208, C_DZ = 0, C_DDZ = 32, C_DY = 64, C_DREGION = 96, NDREG = 3;
+    static_assert(C_D0 >= 2 * C_ASTAGE && C_D0 + NDREG * C_DREGION <= 512, "TMEM budget");
     static_assert(RW == 64 && NBLK * 128 == RH * RW, "blocks of two 64-pixel region rows");
     static_assert(NF_MAX <= 32, "one N = 32 MMA covers the bank");
 };
@@ -49,9 +52,9 @@ struct TcCfg {
 template <int NF_MAX>
 __host__ __device__ constexpr size_t tc_smem_floats() {
     using T = TcCfg<NF_MAX>;
-    // staged planes u hi/lo, du hi/lo; Kf hi/lo, Kt hi/lo; Y ring; region gradient (two tap halves); alpha,
-    // tap 24, 2 alpha; the prologue's fp64 partials of every thread (parked for the epilogue)
-    return 4 * (size_t)T::PLANE + 4 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96 +
+    // staged planes u hi/lo, du hi/lo; Kf hi/lo, Kt hi/lo, four tap-24 B operands; Y ring; region gradient (two tap halves); alpha,
+    // (spare), 2 alpha; the prologue's fp64 partials of every thread (parked for the epilogue)
+    return 4 * (size_t)T::PLANE + 5 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96 +
            2 * (size_t)(kNumPartials - 1) * T::NT;
 }
 
@@ -79,7 +82,7 @@ __device__ __forceinline__ float tc_tap_sum(const float *Yr, int r, int c) {
     return s0 + s1;
 }
 
-// im2col of one pixel's taps {8V..8V+7, 16+4V..16+4V+3} from the interleaved staged cells (u hi, u lo,
+// im2col of one pixel's taps {8V..8V+7, 16+4V..16+4V+3} (and V = 1: the tap-24 group) from the interleaved staged cells (u hi, u lo,
 // du hi, du lo) into A stage columns (TMEM lane = pixel), 4 taps per round
 template <int V, bool TRIAL, class T>
 __device__ __forceinline__ void tc_im2col(const float4 *sp, uint32_t st) {
@@ -99,6 +102,11 @@ __device__ __forceinline__ void tc_im2col(const float4 *sp, uint32_t st) {
             tmem_st4(st + T::C_ADH + c0, dh);
             tmem_st4(st + T::C_ADL + c0, dl);
         }
+    }
+    if (V == 1) {  // tap-24 group: {u hi, u lo, du hi, du lo, 0, 0, 0, 0}
+        const float4 c = sp[(24 / T::M) * T::SW + (24 % T::M)];
+        const float g24[8] = {c.x, c.y, c.z, c.w, 0.0f, 0.0f, 0.0f, 0.0f};
+        tmem_st8(st + T::C_T24, g24);
     }
 }
 
@@ -141,11 +149,11 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     float4 *S4 = reinterpret_cast<float4 *>(sm);
     float *Kf = sm + 4 * T::PLANE;  // [hi | lo], forward B (N = filters, K = taps)
     float *Kt = Kf + 2 * T::BSZ;   // [hi | lo], adjoint B (N = taps, K = filters)
-    float *Yr = Kt + 2 * T::BSZ;   // Y ring [tap][ring row][YW]
+    float *K24 = Kt + 2 * T::BSZ;  // tap-24 B operands (K = 8 x N = 32): u hi+lo . hi, u hi . lo, du ..
+    float *Yr = K24 + T::BSZ;      // Y ring [tap][ring row][YW]
     float *Gr = Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold), two tap halves
     float *s_al = Gr + 2 * T::RH * T::RW;        // alpha_f, zero-padded
-    float *s_k24 = s_al + 32;                    // tap 24 of each filter (outside the K = 24 MMAs)
-    float *s_al2 = s_k24 + 32;                   // 2 alpha_f
+    float *s_al2 = s_al + 64;                    // 2 alpha_f
     // prologue partials 1..6 per thread, [k - 1][tid]: kept out of registers through the block loop
     double *s_acc = reinterpret_cast<double *>(s_al2 + 32);
 
@@ -176,9 +184,19 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         Kt[bsw_offset<32>(n, k)] = ht;
         Kt[T::BSZ + bsw_offset<32>(n, k)] = tf32_rn(vt - ht);
     }
+    // tap-24 operands: the A group holds (u hi, u lo, du hi, du lo) in K rows 0..3; [0] rows 0, 1 = k24 hi,
+    // [1] row 0 = k24 lo (z = ... + uh.k24h + ul.k24h + uh.k24l), [2] / [3] the same on rows 2, 3 (dz)
+    for (int e = tid; e < 4 * 256; e += NT) {
+        const int mtx = e >> 8, n = (e >> 3) & 31, k = e & 7;
+        const float v24 = n < nf ? a.kf[n * T::KT + 24] : 0.0f, h24 = tf32_rn(v24);
+        const int row = mtx >> 1 ? k - 2 : k;  // row within the (hi, lo) pair of the plane
+        float val = 0.0f;
+        if (row == 0) val = (mtx & 1) ? tf32_rn(v24 - h24) : h24;
+        else if (row == 1 && !(mtx & 1)) val = h24;
+        K24[mtx * 256 + bsw_offset<32>(n, k)] = val;
+    }
     for (int e = tid; e < 32; e += NT) {
         s_al[e] = e < nf ? a.alpha[e] : 0.0f;
-        s_k24[e] = e < nf ? a.kf[e * T::KT + 24] : 0.0f;
         s_al2[e] = e < nf ? 2.0f * a.alpha[e] : 0.0f;
     }
     for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {  // zero columns of the Y ring
@@ -317,6 +335,9 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
         BDescs<32, 3> kfd;
         kfd.build(smem_u32(Kf), smem_u32(Kf + T::BSZ));
+        uint64_t k24d[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) k24d[m] = umma_desc_kmajor(smem_u32(K24 + 256 * m), 512, 128);
         for (int j = 0; j < NBLK; ++j) {
             const int s = j & 1;
             if (j >= 2 && warp != 0) named_sync(T::BAR_AFREE + s, 256);  // released by warp 0 (below)
@@ -325,7 +346,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const uint32_t st = tmem + s * T::C_ASTAGE + lane_off;
             const int lr = 2 * j + (pl >> 6), lc = pl & 63;
             // taps {0..7, 16..19} (warps 0-3) / {8..15, 20..23} (warps 4-7) of all four planes (compile-time
-            // tap offsets: one LDS.128 with an immediate offset per tap); tap 24 is done by FFMA
+            // tap offsets: one LDS.128 with an immediate offset per tap); warps 4-7 also the tap-24 group
             if (v == 0)
                 tc_im2col<0, TRIAL, T>(S4 + lr * SW + lc, st);
             else
@@ -348,8 +369,15 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
                 tc_fence_after();
                 if (ph) ph[j * 16 + 7] = clock64();
                 if (elect_one()) {
+                    constexpr uint32_t idesc = idesc_tf32(128, 32);
                     umma_3xtf32_pre<32, 3>(sd + T::C_DZ, sa + T::C_AUH, sa + T::C_AUL, kfd, 3);
-                    if (TRIAL) umma_3xtf32_pre<32, 3>(sd + T::C_DDZ, sa + T::C_ADH, sa + T::C_ADL, kfd, 3);
+                    umma_tf32_ts(sd + T::C_DZ, sa + T::C_T24, k24d[0], idesc, 1u);
+                    umma_tf32_ts(sd + T::C_DZ, sa + T::C_T24, k24d[1], idesc, 1u);
+                    if (TRIAL) {
+                        umma_3xtf32_pre<32, 3>(sd + T::C_DDZ, sa + T::C_ADH, sa + T::C_ADL, kfd, 3);
+                        umma_tf32_ts(sd + T::C_DDZ, sa + T::C_T24, k24d[2], idesc, 1u);
+                        umma_tf32_ts(sd + T::C_DDZ, sa + T::C_T24, k24d[3], idesc, 1u);
+                    }
                     umma_commit(&mb_dfull[rg]);
                 }
                 __syncwarp();
@@ -424,10 +452,6 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const int gy = g.ry0 + lr, gx = g.rx0 + lc;
             const bool in_img = !SYM || (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W);
             const bool owned = gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1;
-            // tap 24 by FFMA from hi + lo (2^-22 relative, as the tensor-core taps)
-            const float4 c24 = S4[(lr + 4) * SW + lc + 4];
-            const float u24 = c24.x + c24.y;
-            const float d24 = TRIAL ? c24.z + c24.w : 0.0f;
             const bool pst = ph && (warp - T::W_PT) % 8 == 0;
             if (pst) ph[j * 16 + 1] = clock64();
             // this half's filters: all z / dz loads in flight at once; psi' (tf32 hi / lo, written over
@@ -446,11 +470,10 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             auto point = [&](auto keep_all) {
 #pragma unroll
                 for (int i = 0; i < FH; ++i) {
-                    const float k24 = s_k24[f0 + i];
-                    const float zz = fmaf(k24, u24, z[i]);  // tap 24
+                    const float zz = z[i];
                     float ps;
                     if (TRIAL) {
-                        const float d = fmaf(k24, d24, dz[i]);
+                        const float d = dz[i];
                         const float zo = zz - d;
                         // one reciprocal for 1/(1+z^2) (psi') and 1/(2+z^2+zo^2) (the atanh argument)
                         const float a1 = fmaf(zz, zz, 1.0f);
