@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const int i = k / C::CW, j = k - i * C::CW;
             if (!TRIAL) {
                 const float x = lu[q] - shift, h = tf32_rn(x);
-                S4[i * SW + j] = make_float4(h, tf32_rn(x - h), 0.0f, 0.0f);
+                S4[i * SW + j] = make_float4(h, tf32_rn_operand(x - h), 0.0f, 0.0f);
                 continue;
             }
             const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             const float un = (p.branch == FOE_QUADRATIC) ? prox_quad(ut, p.t, ob) : prox_idv(ut, p.t, ob);
             const float du = un - u;
             const float x = un - shift, h = tf32_rn(x), hd = tf32_rn(du);
-            S4[i * SW + j] = make_float4(h, tf32_rn(x - h), hd, tf32_rn(du - hd));
+            S4[i * SW + j] = make_float4(h, tf32_rn_operand(x - h), hd, tf32_rn_operand(du - hd));
             if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) {
                 uout[(size_t)(gy - a.lrow0) * a.W + gx] = un;
                 acc[1] += (double)du * (double)du;
@@ -475,12 +475,12 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
                     if (TRIAL) {
                         const float d = dz[i];
                         const float zo = zz - d;
-                        // one reciprocal for 1/(1+z^2) (psi') and 1/(2+z^2+zo^2) (the atanh argument)
+                        // psi' = z / (1+z^2) and t = (z^2 - zo^2) / (2+z^2+zo^2): two MUFU reciprocals (the
+                        // XU pipe has room; fewer issue slots than one reciprocal of the product)
                         const float a1 = fmaf(zz, zz, 1.0f);
                         const float b1 = fmaf(zo, zo, a1) + 1.0f;
-                        const float r = rcp_approx(a1 * b1);
-                        ps = zz * (r * b1);
-                        dz[i] = (d * (zz + zo)) * (r * a1);  // t = (z^2 - zo^2) / (2 + z^2 + zo^2)
+                        ps = zz * rcp_approx(a1);
+                        dz[i] = (d * (zz + zo)) * rcp_approx(b1);
                         tmax = fmaxf(tmax, fabsf(dz[i]));
                     } else {
                         ps = zz * rcp_approx(fmaf(zz, zz, 1.0f));
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     hi[i] = tf32_rn(z[4 * c + i]);
-                    lo[i] = tf32_rn(z[4 * c + i] - hi[i]);
+                    lo[i] = tf32_rn_operand(z[4 * c + i] - hi[i]);
                 }
                 tmem_st4(sd + T::C_DZ + f0 + 4 * c, hi);
                 tmem_st4(sd + T::C_DDZ + f0 + 4 * c, lo);

@@ -18,6 +18,10 @@ __device__ __forceinline__ float tf32_rn(float x) {
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
+// lo operand of a split: x + half a tf32 ulp, left for the MMA to truncate -- the tensor core reads the
+// top 19 bits, so this is rn(x) as an operand without the masking instruction (never used otherwise)
+__device__ __forceinline__ float tf32_rn_operand(float x) { return __uint_as_float(__float_as_uint(x) + 0x1000u); }
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // tcgen05.alloc by one full warp; the allocated base address is written to *slot (shared memory)
