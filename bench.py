@@ -271,6 +271,8 @@ def run_scaling_config(args, rank, local_rank, world):
             e1.record(stream)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
+            if os.environ.get("FOE_BENCH_VERBOSE"):
+                print(f"step {e0.elapsed_time(e1):.3f} ms", file=sys.stderr)
     t = torch.tensor([total_ms, px_it], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.barrier()
@@ -363,6 +365,8 @@ def main():
             e1.record(stream)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
+            if os.environ.get("FOE_BENCH_VERBOSE"):
+                print(f"step {e0.elapsed_time(e1):.3f} ms", file=sys.stderr)
             iters += len(res.traces[0])
             trials += res.traces[0].n_trials
     torch.cuda.synchronize()

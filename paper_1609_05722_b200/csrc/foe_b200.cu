@@ -234,12 +234,22 @@ __device__ __forceinline__ void block_reduce(double (&v)[kNumPartials], double (
         if (lane == 0) red[warp][k] = x;
     }
     __syncthreads();
-    if (threadIdx.x < kNumPartials) {
-        double s = 0.0;
-#pragma unroll 1
-        for (int w = 0; w < NT / 32; ++w) s += red[w][threadIdx.x];
-        out[threadIdx.x] = s;
+    // second level: warp 0, lane w holds warp w's sums (zero beyond NT/32), the same shuffle tree for all
+    // partials at once; out[] is complete for every thread on return
+    static_assert(NT / 32 <= 32, "one warp combines the per-warp sums");
+    if (warp == 0) {
+        double x[kNumPartials];
+#pragma unroll
+        for (int k = 0; k < kNumPartials; ++k) x[k] = lane < NT / 32 ? red[lane][k] : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+            for (int k = 0; k < kNumPartials; ++k) x[k] += __shfl_down_sync(0xffffffffu, x[k], off);
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < kNumPartials; ++k) out[k] = x[k];
     }
+    __syncthreads();
 }
 
 // fixed-order sum of one image's tile partials (layout [tile][B][8]) into s_sum, by a whole CTA:
