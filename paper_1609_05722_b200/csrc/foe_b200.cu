@@ -74,8 +74,15 @@ struct ImgCtl {
     double L, f_u, lam;
     int n, max_iters, trials, status, done, branch, failed_at;
     int iu, iup, inew, ig, ignew;
-    int pad[2];
+    float tau, t;  // fp32 step size tau = step_num / L and prox weight tau * lam, kept in step with L
 };
+
+// the trial step of the current L, computed once per change of L rather than by every thread of a pass
+__host__ __device__ inline void set_step(ImgCtl &c, double step_num) {
+    const double tau = step_num / c.L;  // SolverConfig.step_size, solver.py:64-65
+    c.tau = (float)tau;
+    c.t = (float)(tau * c.lam);
+}
 
 struct PassArgs {
     int B, H, W, n_filters, tiles_x, tiles_y, mode, no_decide, zero_mean;
@@ -206,11 +213,13 @@ __device__ void decide_ctl(const PassArgs &a, int b, const double *s, ImgCtl &c,
         const int og = c.ig; c.ig = c.ignew; c.ignew = og;
         c.f_u = f_new;
         c.L = L / a.relax;  // solver.py:172
+        set_step(c, a.step_num);
         c.n++;
         const double un = sqrt(un2);
         if (step < a.rel_tol * fmax(un, 1e-300) || c.n >= c.max_iters) finish_image(a, c, primary);  // :173-174
     } else {
         c.L = L * a.eta;  // solver.py:158-160
+        set_step(c, a.step_num);
         if (c.L > a.max_L) {
             c.status = FOE_SOLVE_STALLED;
             c.failed_at = c.n;
@@ -221,21 +230,55 @@ __device__ void decide_ctl(const PassArgs &a, int b, const double *s, ImgCtl &c,
 
 __device__ void decide(const PassArgs &a, int b, const double *s) { decide_ctl(a, b, s, a.ctl[b], true, a.mode); }
 
-// fixed-order block reduction of kNumPartials doubles (deterministic)
-template <int NT>
-__device__ __forceinline__ void block_reduce(double (&v)[kNumPartials], double (*red)[kNumPartials],
-                                             double *out) {
+// fixed-order block reduction of kNumPartials doubles (deterministic), in two halves that a kernel may
+// run at different times: per-warp shuffle sums of partials [K0, K1) into red[warp][k], then one warp's
+// shuffle tree over the per-warp sums into out[] (complete for every thread on return)
+template <int K0, int K1>
+__device__ __forceinline__ void warp_partials(const double (&v)[kNumPartials], double (*red)[kNumPartials]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double x[K1 - K0];
 #pragma unroll
-    for (int k = 0; k < kNumPartials; ++k) {
-        double x = v[k];
+    for (int k = K0; k < K1; ++k) x[k - K0] = v[k];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
-        if (lane == 0) red[warp][k] = x;
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int k = K0; k < K1; ++k) x[k - K0] += __shfl_down_sync(0xffffffffu, x[k - K0], off);
+    if (lane == 0)
+#pragma unroll
+        for (int k = K0; k < K1; ++k) red[warp][k] = x[k - K0];
+}
+
+// the per-warp sums through shared memory instead of shuffles (SHFL issues at one warp-instruction per
+// SM clock, so a whole CTA's fp64 shuffle trees cost ~1.5k cycles): each lane parks its values in the
+// warp's scratch (K1 - K0) x 32 doubles, lanes 4k..4k+3 add partial k's four groups of 8 lanes in order,
+// then two shuffle steps combine the groups.  Deterministic, a fixed association of its own.
+// Scratch row r (32 doubles) starts at scratch + r * PITCH doubles; warp w uses rows w * NK .. w * NK + NK - 1.
+template <int K0, int K1, int PITCH>
+__device__ __forceinline__ void warp_partials_smem(const double (&v)[kNumPartials], double (*red)[kNumPartials],
+                                                   double *scratch) {
+    constexpr int NK = K1 - K0;
+    static_assert(4 * NK <= 32 && PITCH >= 32, "four lanes per partial, 32 doubles per row");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *sc = scratch + warp * NK * PITCH;
+#pragma unroll
+    for (int k = 0; k < NK; ++k) sc[k * PITCH + lane] = v[K0 + k];
+    __syncwarp();
+    const int kk = lane >> 2, q = lane & 3;
+    double s = 0.0;
+    if (kk < NK) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += sc[kk * PITCH + 8 * q + i];
     }
+    s += __shfl_down_sync(0xffffffffu, s, 2);
+    s += __shfl_down_sync(0xffffffffu, s, 1);
+    if (q == 0 && kk < NK) red[warp][K0 + kk] = s;
+    __syncwarp();
+}
+
+template <int NT>
+__device__ __forceinline__ void block_combine(double (*red)[kNumPartials], double *out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __syncthreads();
-    // second level: warp 0, lane w holds warp w's sums (zero beyond NT/32), the same shuffle tree for all
-    // partials at once; out[] is complete for every thread on return
     static_assert(NT / 32 <= 32, "one warp combines the per-warp sums");
     if (warp == 0) {
         double x[kNumPartials];
@@ -252,16 +295,41 @@ __device__ __forceinline__ void block_reduce(double (&v)[kNumPartials], double (
     __syncthreads();
 }
 
+template <int NT>
+__device__ __forceinline__ void block_reduce(double (&v)[kNumPartials], double (*red)[kNumPartials],
+                                             double *out) {
+    warp_partials<0, kNumPartials>(v, red);
+    block_combine<NT>(red, out);
+}
+
 // fixed-order sum of one image's tile partials (layout [tile][B][8]) into s_sum, by a whole CTA:
 // thread k < 384 sums tiles k, k+384, ... then a fixed tree.  Shared by the last-CTA path and
 // k_decide, so a band-decomposed solve reduces in exactly the single-device order.
 // The tile stride is a fixed 384 whatever the block size (threads beyond it add exact zeros), so
 // every kernel that decides -- k_pass, k_pass_tc, k_decide -- reduces in the same order.
-constexpr int kReduceNT = 384;
+// Up to kFastReduceTiles tiles (every single-image configuration up to ~2k x 2k) take the one-warp-
+// per-partial path below instead.
+constexpr int kReduceNT = 384, kFastReduceTiles = 1024;
 template <int NT>
 __device__ void reduce_tiles(const double *partials, int ntiles, int B, int b, double (*red)[kNumPartials],
                              double *s_sum) {
     static_assert(NT >= kReduceNT && NT % 32 == 0, "reducing block narrower than the fixed tile stride");
+    if (ntiles <= kFastReduceTiles) {
+        // one warp per partial: lane l adds tiles l, l + 32, ... in order, then a shuffle tree -- one L2
+        // round trip and ~10 shuffles on the decision's critical path (the order depends on ntiles only)
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        __syncthreads();
+        if (warp < kNumPartials) {
+            double x = 0.0;
+#pragma unroll 8
+            for (int tt = lane; tt < ntiles; tt += 32) x += __ldcg(partials + ((size_t)tt * B + b) * kPartialStride + warp);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+            if (lane == 0) s_sum[warp] = x;
+        }
+        __syncthreads();
+        return;
+    }
     double tot[kNumPartials];
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) tot[k] = 0.0;
@@ -1297,6 +1365,7 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
         c.branch = branch[b];
         c.failed_at = -1;
         c.iu = 0; c.iup = 2; c.inew = 1;  // u_prev = u = u0 (solver.py:136-137), distinct slots
+        set_step(c, a.step_num);
         c.ig = 0; c.ignew = 1;
     }
     const size_t HWB = (size_t)B * H * W;
@@ -1532,6 +1601,7 @@ int foe_band_begin(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_ba
         memset(&c, 0, sizeof(c));
         c.L = cfg->lipschitz_init; c.lam = lam[b]; c.max_iters = max_iters[b]; c.branch = branch[b]; c.failed_at = -1;
         c.iu = 0; c.iup = 2; c.inew = 1; c.ig = 0; c.ignew = 1;
+        set_step(c, a.step_num);
     }
     const size_t local = (size_t)B * d->Hl * d->W;
     FOE_CUDA(cudaMemcpyAsync(a.ctl, hc.data(), sizeof(ImgCtl) * B, cudaMemcpyHostToDevice, st));

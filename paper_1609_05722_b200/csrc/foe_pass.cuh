@@ -190,9 +190,8 @@ struct TrialParams {
 __device__ __forceinline__ TrialParams trial_params(const PassArgs &a, const ImgCtl &c) {
     TrialParams p;
     p.iu = c.iu; p.iup = c.iup; p.inew = c.inew; p.ig = c.ig; p.ignew = c.ignew; p.branch = c.branch;
-    const double tau = a.step_num / c.L;  // SolverConfig.step_size, solver.py:64-65
-    p.tau = (float)tau;
-    p.t = (float)(tau * c.lam);
+    p.tau = c.tau;  // set_step: step_num / L (solver.py:64-65) and tau * lam
+    p.t = c.t;
     p.gam = (float)a.gamma;
     return p;
 }

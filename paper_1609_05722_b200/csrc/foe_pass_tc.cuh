@@ -53,9 +53,8 @@ template <int NF_MAX>
 __host__ __device__ constexpr size_t tc_smem_floats() {
     using T = TcCfg<NF_MAX>;
     // staged planes u hi/lo, du hi/lo; Kf hi/lo, Kt hi/lo, four tap-24 B operands; Y ring; region gradient (two tap halves); alpha,
-    // (spare), 2 alpha; the prologue's fp64 partials of every thread (parked for the epilogue)
-    return 4 * (size_t)T::PLANE + 5 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96 +
-           2 * (size_t)(kNumPartials - 1) * T::NT;
+    // (spare), 2 alpha
+    return 4 * (size_t)T::PLANE + 5 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96;
 }
 
 // sum over taps [T0, T1) of Y(row r + a - R, column c + b - R)[a M + b] from the Y ring: one ring-row
@@ -154,8 +153,6 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     float *Gr = Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold), two tap halves
     float *s_al = Gr + 2 * T::RH * T::RW;        // alpha_f, zero-padded
     float *s_al2 = s_al + 64;                    // 2 alpha_f
-    // prologue partials 1..6 per thread, [k - 1][tid]: kept out of registers through the block loop
-    double *s_acc = reinterpret_cast<double *>(s_al2 + 32);
 
     if (warp == 0) tmem_alloc(&s_tmem, 512);
     if (tid == 0) {
@@ -314,8 +311,10 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             }
         }
     }
-#pragma unroll
-    for (int k = 1; k < kNumPartials; ++k) s_acc[(k - 1) * NT + tid] = acc[k];
+    // the prologue's partials 1..6 are summed per warp now (the block loop only adds partial 0)
+    // scratch: the Y ring's data columns 2 .. 65 (its zero columns stay intact), one 32-double row per ring row
+    static_assert(T::YW % 2 == 0 && (NT / 32) * (kNumPartials - 1) <= T::KT * T::YROWS, "partial scratch");
+    warp_partials_smem<1, kNumPartials, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -574,13 +573,25 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         }
         acc[0] = e_own;
     }
-#pragma unroll
-    for (int k = 1; k < kNumPartials; ++k) acc[k] = s_acc[(k - 1) * NT + tid];
     tc_fence_before();
     __syncthreads();
     if (ph && tid == 0) ph[NBLK * 16 + 1] = clock64();  // loop end (cycles), CTA (0, 0)
-    // TMEM is released at the very end: tcgen05.dealloc here stalled warp 0 (and with it the fold and the
-    // block reduction) for ~6,500 cycles
+    // ---- per-tile partials first (last CTA of the image reduces and decides, as k_pass): the ticket's
+    // round trip overlaps the fold below ----
+    warp_partials_smem<0, 1, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));  // Y ring no longer live
+    block_combine<NT>(red, s_sum);
+    if (ph && tid == 0) ph[NBLK * 16 + 5] = clock64();  // block reduction done
+    const int nlaunch = a.tiles_x * a.tiles_y;
+    unsigned ticket = 0u;
+    if (tid == 0) {  // thread 0 publishes the tile's partials and takes the ticket; the rest fold meanwhile
+        double *pp = a.partials + ((size_t)g.t * a.B + b) * kPartialStride;
+#pragma unroll
+        for (int k = 0; k < kNumPartials; ++k) pp[k] = s_sum[k];
+        if (!a.band) {
+            __threadfence();
+            ticket = atomicAdd(a.tickets + b, 1u);
+        }
+    }
 
     // ---- fold padded pixels (symmetric rule) and write the owned gradient ----
     for (int k = tid; k < T::RW * 8; k += NT) {
@@ -612,23 +623,16 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     }
 
     if (ph && tid == 0) ph[NBLK * 16 + 4] = clock64();  // fold done
-    // ---- per-tile partials, last CTA of the image reduces and decides (as k_pass) ----
-    block_reduce<NT>(acc, red, s_sum);
-    if (ph && tid == 0) ph[NBLK * 16 + 5] = clock64();  // block reduction done
-    if (tid < kNumPartials) {
-        a.partials[((size_t)g.t * a.B + b) * kPartialStride + tid] = s_sum[tid];
-        __threadfence();
-    }
+    // TMEM is released at the very end (tcgen05.dealloc right after the loop stalled warp 0, and with it
+    // the whole epilogue, for ~6,500 cycles)
     if (a.band) {
         if (warp == 0) tmem_dealloc(tmem, 512);
         return;
     }
-    const int nlaunch = a.tiles_x * a.tiles_y;
-    __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(a.tickets + b, 1u) == (unsigned)(nlaunch - 1));
+    if (tid == 0) s_last = ticket == (unsigned)(nlaunch - 1);
     __syncthreads();
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
-    if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket taken
+    if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket seen
     if (warp == 0) tmem_dealloc(tmem, 512);
     if (ph && tid == 0) ph[NBLK * 16 + 7] = clock64();  // TMEM released
     if (!s_last) return;
