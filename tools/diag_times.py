@@ -28,9 +28,9 @@ full = t.cpu().numpy()
 a = full[:ncta * 3].reshape(ncta, 3).astype(np.float64)
 phs = full[ncta * 3:ncta * 3 + 18 * 16].reshape(18, 16).astype(np.float64)
 loop0 = float(full[ncta * 3 + 18 * 16])
-ext = full[ncta * 3 + 18 * 16: ncta * 3 + 18 * 16 + 10].astype(np.float64)
+ext = full[ncta * 3 + 18 * 16: ncta * 3 + 18 * 16 + 14].astype(np.float64)
 if ext[2]:
-    names = ["loop start", "loop end", "kernel start", "griddep done", "fold done", "block reduce done", "ticket", "tmem released", "first fold value", "first fold store"]
+    names = ["loop start", "loop end", "kernel start", "griddep done", "fold done", "block reduce done", "ticket", "tmem released", "first fold value", "first fold store", "loads issued", "ctl read", "cells staged", "warp partials"]
     print("CTA (0,0) phase stamps, cycles from kernel start:",
           {n: int(ext[i] - ext[2]) for i, n in enumerate(names) if ext[i]})
 if phs.any():
