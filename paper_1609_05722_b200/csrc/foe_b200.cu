@@ -18,6 +18,9 @@
 //    gradient), so every pass is one trial: ~1.37 passes per accepted iteration.
 #include "foe_b200.h"
 
+#ifndef FOE_ABLATE
+#define FOE_ABLATE 0  // timing ablations of the tensor-core pass (1: no shifted sums, 2: no energy series)
+#endif
 #ifndef FOE_STAMPS
 #define FOE_STAMPS 0  // per-block cycle stamps of the tensor-core pass (timing diagnostic builds only)
 #endif
