@@ -766,10 +766,14 @@ thread_local PinnedFlags t_flags;
 // k_loop_cond] until no image is live, so the tail of a solve needs no host round trip.  n_active[1]
 // counts the passes the loop ran, n_active[2] flags the safety cap.
 
-constexpr int kGraphChunk = 8;
+constexpr int kGraphChunkDefault = 8;
+int graph_chunk() {  // FOE_GRAPH_CHUNK overrides (timing experiments)
+    static const int c = getenv("FOE_GRAPH_CHUNK") ? std::max(1, atoi(getenv("FOE_GRAPH_CHUNK"))) : kGraphChunkDefault;
+    return c;
+}
 
-__global__ void k_loop_cond(cudaGraphConditionalHandle h, int *n_active, int cap) {
-    const int passes = (n_active[1] += kGraphChunk);
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, int *n_active, int cap, int chunk) {
+    const int passes = (n_active[1] += chunk);
     const bool live = n_active[0] > 0;
     if (live && passes >= cap) n_active[2] = 1;
     cudaGraphSetConditional(h, (live && passes < cap) ? 1u : 0u);
@@ -819,8 +823,9 @@ int loop_graph(int m, bool sym, const PassArgs &a, int cap, cudaGraphExec_t *out
     FOE_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     const long long before = g_launches.load();
     int rc = FOE_OK;
-    for (int k = 0; k < kGraphChunk && rc == FOE_OK; ++k) rc = launch_pass(m, sym, a, cs);
-    if (rc == FOE_OK) k_loop_cond<<<1, 1, 0, cs>>>(h, a.n_active, cap);
+    const int chunk = graph_chunk();
+    for (int k = 0; k < chunk && rc == FOE_OK; ++k) rc = launch_pass(m, sym, a, cs);
+    if (rc == FOE_OK) k_loop_cond<<<1, 1, 0, cs>>>(h, a.n_active, cap, chunk);
     cudaGraph_t captured = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(cs, &captured);
     g_launches.store(before);  // captured launches run (and are counted) per graph execution
@@ -1456,7 +1461,7 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     if (graph_loop) FOE_CUDA(cudaMemcpyAsync(loop_info, a.n_active, sizeof(loop_info), cudaMemcpyDeviceToHost, st));
     FOE_CUDA(cudaStreamSynchronize(st));
     if (graph_loop) {
-        g_launches.fetch_add(loop_info[1] + loop_info[1] / kGraphChunk, std::memory_order_relaxed);
+        g_launches.fetch_add(loop_info[1] + loop_info[1] / graph_chunk(), std::memory_order_relaxed);
         if (loop_info[2]) return fail(FOE_E_NUMERICAL, "solver did not terminate after %d passes", loop_info[1]);
     }
     int any_fail = 0;
