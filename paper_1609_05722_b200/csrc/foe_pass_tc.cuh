@@ -109,52 +109,52 @@ __device__ __forceinline__ void tc_im2col(const float4 *sp, uint32_t st) {
     }
 }
 
-template <int NF, bool TRIAL, bool SYM>
-__global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) {
-    static_assert(NF % 8 == 0 && NF <= 32, "filter count rounded up to a multiple of 8");
+// shared-memory carve-up of the tensor-core pass (dynamic buffers + the static arrays of the kernel)
+struct TcSmem {
+    float4 *S4;                           // staged cells {u hi, u lo, du hi, du lo}
+    float *Kf, *Kt, *K24, *Yr, *Gr, *s_al, *s_al2;
+    double (*red)[kNumPartials];
+    double *s_sum;
+    unsigned long long *mb_dfull, *mb_yfull, *mb_ring, *mb_sum;
+};
+
+template <int NF>
+__device__ __forceinline__ TcSmem tc_carve(float *sm, double (*red)[kNumPartials], double *s_sum,
+                                           unsigned long long *mb_dfull, unsigned long long *mb_yfull,
+                                           unsigned long long *mb_ring, unsigned long long *mb_sum) {
+    using T = TcCfg<32>;
+    TcSmem S;
+    // staged planes, split once into tf32 hi + lo (both rounded to nearest): u_new - shift and du
+    // (interleaved per cell as {u hi, u lo, du hi, du lo}: one 16-byte load per tap in the im2col)
+    S.S4 = reinterpret_cast<float4 *>(sm);
+    S.Kf = sm + 4 * T::PLANE;      // [hi | lo], forward B (N = filters, K = taps)
+    S.Kt = S.Kf + 2 * T::BSZ;      // [hi | lo], adjoint B (N = taps, K = filters)
+    S.K24 = S.Kt + 2 * T::BSZ;     // tap-24 B operands (K = 8 x N = 32): u hi+lo . hi, u hi . lo, du ..
+    S.Yr = S.K24 + T::BSZ;         // Y ring [tap][ring row][YW]
+    S.Gr = S.Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold), two tap halves
+    S.s_al = S.Gr + 2 * T::RH * T::RW;       // alpha_f, zero-padded
+    S.s_al2 = S.s_al + 64;                   // 2 alpha_f
+    S.red = red;
+    S.s_sum = s_sum;
+    S.mb_dfull = mb_dfull; S.mb_yfull = mb_yfull; S.mb_ring = mb_ring; S.mb_sum = mb_sum;
+    return S;
+}
+
+// once per CTA: TMEM, barriers, B operands, alpha, the Y ring's zero columns (launch arguments only)
+template <int NF>
+__device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uint32_t *s_tmem) {
     using T = TcCfg<32>;
     using C = PassCfg<5>;
     constexpr int NT = T::NT, R = T::R, SW = T::SW, NBLK = T::NBLK;
-    extern __shared__ __align__(128) float sm[];
-    __shared__ double red[NT / 32][kNumPartials];
-    __shared__ double s_sum[kNumPartials];
-    __shared__ int s_last;
-    __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) unsigned long long mb_dfull[T::NDREG], mb_yfull[T::NDREG];
-    __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK];
-
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int b = blockIdx.y;
+    float4 *S4 = S.S4;
+    float *Kf = S.Kf, *Kt = S.Kt, *K24 = S.K24, *Yr = S.Yr, *Gr = S.Gr, *s_al = S.s_al, *s_al2 = S.s_al2;
+    double(*red)[kNumPartials] = S.red;
+    double *s_sum = S.s_sum;
+    unsigned long long *mb_dfull = S.mb_dfull, *mb_yfull = S.mb_yfull, *mb_ring = S.mb_ring, *mb_sum = S.mb_sum;
+    (void)C::NCELL; (void)R; (void)SW; (void)lane; (void)Kf; (void)Kt; (void)K24; (void)s_al; (void)s_al2;
     const int nf = a.n_filters;
-    const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
-    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3] = globaltimer_ns();
-    // per-block / per-phase cycle stamps of CTA (0, 0) for the timing diagnostic (compiled in only with
-    // -DFOE_STAMPS=1: the predicated-off stamps cost ~3 % of the pass's issue slots)
-#if FOE_STAMPS
-    unsigned long long *ph = (a.dbg_times && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0 && lane == 0)
-                                 ? a.dbg_times + 3 * (size_t)gridDim.x * gridDim.y : nullptr;
-#else
-    constexpr unsigned long long *ph = nullptr;
-#endif
-    if (ph && tid == 0) ph[NBLK * 16 + 2] = clock64();  // kernel start (cycles)
-    // programmatic dependent launch: the next pass may be scheduled as soon as every CTA of this one
-    // has started; everything up to griddep_wait() below depends only on the launch arguments
-    griddep_launch_dependents();
-    const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
-    const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
-
-    // staged planes, split once into tf32 hi + lo (both rounded to nearest): u_new - shift and du
-    // (interleaved per cell as {u hi, u lo, du hi, du lo}: one 16-byte load per tap in the im2col)
-    float4 *S4 = reinterpret_cast<float4 *>(sm);
-    float *Kf = sm + 4 * T::PLANE;  // [hi | lo], forward B (N = filters, K = taps)
-    float *Kt = Kf + 2 * T::BSZ;   // [hi | lo], adjoint B (N = taps, K = filters)
-    float *K24 = Kt + 2 * T::BSZ;  // tap-24 B operands (K = 8 x N = 32): u hi+lo . hi, u hi . lo, du ..
-    float *Yr = K24 + T::BSZ;      // Y ring [tap][ring row][YW]
-    float *Gr = Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold), two tap halves
-    float *s_al = Gr + 2 * T::RH * T::RW;        // alpha_f, zero-padded
-    float *s_al2 = s_al + 64;                    // 2 alpha_f
-
-    if (warp == 0) tmem_alloc(&s_tmem, 512);
+    if (warp == 0) tmem_alloc(s_tmem, 512);
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
             mbar_init(&mb_dfull[s], 1);
@@ -200,8 +200,29 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         const int col = e & 3, rr = e >> 2;
         Yr[rr * T::YW + (col < 2 ? col : T::YW - 4 + col)] = 0.0f;
     }
-    griddep_wait();  // the previous pass (control block, iterates, gradients, partials) is complete
-    if (ph && tid == 0) ph[NBLK * 16 + 3] = clock64();  // dependency resolved
+}
+
+// One trial (TRIAL) or evaluation pass of this CTA's tile: stage the trial point, the 18-block tensor-core
+// loop, the fold; thread 0 publishes the tile's fp64 partials in buffer `pbuf` of a.partials.  ctl: the
+// image's control block (global or a resident copy; null in MODE_EVAL); rpar: phase parity of the
+// once-per-pass ring mbarriers; take_ticket: thread 0 then takes the image's ticket (the last CTA reduces
+// and decides).  Returns -1, before touching shared state, if the image is done; else thread 0's ticket.
+template <int NF, bool TRIAL, bool SYM>
+__device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const TileGeom &g, const ImgCtl *ctl,
+                                       unsigned rpar, int pbuf, bool take_ticket, unsigned long long *ph) {
+    using T = TcCfg<32>;
+    using C = PassCfg<5>;
+    constexpr int NT = T::NT, R = T::R, SW = T::SW, NBLK = T::NBLK;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int b = blockIdx.y;
+    float4 *S4 = S.S4;
+    float *Kf = S.Kf, *Kt = S.Kt, *K24 = S.K24, *Yr = S.Yr, *Gr = S.Gr, *s_al = S.s_al, *s_al2 = S.s_al2;
+    double(*red)[kNumPartials] = S.red;
+    double *s_sum = S.s_sum;
+    unsigned long long *mb_dfull = S.mb_dfull, *mb_yfull = S.mb_yfull, *mb_ring = S.mb_ring, *mb_sum = S.mb_sum;
+    (void)C::NCELL; (void)R; (void)SW; (void)lane; (void)Kf; (void)Kt; (void)K24; (void)s_al; (void)s_al2;
+    const int nf = a.n_filters;
+    (void)nf;
     constexpr int CPT = (C::NCELL + NT - 1) / NT;
     const size_t ioff = (size_t)b * a.Hl * a.W;
     // TRIAL: every candidate slot (3 iterate planes, 2 gradient planes) and the observation are loaded
@@ -228,12 +249,8 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     }
     TrialParams p{};
     if (a.mode != MODE_EVAL) {
-        const ImgCtl &c = a.ctl[b];
-        if (c.done && !a.no_decide) {  // image converged: release TMEM and leave
-            __syncthreads();
-            if (warp == 0) tmem_dealloc(s_tmem, 512);
-            return;
-        }
+        const ImgCtl c = *ctl;
+        if (c.done && !a.no_decide) return -1;  // image converged
         p = trial_params(a, c);
     }
     const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
@@ -319,11 +336,10 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 1] = globaltimer_ns();
+    if (a.dbg_times && tid == 0) a.dbg_times[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 3 + 1] = globaltimer_ns();
     // the CTA owns all 512 columns (one CTA per SM), so the allocation starts at column 0: constant
     // TMEM addresses keep the MMA operands in uniform registers
     constexpr uint32_t tmem = 0u;
-    if (tid == 0 && s_tmem != 0u) __trap();
     // per-block role stamps: [block][im2col, fwd, point, sum]
     if (ph && tid == 0) ph[NBLK * 16] = clock64();  // loop start (cycles)
 
@@ -419,7 +435,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
                 if (jd + T::NDREG < NBLK) named_arrive(T::BAR_DFREE + jd % T::NDREG, 288);  // for forward(jd + 3)
                 // the slot held Y(jd - 4), read by g(jd - 5) .. g(jd - 3): g(jd - 5) and g(jd - 3) were summed
                 // by this set (steps j - 4, j - 2), g(jd - 4) by the other one
-                if (jd >= T::RING) mbar_wait_sleep(&mb_sum[jd - T::RING], 0);
+                if (jd >= T::RING) mbar_wait_sleep(&mb_sum[jd - T::RING], rpar);
                 const int lr = 2 * jd + (pl >> 6), lc = pl & 63;
                 float *yrow = Yr + (lr & (T::YROWS - 1)) * T::YW + 2 + lc;
 #pragma unroll
@@ -433,7 +449,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             }
             if (sum) {  // g(js) over this warp's tap half (0..11 / 12..24) once Y(js-1 .. js+1) are in the ring
                 for (int n = js - 1; n <= js + 1; ++n)
-                    if (n >= 0 && n < NBLK) mbar_wait_sleep(&mb_ring[n], 0);
+                    if (n >= 0 && n < NBLK) mbar_wait_sleep(&mb_ring[n], rpar);
                 const int r = 2 * js + (pl >> 6), c = pl & 63;
                 float gsum;
                 if (js == 0 || js == NBLK - 1)
@@ -581,15 +597,14 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     warp_partials_smem<0, 1, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));  // Y ring no longer live
     block_combine<NT>(red, s_sum);
     if (ph && tid == 0) ph[NBLK * 16 + 5] = clock64();  // block reduction done
-    const int nlaunch = a.tiles_x * a.tiles_y;
-    unsigned ticket = 0u;
-    if (tid == 0) {  // thread 0 publishes the tile's partials and takes the ticket; the rest fold meanwhile
-        double *pp = a.partials + ((size_t)g.t * a.B + b) * kPartialStride;
+    int ticket = 0;
+    if (tid == 0) {  // thread 0 publishes the tile's partials (and takes the ticket); the rest fold meanwhile
+        double *parts = a.partials + (((size_t)pbuf * a.tiles_x * a.tiles_y + g.t) * a.B + b) * kPartialStride;
 #pragma unroll
-        for (int k = 0; k < kNumPartials; ++k) pp[k] = s_sum[k];
-        if (!a.band) {
+        for (int k = 0; k < kNumPartials; ++k) parts[k] = s_sum[k];
+        if (take_ticket) {
             __threadfence();
-            ticket = atomicAdd(a.tickets + b, 1u);
+            ticket = (int)atomicAdd(a.tickets + b, 1u);
         }
     }
 
@@ -623,13 +638,61 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     }
 
     if (ph && tid == 0) ph[NBLK * 16 + 4] = clock64();  // fold done
+    return ticket;
+}
+
+template <int NF, bool TRIAL, bool SYM>
+__global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) {
+    static_assert(NF % 8 == 0 && NF <= 32, "filter count rounded up to a multiple of 8");
+    using T = TcCfg<32>;
+    constexpr int NT = T::NT, NBLK = T::NBLK;
+    extern __shared__ __align__(128) float sm[];
+    __shared__ double red[NT / 32][kNumPartials];
+    __shared__ double s_sum[kNumPartials];
+    __shared__ int s_last;
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) unsigned long long mb_dfull[T::NDREG], mb_yfull[T::NDREG];
+    __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int b = blockIdx.y;
+    const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3] = globaltimer_ns();
+    // per-block / per-phase cycle stamps of CTA (0, 0) for the timing diagnostic (compiled in only with
+    // -DFOE_STAMPS=1: the predicated-off stamps cost ~3 % of the pass's issue slots)
+#if FOE_STAMPS
+    unsigned long long *ph = (a.dbg_times && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0 && lane == 0)
+                                 ? a.dbg_times + 3 * (size_t)gridDim.x * gridDim.y : nullptr;
+#else
+    constexpr unsigned long long *ph = nullptr;
+    (void)lane;
+#endif
+    if (ph && tid == 0) ph[NBLK * 16 + 2] = clock64();  // kernel start (cycles)
+    // programmatic dependent launch: the next pass may be scheduled as soon as every CTA of this one
+    // has started; everything up to griddep_wait() below depends only on the launch arguments
+    griddep_launch_dependents();
+    const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
+    const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
+    const TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_ring, mb_sum);
+    tc_setup<NF>(a, S, &s_tmem);
+    griddep_wait();  // the previous pass (control block, iterates, gradients, partials) is complete
+    if (ph && tid == 0) ph[NBLK * 16 + 3] = clock64();  // dependency resolved
+    if (tid == 0 && s_tmem != 0u) __trap();
+    constexpr uint32_t tmem = 0u;
+    const int ticket = tc_body<NF, TRIAL, SYM>(a, S, g, a.mode == MODE_EVAL ? nullptr : a.ctl + b, 0u, 0, !a.band, ph);
+    if (ticket < 0) {
+        __syncthreads();  // image converged: release TMEM and leave
+        if (warp == 0) tmem_dealloc(tmem, 512);
+        return;
+    }
+    const int nlaunch = a.tiles_x * a.tiles_y;
     // TMEM is released at the very end (tcgen05.dealloc right after the loop stalled warp 0, and with it
     // the whole epilogue, for ~6,500 cycles)
     if (a.band) {
         if (warp == 0) tmem_dealloc(tmem, 512);
         return;
     }
-    if (tid == 0) s_last = ticket == (unsigned)(nlaunch - 1);
+    if (tid == 0) s_last = ticket == nlaunch - 1;
     __syncthreads();
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
     if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket seen
