@@ -654,6 +654,35 @@ int launch_pass_tc_t(const PassArgs &a, cudaStream_t st) {
     return FOE_OK;
 }
 
+// resident tensor-core solve (one cooperative launch for the whole solve): FOE_OK if launched, 1 if not
+// applicable (filter count, co-residency, cooperative launch support)
+template <int NF, bool SYM>
+int launch_resident_tc_t(const PassArgs &a, cudaStream_t st) {
+    using T = TcCfg<32>;
+    const size_t smem = std::max<size_t>(sizeof(float) * (tc_smem_floats<32>() + 64), 116 * 1024);
+    int dev = 0, nsm = 0, nb = 0, coop = 0;
+    FOE_CUDA(cudaGetDevice(&dev));
+    FOE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    FOE_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    if (!coop) return 1;
+    FOE_CUDA(cudaFuncSetAttribute(k_solve_resident_tc<NF, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FOE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_solve_resident_tc<NF, SYM>, T::NT, smem));
+    if ((long)nb * nsm < (long)a.tiles_x * a.tiles_y * a.B) return 1;
+    dim3 grid(a.tiles_x * a.tiles_y, a.B);
+    void *args[] = {(void *)&a};
+    FOE_CUDA(cudaLaunchCooperativeKernel((const void *)k_solve_resident_tc<NF, SYM>, grid, dim3(T::NT), args, smem, st));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return FOE_OK;
+}
+
+int launch_resident_tc(bool sym, const PassArgs &a, cudaStream_t st) {
+    switch ((a.n_filters + 7) / 8) {
+        case 3: return sym ? launch_resident_tc_t<24, true>(a, st) : launch_resident_tc_t<24, false>(a, st);
+        case 4: return sym ? launch_resident_tc_t<32, true>(a, st) : launch_resident_tc_t<32, false>(a, st);
+        default: return 1;
+    }
+}
+
 int launch_pass(int m, bool sym, const PassArgs &a, cudaStream_t st) {
     const bool trial = a.mode == MODE_TRIAL;
     if (use_tc(m, a.n_filters)) {
@@ -1392,7 +1421,17 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     const char *env = getenv("FOE_RESIDENT");
     const bool try_resident = B <= kResidentMaxB && env && env[0] == '1';
     bool resident = false, graph_loop = false;
-    if (try_resident) {
+    // the tensor-core pass has its own resident solve, opt-in (FOE_RESIDENT_TC=1): measured ~13 % slower
+    // per pass than the programmatic-dependent per-pass launches (grid barrier + every CTA deciding)
+    const char *env_tc = getenv("FOE_RESIDENT_TC");
+    if (B <= kResidentMaxB && use_tc(bank->m, bank->n) && env_tc && env_tc[0] == '1') {
+        FOE_CUDA(cudaMemsetAsync(a.grid_bar, 0, sizeof(unsigned) * 2, st));
+        a.mode = MODE_TRIAL;
+        rc = launch_resident_tc(bank->boundary == FOE_SYMMETRIC, a, st);
+        if (rc < 0) return rc;
+        resident = rc == FOE_OK;
+    }
+    if (!resident && try_resident) {
         FOE_CUDA(cudaMemsetAsync(a.grid_bar, 0, sizeof(unsigned) * 2, st));
         rc = launch_resident(bank->m, bank->boundary == FOE_SYMMETRIC, a, st);
         if (rc < 0) return rc;
