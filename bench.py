@@ -463,7 +463,7 @@ def main():
                                             "per pixel) / pass time"},
                 "e2e": {"value": e2e_value, "unit": "Mpixel*iter/s", "ms_per_denoise": float(e2e_t.item()),
                         "h2d_bytes_per_step": int(y.nbytes),
-                        "d2h_bytes_per_step": int(H * W * (8 + 4))},  # image (f64) + transformed (f32)
+                        "d2h_bytes_per_step": int(H * W * (8 + 8))},  # image (f64) + transformed (f64, cast on the device)
                 "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
                 "clocks": clk.summary(),
                 "fallback_48x7": fallback,
