@@ -13,6 +13,7 @@ semantics.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -141,6 +142,25 @@ class DeviceSolveResult:
     failed_at: list
 
 
+_tls = threading.local()
+
+
+def _workspace(nbytes: int, device):
+    """Per-thread cached solve workspace: stable device pointers keep the captured solve-loop graph
+    (keyed by the pass arguments, hence by the workspace address) valid across calls."""
+    import torch
+    cache = getattr(_tls, "ws", None)
+    if cache is None:
+        cache = _tls.ws = {}
+    key = (str(device), nbytes)
+    ws = cache.get(key)
+    if ws is None:
+        if len(cache) >= 4:
+            cache.clear()
+        ws = cache[key] = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    return ws
+
+
 def solve_device(model, u0, obs, lam, branch, max_iters, cfg: SolverConfig | None = None,
                  raise_on_failure: bool = True) -> DeviceSolveResult:
     """Device-resident iPiano over the FoE energy for a batch (B,H,W) of fp32 CUDA tensors.
@@ -173,7 +193,7 @@ def solve_device(model, u0, obs, lam, branch, max_iters, cfg: SolverConfig | Non
     bank = device_bank(model)
     L = _lib.lib()
     ws_bytes = L.foe_solve_workspace_size(bank.handle, B, H, W, cap)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=u0.device)
+    ws = _workspace(ws_bytes, u0.device)
     u_out = torch.empty_like(u0)
     status = (_lib.ImageStatusC * B)()
     trace = np.zeros((B, cap, 6))
