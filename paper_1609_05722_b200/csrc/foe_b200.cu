@@ -347,6 +347,7 @@ __device__ void reduce_tiles(const double *partials, int ntiles, int B, int b, d
 #include "foe_pass.cuh"
 #include "foe_tc.cuh"
 #include "foe_pass_tc.cuh"
+#include "foe_pass_tc7.cuh"
 
 // ------------------------------------------------------------------------------------------------
 // elementwise kernels
@@ -683,8 +684,32 @@ int launch_resident_tc(bool sym, const PassArgs &a, cudaStream_t st) {
     }
 }
 
+// tensor-core pass for 7x7 banks with <= 48 filters (k_pass_tc7): opt-in, FOE_TC7=1
+bool use_tc7(int m, int nf) {
+    const char *e = getenv("FOE_TC7");
+    return m == 7 && nf <= 48 && e && e[0] == '1';
+}
+
+template <bool TRIAL, bool SYM>
+int launch_pass_tc7_t(const PassArgs &a, cudaStream_t st) {
+    const size_t smem = sizeof(float) * (tc7_smem_floats() + 64);
+    static unsigned long long configured = 0;
+    int dev = 0;
+    FOE_CUDA(cudaGetDevice(&dev));
+    if (!(configured >> (dev & 63) & 1ull)) {
+        FOE_CUDA(cudaFuncSetAttribute(k_pass_tc7<TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured |= 1ull << (dev & 63);
+    }
+    FOE_CUDA(launch_pdl(k_pass_tc7<TRIAL, SYM>, dim3(a.tiles_x * a.tiles_yl, a.B), dim3(TcCfg7::NT), smem, st, a));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return FOE_OK;
+}
+
 int launch_pass(int m, bool sym, const PassArgs &a, cudaStream_t st) {
     const bool trial = a.mode == MODE_TRIAL;
+    if (use_tc7(m, a.n_filters))
+        return trial ? (sym ? launch_pass_tc7_t<true, true>(a, st) : launch_pass_tc7_t<true, false>(a, st))
+                     : (sym ? launch_pass_tc7_t<false, true>(a, st) : launch_pass_tc7_t<false, false>(a, st));
     if (use_tc(m, a.n_filters)) {
         switch ((a.n_filters + 7) / 8) {
             case 1: return trial ? (sym ? launch_pass_tc_t<8, true, true>(a, st) : launch_pass_tc_t<8, true, false>(a, st))
