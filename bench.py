@@ -129,7 +129,8 @@ def bench_fallback_bank(fp, _lib, L, y_dev, lam, cfg, stream, fp32_peak_tflops, 
     return {"model": f"foe_fallback48x7 ({n} filters {k}x{k}, dct7, symmetric)", "ms_per_denoise": ms / steps,
             "value": H * W * iters / (ms * 1e-3) / 1e6, "unit": "Mpixel*iter/s", "iterations": iters / steps,
             "pass_ms": pass_ms, "alg_flop_per_px_it": flop_px_it,
-            "kernel": "k_pass_tc" if tc else f"k_pass<{k},TRIAL,SYM> (FFMA)",
+            "kernel": (f"k_pass_tc7<TRIAL,SYM> (tcgen05 3xTF32, {k}x{k})" if k == 7 else "k_pass_tc") if tc
+            else f"k_pass<{k},TRIAL,SYM> (FFMA)",
             "roofline_frac": achieved / fp32_peak_tflops, "achieved_tflops": achieved}
 
 

@@ -684,10 +684,10 @@ int launch_resident_tc(bool sym, const PassArgs &a, cudaStream_t st) {
     }
 }
 
-// tensor-core pass for 7x7 banks with <= 48 filters (k_pass_tc7): opt-in, FOE_TC7=1
+// tensor-core pass for 7x7 banks with <= 48 filters (k_pass_tc7); FOE_TC7=0 (or FOE_TC=0) forces the FFMA pass
 bool use_tc7(int m, int nf) {
-    const char *e = getenv("FOE_TC7");
-    return m == 7 && nf <= 48 && e && e[0] == '1';
+    const char *e = getenv("FOE_TC7"), *e5 = getenv("FOE_TC");
+    return m == 7 && nf <= 48 && !(e && e[0] == '0') && !(e5 && e5[0] == '0');
 }
 
 template <bool TRIAL, bool SYM>
@@ -1830,7 +1830,7 @@ int foe_adjoint_bank64(const double *filters, int n, int m, int boundary, const 
     return bank64<true>(filters, n, m, boundary, y, out, B, H, W, stream);
 }
 
-int foe_pass_uses_tensor_cores(int m, int nf) { return use_tc(m, nf) ? 1 : 0; }
+int foe_pass_uses_tensor_cores(int m, int nf) { return (use_tc(m, nf) || use_tc7(m, nf)) ? 1 : 0; }
 
 int foe_debug_tc_rate(int n, int ts, int nmma, long long *out_cycles, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;

@@ -1,6 +1,6 @@
 // foe_pass_tc7.cuh -- tensor-core (tcgen05, 3xTF32) variant of the fused FoE pass for 7x7 banks with up
 // to 48 filters (the BASELINE 48 x 7 x 7 fallback bank; the paper's filter-bank size).  Included by
-// foe_b200.cu after foe_pass_tc.cuh; opt-in (FOE_TC7=1) until measured and parity-tested on the device.
+// foe_b200.cu after foe_pass_tc.cuh; the default for such banks (FOE_TC7=0 forces the FFMA pass).
 //
 // Same tile geometry as k_pass<7> (48 x 64 regions, 42 x 58 owned), prologue, fold and reductions as
 // k_pass_tc; per 128-pixel block (two region rows, 24 blocks per tile):
