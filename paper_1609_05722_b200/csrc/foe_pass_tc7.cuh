@@ -38,7 +38,7 @@ struct TcCfg7 {
     static constexpr int BKF = 48 * 48, BK48 = 48 * 8, BKT = 64 * 48;
     static constexpr int YBW = RW + 6;                 // Y block buffer row (3 zero columns each side)
     static constexpr int YB = KT * 2 * YBW;            // one block's Y: [tap][row][YBW]
-    static constexpr int HSLOTS = 6, HROWS = 2 * HSLOTS;  // H ring: [a][ring row][RW]
+    static constexpr int HSLOTS = 8, HROWS = 2 * HSLOTS;  // H ring: [a][ring row][RW] (power of two: masks)
     // named barriers
     static constexpr int BAR_AFREE = 1, BAR_AFULL = 2, BAR_DFREE = 3, BAR_DFULL = 5, BAR_PFULL = 7, BAR_YFULL = 9,
                          BAR_SET = 11;
@@ -372,22 +372,50 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                     }
                     if (TRIAL) {
                         const float wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
+                        // series cut per warp as in k_pass_tc (first omitted term below 2^-25 relative)
+                        auto series = [&](auto deg) {
+                            constexpr int D = decltype(deg)::value;
+#pragma unroll
+                            for (int i = 0; i < 12; ++i) {
+                                const float t1 = dz[i], w = s_al2[f0 + i] * t1;
+                                if (D == 1) {
+                                    if (i & 1) e1 += w; else e0 += w;
+                                    continue;
+                                }
+                                const float sq = t1 * t1;
+                                float pp;
+                                if (D == 9) {
+                                    pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
+                                    pp = fmaf(sq, pp, 1.0f / 5.0f);
+                                    pp = fmaf(sq, pp, 1.0f / 3.0f);
+                                } else if (D == 7) {
+                                    pp = fmaf(sq, 1.0f / 7.0f, 1.0f / 5.0f);
+                                    pp = fmaf(sq, pp, 1.0f / 3.0f);
+                                } else if (D == 5) {
+                                    pp = fmaf(sq, 1.0f / 5.0f, 1.0f / 3.0f);
+                                } else {
+                                    pp = 1.0f / 3.0f;
+                                }
+                                pp = fmaf(sq, pp, 1.0f);
+                                if (i & 1) e1 = fmaf(w, pp, e1); else e0 = fmaf(w, pp, e0);
+                            }
+                        };
                         if (wmax > 0.2f) {
 #pragma unroll
                             for (int i = 0; i < 12; ++i) {
                                 const float term = s_al[f0 + i] * two_atanh(dz[i]);
                                 if (i & 1) e1 += term; else e0 += term;
                             }
+                        } else if (wmax > 0.12f) {
+                            series(std::integral_constant<int, 9>{});
+                        } else if (wmax > 0.04f) {
+                            series(std::integral_constant<int, 7>{});
+                        } else if (wmax > 0.015f) {
+                            series(std::integral_constant<int, 5>{});
+                        } else if (wmax > 2.5e-4f) {
+                            series(std::integral_constant<int, 3>{});
                         } else {
-#pragma unroll
-                            for (int i = 0; i < 12; ++i) {
-                                const float t1 = dz[i], sq = t1 * t1, w = s_al2[f0 + i] * t1;
-                                float pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
-                                pp = fmaf(sq, pp, 1.0f / 5.0f);
-                                pp = fmaf(sq, pp, 1.0f / 3.0f);
-                                pp = fmaf(sq, pp, 1.0f);
-                                if (i & 1) e1 = fmaf(w, pp, e1); else e0 = fmaf(w, pp, e0);
-                            }
+                            series(std::integral_constant<int, 1>{});
                         }
                     } else {
 #pragma unroll
@@ -435,13 +463,13 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                 }
                 named_sync(T::BAR_SET + set, 256);  // the whole block's Y is in the buffer
                 // H(j): thread (pixel, a-half) -> H_a for a in {0..3} / {4..6}; ring slot j % HSLOTS held
-                // H(j - 6), last read by the vertical sums of blocks j - 8 .. j - 4 (j - 5 the other set's)
-                if (j >= 5) mbar_wait_sleep(&mb_vdone[j - 5], 0);
+                // H(j - 8), last read by the vertical sums of blocks j - 10 .. j - 6 (j - 7 the other set's)
+                if (j >= 7) mbar_wait_sleep(&mb_vdone[j - 7], 0);
                 {
                     const int p2 = ws * 32 + lane;  // 0..255
                     const int px = p2 & 127, ah = p2 >> 7;
                     const int rr = px >> 6, cc = px & 63;
-                    const int hrow = (j % T::HSLOTS) * 2 + rr;
+                    const int hrow = (2 * j + rr) & (T::HROWS - 1);
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const int aa = 4 * ah + k;
@@ -468,15 +496,21 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                 const int px = p2 & 127, ah = p2 >> 7;
                 const int r = 2 * q + (px >> 6), c = px & 63;
                 float s0 = 0.0f, s1 = 0.0f;
+                auto vsum = [&](auto edge) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int aa = 4 * ah + k;
-                    if (aa >= 7) continue;
-                    const int rr = r + aa - R;
-                    if (rr < 0 || rr >= T::RH) continue;
-                    const float vv = Hr[(aa * T::HROWS + ((rr >> 1) % T::HSLOTS) * 2 + (rr & 1)) * T::RW + c];
-                    if (k & 1) s1 += vv; else s0 += vv;
-                }
+                    for (int k = 0; k < 4; ++k) {
+                        const int aa = 4 * ah + k;
+                        if (aa >= 7) continue;
+                        const int rr = r + aa - R;
+                        if (decltype(edge)::value && (rr < 0 || rr >= T::RH)) continue;
+                        const float vv = Hr[(aa * T::HROWS + (rr & (T::HROWS - 1))) * T::RW + c];
+                        if (k & 1) s1 += vv; else s0 += vv;
+                    }
+                };
+                if (q < 2 || q >= NBLK - 2)
+                    vsum(std::true_type{});
+                else
+                    vsum(std::false_type{});
                 Gr[ah * T::RH * T::RW + r * T::RW + c] = s0 + s1;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&mb_vdone[q]);
