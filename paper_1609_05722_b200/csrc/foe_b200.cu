@@ -853,7 +853,7 @@ thread_local LoopGraphCache t_graphs;
 // the instantiated loop graph for these pass arguments (captured once, reused while the workspace,
 // shape and solver constants stay the same)
 int loop_graph(int m, bool sym, const PassArgs &a, int cap, cudaGraphExec_t *out) {
-    const int tc = use_tc(m, a.n_filters) ? 1 : 0;
+    const int tc = use_tc(m, a.n_filters) ? 1 : use_tc7(m, a.n_filters) ? 2 : 0;
     for (auto &e : t_graphs.entries)
         if (e.m == m && e.sym == (int)sym && e.cap == cap && e.tc == tc && !memcmp(&e.key, &a, sizeof(PassArgs))) {
             *out = e.exec;

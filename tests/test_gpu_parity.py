@@ -493,3 +493,38 @@ def test_hessian_cg_and_param_gradients_vs_reference_golden(golden):
     d_beta, d_logw = tr.param_gradients(w_star, model, smp, objective, tr.TrainConfig())
     assert rel_l2(d_beta, g["tr_dbeta"]) <= 1e-8
     assert rel_l2(d_logw, g["tr_dlogw"]) <= 1e-8
+
+
+@pytest.mark.parametrize("kernel", ["ffma", "tc7"])
+def test_fallback_bank_solve_vs_oracle(monkeypatch, kernel):
+    """48 x 7 x 7 fallback bank through each 7x7 pass kernel (k_pass<7> FFMA, k_pass_tc7): parity gates vs the
+    oracle on a 96 x 112 transform / quadratic solve (150 iterations)."""
+    monkeypatch.setenv("FOE_TC7", "1" if kernel == "tc7" else "0")
+    model = fp.load_packaged_model("foe_fallback48x7")
+    x, y = make_counts(96, 112, 3, 2.0)
+    ref = orc.denoise(y, 2.0, oracle_model(model), "transform", TABLE, force_branch="quadratic", rel_tol=0.0)
+    r = fp.denoise(fp.DenoiseRequest(noisy=y, peak=2.0, model=model, variant="transform", force_branch="quadratic"),
+                   fp.SolverConfig(rel_tol=0.0))
+    assert len(r.trace) == 150
+    _check_solve(r.image, ref["image"], 2.0, x, f"{kernel} fallback bank")
+
+
+def test_tc7_matches_ffma_7x7(monkeypatch):
+    """k_pass_tc7 and k_pass<7> take the same decisions on a 256^2 48 x 7 x 7 solve (identical L-trace) and agree
+    to fp32 rounding on the result; the fused gradient agrees to 1e-5 (both vs each other)."""
+    model = fp.load_packaged_model("foe_fallback48x7")
+    x, y = make_counts(256, 256, 5, 1.0)
+    out = {}
+    for k in ("0", "1"):
+        monkeypatch.setenv("FOE_TC7", k)
+        r = fp.denoise(fp.DenoiseRequest(noisy=y, peak=1.0, model=model, variant="transform",
+                                         force_branch="quadratic"), fp.SolverConfig(rel_tol=0.0))
+        out[k] = (np.asarray(r.trace.L), r.image, r.transformed.astype(np.float32).astype(np.float64))
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert np.max(np.abs(out["0"][1] - out["1"][1])) <= 1e-4
+    u = out["0"][2]  # both kernels' gradients at the same (converged, fp32) iterate
+    g = {}
+    for k in ("0", "1"):
+        monkeypatch.setenv("FOE_TC7", k)
+        g[k] = fp.foe_gradient(u, model)
+    assert rel_l2(g["1"], g["0"]) <= 1e-5
