@@ -241,7 +241,10 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
             }
         }
     }
-    warp_partials<1, kNumPartials>(acc, red);
+    // the prologue's partials 1..6 summed per warp through shared memory (the H ring and region gradient are
+    // not live yet; CTA-wide fp64 shuffle trees cost ~1.5k cycles of SHFL issue)
+    static_assert((NT / 32) * (kNumPartials - 1) * 32 <= (7 * T::HROWS * T::RW + 2 * T::RH * T::RW) / 2, "scratch");
+    warp_partials_smem<1, kNumPartials, 32>(acc, red, reinterpret_cast<double *>(Hr));
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -520,7 +523,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
     }
     tc_fence_before();
     __syncthreads();
-    warp_partials<0, 1>(acc, red);
+    warp_partials_smem<0, 1, 32>(acc, red, reinterpret_cast<double *>(Hr));  // H ring no longer live
     block_combine<NT>(red, s_sum);
     const int nlaunch = a.tiles_x * a.tiles_y;
     int ticket = 0;
