@@ -685,10 +685,8 @@ int launch_resident_tc(bool sym, const PassArgs &a, cudaStream_t st) {
 }
 
 // tensor-core pass for 7x7 banks with <= 48 filters (k_pass_tc7); FOE_TC7=0 (or FOE_TC=0) forces the FFMA pass
-bool use_tc7(int m, int nf) {
-    const char *e = getenv("FOE_TC7"), *e5 = getenv("FOE_TC");
-    return m == 7 && nf <= 48 && !(e && e[0] == '0') && !(e5 && e5[0] == '0');
-}
+bool tc7_enabled();
+bool use_tc7(int m, int nf) { return m == 7 && nf <= 48 && tc7_enabled(); }
 
 template <bool TRIAL, bool SYM>
 int launch_pass_tc7_t(const PassArgs &a, cudaStream_t st) {
@@ -707,6 +705,8 @@ int launch_pass_tc7_t(const PassArgs &a, cudaStream_t st) {
 
 int launch_pass(int m, bool sym, const PassArgs &a, cudaStream_t st) {
     const bool trial = a.mode == MODE_TRIAL;
+    if (m == 7 && tc7_enabled() && a.n_filters > 48)
+        return fail(FOE_E_UNSUPPORTED, "7x7 banks with more than 48 filters need FOE_TC7=0 (FFMA pass)");
     if (use_tc7(m, a.n_filters))
         return trial ? (sym ? launch_pass_tc7_t<true, true>(a, st) : launch_pass_tc7_t<true, false>(a, st))
                      : (sym ? launch_pass_tc7_t<false, true>(a, st) : launch_pass_tc7_t<false, false>(a, st));
@@ -759,10 +759,20 @@ int launch_resident(int m, bool sym, const PassArgs &a, cudaStream_t st) {
     }
 }
 
+// region rows of the pass kernel that runs filter side m: 7x7 banks take the tensor-core pass's 40-row
+// regions unless it is switched off (FOE_TC7=0 / FOE_TC=0: the FFMA k_pass<7>'s 48)
+bool tc7_enabled() {
+    const char *e = getenv("FOE_TC7"), *e5 = getenv("FOE_TC");
+    return !(e && e[0] == '0') && !(e5 && e5[0] == '0');
+}
+int region_rows(int m) {
+    if (m == 7) return tc7_enabled() ? TcCfg7::RH : PassCfg<7>::RH;
+    return PassCfg<1>::RH;
+}
+
 void tile_counts(int m, int H, int W, int *tx, int *ty) {
     const int r = m / 2;
-    const int RH = m == 7 ? PassCfg<7>::RH : PassCfg<1>::RH;  // region rows by filter size
-    const int TH = RH - 2 * r, TW = PassCfg<1>::RW - 2 * r;     // PassCfg<M>::TH / TW
+    const int TH = region_rows(m) - 2 * r, TW = PassCfg<1>::RW - 2 * r;  // owned tile
     *ty = (H + TH - 1) / TH;
     *tx = (W + TW - 1) / TW;
 }
@@ -1444,7 +1454,8 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     // the resident single-launch solver is opt-in (FOE_RESIDENT=1): measured no faster than the
     // per-pass launches on B200 (grid barrier + redundant decisions cost what the launches did)
     const char *env = getenv("FOE_RESIDENT");
-    const bool try_resident = B <= kResidentMaxB && env && env[0] == '1';
+    // (the FFMA resident solver tiles 7x7 banks with 48-row regions: not with the tensor-core 7x7 geometry)
+    const bool try_resident = B <= kResidentMaxB && env && env[0] == '1' && !(bank->m == 7 && tc7_enabled());
     bool resident = false, graph_loop = false;
     // the tensor-core pass has its own resident solve, opt-in (FOE_RESIDENT_TC=1): measured ~13 % slower
     // per pass than the programmatic-dependent per-pass launches (grid barrier + every CTA deciding)
@@ -1612,7 +1623,7 @@ int foe_band_geometry(int m, int B, int H, int W, int ty0, int ty1, foe_band_des
     int tx, ty;
     tile_counts(m, H, W, &tx, &ty);
     if (ty0 < 0 || ty1 > ty || ty0 >= ty1) return fail(FOE_E_INVALID, "tile rows [%d, %d) outside [0, %d)", ty0, ty1, ty);
-    const int r = m / 2, T = (m == 7 ? PassCfg<7>::RH : PassCfg<1>::RH) - 2 * r;
+    const int r = m / 2, T = region_rows(m) - 2 * r;
     d->B = B; d->H = H; d->W = W; d->ty0 = ty0; d->ty1 = ty1; d->tiles_x = tx; d->tiles_y = ty;
     d->row0 = tile_start(ty0, ty, T, H, r);
     d->row1 = tile_start(ty1, ty, T, H, r);

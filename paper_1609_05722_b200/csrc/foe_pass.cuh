@@ -110,20 +110,25 @@ struct TileGeom {
     bool edge;             // touches the image edge (symmetric rule needs the psi ring zeroed)
 };
 
-template <int M, bool SYM>
-__device__ __forceinline__ TileGeom tile_geom(const PassArgs &a, int tyl, int txi) {
-    using C = PassCfg<M>;
+template <int TH, int TW, int R, bool SYM>
+__device__ __forceinline__ TileGeom tile_geom_t(const PassArgs &a, int tyl, int txi) {
     TileGeom g;
     const int tyi = a.ty0 + tyl;
     g.t = tyi * a.tiles_x + txi;
-    g.s0 = tile_start(tyi, a.tiles_y, C::TH, a.H, C::R);
-    g.s1 = tile_start(tyi + 1, a.tiles_y, C::TH, a.H, C::R);
-    g.c0 = tile_start(txi, a.tiles_x, C::TW, a.W, C::R);
-    g.c1 = tile_start(txi + 1, a.tiles_x, C::TW, a.W, C::R);
-    g.ry0 = g.s0 - C::R;
-    g.rx0 = g.c0 - C::R;
+    g.s0 = tile_start(tyi, a.tiles_y, TH, a.H, R);
+    g.s1 = tile_start(tyi + 1, a.tiles_y, TH, a.H, R);
+    g.c0 = tile_start(txi, a.tiles_x, TW, a.W, R);
+    g.c1 = tile_start(txi + 1, a.tiles_x, TW, a.W, R);
+    g.ry0 = g.s0 - R;
+    g.rx0 = g.c0 - R;
     g.edge = SYM && (g.s0 == 0 || g.c0 == 0 || g.s1 == a.H || g.c1 == a.W);
     return g;
+}
+
+template <int M, bool SYM>
+__device__ __forceinline__ TileGeom tile_geom(const PassArgs &a, int tyl, int txi) {
+    using C = PassCfg<M>;
+    return tile_geom_t<C::TH, C::TW, C::R, SYM>(a, tyl, txi);
 }
 
 template <int M>

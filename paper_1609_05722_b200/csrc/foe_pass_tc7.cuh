@@ -2,8 +2,8 @@
 // to 48 filters (the BASELINE 48 x 7 x 7 fallback bank; the paper's filter-bank size).  Included by
 // foe_b200.cu after foe_pass_tc.cuh; the default for such banks (FOE_TC7=0 forces the FFMA pass).
 //
-// Same tile geometry as k_pass<7> (48 x 64 regions, 42 x 58 owned), prologue, fold and reductions as
-// k_pass_tc; per 128-pixel block (two region rows, 24 blocks per tile):
+// 40 x 64 regions (34 x 58 owned; the FFMA k_pass<7> uses 48 rows), prologue, fold and reductions as
+// k_pass_tc; per 128-pixel block (two region rows, 20 blocks per tile):
 //   forward   Z  = A_u  . Kf^T     K = 48 taps (6 K = 8 steps) + one tap-48 step, N = 48 filters
 //             dZ = A_du . Kf^T
 //   adjoint   Y  = Psi . Kt^T      K = 48 filters, N = 64 (49 taps)
@@ -25,10 +25,12 @@
 // set's, flagged by mbarriers).
 
 struct TcCfg7 {
-    using P = PassCfg<7>;
     static constexpr int R = 3, M = 7, KT = 49, NFX = 48;
-    static constexpr int RH = P::RH, RW = P::RW, SH = P::SH, CW = P::CW, SW = P::SW, PLANE = P::PLANE;
-    static constexpr int NBLK = RH * RW / 128;  // 24
+    // 40 x 64 regions (34 x 58 owned): a 512^2 image is 16 x 9 = 144 tiles, one wave on 148 SMs (the FFMA
+    // pass's 48-row regions give 117); the host tile grid follows the 7x7 kernel in use (region_rows)
+    static constexpr int RH = 40, RW = 64, SH = RH + 2 * R, CW = RW + 2 * R, SW = (CW + 3) & ~3, PLANE = SH * SW;
+    static constexpr int NCELL = SH * CW, TH = RH - 2 * R, TW = RW - 2 * R;
+    static constexpr int NBLK = RH * RW / 128;  // 20
     static constexpr int W_PT = 8, NWARPS = 24, NT = NWARPS * 32;
     // TMEM columns
     static constexpr int C_AUH = 0, C_AUL = 48, C_ADH = 96, C_ADL = 144;  // A stage
@@ -80,7 +82,7 @@ __device__ __forceinline__ void tc7_im2col(const float4 *sp, uint32_t st) {
 template <bool TRIAL, bool SYM>
 __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
     using T = TcCfg7;
-    using C = PassCfg<7>;
+    using C = TcCfg7;
     constexpr int NT = T::NT, R = T::R, SW = T::SW, NBLK = T::NBLK;
     extern __shared__ __align__(128) float sm[];
     __shared__ double red[NT / 32][kNumPartials];
@@ -95,7 +97,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
     const int nf = a.n_filters;
     griddep_launch_dependents();
     const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
-    const TileGeom g = tile_geom<7, SYM>(a, tyl, txi);
+    const TileGeom g = tile_geom_t<T::TH, T::TW, T::R, SYM>(a, tyl, txi);
 
     float4 *S4 = reinterpret_cast<float4 *>(sm);
     float *Kf = sm + 4 * T::PLANE;       // [hi | lo]
