@@ -95,6 +95,12 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b = blockIdx.y;
     const int nf = a.n_filters;
+#if FOE_STAMPS
+    unsigned long long *ph = (a.dbg_times && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0 && lane == 0)
+                                 ? a.dbg_times + 3 * (size_t)gridDim.x * gridDim.y : nullptr;
+#else
+    constexpr unsigned long long *ph = nullptr;
+#endif
     griddep_launch_dependents();
     const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
     const TileGeom g = tile_geom_t<T::TH, T::TW, T::R, SYM>(a, tyl, txi);
@@ -253,6 +259,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
     tc_fence_after();
     constexpr uint32_t tmem = 0u;
     if (tid == 0 && s_tmem != 0u) __trap();
+    if (ph && tid == 0) ph[NBLK * 16] = clock64();  // loop start
 
     if (warp < T::W_PT) {
         // ================= operand warps =================
@@ -269,6 +276,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
             if (warp == 0 && j >= 1) mbar_wait_sleep(&mb_dfull[(j - 1) & 1], ((j - 1) >> 1) & 1);
             named_sync(T::BAR_AFREE, 256);
             tc_fence_after();
+            if (ph && warp == 0) ph[j * 16 + 5] = clock64();
             const int lr = 2 * j + (pl >> 6), lc = pl & 63;
             const float4 *sp = S4 + lr * SW + lc;
             // taps 0..47: warps 0-3 rounds 0..5, warps 4-7 rounds 6..11
@@ -304,6 +312,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                     umma_commit(&mb_dfull[s]);
                 }
                 __syncwarp();
+                if (ph) ph[j * 16 + 0] = clock64();
             }
         }
     } else {
@@ -330,6 +339,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                     named_sync(T::BAR_DFULL + set, 256);
                 }
                 tc_fence_after();
+                if (ph && ws == 0) ph[j * 16 + 1] = clock64();
                 const int lr = 2 * j + (pl >> 6), lc = pl & 63;
                 const int gy = g.ry0 + lr, gx = g.rx0 + lc;
                 const bool in_img = !SYM || (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W);
@@ -444,6 +454,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                         umma_commit(&mb_yfull[set]);
                     }
                     __syncwarp();
+                    if (ph) ph[j * 16 + 2] = clock64();
                 }
                 // Y(j) -> block buffer (frees the D region for block j + 2)
                 if (issuer) {
@@ -467,6 +478,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                     }
                 }
                 named_sync(T::BAR_SET + set, 256);  // the whole block's Y is in the buffer
+                if (ph && ws == 0) ph[j * 16 + 3] = clock64();
                 // H(j): thread (pixel, a-half) -> H_a for a in {0..3} / {4..6}; ring slot j % HSLOTS held
                 // H(j - 8), last read by the vertical sums of blocks j - 10 .. j - 6 (j - 7 the other set's)
                 if (j >= 7) mbar_wait_sleep(&mb_vdone[j - 7], 0);
@@ -491,6 +503,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&mb_hfull[j]);
+                if (ph && ws == 0) ph[j * 16 + 4] = clock64();
             }
             // vertical sums of block q = j - 2 (rows 2q, 2q+1) once H(q-2 .. q+2) are in the ring
             const int q = j - 2;
@@ -519,6 +532,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                 Gr[ah * T::RH * T::RW + r * T::RW + c] = s0 + s1;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&mb_vdone[q]);
+                if (ph && ws == 0) ph[q * 16 + 6] = clock64();
             }
         }
         acc[0] = e_own;
