@@ -34,7 +34,7 @@ struct TcCfg {
     static constexpr int W_PT = 8, NWARPS = 24, NT = NWARPS * 32;
     // named barriers, one per stage / set: A complete, Psi complete, D region free, forward done (relayed
     // to the set), adjoint done (relayed to the set), A stage free (relayed to the im2col warps)
-    static constexpr int BAR_AFULL = 1, BAR_PFULL = 3, BAR_DFULL = 5, BAR_AFREE = 9, BAR_DFREE = 11;
+    static constexpr int BAR_AFULL = 1, BAR_PFULL = 3, BAR_DFULL = 5, BAR_AFREE = 9, BAR_DFREE = 11, BAR_EPI = 14;
     static constexpr int RING = 4;                       // Y ring: 4 blocks = 8 region rows
     static constexpr int YROWS = 2 * RING, YW = RW + 4;  // 2 zero columns each side
     static constexpr int BSZ = 32 * 32;                  // one 32 x 32 B operand (floats)
@@ -209,7 +209,8 @@ __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uin
 // and decides).  Returns -1, before touching shared state, if the image is done; else thread 0's ticket.
 template <int NF, bool TRIAL, bool SYM>
 __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const TileGeom &g, const ImgCtl *ctl,
-                                       unsigned rpar, int pbuf, bool take_ticket, unsigned long long *ph) {
+                                       unsigned rpar, int pbuf, bool take_ticket, int fold_t0,
+                                       unsigned long long *ph) {
     using T = TcCfg<32>;
     using C = PassCfg<5>;
     constexpr int NT = T::NT, R = T::R, SW = T::SW, NBLK = T::NBLK;
@@ -608,8 +609,10 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         }
     }
 
-    // ---- fold padded pixels (symmetric rule) and write the owned gradient ----
-    for (int k = tid; k < T::RW * 8; k += NT) {
+    // ---- fold padded pixels (symmetric rule) and write the owned gradient: threads [fold_t0, NT) (the
+    // rest return to run the image's reduction and decision meanwhile if this CTA is the last) ----
+    if (tid < fold_t0) return ticket;
+    for (int k = tid - fold_t0; k < T::RW * 8; k += NT - fold_t0) {
         const int xx = k % T::RW, rows0 = k / T::RW;
         const int gx = g.c0 + xx;
         if (gx >= g.c1) continue;
@@ -631,13 +634,13 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 if (mx >= 0) val += gr(ly, mx);
                 if (my >= 0 && mx >= 0) val += gr(my, mx);
             }
-            if (ph && tid == 0 && gy == g.s0) ph[NBLK * 16 + 8] = clock64();  // first value folded
+            if (ph && tid == fold_t0 && gy == g.s0) ph[NBLK * 16 + 8] = clock64();  // first value folded
             gout[(size_t)(gy - a.lrow0) * a.W + gx] = val;
-            if (ph && tid == 0 && gy == g.s0) ph[NBLK * 16 + 9] = clock64();  // first store issued
+            if (ph && tid == fold_t0 && gy == g.s0) ph[NBLK * 16 + 9] = clock64();  // first store issued
         }
     }
 
-    if (ph && tid == 0) ph[NBLK * 16 + 4] = clock64();  // fold done
+    if (ph && tid == fold_t0) ph[NBLK * 16 + 4] = clock64();  // fold done
     return ticket;
 }
 
@@ -679,28 +682,52 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     if (ph && tid == 0) ph[NBLK * 16 + 3] = clock64();  // dependency resolved
     if (tid == 0 && s_tmem != 0u) __trap();
     constexpr uint32_t tmem = 0u;
-    const int ticket = tc_body<NF, TRIAL, SYM>(a, S, g, a.mode == MODE_EVAL ? nullptr : a.ctl + b, 0u, 0, !a.band, ph);
+    const int nlaunch = a.tiles_x * a.tiles_y;
+    // warps 0-7 skip the fold when the image's reduction fits the one-warp-per-partial path: the last CTA
+    // reduces and decides while warps 8-23 fold (RW * 8 = 512 items, one each)
+    const bool split = !a.band && nlaunch <= kFastReduceTiles && T::RW * 8 <= NT - 256;
+    const int ticket = tc_body<NF, TRIAL, SYM>(a, S, g, a.mode == MODE_EVAL ? nullptr : a.ctl + b, 0u, 0, !a.band,
+                                               split ? 256 : 0, ph);
     if (ticket < 0) {
         __syncthreads();  // image converged: release TMEM and leave
         if (warp == 0) tmem_dealloc(tmem, 512);
         return;
     }
-    const int nlaunch = a.tiles_x * a.tiles_y;
     // TMEM is released at the very end (tcgen05.dealloc right after the loop stalled warp 0, and with it
     // the whole epilogue, for ~6,500 cycles)
     if (a.band) {
         if (warp == 0) tmem_dealloc(tmem, 512);
         return;
     }
-    if (tid == 0) s_last = ticket == nlaunch - 1;
-    __syncthreads();
-    if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
-    if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket seen
-    if (warp == 0) tmem_dealloc(tmem, 512);
-    if (ph && tid == 0) ph[NBLK * 16 + 7] = clock64();  // TMEM released
-    if (!s_last) return;
-    __threadfence();
-    reduce_tiles<NT>(a.partials, a.tiles_x * a.tiles_y, a.B, b, red, s_sum);
+    if (split) {
+        if (warp >= 8) return;  // folded
+        if (tid == 0) s_last = ticket == nlaunch - 1;
+        named_sync(T::BAR_EPI, 256);
+        if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
+        if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket seen
+        if (warp == 0) tmem_dealloc(tmem, 512);
+        if (!s_last) return;
+        __threadfence();
+        if (warp < kNumPartials) {  // the fixed order of reduce_tiles' fast path
+            double x = 0.0;
+#pragma unroll 8
+            for (int tt = lane; tt < nlaunch; tt += 32)
+                x += __ldcg(a.partials + ((size_t)tt * a.B + b) * kPartialStride + warp);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+            if (lane == 0) s_sum[warp] = x;
+        }
+        named_sync(T::BAR_EPI, 256);
+    } else {
+        if (tid == 0) s_last = ticket == nlaunch - 1;
+        __syncthreads();
+        if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
+        if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket seen
+        if (warp == 0) tmem_dealloc(tmem, 512);
+        if (!s_last) return;
+        __threadfence();
+        reduce_tiles<NT>(a.partials, nlaunch, a.B, b, red, s_sum);
+    }
     if (tid == 0) {
         a.tickets[b] = 0u;
         if (a.mode == MODE_EVAL) {
@@ -766,9 +793,9 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_solve_resident_tc(const Pa
         const int pbuf = pass & 1;
         if (!s_ctl[b].done) {
             if (init)
-                tc_body<NF, false, SYM>(a, S, g, &s_ctl[b], (unsigned)pbuf, pbuf, false, nullptr);
+                tc_body<NF, false, SYM>(a, S, g, &s_ctl[b], (unsigned)pbuf, pbuf, false, 0, nullptr);
             else
-                tc_body<NF, true, SYM>(a, S, g, &s_ctl[b], (unsigned)pbuf, pbuf, false, nullptr);
+                tc_body<NF, true, SYM>(a, S, g, &s_ctl[b], (unsigned)pbuf, pbuf, false, 0, nullptr);
         }
         grid_barrier(a.grid_bar, nblocks, gen);
         if (resident_decide(a, a.partials + (size_t)pbuf * ntiles * B * kPartialStride, ntiles, red, s_sum, s_ctl,
