@@ -248,6 +248,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
 #pragma unroll
         for (int sl = 0; sl < 3; ++sl) canc[sl] = a.zero_mean ? __ldg(a.U + sl * a.plane + oa) : 0.0f;
     }
+    if (ph && tid == 0) ph[NBLK * 16 + 10] = clock64();  // candidate loads issued
     TrialParams p{};
     if (a.mode != MODE_EVAL) {
         const ImgCtl c = *ctl;
@@ -271,6 +272,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             gout = a.Gs + p.ig * a.plane + ioff;
         }
     }
+    if (ph && tid == 0) ph[NBLK * 16 + 11] = clock64();  // control block read
     const float shift = TRIAL ? (p.iu == 0 ? canc[0] : p.iu == 1 ? canc[1] : canc[2])
                               : a.zero_mean ? __ldg(uin + (size_t)(g.s0 - a.lrow0) * a.W + g.c0) : 0.0f;
     double acc[kNumPartials];
@@ -329,10 +331,12 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             }
         }
     }
+    if (ph && tid == 0) ph[NBLK * 16 + 12] = clock64();  // cells staged
     // the prologue's partials 1..6 are summed per warp now (the block loop only adds partial 0)
     // scratch: the Y ring's data columns 2 .. 65 (its zero columns stay intact), one 32-double row per ring row
     static_assert(T::YW % 2 == 0 && (NT / 32) * (kNumPartials - 1) <= T::KT * T::YROWS, "partial scratch");
     warp_partials_smem<1, kNumPartials, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));
+    if (ph && tid == 0) ph[NBLK * 16 + 13] = clock64();  // warp partials
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -484,24 +488,31 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             float tmax = 0.0f;
             // psi' (zero on padded cells outside the image: a warp-uniform test, edge tiles only)
             auto point = [&](auto keep_all) {
+                if (TRIAL) {  // filter pairs in packed fp32 (FFMA2 / FMUL2 / FADD2: one issue slot per pair)
+#pragma unroll
+                    for (int i = 0; i < FH; i += 2) {
+                        const float2 zz = make_float2(z[i], z[i + 1]), d = make_float2(dz[i], dz[i + 1]);
+                        const float2 zo = __fadd2_rn(zz, make_float2(-d.x, -d.y));
+                        // psi' = z / (1+z^2) and t = (z^2 - zo^2) / (2+z^2+zo^2): two MUFU reciprocals (the
+                        // XU pipe has room; fewer issue slots than one reciprocal of the product)
+                        const float2 a1 = __ffma2_rn(zz, zz, make_float2(1.0f, 1.0f));
+                        const float2 b1 = __fadd2_rn(__ffma2_rn(zo, zo, a1), make_float2(1.0f, 1.0f));
+                        const float2 ps = __fmul2_rn(zz, make_float2(rcp_approx(a1.x), rcp_approx(a1.y)));
+                        const float2 tt = __fmul2_rn(__fmul2_rn(d, __fadd2_rn(zz, zo)),
+                                                     make_float2(rcp_approx(b1.x), rcp_approx(b1.y)));
+                        dz[i] = tt.x;
+                        dz[i + 1] = tt.y;
+                        tmax = fmaxf(tmax, fmaxf(fabsf(tt.x), fabsf(tt.y)));
+                        z[i] = (decltype(keep_all)::value || in_img) ? ps.x : 0.0f;
+                        z[i + 1] = (decltype(keep_all)::value || in_img) ? ps.y : 0.0f;
+                    }
+                    return;
+                }
 #pragma unroll
                 for (int i = 0; i < FH; ++i) {
                     const float zz = z[i];
-                    float ps;
-                    if (TRIAL) {
-                        const float d = dz[i];
-                        const float zo = zz - d;
-                        // psi' = z / (1+z^2) and t = (z^2 - zo^2) / (2+z^2+zo^2): two MUFU reciprocals (the
-                        // XU pipe has room; fewer issue slots than one reciprocal of the product)
-                        const float a1 = fmaf(zz, zz, 1.0f);
-                        const float b1 = fmaf(zo, zo, a1) + 1.0f;
-                        ps = zz * rcp_approx(a1);
-                        dz[i] = (d * (zz + zo)) * rcp_approx(b1);
-                        tmax = fmaxf(tmax, fabsf(dz[i]));
-                    } else {
-                        ps = zz * rcp_approx(fmaf(zz, zz, 1.0f));
-                        dz[i] = zz;  // keep z for log1p(z^2)
-                    }
+                    const float ps = zz * rcp_approx(fmaf(zz, zz, 1.0f));
+                    dz[i] = zz;  // keep z for log1p(z^2)
                     z[i] = (decltype(keep_all)::value || in_img) ? ps : 0.0f;
                 }
             };
@@ -540,29 +551,33 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 // 2 a atanh(t) = 2 a (t + t^3/3 + ...): the series is cut where the next term is below fp32
                 // rounding for the warp's largest |t| (degree 9 up to 0.2, then 5, 3, 1); MUFU log beyond
                 const float wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));  // tmax >= 0
-                auto series = [&](auto deg) {
+                auto series = [&](auto deg) {  // filter pairs packed: (e0, e1) = (even, odd) filters
                     constexpr int D = decltype(deg)::value;
+                    float2 e = make_float2(e0, e1);
 #pragma unroll
-                    for (int i = 0; i < FH; ++i) {
-                        const float t1 = dz[i], w = s_al2[f0 + i] * t1;  // 2 alpha t
+                    for (int i = 0; i < FH; i += 2) {
+                        const float2 t1 = make_float2(dz[i], dz[i + 1]);
+                        const float2 w = __fmul2_rn(*reinterpret_cast<const float2 *>(s_al2 + f0 + i), t1);  // 2 alpha t
                         if (D == 1) {
-                            if (i & 1) e1 += w; else e0 += w;
+                            e = __fadd2_rn(e, w);
                             continue;
                         }
-                        const float sq = t1 * t1;
-                        float pp;
+                        const float2 sq = __fmul2_rn(t1, t1);
+                        float2 pp;
                         if (D == 9) {
-                            pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
-                            pp = fmaf(sq, pp, 1.0f / 5.0f);
-                            pp = fmaf(sq, pp, 1.0f / 3.0f);
+                            pp = __ffma2_rn(sq, make_float2(1.0f / 9.0f, 1.0f / 9.0f), make_float2(1.0f / 7.0f, 1.0f / 7.0f));
+                            pp = __ffma2_rn(sq, pp, make_float2(1.0f / 5.0f, 1.0f / 5.0f));
+                            pp = __ffma2_rn(sq, pp, make_float2(1.0f / 3.0f, 1.0f / 3.0f));
                         } else if (D == 5) {
-                            pp = fmaf(sq, 1.0f / 5.0f, 1.0f / 3.0f);
+                            pp = __ffma2_rn(sq, make_float2(1.0f / 5.0f, 1.0f / 5.0f), make_float2(1.0f / 3.0f, 1.0f / 3.0f));
                         } else {
-                            pp = 1.0f / 3.0f;
+                            pp = make_float2(1.0f / 3.0f, 1.0f / 3.0f);
                         }
-                        pp = fmaf(sq, pp, 1.0f);
-                        if (i & 1) e1 = fmaf(w, pp, e1); else e0 = fmaf(w, pp, e0);
+                        pp = __ffma2_rn(sq, pp, make_float2(1.0f, 1.0f));
+                        e = __ffma2_rn(w, pp, e);
                     }
+                    e0 = e.x;
+                    e1 = e.y;
                 };
                 if (wmax > 0.2f) {
 #pragma unroll
