@@ -63,6 +63,10 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            # first queries outside the timed region: NVML initialises its per-device clock state lazily
+            # (tens of ms, holding driver locks that stall the timed step's launches and copies)
+            pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
         except Exception:
             self.nv = None
 
@@ -257,8 +261,11 @@ def run_scaling_config(args, rank, local_rank, world):
         workload = f"cfg5: 8192x8192, peak 2, quadratic, foe_a, 150 iters, {world} row band(s), 4-row halo " \
                    f"+ per-pass partials all-gather"
         dtag = "bands"
+    out = None
     for _ in range(args.warmup):
-        step()
+        # the previous step's outputs stay alive while the next one runs, as in the timed loop, so the
+        # caching allocator has grown to its steady state before timing starts
+        out = step()  # noqa: F841
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -349,8 +356,11 @@ def main():
     # the FFMA peak probe (~0.1 s of full-chip work) also brings an idle GPU up to its boost clock
     # before the warm-up steps
     fp32_peak_tflops, ffma_clk = measure_ffma_peak(L, dev, local_rank)
+    out = None
     for _ in range(args.warmup):
-        step()
+        # the previous step's outputs stay alive while the next one runs, as in the timed loop, so the
+        # caching allocator has grown to its steady state before timing starts
+        out = step()  # noqa: F841
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

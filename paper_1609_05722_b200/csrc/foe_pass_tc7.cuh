@@ -357,22 +357,30 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                     }
                     tc_wait_ld();
                     float tmax = 0.0f;
+                    if (TRIAL) {  // filter pairs in packed fp32 (FFMA2 / FMUL2 / FADD2), as k_pass_tc
 #pragma unroll
-                    for (int i = 0; i < 12; ++i) {
-                        const float zz = z[i];
-                        float ps;
-                        if (TRIAL) {
-                            const float d = dz[i], zo = zz - d;
-                            const float a1 = fmaf(zz, zz, 1.0f);
-                            const float b1 = fmaf(zo, zo, a1) + 1.0f;
-                            ps = zz * rcp_approx(a1);
-                            dz[i] = (d * (zz + zo)) * rcp_approx(b1);
-                            tmax = fmaxf(tmax, fabsf(dz[i]));
-                        } else {
-                            ps = zz * rcp_approx(fmaf(zz, zz, 1.0f));
-                            dz[i] = zz;
+                        for (int i = 0; i < 12; i += 2) {
+                            const float2 zz = make_float2(z[i], z[i + 1]), d = make_float2(dz[i], dz[i + 1]);
+                            const float2 zo = __fadd2_rn(zz, make_float2(-d.x, -d.y));
+                            const float2 a1 = __ffma2_rn(zz, zz, make_float2(1.0f, 1.0f));
+                            const float2 b1 = __fadd2_rn(__ffma2_rn(zo, zo, a1), make_float2(1.0f, 1.0f));
+                            const float2 ps = __fmul2_rn(zz, make_float2(rcp_approx(a1.x), rcp_approx(a1.y)));
+                            const float2 tt = __fmul2_rn(__fmul2_rn(d, __fadd2_rn(zz, zo)),
+                                                         make_float2(rcp_approx(b1.x), rcp_approx(b1.y)));
+                            dz[i] = tt.x;
+                            dz[i + 1] = tt.y;
+                            tmax = fmaxf(tmax, fmaxf(fabsf(tt.x), fabsf(tt.y)));
+                            z[i] = (keep_all || in_img) ? ps.x : 0.0f;
+                            z[i + 1] = (keep_all || in_img) ? ps.y : 0.0f;
                         }
-                        z[i] = (keep_all || in_img) ? ps : 0.0f;
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 12; ++i) {
+                            const float zz = z[i];
+                            const float ps = zz * rcp_approx(fmaf(zz, zz, 1.0f));
+                            dz[i] = zz;
+                            z[i] = (keep_all || in_img) ? ps : 0.0f;
+                        }
                     }
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
@@ -388,32 +396,36 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                     if (TRIAL) {
                         const float wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));
                         // series cut per warp as in k_pass_tc (first omitted term below 2^-25 relative)
-                        auto series = [&](auto deg) {
+                        auto series = [&](auto deg) {  // filter pairs packed: (e0, e1) = (even, odd)
                             constexpr int D = decltype(deg)::value;
+                            float2 e = make_float2(e0, e1);
 #pragma unroll
-                            for (int i = 0; i < 12; ++i) {
-                                const float t1 = dz[i], w = s_al2[f0 + i] * t1;
+                            for (int i = 0; i < 12; i += 2) {
+                                const float2 t1 = make_float2(dz[i], dz[i + 1]);
+                                const float2 w = __fmul2_rn(*reinterpret_cast<const float2 *>(s_al2 + f0 + i), t1);
                                 if (D == 1) {
-                                    if (i & 1) e1 += w; else e0 += w;
+                                    e = __fadd2_rn(e, w);
                                     continue;
                                 }
-                                const float sq = t1 * t1;
-                                float pp;
+                                const float2 sq = __fmul2_rn(t1, t1);
+                                float2 pp;
                                 if (D == 9) {
-                                    pp = fmaf(sq, 1.0f / 9.0f, 1.0f / 7.0f);
-                                    pp = fmaf(sq, pp, 1.0f / 5.0f);
-                                    pp = fmaf(sq, pp, 1.0f / 3.0f);
+                                    pp = __ffma2_rn(sq, make_float2(1.0f / 9.0f, 1.0f / 9.0f), make_float2(1.0f / 7.0f, 1.0f / 7.0f));
+                                    pp = __ffma2_rn(sq, pp, make_float2(1.0f / 5.0f, 1.0f / 5.0f));
+                                    pp = __ffma2_rn(sq, pp, make_float2(1.0f / 3.0f, 1.0f / 3.0f));
                                 } else if (D == 7) {
-                                    pp = fmaf(sq, 1.0f / 7.0f, 1.0f / 5.0f);
-                                    pp = fmaf(sq, pp, 1.0f / 3.0f);
+                                    pp = __ffma2_rn(sq, make_float2(1.0f / 7.0f, 1.0f / 7.0f), make_float2(1.0f / 5.0f, 1.0f / 5.0f));
+                                    pp = __ffma2_rn(sq, pp, make_float2(1.0f / 3.0f, 1.0f / 3.0f));
                                 } else if (D == 5) {
-                                    pp = fmaf(sq, 1.0f / 5.0f, 1.0f / 3.0f);
+                                    pp = __ffma2_rn(sq, make_float2(1.0f / 5.0f, 1.0f / 5.0f), make_float2(1.0f / 3.0f, 1.0f / 3.0f));
                                 } else {
-                                    pp = 1.0f / 3.0f;
+                                    pp = make_float2(1.0f / 3.0f, 1.0f / 3.0f);
                                 }
-                                pp = fmaf(sq, pp, 1.0f);
-                                if (i & 1) e1 = fmaf(w, pp, e1); else e0 = fmaf(w, pp, e0);
+                                pp = __ffma2_rn(sq, pp, make_float2(1.0f, 1.0f));
+                                e = __ffma2_rn(w, pp, e);
                             }
+                            e0 = e.x;
+                            e1 = e.y;
                         };
                         if (wmax > 0.2f) {
 #pragma unroll
