@@ -68,6 +68,9 @@ typedef struct foe_image_status {
 int foe_abi_version(void);
 const char *foe_last_error(void);
 int foe_device_sm_count(int device);
+/* DenoiseRequest's count validation (pipeline.py:50-56) on a host float64 array: 0 if every value
+ * is >= 0 and integral, 1 otherwise (negative, NaN or fractional); host only, no device work. */
+int foe_counts_check(const double *x, size_t n);
 /* number of CUDA kernels this library has launched in the process (launch accounting for bench.py) */
 long long foe_kernel_launch_count(void);
 

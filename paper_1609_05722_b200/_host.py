@@ -39,8 +39,15 @@ def upload(arr: np.ndarray):
     return out
 
 
+_DIRECT_MAX = 64 << 20  # results up to this size are returned in the page-locked memory they land in
+
+
 def download(*tensors):
-    """CUDA tensors -> numpy arrays (copies), all transfers issued before one stream synchronise."""
+    """CUDA tensors -> numpy arrays (fresh, caller-owned), all transfers issued before one stream synchronise.
+
+    Results up to 64 MiB are copied straight into page-locked blocks from torch's caching host allocator
+    and returned as views that own them (no host-side copy; a block returns to the cache when its array
+    is freed); larger ones go through the cached staging buffers and a host copy."""
     import torch
     outs = []
     with _lock:
@@ -48,11 +55,15 @@ def download(*tensors):
         for i, t in enumerate(tensors):
             t = t.contiguous()
             nbytes = t.numel() * t.element_size()
-            buf, _ = _pinned(("down", i), nbytes)
-            host = buf[:nbytes].view(t.dtype).view(t.shape)
+            if nbytes <= _DIRECT_MAX:
+                host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                views.append((host, False))
+            else:
+                buf, _ = _pinned(("down", i), nbytes)
+                host = buf[:nbytes].view(t.dtype).view(t.shape)
+                views.append((host, True))
             host.copy_(t, non_blocking=True)
-            views.append(host)
         torch.cuda.current_stream().synchronize()
-        for h in views:
-            outs.append(h.numpy().copy())
+        for h, staged in views:
+            outs.append(h.numpy().copy() if staged else h.numpy())
     return outs

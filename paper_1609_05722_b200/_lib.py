@@ -87,6 +87,7 @@ def lib():
     L.foe_last_error.restype = ctypes.c_char_p
     L.foe_abi_version.restype = ctypes.c_int
     L.foe_device_sm_count.argtypes = [ctypes.c_int]
+    L.foe_counts_check.argtypes = [_vp, ctypes.c_size_t]
     L.foe_kernel_launch_count.restype = ctypes.c_longlong
     L.foe_bank_create.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]
     L.foe_bank_destroy.argtypes = [_vp]
@@ -138,7 +139,7 @@ def check(rc: int, what: str = "") -> int:
 
 
 EXPORTED_SYMBOLS = [
-    "foe_abi_version", "foe_last_error", "foe_device_sm_count", "foe_kernel_launch_count", "foe_bank_create", "foe_bank_destroy",
+    "foe_abi_version", "foe_last_error", "foe_device_sm_count", "foe_counts_check", "foe_kernel_launch_count", "foe_bank_create", "foe_bank_destroy",
     "foe_bank_info", "foe_anscombe_forward", "foe_direct_obs", "foe_anscombe_inverse_exact_unbiased",
     "foe_prox_quadratic", "foe_prox_idiv", "foe_bin", "foe_unbin_bilinear", "foe_convolve_same", "foe_convolve_adjoint",
     "foe_eval_workspace_size", "foe_energy_grad", "foe_solve_workspace_size", "foe_solve",

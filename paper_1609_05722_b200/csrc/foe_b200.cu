@@ -1181,6 +1181,25 @@ int foe_abi_version(void) { return 1; }
 long long foe_kernel_launch_count(void) { return g_launches.load(); }
 const char *foe_last_error(void) { return g_err.c_str(); }
 
+// DenoiseRequest's count check (pipeline.py:50-56): every value >= 0 (NaN fails) and integral.  One
+// branch-free pass the compiler vectorises: below 2^52, (v + 2^52) - 2^52 is v rounded to an integer
+// (round-to-nearest-even, as np.rint); from 2^52 up every double is an integer (and +inf = rint(+inf)).
+int foe_counts_check(const double *x, size_t n) {
+    if (!x && n) return fail(FOE_E_INVALID, "null argument");
+    constexpr double k52 = 4503599627370496.0;
+    for (size_t i0 = 0; i0 < n; i0 += 8192) {
+        const size_t i1 = std::min(n, i0 + 8192);
+        int bad = 0;
+        for (size_t i = i0; i < i1; ++i) {
+            const double v = x[i];
+            const double r = (v + k52) - k52;
+            bad |= !(v >= 0.0) | ((v < k52) & (r != v));
+        }
+        if (bad) return 1;
+    }
+    return 0;
+}
+
 int foe_device_sm_count(int device) {
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;

@@ -112,6 +112,27 @@ def test_request_validation():
         fp.SolverConfig(backtrack_factor=1.0)
 
 
+def test_counts_check_matches_reference_rule():
+    """foe_counts_check == the reference's `np.any(x < 0) or not np.array_equal(x, np.rint(x))`
+    (pipeline.py:54), element by element over the edge values, and at every position of a long array."""
+    L = _lib.lib()
+    edge = [0.0, -0.0, 1.0, 7.0, 0.5, 2.5, -1.0, 1e-300, 2.0 ** 52 - 0.5, 2.0 ** 52, 2.0 ** 52 + 2, 2.0 ** 53 + 2,
+            1e300, np.inf, -np.inf, np.nan, 3.0000000000000004, 12345678.0]
+    for v in edge:
+        x = np.array([v])
+        ref = bool(np.any(x < 0) or not np.array_equal(x, np.rint(x)))
+        assert bool(L.foe_counts_check(x.ctypes.data, 1)) == ref, v
+    rng = np.random.default_rng(3)
+    base = rng.poisson(3.0, size=20000).astype(np.float64)
+    assert L.foe_counts_check(base.ctypes.data, base.size) == 0
+    for pos in (0, 8191, 8192, 19999):
+        for bad in (-1.0, 0.25, np.nan):
+            y = base.copy()
+            y[pos] = bad
+            assert L.foe_counts_check(y.ctypes.data, y.size) == 1, (pos, bad)
+    assert L.foe_counts_check(None, 0) == 0
+
+
 def test_synthetic_generator_is_deterministic():
     from paper_1609_05722_b200.synth import make_counts, synthetic_clean
     a = synthetic_clean(64, 48, 3)
