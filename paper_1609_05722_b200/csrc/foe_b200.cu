@@ -231,7 +231,13 @@ __device__ void decide_ctl(const PassArgs &a, int b, const double *s, ImgCtl &c,
     }
 }
 
-__device__ void decide(const PassArgs &a, int b, const double *s) { decide_ctl(a, b, s, a.ctl[b], true, a.mode); }
+// on a register copy: one batch of loads, the logic, one batch of stores (operating on the global block in
+// place serialised L2 round trips behind the trace-row stores, which may alias it)
+__device__ void decide(const PassArgs &a, int b, const double *s) {
+    ImgCtl c = a.ctl[b];
+    decide_ctl(a, b, s, c, true, a.mode);
+    a.ctl[b] = c;
+}
 
 // fixed-order block reduction of kNumPartials doubles (deterministic), in two halves that a kernel may
 // run at different times: per-warp shuffle sums of partials [K0, K1) into red[warp][k], then one warp's
