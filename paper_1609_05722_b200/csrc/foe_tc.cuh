@@ -125,8 +125,13 @@ __device__ __forceinline__ bool mbar_test(unsigned long long *bar, unsigned pari
         : "memory");
     return ok != 0u;
 }
+#ifndef FOE_SLEEP_NS
+#define FOE_SLEEP_NS 32  // measured: 0 -> +2 %, 16-32 best, 64 +0.5 %, 128 +1 % solve time
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(unsigned long long *bar, unsigned parity) {
-    while (!mbar_test(bar, parity)) __nanosleep(64);
+    while (!mbar_test(bar, parity)) {
+        if (FOE_SLEEP_NS > 0) __nanosleep(FOE_SLEEP_NS);
+    }
 }
 
 // hardware named barriers: producers arrive without blocking, the consumer warp blocks in sync
