@@ -210,7 +210,7 @@ __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uin
 template <int NF, bool TRIAL, bool SYM>
 __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const TileGeom &g, const ImgCtl *ctl,
                                        unsigned rpar, int pbuf, bool take_ticket, int fold_t0,
-                                       unsigned long long *ph) {
+                                       unsigned long long *ph, ImgCtl *ctl_keep = nullptr) {
     using T = TcCfg<32>;
     using C = PassCfg<5>;
     constexpr int NT = T::NT, R = T::R, SW = T::SW, NBLK = T::NBLK;
@@ -254,6 +254,9 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         const ImgCtl c = *ctl;
         if (c.done && !a.no_decide) return -1;  // image converged
         p = trial_params(a, c);
+        // ctl_keep: the whole block parked in shared memory for this pass's decision (the deciding CTA then
+        // needs no L2 round trip for it on the pass-to-pass critical path; only that CTA writes it)
+        if (ctl_keep && tid == 0) *ctl_keep = c;
     }
     const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
     float *gout, *uout = nullptr;
@@ -701,8 +704,9 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     // warps 0-7 skip the fold when the image's reduction fits the one-warp-per-partial path: the last CTA
     // reduces and decides while warps 8-23 fold (RW * 8 = 512 items, one each)
     const bool split = !a.band && nlaunch <= kFastReduceTiles && T::RW * 8 <= NT - 256;
+    __shared__ ImgCtl s_ctl;
     const int ticket = tc_body<NF, TRIAL, SYM>(a, S, g, a.mode == MODE_EVAL ? nullptr : a.ctl + b, 0u, 0, !a.band,
-                                               split ? 256 : 0, ph);
+                                               split ? 256 : 0, ph, &s_ctl);
     if (ticket < 0) {
         __syncthreads();  // image converged: release TMEM and leave
         if (warp == 0) tmem_dealloc(tmem, 512);
@@ -748,7 +752,9 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         if (a.mode == MODE_EVAL) {
             a.energy_out[b] = s_sum[0];
         } else if (!a.no_decide) {
-            decide(a, b, s_sum);
+            ImgCtl c = s_ctl;  // = a.ctl[b]: read at this pass's start, written only by this decision
+            decide_ctl(a, b, s_sum, c, true, a.mode);
+            a.ctl[b] = c;
         }
     }
 }
