@@ -621,9 +621,10 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         double *parts = a.partials + (((size_t)pbuf * a.tiles_x * a.tiles_y + g.t) * a.B + b) * kPartialStride;
 #pragma unroll
         for (int k = 0; k < kNumPartials; ++k) parts[k] = s_sum[k];
-        if (take_ticket) {
-            __threadfence();
-            ticket = (int)atomicAdd(a.tickets + b, 1u);
+        if (take_ticket) {  // release: this thread's partial stores; acquire: every earlier CTA's
+            unsigned t;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(a.tickets + b) : "memory");
+            ticket = (int)t;
         }
     }
 
@@ -726,7 +727,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket seen
         if (warp == 0) tmem_dealloc(tmem, 512);
         if (!s_last) return;
-        __threadfence();
+        // (no fence: thread 0's acquiring ticket and the barrier above order the loads below)
         if (warp < kNumPartials) {  // the fixed order of reduce_tiles' fast path
             double x = 0.0;
 #pragma unroll 8
@@ -744,7 +745,6 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket seen
         if (warp == 0) tmem_dealloc(tmem, 512);
         if (!s_last) return;
-        __threadfence();
         reduce_tiles<NT>(a.partials, nlaunch, a.B, b, red, s_sum);
     }
     if (tid == 0) {
