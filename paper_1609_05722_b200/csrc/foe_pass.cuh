@@ -64,6 +64,14 @@ __device__ __forceinline__ float rcp_approx(float x) {  // MUFU.RCP, no denormal
 
 // programmatic dependent launch (the launch carries cudaLaunchAttributeProgrammaticStreamSerialization)
 __device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// the image's ticket: release orders this thread's partial stores before it, acquire makes every earlier
+// ticket holder's partials visible to the CTA that draws the last one (after a CTA barrier) -- one
+// MEMBAR.ALL.GPU + CCTL instead of a seq-cst fence on each side
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned *t) {
+    unsigned v;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(t) : "memory");
+    return v;
+}
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {

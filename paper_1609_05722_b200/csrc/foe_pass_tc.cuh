@@ -622,9 +622,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
 #pragma unroll
         for (int k = 0; k < kNumPartials; ++k) parts[k] = s_sum[k];
         if (take_ticket) {  // release: this thread's partial stores; acquire: every earlier CTA's
-            unsigned t;
-            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(a.tickets + b) : "memory");
-            ticket = (int)t;
+            ticket = (int)ticket_acq_rel(a.tickets + b);
         }
     }
 

@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
     __shared__ double s_sum[kNumPartials];
     __shared__ int s_last;
     __shared__ uint32_t s_tmem;
+    __shared__ ImgCtl s_ctl;  // the control block as read at the pass's start (the decision's input)
     __shared__ __align__(8) unsigned long long mb_dfull[2], mb_yfull[2];
     __shared__ __align__(8) unsigned long long mb_hfull[NBLK], mb_vdone[NBLK];
 
@@ -168,13 +169,14 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
     const size_t ioff = (size_t)b * a.Hl * a.W;
     TrialParams p{};
     if (a.mode != MODE_EVAL) {
-        const ImgCtl &c = a.ctl[b];
+        const ImgCtl c = a.ctl[b];
         if (c.done && !a.no_decide) {
             __syncthreads();
             if (warp == 0) tmem_dealloc(s_tmem, 512);
             return;
         }
         p = trial_params(a, c);
+        if (tid == 0) s_ctl = c;
     }
     const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
     float *gout, *uout = nullptr;
@@ -559,10 +561,7 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
         double *pp = a.partials + ((size_t)g.t * a.B + b) * kPartialStride;
 #pragma unroll
         for (int k = 0; k < kNumPartials; ++k) pp[k] = s_sum[k];
-        if (!a.band) {
-            __threadfence();
-            ticket = (int)atomicAdd(a.tickets + b, 1u);
-        }
+        if (!a.band) ticket = (int)ticket_acq_rel(a.tickets + b);
     }
     // ---- fold padded pixels (symmetric rule) and write the owned gradient ----
     for (int k = tid; k < T::RW * 8; k += NT) {
@@ -599,14 +598,16 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, 512);
     if (!s_last) return;
-    __threadfence();
+    // (no fence: thread 0's acquiring ticket and the barrier above order the loads below)
     reduce_tiles<NT>(a.partials, a.tiles_x * a.tiles_y, a.B, b, red, s_sum);
     if (tid == 0) {
         a.tickets[b] = 0u;
         if (a.mode == MODE_EVAL) {
             a.energy_out[b] = s_sum[0];
         } else if (!a.no_decide) {
-            decide(a, b, s_sum);
+            ImgCtl c = s_ctl;  // = a.ctl[b]: read at this pass's start, written only by this decision
+            decide_ctl(a, b, s_sum, c, true, a.mode);
+            a.ctl[b] = c;
         }
     }
 }
