@@ -542,6 +542,7 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     __shared__ double red[NT / 32][kNumPartials];
     __shared__ double s_sum[kNumPartials];
     __shared__ int s_last;
+    __shared__ ImgCtl s_ctl;  // the control block as read at the pass's start (the decision's input)
     __shared__ unsigned long long s_mbar[C::G][C::NBUF];
 
     const int tid = threadIdx.x;
@@ -560,9 +561,10 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     griddep_wait();  // the previous pass (control block, iterates, gradients, partials) is complete
     TrialParams p{};
     if (a.mode != MODE_EVAL) {
-        const ImgCtl &c = a.ctl[b];
+        const ImgCtl c = a.ctl[b];
         if (c.done && !a.no_decide) return;
         p = trial_params(a, c);
+        if (tid == 0) s_ctl = c;
     }
     // local buffers hold global rows [lrow0, lrow0 + Hl) of each image (the whole image unless this
     // launch is one row band of a decomposed image)
@@ -601,25 +603,25 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 1] = globaltimer_ns();
     // per-tile partials, last CTA of the image reduces and decides
     block_reduce<NT>(acc, red, s_sum);
-    if (tid < kNumPartials) {
-        a.partials[((size_t)g.t * a.B + b) * kPartialStride + tid] = s_sum[tid];
-        __threadfence();
-    }
+    if (tid < kNumPartials) a.partials[((size_t)g.t * a.B + b) * kPartialStride + tid] = s_sum[tid];
     if (a.band) return;  // band mode: partials are all-gathered and decided by k_decide
     const int nlaunch = a.tiles_x * a.tiles_y;
     __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(a.tickets + b, 1u) == (unsigned)(nlaunch - 1));
+    // thread 0's acq_rel ticket releases the CTA's partial stores (ordered before it by the barrier;
+    // release is cumulative) and, in the last CTA, acquires every earlier CTA's
+    if (tid == 0) s_last = (ticket_acq_rel(a.tickets + b) == (unsigned)(nlaunch - 1));
     __syncthreads();
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
     if (!s_last) return;
-    __threadfence();
     reduce_tiles<NT>(a.partials, a.tiles_x * a.tiles_y, a.B, b, red, s_sum);
     if (tid == 0) {
         a.tickets[b] = 0u;
         if (a.mode == MODE_EVAL) {
             a.energy_out[b] = s_sum[0];
         } else if (!a.no_decide) {
-            decide(a, b, s_sum);
+            ImgCtl c = s_ctl;  // = a.ctl[b]: read at this pass's start, written only by this decision
+            decide_ctl(a, b, s_sum, c, true, a.mode);
+            a.ctl[b] = c;
         }
     }
 }
