@@ -105,6 +105,11 @@ int foe_bin(const double *y, double *yb, int H, int W, int factor, void *stream)
 int foe_unbin_bilinear(const double *xb, double *out, int h, int w, int H, int W, int factor,
                        void *stream);
 
+/* estimate_peak (pipeline.py:247-254, used by cli.py:69-73 when --peak is omitted): max of the 3 x 3
+ * median filter (scipy "reflect" = edge-inclusive mirror boundary) of y (H x W fp64, device).
+ * scratch: 8 bytes of device memory; *peak (host) is written after a stream synchronise. */
+int foe_estimate_peak(const double *y, int H, int W, unsigned long long *scratch, double *peak, void *stream);
+
 /* ---- operators ---------------------------------------------------------------------------------
  * convolve_same (image.py:37-58) / convolve_adjoint (image.py:68-83) with filter `index` of the
  * bank, B images of H x W.  Reference-operator surface for tests; the solve uses the fused pass. */

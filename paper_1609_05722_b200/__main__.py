@@ -6,7 +6,10 @@
                                               [--variants transform ...] [--csv OUT.csv]
 
 Raster I/O of the reference CLI is out of scope; counts and images are
-.npy arrays.  Exit codes follow cli.py:247-257: 0 ok, 1 invalid input, 2 numerical failure.
+.npy arrays.  Exit codes are the reference's (cli.py:1-5, 28-31, 244-257): 0 success, 1 usage error
+(bad flags or invalid arguments), 2 data error (unreadable or malformed files), 3 numerical failure.
+Without --peak the peak is estimated as the reference does (estimate_peak, pipeline.py:247-254:
+max of the 3x3 median filter), on the device.
 """
 from __future__ import annotations
 
@@ -15,19 +18,41 @@ import sys
 
 import numpy as np
 
-EXIT_OK, EXIT_INVALID, EXIT_NUMERICAL = 0, 1, 2
+EXIT_OK, EXIT_USAGE, EXIT_DATA, EXIT_NUMERIC = 0, 1, 2, 3
 
 
-def _estimate_peak(noisy: np.ndarray) -> float:
-    return float(max(np.max(noisy), 1e-3))
+class _Parser(argparse.ArgumentParser):
+    """argparse exits with 2 on bad flags; the contract reserves 2 for data errors (cli.py:37-43)."""
+
+    def error(self, message):
+        self.print_usage(sys.stderr)
+        self.exit(EXIT_USAGE, f"{self.prog}: error: {message}\n")
+
+
+def _read_counts(path: str) -> np.ndarray:
+    from .fileio import FileFormatError
+    try:
+        arr = np.load(path, allow_pickle=False)
+    except (FileNotFoundError, OSError):
+        raise
+    except ValueError as exc:  # not an .npy file / pickled payload
+        raise FileFormatError(f"{path}: {exc}") from exc
+    if not isinstance(arr, np.ndarray) or arr.ndim != 2:
+        raise FileFormatError(f"{path}: expected a 2-d array")
+    return arr.astype(np.float64)
 
 
 def cmd_denoise(args) -> int:
     from . import DenoiseRequest, denoise, load_model, load_packaged_model
+    from .pipeline import estimate_peak
     model = load_model(args.model) if args.model else load_packaged_model(
         "foe_s" if args.variant == "direct" else "foe_a")
-    noisy = np.load(args.input).astype(np.float64)
-    peak = args.peak if args.peak is not None else _estimate_peak(noisy)
+    noisy = _read_counts(args.input)
+    if args.peak is not None:
+        peak = args.peak
+    else:
+        peak = estimate_peak(noisy)
+        print(f"peak estimated from input: {peak:g}")
     req = DenoiseRequest(noisy=noisy, peak=peak, model=model, variant=args.variant,
                          lam=args.lam if args.lam is not None else "auto", zero_offset_c=args.c)
     out = denoise(req)
@@ -58,9 +83,9 @@ def cmd_benchmark(args) -> int:
     return EXIT_OK
 
 
-def main(argv=None) -> int:
-    ap = argparse.ArgumentParser(prog="python -m paper_1609_05722_b200")
-    sub = ap.add_subparsers(dest="cmd", required=True)
+def build_parser() -> argparse.ArgumentParser:
+    ap = _Parser(prog="python -m paper_1609_05722_b200")
+    sub = ap.add_subparsers(dest="cmd", required=True, parser_class=_Parser)
     d = sub.add_parser("denoise", help="denoise one count image (.npy)")
     d.add_argument("input")
     d.add_argument("output")
@@ -76,16 +101,24 @@ def main(argv=None) -> int:
     b.add_argument("--variants", nargs="+", default=["transform"])
     b.add_argument("--seed", type=int, default=0)
     b.add_argument("--csv")
-    args = ap.parse_args(argv)
+    return ap
+
+
+def main(argv=None) -> int:
+    args = build_parser().parse_args(argv)
+    from .fileio import FileFormatError
     from .solver import NumericalFailure
     try:
         return cmd_denoise(args) if args.cmd == "denoise" else cmd_benchmark(args)
-    except NumericalFailure as e:
-        print(f"numerical failure: {e}", file=sys.stderr)
-        return EXIT_NUMERICAL
-    except (ValueError, OSError) as e:
-        print(f"error: {e}", file=sys.stderr)
-        return EXIT_INVALID
+    except (FileFormatError, FileNotFoundError, OSError) as err:  # cli.py:247-249
+        print(f"error: {err}", file=sys.stderr)
+        return EXIT_DATA
+    except NumericalFailure as err:  # cli.py:250-252
+        print(f"numerical failure: {err}", file=sys.stderr)
+        return EXIT_NUMERIC
+    except ValueError as err:  # cli.py:253-255
+        print(f"error: {err}", file=sys.stderr)
+        return EXIT_USAGE
 
 
 if __name__ == "__main__":

@@ -100,6 +100,7 @@ def lib():
     L.foe_bin.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp]
     L.foe_unbin_bilinear.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      _vp]
+    L.foe_estimate_peak.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]
     L.foe_convolve_same.argtypes = [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp]
     L.foe_convolve_adjoint.argtypes = L.foe_convolve_same.argtypes
     L.foe_eval_workspace_size.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
@@ -141,7 +142,7 @@ def check(rc: int, what: str = "") -> int:
 EXPORTED_SYMBOLS = [
     "foe_abi_version", "foe_last_error", "foe_device_sm_count", "foe_counts_check", "foe_kernel_launch_count", "foe_bank_create", "foe_bank_destroy",
     "foe_bank_info", "foe_anscombe_forward", "foe_direct_obs", "foe_anscombe_inverse_exact_unbiased",
-    "foe_prox_quadratic", "foe_prox_idiv", "foe_bin", "foe_unbin_bilinear", "foe_convolve_same", "foe_convolve_adjoint",
+    "foe_prox_quadratic", "foe_prox_idiv", "foe_bin", "foe_unbin_bilinear", "foe_estimate_peak", "foe_convolve_same", "foe_convolve_adjoint",
     "foe_eval_workspace_size", "foe_energy_grad", "foe_solve_workspace_size", "foe_solve",
     "foe_bench_trial_pass", "foe_debug_pass_times", "foe_tc_selftest", "foe_pass_uses_tensor_cores",
     "foe_debug_tc_rate", "foe_measure_ffma_peak", "foe_debug_pass_times_seq", "foe_score_workspace_size", "foe_score",

@@ -95,7 +95,6 @@ struct PassArgs {
     int lrow0;  // global row stored in local row 0
     int Hl;     // local rows per image (plane stride = Hl * W)
     int band;   // 1: write partials only, decisions by k_decide after the all-gather
-    unsigned *grid_bar;  // resident solver: [0] arrival count, [1] generation
     unsigned long long *dbg_times;  // optional per-CTA [start, end-of-compute, exit] %globaltimer (ns)
     size_t plane;  // B*H*W: distance between state slots
     const float *kf;     // (n, M*M) flipped taps (correlation orientation of the forward conv)
@@ -183,8 +182,7 @@ __device__ void finish_image(const PassArgs &a, ImgCtl &c, bool primary) {
 }
 
 // Apply one pass's summed partials s[0..6] to image b's control block c.  `primary` = this copy of
-// the control block is the authoritative one (writes the trace row and the live counter); the
-// resident solver runs the same function on a private copy in every CTA.
+// the control block is the authoritative one (writes the trace row and the live counter).
 __device__ void decide_ctl(const PassArgs &a, int b, const double *s, ImgCtl &c, bool primary, int mode) {
     if (mode == MODE_INIT) {
         c.f_u = s[0];
@@ -512,6 +510,48 @@ __global__ void k_unbin(const double *__restrict__ xb, double *__restrict__ out,
     }
 }
 
+// estimate_peak (pipeline.py:247-254): the max over pixels of the 3 x 3 median filter of the counts, with
+// scipy.ndimage.median_filter's default "reflect" boundary (edge-inclusive mirror, the symmetric rule of
+// src_idx).  The median is the 19-exchange selection network for 9 values; the max is an atomicMax on an
+// order-preserving integer image of the double.
+__device__ __forceinline__ unsigned long long ordered_bits(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ void cswap(double &a, double &b) {
+    const double lo = fmin(a, b), hi = fmax(a, b);
+    a = lo;
+    b = hi;
+}
+__global__ void k_median3_max(const double *__restrict__ y, int H, int W, unsigned long long *out) {
+    const int64_t n = (int64_t)H * W;
+    unsigned long long best = 0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int Y = (int)(i / W), X = (int)(i - (int64_t)Y * W);
+        double p[9];
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx)
+                p[3 * dy + dx] = y[(size_t)src_idx<true>(Y + dy - 1, H) * W + src_idx<true>(X + dx - 1, W)];
+        cswap(p[1], p[2]); cswap(p[4], p[5]); cswap(p[7], p[8]);
+        cswap(p[0], p[1]); cswap(p[3], p[4]); cswap(p[6], p[7]);
+        cswap(p[1], p[2]); cswap(p[4], p[5]); cswap(p[7], p[8]);
+        cswap(p[0], p[3]); cswap(p[5], p[8]); cswap(p[4], p[7]);
+        cswap(p[3], p[6]); cswap(p[1], p[4]); cswap(p[2], p[5]);
+        cswap(p[4], p[7]); cswap(p[4], p[2]); cswap(p[6], p[4]);
+        cswap(p[4], p[2]);
+        const unsigned long long o = ordered_bits(p[4]);
+        best = o > best ? o : best;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long v = __shfl_down_sync(0xffffffffu, best, off);
+        best = v > best ? v : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
+}
+
 // ------------------------------------------------------------------------------------------------
 // row-band decomposition (BASELINE config 5): decisions after the partials all-gather, halo rows
 
@@ -587,16 +627,29 @@ int grid_1d(int64_t n, int block = 256) {
 }
 
 template <int M>
-size_t pass_smem_bytes(int nf, bool trial, bool resident = false) {
-    return sizeof(float) * smem_floats<M>(nf, trial, resident);
+size_t pass_smem_bytes(int nf, bool trial) {
+    return sizeof(float) * smem_floats<M>(nf, trial);
 }
 
 // programmatic dependent launch of a pass kernel: its CTAs may start (bank staging, TMEM, barriers)
 // while the previous kernel in the stream drains; the kernel waits (griddepcontrol.wait) before
-// reading the state that kernel wrote.  FOE_PDL=0 launches in plain stream order.
+// reading the state that kernel wrote.
+// raise a kernel's dynamic shared-memory limit once per device (the bitmask is shared by concurrent
+// host threads; a race only repeats the idempotent attribute call)
+template <class K>
+int ensure_smem(K kernel, int bytes, std::atomic<unsigned long long> &configured) {
+    int dev = 0;
+    FOE_CUDA(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(configured.load(std::memory_order_acquire) & bit)) {
+        FOE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        configured.fetch_or(bit, std::memory_order_release);
+    }
+    return FOE_OK;
+}
+
 template <class K>
 cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const PassArgs &a) {
-    static const bool pdl = !(getenv("FOE_PDL") && getenv("FOE_PDL")[0] == '0');
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -606,7 +659,7 @@ cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
@@ -614,13 +667,8 @@ template <int M, bool TRIAL, bool SYM>
 int launch_pass_t(const PassArgs &a, cudaStream_t st) {
     using C = PassCfg<M>;
     const size_t smem = pass_smem_bytes<M>(a.n_filters, TRIAL);
-    static unsigned long long configured = 0;  // one bit per device
-    int dev = 0;
-    FOE_CUDA(cudaGetDevice(&dev));
-    if (!(configured >> (dev & 63) & 1ull)) {
-        FOE_CUDA(cudaFuncSetAttribute(k_pass<M, TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured |= 1ull << (dev & 63);
-    }
+    static std::atomic<unsigned long long> configured{0};  // one bit per device
+    if (int rc = ensure_smem(k_pass<M, TRIAL, SYM>, 200 * 1024, configured)) return rc;
     FOE_CUDA(launch_pdl(k_pass<M, TRIAL, SYM>, dim3(a.tiles_x * a.tiles_yl, a.B), dim3(C::NT), smem, st, a));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return FOE_OK;
@@ -649,45 +697,11 @@ int launch_pass_tc_t(const PassArgs &a, cudaStream_t st) {
     using T = TcCfg<32>;
     // >= 116 KB keeps one CTA per SM: the 512 TMEM columns it allocates are the whole SM's
     const size_t smem = std::max<size_t>(sizeof(float) * (tc_smem_floats<32>() + 64), 116 * 1024);
-    static unsigned long long configured = 0;
-    int dev = 0;
-    FOE_CUDA(cudaGetDevice(&dev));
-    if (!(configured >> (dev & 63) & 1ull)) {
-        FOE_CUDA(cudaFuncSetAttribute(k_pass_tc<NF, TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured |= 1ull << (dev & 63);
-    }
+    static std::atomic<unsigned long long> configured{0};  // one bit per device
+    if (int rc = ensure_smem(k_pass_tc<NF, TRIAL, SYM>, (int)smem, configured)) return rc;
     FOE_CUDA(launch_pdl(k_pass_tc<NF, TRIAL, SYM>, dim3(a.tiles_x * a.tiles_yl, a.B), dim3(T::NT), smem, st, a));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return FOE_OK;
-}
-
-// resident tensor-core solve (one cooperative launch for the whole solve): FOE_OK if launched, 1 if not
-// applicable (filter count, co-residency, cooperative launch support)
-template <int NF, bool SYM>
-int launch_resident_tc_t(const PassArgs &a, cudaStream_t st) {
-    using T = TcCfg<32>;
-    const size_t smem = std::max<size_t>(sizeof(float) * (tc_smem_floats<32>() + 64), 116 * 1024);
-    int dev = 0, nsm = 0, nb = 0, coop = 0;
-    FOE_CUDA(cudaGetDevice(&dev));
-    FOE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    FOE_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    if (!coop) return 1;
-    FOE_CUDA(cudaFuncSetAttribute(k_solve_resident_tc<NF, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FOE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_solve_resident_tc<NF, SYM>, T::NT, smem));
-    if ((long)nb * nsm < (long)a.tiles_x * a.tiles_y * a.B) return 1;
-    dim3 grid(a.tiles_x * a.tiles_y, a.B);
-    void *args[] = {(void *)&a};
-    FOE_CUDA(cudaLaunchCooperativeKernel((const void *)k_solve_resident_tc<NF, SYM>, grid, dim3(T::NT), args, smem, st));
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return FOE_OK;
-}
-
-int launch_resident_tc(bool sym, const PassArgs &a, cudaStream_t st) {
-    switch ((a.n_filters + 7) / 8) {
-        case 3: return sym ? launch_resident_tc_t<24, true>(a, st) : launch_resident_tc_t<24, false>(a, st);
-        case 4: return sym ? launch_resident_tc_t<32, true>(a, st) : launch_resident_tc_t<32, false>(a, st);
-        default: return 1;
-    }
 }
 
 // tensor-core pass for 7x7 banks with <= 48 filters (k_pass_tc7); FOE_TC7=0 (or FOE_TC=0) forces the FFMA pass
@@ -697,13 +711,8 @@ bool use_tc7(int m, int nf) { return m == 7 && nf <= 48 && tc7_enabled(); }
 template <bool TRIAL, bool SYM>
 int launch_pass_tc7_t(const PassArgs &a, cudaStream_t st) {
     const size_t smem = sizeof(float) * (tc7_smem_floats() + 64);
-    static unsigned long long configured = 0;
-    int dev = 0;
-    FOE_CUDA(cudaGetDevice(&dev));
-    if (!(configured >> (dev & 63) & 1ull)) {
-        FOE_CUDA(cudaFuncSetAttribute(k_pass_tc7<TRIAL, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured |= 1ull << (dev & 63);
-    }
+    static std::atomic<unsigned long long> configured{0};  // one bit per device
+    if (int rc = ensure_smem(k_pass_tc7<TRIAL, SYM>, (int)smem, configured)) return rc;
     FOE_CUDA(launch_pdl(k_pass_tc7<TRIAL, SYM>, dim3(a.tiles_x * a.tiles_yl, a.B), dim3(TcCfg7::NT), smem, st, a));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return FOE_OK;
@@ -732,39 +741,6 @@ int launch_pass(int m, bool sym, const PassArgs &a, cudaStream_t st) {
     return sym ? launch_pass_m<false, true>(m, a, st) : launch_pass_m<false, false>(m, a, st);
 }
 
-// resident (single cooperative launch) solve: returns FOE_OK if launched, 1 if not applicable
-template <int M, bool SYM>
-int launch_resident_t(const PassArgs &a, cudaStream_t st) {
-    using C = PassCfg<M>;
-    const size_t smem = pass_smem_bytes<M>(a.n_filters, true, true);
-    int dev = 0, nsm = 0, nb = 0, coop = 0, optin = 0;
-    FOE_CUDA(cudaGetDevice(&dev));
-    FOE_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    FOE_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-    FOE_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    cudaFuncAttributes fa;
-    FOE_CUDA(cudaFuncGetAttributes(&fa, k_solve_resident<M, SYM>));
-    if (!coop || smem + fa.sharedSizeBytes > (size_t)optin) return 1;
-    FOE_CUDA(cudaFuncSetAttribute(k_solve_resident<M, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FOE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_solve_resident<M, SYM>, C::NT, smem));
-    if ((long)nb * nsm < (long)a.tiles_x * a.tiles_y * a.B) return 1;
-    dim3 grid(a.tiles_x * a.tiles_y, a.B);
-    void *args[] = {(void *)&a};
-    FOE_CUDA(cudaLaunchCooperativeKernel((const void *)k_solve_resident<M, SYM>, grid, dim3(C::NT), args, smem, st));
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return FOE_OK;
-}
-
-int launch_resident(int m, bool sym, const PassArgs &a, cudaStream_t st) {
-    switch (m) {
-        case 1: return sym ? launch_resident_t<1, true>(a, st) : launch_resident_t<1, false>(a, st);
-        case 3: return sym ? launch_resident_t<3, true>(a, st) : launch_resident_t<3, false>(a, st);
-        case 5: return sym ? launch_resident_t<5, true>(a, st) : launch_resident_t<5, false>(a, st);
-        case 7: return sym ? launch_resident_t<7, true>(a, st) : launch_resident_t<7, false>(a, st);
-        default: return 1;
-    }
-}
-
 // region rows of the pass kernel that runs filter side m: 7x7 banks take the tensor-core pass's 40-row
 // regions unless it is switched off (FOE_TC7=0 / FOE_TC=0: the FFMA k_pass<7>'s 48)
 bool tc7_enabled() {
@@ -786,7 +762,7 @@ void tile_counts(int m, int H, int W, int *tx, int *ty) {
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct SolveLayout {
-    size_t U, G, O, ctl, partials, tickets, trace, n_active, send, recv, grid_bar, total;
+    size_t U, G, O, ctl, partials, tickets, trace, n_active, send, recv, total;
     size_t halo_floats;  // per direction
 };
 
@@ -802,15 +778,13 @@ SolveLayout solve_layout(int m, int B, int H, int W, int trace_cap, int Hl = -1,
     L.G = off; off = align_up(off + 2 * plane);
     L.O = off; off = align_up(off + plane);
     L.ctl = off; off = align_up(off + sizeof(ImgCtl) * B);
-    // partials double-buffered by pass parity (the resident solver reads pass k while writing k+1)
-    L.partials = off; off = align_up(off + 2 * sizeof(double) * kPartialStride * (size_t)B * tx * ty);
+    L.partials = off; off = align_up(off + sizeof(double) * kPartialStride * (size_t)B * tx * ty);
     L.tickets = off; off = align_up(off + sizeof(unsigned) * B);
     L.trace = off; off = align_up(off + sizeof(double) * 6 * (size_t)B * trace_cap);
     L.n_active = off; off = align_up(off + sizeof(int) * 4);
     L.halo_floats = (size_t)B * 2 * halo * W;
     L.send = off; off = align_up(off + sizeof(float) * 2 * L.halo_floats);
     L.recv = off; off = align_up(off + sizeof(float) * 2 * L.halo_floats);
-    L.grid_bar = off; off = align_up(off + sizeof(unsigned) * 2);
     L.total = off;
     return L;
 }
@@ -823,11 +797,6 @@ int check_dims(const foe_bank *bank, int B, int H, int W) {
     return FOE_OK;
 }
 
-struct PinnedFlags {
-    int *p = nullptr;
-    ~PinnedFlags() { if (p) cudaFreeHost(p); }
-};
-thread_local PinnedFlags t_flags;
 
 }  // namespace
 
@@ -836,11 +805,7 @@ thread_local PinnedFlags t_flags;
 // k_loop_cond] until no image is live, so the tail of a solve needs no host round trip.  n_active[1]
 // counts the passes the loop ran, n_active[2] flags the safety cap.
 
-constexpr int kGraphChunkDefault = 8;
-int graph_chunk() {  // FOE_GRAPH_CHUNK overrides (timing experiments)
-    static const int c = getenv("FOE_GRAPH_CHUNK") ? std::max(1, atoi(getenv("FOE_GRAPH_CHUNK"))) : kGraphChunkDefault;
-    return c;
-}
+constexpr int kGraphChunk = 8;  // trial passes per evaluation of the loop condition
 
 __global__ void k_loop_cond(cudaGraphConditionalHandle h, int *n_active, int cap, int chunk) {
     const int passes = (n_active[1] += chunk);
@@ -875,7 +840,6 @@ int loop_graph(int m, bool sym, const PassArgs &a, int cap, cudaGraphExec_t *out
             *out = e.exec;
             return FOE_OK;
         }
-    if (getenv("FOE_GRAPH_DEBUG")) fprintf(stderr, "foe: capturing solve-loop graph (%zu cached)\n", t_graphs.entries.size());
     if (!t_graphs.cap_stream) FOE_CUDA(cudaStreamCreateWithFlags(&t_graphs.cap_stream, cudaStreamNonBlocking));
     cudaGraph_t g = nullptr;
     FOE_CUDA(cudaGraphCreate(&g, 0));
@@ -893,7 +857,7 @@ int loop_graph(int m, bool sym, const PassArgs &a, int cap, cudaGraphExec_t *out
     FOE_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     const long long before = g_launches.load();
     int rc = FOE_OK;
-    const int chunk = graph_chunk();
+    const int chunk = kGraphChunk;
     for (int k = 0; k < chunk && rc == FOE_OK; ++k) rc = launch_pass(m, sym, a, cs);
     if (rc == FOE_OK) k_loop_cond<<<1, 1, 0, cs>>>(h, a.n_active, cap, chunk);
     cudaGraph_t captured = nullptr;
@@ -1414,7 +1378,6 @@ static void fill_solve_args(PassArgs &a, const foe_bank *bank, const foe_solver_
     a.trace = (double *)(ws + L.trace);
     a.trace_cap = trace_cap;
     a.n_active = (int *)(ws + L.n_active);
-    a.grid_bar = (unsigned *)(ws + L.grid_bar);
     a.gamma = cfg.gamma;
     a.step_num = 1.99 * (1.0 - cfg.gamma);  // solver.py:64-65
     a.eta = cfg.backtrack_factor;
@@ -1476,79 +1439,18 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     FOE_CUDA(cudaMemcpyAsync(a.U + 2 * a.plane, u0, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
     FOE_CUDA(cudaMemcpyAsync((float *)(ws + L.O), obs, sizeof(float) * HWB, cudaMemcpyDeviceToDevice, st));
 
-    // the resident single-launch solver is opt-in (FOE_RESIDENT=1): measured no faster than the
-    // per-pass launches on B200 (grid barrier + redundant decisions cost what the launches did)
-    const char *env = getenv("FOE_RESIDENT");
-    // (the FFMA resident solver tiles 7x7 banks with 48-row regions: not with the tensor-core 7x7 geometry)
-    const bool try_resident = B <= kResidentMaxB && env && env[0] == '1' && !(bank->m == 7 && tc7_enabled());
-    bool resident = false, graph_loop = false;
-    // the tensor-core pass has its own resident solve, opt-in (FOE_RESIDENT_TC=1): measured ~13 % slower
-    // per pass than the programmatic-dependent per-pass launches (grid barrier + every CTA deciding)
-    const char *env_tc = getenv("FOE_RESIDENT_TC");
-    if (B <= kResidentMaxB && use_tc(bank->m, bank->n) && env_tc && env_tc[0] == '1') {
-        FOE_CUDA(cudaMemsetAsync(a.grid_bar, 0, sizeof(unsigned) * 2, st));
-        a.mode = MODE_TRIAL;
-        rc = launch_resident_tc(bank->boundary == FOE_SYMMETRIC, a, st);
-        if (rc < 0) return rc;
-        resident = rc == FOE_OK;
-    }
-    if (!resident && try_resident) {
-        FOE_CUDA(cudaMemsetAsync(a.grid_bar, 0, sizeof(unsigned) * 2, st));
-        rc = launch_resident(bank->m, bank->boundary == FOE_SYMMETRIC, a, st);
-        if (rc < 0) return rc;
-        resident = rc == FOE_OK;
-    }
-    if (!resident) {
     // iteration 0 needs F(u0) and grad F(u0)
     a.mode = MODE_INIT;
     if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, st))) return rc;
-
-    static const bool use_graph = !(getenv("FOE_GRAPH") && getenv("FOE_GRAPH")[0] == '0');
-    if (use_graph) {
-        // every image needs >= 1 trial per accepted iteration: min_it passes straight away, then the
-        // device-side loop graph until no image is live
-        a.mode = MODE_TRIAL;
-        for (int k = 0; k < std::max(1, min_it); ++k)
-            if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, st))) return rc;
-        const int cap = max_it * 200 + 64;
-        cudaGraphExec_t exec = nullptr;
-        if ((rc = loop_graph(bank->m, bank->boundary == FOE_SYMMETRIC, a, cap, &exec))) return rc;
-        FOE_CUDA(cudaGraphLaunch(exec, st));
-        graph_loop = true;
-    } else {
-    if (!t_flags.p) FOE_CUDA(cudaHostAlloc(&t_flags.p, 4 * sizeof(int), cudaHostAllocDefault));
-    cudaEvent_t ev[2];
-    FOE_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-    FOE_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    // every image needs >= 1 trial per accepted iteration: min_it passes straight away, then the
+    // device-side loop graph until no image is live
     a.mode = MODE_TRIAL;
-    // every image needs >= 1 trial per accepted iteration; afterwards poll the live count every chunk
-    const long hard_cap = (long)max_it * 200 + 64;
-    long launched = 0;
-    int slot = 0, pending = -1;
-    int chunk = std::max(1, min_it);
-    for (;;) {
-        for (int k = 0; k < chunk; ++k)
-            if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, st))) return rc;
-        launched += chunk;
-        FOE_CUDA(cudaMemcpyAsync(t_flags.p + slot, a.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
-        FOE_CUDA(cudaEventRecord(ev[slot], st));
-        if (pending >= 0) {
-            FOE_CUDA(cudaEventSynchronize(ev[pending]));
-            if (t_flags.p[pending] == 0) break;
-        }
-        pending = slot;
-        slot ^= 1;
-        chunk = 8;
-        if (launched > hard_cap) {
-            cudaEventDestroy(ev[0]);
-            cudaEventDestroy(ev[1]);
-            return fail(FOE_E_NUMERICAL, "solver did not terminate after %ld passes", launched);
-        }
-    }
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
-    }  // host-polled loop
-    }  // per-launch path
+    for (int k = 0; k < std::max(1, min_it); ++k)
+        if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, st))) return rc;
+    const int cap = max_it * 200 + 64;
+    cudaGraphExec_t exec = nullptr;
+    if ((rc = loop_graph(bank->m, bank->boundary == FOE_SYMMETRIC, a, cap, &exec))) return rc;
+    FOE_CUDA(cudaGraphLaunch(exec, st));
     {
         dim3 grid(std::max(1, std::min(148, (int)((size_t)H * W / 1024 + 1))), B);
         g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1558,12 +1460,10 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     FOE_CUDA(cudaMemcpyAsync(hc.data(), a.ctl, sizeof(ImgCtl) * B, cudaMemcpyDeviceToHost, st));
     FOE_CUDA(cudaMemcpyAsync(trace, a.trace, sizeof(double) * 6 * (size_t)B * trace_cap, cudaMemcpyDeviceToHost, st));
     int loop_info[4] = {0, 0, 0, 0};
-    if (graph_loop) FOE_CUDA(cudaMemcpyAsync(loop_info, a.n_active, sizeof(loop_info), cudaMemcpyDeviceToHost, st));
+    FOE_CUDA(cudaMemcpyAsync(loop_info, a.n_active, sizeof(loop_info), cudaMemcpyDeviceToHost, st));
     FOE_CUDA(cudaStreamSynchronize(st));
-    if (graph_loop) {
-        g_launches.fetch_add(loop_info[1] + loop_info[1] / graph_chunk(), std::memory_order_relaxed);
-        if (loop_info[2]) return fail(FOE_E_NUMERICAL, "solver did not terminate after %d passes", loop_info[1]);
-    }
+    g_launches.fetch_add(loop_info[1] + loop_info[1] / kGraphChunk, std::memory_order_relaxed);
+    if (loop_info[2]) return fail(FOE_E_NUMERICAL, "solver did not terminate after %d passes", loop_info[1]);
     int any_fail = 0;
     for (int b = 0; b < B; ++b) {
         status[b].status = hc[b].status;
@@ -1803,6 +1703,23 @@ int foe_unbin_bilinear(const double *xb, double *out, int h, int w, int H, int W
 }
 
 
+
+int foe_estimate_peak(const double *y, int H, int W, unsigned long long *scratch, double *peak, void *stream) {
+    if (!y || !scratch || !peak || H < 1 || W < 1) return fail(FOE_E_INVALID, "bad estimate_peak arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long host = 0ull;
+    FOE_CUDA(cudaMemsetAsync(scratch, 0, sizeof(unsigned long long), st));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_median3_max<<<grid_1d((int64_t)H * W), 256, 0, st>>>(y, H, W, scratch);
+    FOE_CUDA(cudaGetLastError());
+    FOE_CUDA(cudaMemcpyAsync(&host, scratch, sizeof(host), cudaMemcpyDeviceToHost, st));
+    FOE_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long b = (host >> 63) ? (host & 0x7fffffffffffffffull) : ~host;
+    double v;
+    memcpy(&v, &b, sizeof(v));
+    *peak = v;
+    return FOE_OK;
+}
 
 int foe_measure_ffma_peak(int iters, float *scratch, double *flop_out, void *stream) {
     int dev = 0, sms = 0;

@@ -13,13 +13,8 @@
 // a*log1p(dz(2z_o+dz)/(1+z_o^2)) evaluated as 2a*atanh(t), t = (z^2-z_o^2)/((1+z^2)+(1+z_o^2)),
 // then the adjoint K^T psi (300 FFMA).
 //
-// Two drivers share the tile code:
-//  * k_pass: one launch per trial pass (any batch size, row bands); the last CTA of an image
-//    reduces the tile partials and decides.
-//  * k_solve_resident: the whole solve in one cooperative launch when every (image, tile) has its
-//    own SM.  Each CTA keeps its tile's u, u_prev, grad, obs in shared memory across passes (only
-//    the 2r halo comes from global memory), passes are separated by a grid barrier, and every CTA
-//    reduces the partials and takes the (identical) decision itself.
+// k_pass: one launch per trial pass (any batch size, row bands); the last CTA of an image reduces
+// the tile partials and decides.
 
 template <int M_>
 struct PassCfg {
@@ -38,7 +33,6 @@ struct PassCfg {
     static constexpr int PLANE = SH * SW;
     static constexpr int NPSI = G * NBUF;       // psi planes
     static constexpr int TH = RH - 2 * R, TW = RW - 2 * R;  // max owned tile
-    static constexpr int TOWN = TH * TW;                    // resident state plane (owned pixels)
     static constexpr int TAPS = (M * M + 3) & ~3;           // per-filter tap stride (float4)
     static constexpr int NCELL = SH * CW;
     static constexpr int CPT = (NCELL + NT - 1) / NT;       // staged cells per thread
@@ -48,7 +42,6 @@ struct PassCfg {
     static_assert(NT % RW == 0, "fold walk assumes whole region rows per pass");
 };
 
-constexpr int kResidentMaxB = 8;  // images per resident solve (control blocks kept in smem)
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
@@ -142,7 +135,6 @@ __device__ __forceinline__ TileGeom tile_geom(const PassArgs &a, int tyl, int tx
 template <int M>
 struct Smem {
     float *Un, *Du, *Psi, *taps, *alpha;
-    float *Su, *Sg, *So;  // resident state: u slots [3][TOWN], grad slots [2][TOWN], obs [TOWN]
     __device__ Smem(float *sm, int nf, bool trial_planes) {
         using C = PassCfg<M>;
         Un = sm;
@@ -150,17 +142,14 @@ struct Smem {
         Psi = trial_planes ? Du + C::PLANE : Du;
         taps = Psi + C::NPSI * C::PLANE;
         alpha = taps + nf * C::TAPS;
-        Su = alpha + ((nf + 3) & ~3);
-        Sg = Su + 3 * C::TOWN;
-        So = Sg + 2 * C::TOWN;
     }
 };
 
 template <int M>
-__host__ __device__ constexpr size_t smem_floats(int nf, bool trial, bool resident) {
+__host__ __device__ constexpr size_t smem_floats(int nf, bool trial) {
     using C = PassCfg<M>;
     return (size_t)(trial ? 2 : 1) * C::PLANE + (size_t)C::NPSI * C::PLANE + (size_t)nf * C::TAPS +
-           (size_t)((nf + 3) & ~3) + (resident ? (size_t)6 * C::TOWN : 0);
+           (size_t)((nf + 3) & ~3);
 }
 
 template <int M>
@@ -211,17 +200,15 @@ __device__ __forceinline__ TrialParams trial_params(const PassArgs &a, const Img
 
 // ------------------------------------------------------------------------------------------------
 // prologue: stage u (EVAL/INIT) or the trial point u_new and du (TRIAL) into Un/Du
-//   global inputs are image-offset pointers to local buffers holding rows [lrow0, lrow0 + Hl);
-//   RES: the owned pixels come from the resident smem state, only the halo from global (L2)
+//   global inputs are image-offset pointers to local buffers holding rows [lrow0, lrow0 + Hl)
 
-template <int M, bool TRIAL, bool SYM, bool RES>
+template <int M, bool TRIAL, bool SYM>
 __device__ void stage(const PassArgs &a, const TileGeom &g, const Smem<M> &S, const TrialParams &p, const float *uin,
                       const float *upv, const float *gin, const float *obs, float *uout, float shift,
                       double (&acc)[kNumPartials]) {
     using C = PassCfg<M>;
     constexpr int R = C::R, CW = C::CW, SW = C::SW, NT = C::NT, CPT = C::CPT, NCELL = C::NCELL;
     const int H = a.H, W = a.W, lrow0 = a.lrow0, tid = threadIdx.x;
-    const int ow = g.c1 - g.c0;
     // load phase: every global read of this thread's cells in flight before any use
     float lu[CPT], lup[CPT], lg[CPT], lob[CPT];
 #pragma unroll
@@ -230,24 +217,9 @@ __device__ void stage(const PassArgs &a, const TileGeom &g, const Smem<M> &S, co
         if (k < NCELL) {
             const int i = k / CW, j = k - i * CW;
             const int sy = src_idx<SYM>(g.ry0 - R + i, H), sx = src_idx<SYM>(g.rx0 - R + j, W);
-            if (RES && sy >= g.s0 && sy < g.s1 && sx >= g.c0 && sx < g.c1) {
-                const int ri = (sy - g.s0) * ow + (sx - g.c0);
-                lu[q] = S.Su[p.iu * C::TOWN + ri];
-                if (TRIAL) {
-                    lup[q] = S.Su[p.iup * C::TOWN + ri];
-                    lg[q] = S.Sg[p.ig * C::TOWN + ri];
-                    lob[q] = S.So[ri];
-                }
-            } else {
-                const size_t o = (size_t)(sy - lrow0) * W + sx;
-                if (RES) {  // written by other CTAs during this kernel: bypass L1
-                    lu[q] = __ldcg(uin + o);
-                    if (TRIAL) { lup[q] = __ldcg(upv + o); lg[q] = __ldcg(gin + o); lob[q] = __ldg(obs + o); }
-                } else {
-                    lu[q] = __ldg(uin + o);
-                    if (TRIAL) { lup[q] = __ldg(upv + o); lg[q] = __ldg(gin + o); lob[q] = __ldg(obs + o); }
-                }
-            }
+            const size_t o = (size_t)(sy - lrow0) * W + sx;
+            lu[q] = __ldg(uin + o);
+            if (TRIAL) { lup[q] = __ldg(upv + o); lg[q] = __ldg(gin + o); lob[q] = __ldg(obs + o); }
         }
     }
 #pragma unroll
@@ -269,7 +241,6 @@ __device__ void stage(const PassArgs &a, const TileGeom &g, const Smem<M> &S, co
         S.Du[i * SW + j] = du;
         if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) {
             uout[(size_t)(gy - lrow0) * W + gx] = un;
-            if (RES) S.Su[p.inew * C::TOWN + (gy - g.s0) * ow + (gx - g.c0)] = un;
             acc[1] += (double)du * (double)du;  // vdot(du, du)  solver.py:152
             acc[2] += (double)gg * (double)du;  // vdot(g, du)   solver.py:153
             acc[3] += (double)u * (double)u;    // |u|^2 for the stop test, solver.py:173
@@ -290,7 +261,7 @@ __device__ void stage(const PassArgs &a, const TileGeom &g, const Smem<M> &S, co
 // ------------------------------------------------------------------------------------------------
 // filter loop: per filter forward responses, pointwise, adjoint; returns this thread's owned
 // energy terms (fp64) and leaves the group's partial gradient in gacc.  `phase` carries the
-// mbarrier parities of the NBUF slots across calls (the resident solver reuses the barriers).
+// mbarrier parities of the NBUF slots across calls.
 
 template <int M, bool TRIAL, bool SYM>
 __device__ double filter_loop(const PassArgs &a, const TileGeom &g, const Smem<M> &S,
@@ -479,10 +450,10 @@ __device__ double filter_loop(const PassArgs &a, const TileGeom &g, const Smem<M
 }
 
 // combine the group partial gradients, fold padded pixels onto their mirror sources (P^T,
-// image.py:88-90) and write the owned gradient (global, and resident smem slot if Sgo != null)
+// image.py:76-83) and write the owned gradient
 template <int M, bool SYM>
 __device__ void fold_and_write(const PassArgs &a, const TileGeom &g, const Smem<M> &S,
-                               const float (&gacc)[PassCfg<M>::MY][PassCfg<M>::MX], float *gout, float *Sgo) {
+                               const float (&gacc)[PassCfg<M>::MY][PassCfg<M>::MX], float *gout) {
     using C = PassCfg<M>;
     constexpr int R = C::R, NT = C::NT, MY = C::MY;
     const int tid = threadIdx.x, H = a.H, W = a.W;
@@ -506,7 +477,6 @@ __device__ void fold_and_write(const PassArgs &a, const TileGeom &g, const Smem<
     // 2-D ownership walk: column = tid % RW, rows strided by NT / RW (no integer division)
     const int xx = tid % C::RW;
     const int gx = g.c0 + xx;
-    const int ow = g.c1 - g.c0;
     if (gx < g.c1) {
         const int lx = gx - g.rx0;
         int mx = -1;
@@ -526,7 +496,6 @@ __device__ void fold_and_write(const PassArgs &a, const TileGeom &g, const Smem<
                 if (my >= 0 && mx >= 0) val += gsum(my, mx);
             }
             gout[(size_t)(gy - a.lrow0) * W + gx] = val;
-            if (Sgo) Sgo[(gy - g.s0) * ow + xx] = val;
         }
     }
 }
@@ -592,13 +561,13 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     double acc[kNumPartials];
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
-    stage<M, TRIAL, SYM, false>(a, g, S, p, uin, upv, gin, obs, uout, shift, acc);
+    stage<M, TRIAL, SYM>(a, g, S, p, uin, upv, gin, obs, uout, shift, acc);
     __syncthreads();  // staged tile, taps and mbarrier init visible
 
     float gacc[C::MY][C::MX];
     unsigned phase = 0u;
     acc[0] = filter_loop<M, TRIAL, SYM>(a, g, S, s_mbar, phase, gacc);
-    fold_and_write<M, SYM>(a, g, S, gacc, gout, nullptr);
+    fold_and_write<M, SYM>(a, g, S, gacc, gout);
 
     if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 1] = globaltimer_ns();
     // per-tile partials, last CTA of the image reduces and decides
@@ -624,122 +593,4 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
             a.ctl[b] = c;
         }
     }
-}
-
-// ------------------------------------------------------------------------------------------------
-// k_solve_resident: the whole device-resident solve in one cooperative launch
-
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// generation barrier across the (co-resident) grid; bounded spin -> trap on a hang
-__device__ void grid_barrier(unsigned *bar, unsigned nblocks, unsigned &gen) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(bar, 1u) == nblocks - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            unsigned long long spins = 0;
-            while (ld_acquire_gpu(bar + 1) == gen) {
-                __nanosleep(64);
-                if (++spins > (1ull << 28)) __trap();  // ~> 20 s: a co-residency bug, not a slow pass
-            }
-        }
-        __threadfence();
-    }
-    ++gen;
-    __syncthreads();
-}
-
-template <int M, bool SYM>
-__global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_solve_resident(const PassArgs a) {
-    using C = PassCfg<M>;
-    constexpr int NT = C::NT;
-    extern __shared__ __align__(16) float sm[];
-    __shared__ double red[NT / 32][kNumPartials];
-    __shared__ double s_sum[kNumPartials];
-    __shared__ unsigned long long s_mbar[C::G][C::NBUF];
-    __shared__ ImgCtl s_ctl[kResidentMaxB];
-
-    const int tid = threadIdx.x;
-    const int b = blockIdx.y;
-    const int B = a.B;
-    const bool primary = blockIdx.x == 0 && blockIdx.y == 0;
-    const unsigned nblocks = gridDim.x * gridDim.y;
-    const int ntiles = a.tiles_x * a.tiles_y;
-    unsigned gen = 0;
-    if (tid == 0) gen = ld_acquire_gpu(a.grid_bar + 1);
-
-    const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
-    const TileGeom g = tile_geom<M, SYM>(a, tyl, txi);
-    const Smem<M> S(sm, a.n_filters, true);
-    stage_bank<M>(a, S);
-    if (tid < C::G * C::NBUF) mbar_init(&s_mbar[tid / C::NBUF][tid % C::NBUF], C::NTG / 32);
-    if (tid < B) s_ctl[tid] = a.ctl[tid];
-    const size_t ioff = (size_t)b * a.Hl * a.W;
-    const int ow = g.c1 - g.c0, oh = g.s1 - g.s0;
-    __syncthreads();
-    {   // resident state: u_prev = u = u0 (slots iu, iup), obs
-        const ImgCtl &c = s_ctl[b];
-        for (int k = tid; k < oh * ow; k += NT) {
-            const int yy = k / ow, xx = k - yy * ow;
-            const size_t o = (size_t)(g.s0 + yy - a.lrow0) * a.W + g.c0 + xx;
-            const float u0 = a.U[c.iu * a.plane + ioff + o];
-            S.Su[c.iu * C::TOWN + k] = u0;
-            S.Su[c.iup * C::TOWN + k] = u0;
-            S.So[k] = a.obs[ioff + o];
-        }
-    }
-    __syncthreads();
-    unsigned phase = 0u;
-
-    for (int pass = 0;; ++pass) {
-        const bool init = pass == 0;
-        double *parts = a.partials + (size_t)(pass & 1) * ntiles * B * kPartialStride;  // double-buffered
-        const ImgCtl c = s_ctl[b];
-        if (!c.done) {
-            const TrialParams p = trial_params(a, c);
-            // zero-mean shift anchor = current u at the tile's first owned pixel (as in k_pass)
-            const float shift = a.zero_mean ? S.Su[p.iu * C::TOWN] : 0.0f;
-            if (g.edge) zero_psi_ring<M>(S);  // the previous pass's gradient combine reused the planes
-            double acc[kNumPartials];
-#pragma unroll
-            for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
-            float gacc[C::MY][C::MX];
-            if (init) {
-                stage<M, false, SYM, true>(a, g, S, p, a.U + p.iu * a.plane + ioff, nullptr, nullptr, nullptr,
-                                           nullptr, shift, acc);
-                __syncthreads();
-                acc[0] = filter_loop<M, false, SYM>(a, g, S, s_mbar, phase, gacc);
-                fold_and_write<M, SYM>(a, g, S, gacc, a.Gs + p.ig * a.plane + ioff, S.Sg + p.ig * C::TOWN);
-            } else {
-                stage<M, true, SYM, true>(a, g, S, p, a.U + p.iu * a.plane + ioff, a.U + p.iup * a.plane + ioff,
-                                          a.Gs + p.ig * a.plane + ioff, a.obs + ioff,
-                                          a.U + p.inew * a.plane + ioff, shift, acc);
-                __syncthreads();
-                acc[0] = filter_loop<M, true, SYM>(a, g, S, s_mbar, phase, gacc);
-                fold_and_write<M, SYM>(a, g, S, gacc, a.Gs + p.ignew * a.plane + ioff, S.Sg + p.ignew * C::TOWN);
-            }
-            block_reduce<NT>(acc, red, s_sum);
-            if (tid < kNumPartials) parts[((size_t)g.t * B + b) * kPartialStride + tid] = s_sum[tid];
-        }
-        grid_barrier(a.grid_bar, nblocks, gen);
-        // every CTA reduces every live image's partials in the fixed order and decides identically
-        bool all_done = true;
-        for (int bb = 0; bb < B; ++bb) {
-            if (s_ctl[bb].done) continue;
-            reduce_tiles<NT>(parts, ntiles, B, bb, red, s_sum);
-            if (tid == 0) decide_ctl(a, bb, s_sum, s_ctl[bb], primary, init ? MODE_INIT : MODE_TRIAL);
-            __syncthreads();
-            all_done &= s_ctl[bb].done != 0;
-        }
-        if (all_done) break;
-    }
-    if (primary && tid < B) a.ctl[tid] = s_ctl[tid];
 }

@@ -204,7 +204,7 @@ __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uin
 
 // One trial (TRIAL) or evaluation pass of this CTA's tile: stage the trial point, the 18-block tensor-core
 // loop, the fold; thread 0 publishes the tile's fp64 partials in buffer `pbuf` of a.partials.  ctl: the
-// image's control block (global or a resident copy; null in MODE_EVAL); rpar: phase parity of the
+// image's control block (null in MODE_EVAL); rpar: phase parity of the
 // once-per-pass ring mbarriers; take_ticket: thread 0 then takes the image's ticket (the last CTA reduces
 // and decides).  Returns -1, before touching shared state, if the image is done; else thread 0's ticket.
 template <int NF, bool TRIAL, bool SYM>
@@ -755,73 +755,4 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             a.ctl[b] = c;
         }
     }
-}
-
-// ------------------------------------------------------------------------------------------------
-// k_solve_resident_tc: the whole solve of a batch whose (image, tile) CTAs are all co-resident (one per
-// SM; a 512^2 image is 144) in one cooperative launch.  Per pass: the tile body (the init evaluation,
-// then trial passes), a grid barrier, and every CTA reduces each live image's tile partials in the fixed
-// order and takes the identical decision on its own copy of the control blocks (the primary CTA writes
-// the trace rows and the live count).  TMEM, barriers and B operands are set up once; the pass-to-pass
-// hand-off is a barrier instead of a kernel boundary (no launch, no programmatic-dependency release,
-// no single deciding CTA on the critical path).  Partials are double-buffered by pass parity.
-
-// the per-pass decision of the resident solve, kept out of line (the pass body needs every register)
-__device__ __noinline__ bool resident_decide(const PassArgs &a, const double *parts, int ntiles, double (*red)[kNumPartials],
-                                             double *s_sum, ImgCtl *s_ctl, bool primary, bool init) {
-    constexpr int NT = TcCfg<32>::NT;
-    bool all_done = true;
-    for (int bb = 0; bb < a.B; ++bb) {
-        if (s_ctl[bb].done) continue;
-        reduce_tiles<NT>(parts, ntiles, a.B, bb, red, s_sum);
-        if (threadIdx.x == 0) decide_ctl(a, bb, s_sum, s_ctl[bb], primary, init ? MODE_INIT : MODE_TRIAL);
-        __syncthreads();
-        all_done &= s_ctl[bb].done != 0;
-    }
-    return all_done;
-}
-
-template <int NF, bool SYM>
-__global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_solve_resident_tc(const PassArgs a) {
-    using T = TcCfg<32>;
-    constexpr int NT = T::NT, NBLK = T::NBLK;
-    extern __shared__ __align__(128) float sm[];
-    __shared__ double red[NT / 32][kNumPartials];
-    __shared__ double s_sum[kNumPartials];
-    __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) unsigned long long mb_dfull[T::NDREG], mb_yfull[T::NDREG];
-    __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK];
-    __shared__ ImgCtl s_ctl[kResidentMaxB];
-
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int b = blockIdx.y, B = a.B;
-    const bool primary = blockIdx.x == 0 && blockIdx.y == 0;
-    const unsigned nblocks = gridDim.x * gridDim.y;
-    const int ntiles = a.tiles_x * a.tiles_y;
-    unsigned gen = 0;
-    if (tid == 0) gen = ld_acquire_gpu(a.grid_bar + 1);
-    const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
-    const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
-    const TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_ring, mb_sum);
-    tc_setup<NF>(a, S, &s_tmem);
-    if (tid < B) s_ctl[tid] = a.ctl[tid];
-    __syncthreads();
-    if (tid == 0 && s_tmem != 0u) __trap();
-    for (int pass = 0;; ++pass) {
-        const bool init = pass == 0;
-        const int pbuf = pass & 1;
-        if (!s_ctl[b].done) {
-            if (init)
-                tc_body<NF, false, SYM>(a, S, g, &s_ctl[b], (unsigned)pbuf, pbuf, false, 0, nullptr);
-            else
-                tc_body<NF, true, SYM>(a, S, g, &s_ctl[b], (unsigned)pbuf, pbuf, false, 0, nullptr);
-        }
-        grid_barrier(a.grid_bar, nblocks, gen);
-        if (resident_decide(a, a.partials + (size_t)pbuf * ntiles * B * kPartialStride, ntiles, red, s_sum, s_ctl,
-                            primary, init))
-            break;
-    }
-    __syncthreads();
-    if (warp == 0) tmem_dealloc(0u, 512);
-    if (primary && tid < B) a.ctl[tid] = s_ctl[tid];
 }

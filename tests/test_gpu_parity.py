@@ -278,28 +278,6 @@ def test_row_bands_equal_single_device_bitwise(n_bands, H, W, iters):
     assert torch.equal(u[0], single.u)
 
 
-@pytest.mark.parametrize("shape,peak,variant", [((512, 512), 1.0, "transform"), ((200, 136), 2.0, "transform"),
-                                                ((130, 97), 8.0, "direct")])
-def test_resident_solver_equals_per_pass_launches_bitwise(monkeypatch, shape, peak, variant):
-    """The single cooperative launch (state resident in smem, grid barrier per pass) reproduces the
-    per-pass launch path bit for bit, trace included."""
-    import dataclasses
-    model = fp.load_packaged_model("foe_a")
-    if variant == "direct":
-        model = dataclasses.replace(model, domain_tag="original")
-    _, y = make_counts(*shape, 11, peak)
-    req = fp.DenoiseRequest(noisy=y, peak=peak, model=model, variant=variant)
-    cfg = fp.SolverConfig(rel_tol=0.0)
-    monkeypatch.setenv("FOE_TC", "0")  # the resident solver is the FFMA formulation
-    monkeypatch.setenv("FOE_RESIDENT", "0")
-    a = fp.denoise(req, cfg)
-    monkeypatch.setenv("FOE_RESIDENT", "1")
-    b = fp.denoise(req, cfg)
-    np.testing.assert_array_equal(a.image, b.image)
-    assert a.trace.L == b.trace.L and a.trace.F == b.trace.F and a.trace.G == b.trace.G
-    assert a.trace.n_trials == b.trace.n_trials
-
-
 def test_transform_binned_vs_reference_golden(golden):
     """transform_binned on the device (bin3 / unbin kernels around the solve) vs the reference output."""
     g = golden("binned")

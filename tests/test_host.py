@@ -156,3 +156,44 @@ def test_training_host_validation():
         tr.TrainConfig(objective="nope")
     with pytest.raises(ValueError):
         tr._check_domain(fp.load_packaged_model("foe_a"), "original_domain")
+
+
+def test_request_accepts_strided_views():
+    """Non-contiguous inputs (flipped / transposed views, as the reference accepts) are validated on a
+    buffer that outlives the native check -- no use-after-free of a temporary copy (large enough that a
+    freed block would be returned to the OS)."""
+    m = fp.load_packaged_model("foe_a")
+    y = np.zeros((3000, 2000))
+    y[5, 7] = 3.0
+    for view in (y[::-1], y.T, y[:, ::2]):
+        r = fp.DenoiseRequest(noisy=view, peak=1.0, model=m, variant="transform")
+        assert r.noisy.flags.c_contiguous
+        np.testing.assert_array_equal(r.noisy, view)
+    bad = y.copy()
+    bad[-1, -1] = 0.5
+    with pytest.raises(ValueError):
+        fp.DenoiseRequest(noisy=bad.T, peak=1.0, model=m, variant="transform")
+
+
+def test_cli_exit_codes_without_a_gpu(tmp_path, capsys):
+    """cli.py:28-31, 244-257: 1 usage (bad flags, invalid arguments), 2 data (missing / malformed
+    files).  The numerical-failure code 3 needs a solve and is covered in the GPU suite."""
+    from paper_1609_05722_b200.__main__ import EXIT_DATA, EXIT_USAGE, main
+    with pytest.raises(SystemExit) as e:
+        main(["denoise", "a.npy", "b.npy", "--bogus"])
+    assert e.value.code == EXIT_USAGE
+    with pytest.raises(SystemExit) as e:
+        main(["nope"])
+    assert e.value.code == EXIT_USAGE
+    assert main(["denoise", str(tmp_path / "missing.npy"), str(tmp_path / "o.npy"), "--peak", "1"]) == EXIT_DATA
+    (tmp_path / "junk.npy").write_bytes(b"not an npy file")
+    assert main(["denoise", str(tmp_path / "junk.npy"), str(tmp_path / "o.npy"), "--peak", "1"]) == EXIT_DATA
+    np.save(tmp_path / "vec.npy", np.zeros(5))
+    assert main(["denoise", str(tmp_path / "vec.npy"), str(tmp_path / "o.npy"), "--peak", "1"]) == EXIT_DATA
+    (tmp_path / "bad.foe").write_text("FOE 1\nanscombe 1 5\n")
+    np.save(tmp_path / "y.npy", np.ones((8, 8)))
+    assert main(["denoise", str(tmp_path / "y.npy"), str(tmp_path / "o.npy"), "--peak", "1",
+                 "--model", str(tmp_path / "bad.foe")]) == EXIT_DATA
+    np.save(tmp_path / "neg.npy", -np.ones((8, 8)))  # invalid counts: a usage-class ValueError
+    assert main(["denoise", str(tmp_path / "neg.npy"), str(tmp_path / "o.npy"), "--peak", "1"]) == EXIT_USAGE
+    assert main(["denoise", str(tmp_path / "y.npy"), str(tmp_path / "o.npy"), "--peak", "0"]) == EXIT_USAGE
