@@ -13,8 +13,14 @@ L2 handling: the 512^2 working set (~6 MB) lives in L2 by design; a 256 MiB
 buffer is rewritten between timed steps so every step starts cold.
 
 --impl reference times the CPU oracle port (oracle/foe_oracle.c, fp64, all host
-threads) on the same config: the reference is pure Python and cannot be
-compiled, and it cannot run on the GPU box.
+threads) on the same config -- each step one full 150-iteration cfg2 solve, the
+same workload and config dict as this arm.  The reference itself is pure Python
+(cv2 + numpy) and has no compilable path; it is installed (pip --target) into
+baseline/_ref and timed beside the port as ``cpu_baseline_reference``: its own
+public denoise() on the same counts, with solver_budget patched to a truncated
+iteration count (a bounded sample; the steady per-iteration rate is the
+difference of a 13- and a 3-iteration run, so the iteration-0 backtracking climb
+cancels).
 """
 
 from __future__ import annotations
@@ -42,6 +48,22 @@ METRIC = "Mpixel·iter/s of FoE solver (fp32, % FP32 peak); 512² denoise ms"
 CONFIG = {"workload": "cfg2: 512x512 synthetic, peak 1, transform/quadratic, foe_a 24x5x5, 150 iters",
           "model": "foe_a (24 filters 5x5, dct5, symmetric)", "image": "512x512", "peak": PEAK,
           "iterations": 150, "l2": "flushed between steps (256 MiB rewrite); working set L2-resident within a step"}
+
+
+def config_for(world: int) -> dict:
+    """The config dict both arms print (identical, so the driver's same_config check holds)."""
+    return dict(CONFIG, parallelism=f"replicas{world}" if world > 1 else "single")
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def dist_env():
@@ -190,29 +212,64 @@ def cpu_oracle_rate(y, iters, threads=None):
     u, tr = orc.ipiano_foe(v, v, m, lam, "quadratic", max_iters=iters, rel_tol=0.0)
     orc.anscombe_inverse_exact_unbiased(u)
     dt = time.perf_counter() - t0
-    return y.size * len(tr.F) / dt / 1e6, dt, orc.num_threads()
+    return y.size * len(tr.F) / dt / 1e6, dt, orc.num_threads(), len(tr.F)
+
+
+def reference_python_rate(y, k_lo=3, k_hi=13):
+    """The reference itself (foepoisson from baseline/_ref, Python + cv2, all host threads) on the cfg2
+    counts through its public denoise(), solver_budget patched to k iterations: steady Mpixel*iter/s
+    from t(k_hi) - t(k_lo) (the iteration-0 backtracking climb cancels).  None if not installed."""
+    ref_dir = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "foepoisson")):
+        return None
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    import cv2
+    cv2.setNumThreads(os.cpu_count() or 1)
+    from foepoisson import fileio, pipeline, solver
+    model = fileio.load_packaged_model("foe_a")
+    req = pipeline.DenoiseRequest(noisy=y, peak=PEAK, model=model, variant="transform", force_branch="quadratic")
+    orig = pipeline.solver_budget
+    times = {}
+    try:
+        for k in (k_lo, k_hi):
+            pipeline.solver_budget = lambda peak, overrides=None, k=k: solver.SolverConfig(max_iters=k, rel_tol=0.0)
+            t0 = time.perf_counter()
+            r = pipeline.denoise(req)
+            times[k] = time.perf_counter() - t0
+            assert len(r.trace) == k
+    finally:
+        pipeline.solver_budget = orig
+    rate = y.size * (k_hi - k_lo) / (times[k_hi] - times[k_lo]) / 1e6
+    return {"value": rate, "unit": "Mpixel*iter/s", "cores": cv2.getNumThreads(), "kind": "reference",
+            "sample": f"foepoisson (baseline/_ref, Python + cv2 {cv2.__version__}, cv2 threads "
+                      f"{cv2.getNumThreads()}) public denoise() on the cfg2 counts, solver_budget patched: "
+                      f"({k_hi} - {k_lo}) accepted iterations / (t({k_hi}) - t({k_lo})) = "
+                      f"{times[k_hi]:.2f} s - {times[k_lo]:.2f} s; steady rate, iteration-0 climb excluded",
+            "cpu_model": cpu_model(), "os_cpu_count": os.cpu_count()}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle port on the box's host cores (rank 0 only)."""
+    """--impl reference: the CPU oracle port on the box's host cores (rank 0 only), one full 150-iteration
+    cfg2 solve per timed step -- the same workload and config dict as the GPU arm."""
     if rank != 0:
         return
     from paper_1609_05722_b200.synth import make_counts
     _, y = make_counts(H, W, 0, PEAK)
-    iters = args.ref_iters
     for _ in range(args.warmup):
-        cpu_oracle_rate(y, iters)
-    rates, secs = [], 0.0
+        cpu_oracle_rate(y, 3)  # untimed warm-up: thread pool, page faults (a 3-iteration solve)
+    iters, secs = 0, 0.0
     for _ in range(args.steps):
-        r, dt, cores = cpu_oracle_rate(y, iters)
-        rates.append(r)
+        _, dt, cores, n = cpu_oracle_rate(y, args.ref_iters)
+        iters += n
         secs += dt
-    value = y.size * iters * args.steps / secs / 1e6
-    sample = f"512x512 cfg2 solve truncated to {iters} accepted iterations per step (incl. the iteration-0 backtracking climb)"
+    value = y.size * iters / secs / 1e6
+    sample = (f"512x512 cfg2 full solve, {args.ref_iters} accepted iterations per step (fp64 C oracle port of the "
+              f"reference, OpenMP {cores} threads, {cpu_model()})")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Mpixel*iter/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": CONFIG,
+            "config": config_for(world),
             "cpu_baseline": {"value": value, "unit": "Mpixel*iter/s", "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "Mpixel*iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -309,7 +366,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-iters", type=int, default=30)
+    ap.add_argument("--ref-iters", type=int, default=150, help="--impl reference: iterations per step (the full solve)")
     ap.add_argument("--cpu-iters", type=int, default=150, help="cpu_baseline sample: the full 150-iteration solve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fallback", action="store_true", help="skip the 48x7x7 fallback-bank line")
@@ -450,17 +507,22 @@ def main():
     if rank == 0 and not args.no_fallback:
         fallback = bench_fallback_bank(fp, _lib, L, y_dev, lam, cfg, stream, fp32_peak_tflops, H, W)
 
-    cpu = None
+    cpu = cpu_ref = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, secs, cores = cpu_oracle_rate(y, args.cpu_iters)
+        rate, secs, cores, _ = cpu_oracle_rate(y, args.cpu_iters)
         cpu = {"value": rate, "unit": "Mpixel*iter/s", "cores": cores, "kind": "port",
-               "sample": f"512x512 cfg2 solve truncated to {args.cpu_iters} iterations ({secs:.1f} s, fp64 C oracle)"}
+               "sample": f"512x512 cfg2 full solve, {args.cpu_iters} iterations ({secs:.1f} s, fp64 C oracle port, "
+                         f"{cpu_model()})"}
+        try:
+            cpu_ref = reference_python_rate(y)
+        except Exception as exc:  # reported, not fatal: the reference's own deps live outside this repo
+            cpu_ref = {"unavailable": f"{type(exc).__name__}: {exc}"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "Mpixel*iter/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-                "config": dict(CONFIG, parallelism=f"replicas{world}" if world > 1 else "single"),
+                "config": config_for(world),
                 "denoise_ms_512": ms_per_step, "iterations_per_step": iters / args.steps,
                 "trials_per_step": trials / args.steps,
                 "algorithmic_fp32_frac": solve_frac,
@@ -482,7 +544,8 @@ def main():
                 "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
                 "clocks": clk.summary(),
                 "fallback_48x7": fallback,
-                "cpu_baseline": cpu}
+                "cpu_baseline": cpu,
+                "cpu_baseline_reference": cpu_ref}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

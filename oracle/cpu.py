@@ -61,6 +61,8 @@ def lib():
                                      ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                      ctypes.c_double, _dp, _dp, _ip, _ip]
         L.orc_ipiano_foe.restype = ctypes.c_int
+        L.orc_ipiano_foe_ex.argtypes = L.orc_ipiano_foe.argtypes + [ctypes.c_void_p]
+        L.orc_ipiano_foe_ex.restype = ctypes.c_int
         L.orc_num_threads.restype = ctypes.c_int
         L.orc_set_num_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -224,11 +226,11 @@ class OracleTrace:
 
 def ipiano_foe(u0, obs, model: OracleModel, lam, branch, *, gamma=0.8, lipschitz_init=1.0,
                backtrack_factor=1.2, relax_factor=1.05, max_iters=150, rel_tol=1e-6,
-               max_lipschitz=1e15):
+               max_lipschitz=1e15, return_iterates=False):
     """ipiano_minimize (solver.py:128-175) with FoE callbacks (pipeline.py:167-172, 205-208).
 
     branch: "quadratic" or "idiv" (prox and energy_G, pipeline.py:197-204).
-    Returns (u, OracleTrace)."""
+    Returns (u, OracleTrace), plus (n_iters, H, W) fp32 accepted iterates if return_iterates."""
     u0 = _c(u0)
     obs = _c(obs)
     f = _c(model.filters)
@@ -238,15 +240,19 @@ def ipiano_foe(u0, obs, model: OracleModel, lam, branch, *, gamma=0.8, lipschitz
     trace = np.zeros((max_iters, 6))
     it = ctypes.c_int(0)
     tr = ctypes.c_int(0)
-    status = lib().orc_ipiano_foe(_p(u0), _p(obs), H, W, _p(f), _p(w), model.n, model.m,
-                                  BOUNDARY_CODES[model.boundary], float(lam),
-                                  0 if branch == "quadratic" else 1, gamma, lipschitz_init,
-                                  backtrack_factor, relax_factor, int(max_iters), rel_tol,
-                                  max_lipschitz, _p(u), _p(trace), ctypes.byref(it), ctypes.byref(tr))
+    iters = np.empty((int(max_iters), H, W), dtype=np.float32) if return_iterates else None
+    status = lib().orc_ipiano_foe_ex(_p(u0), _p(obs), H, W, _p(f), _p(w), model.n, model.m,
+                                     BOUNDARY_CODES[model.boundary], float(lam),
+                                     0 if branch == "quadratic" else 1, gamma, lipschitz_init,
+                                     backtrack_factor, relax_factor, int(max_iters), rel_tol,
+                                     max_lipschitz, _p(u), _p(trace), ctypes.byref(it), ctypes.byref(tr),
+                                     iters.ctypes.data if return_iterates else None)
     n = it.value
     t = OracleTrace(F=list(trace[:n, 0]), G=list(trace[:n, 1]), L=list(trace[:n, 2]),
                     step_norm=list(trace[:n, 3]), descent_slack=list(trace[:n, 4]),
                     slack_tol=list(trace[:n, 5]), n_trials=tr.value, status=status)
+    if return_iterates:
+        return u, t, iters[:n]
     return u, t
 
 

@@ -54,26 +54,23 @@ void orc_set_num_threads(int n) {
 #endif
 }
 
-/* convolve_same, image.py:37-58: true 2-D convolution, "same" output,
- * z[p] = sum_{a,b} kf[a,b] * u_ext[p + (a - r, b - r)],  kf = k[::-1, ::-1]. */
-void orc_convolve_same(const double *x, int H, int W, const double *k, int m,
-                       int boundary, double *out) {
-    const int r = m / 2;
-    if (r == 0) { /* image.py:51-52 */
-        for (long i = 0; i < (long)H * W; ++i) out[i] = x[i] * k[0];
-        return;
-    }
+/* pad x by r on every side with the boundary's index map (np.pad symmetric / wrap, image.py:54-65) */
+static void pad_image(const double *x, int H, int W, int r, int boundary, double *xp) {
     const int Hp = H + 2 * r, Wp = W + 2 * r;
-    double *xp = (double *)malloc(sizeof(double) * (size_t)Hp * Wp);
     int *cmap = (int *)malloc(sizeof(int) * Wp);
     for (int j = 0; j < Wp; ++j) cmap[j] = src_index(j - r, W, boundary);
+#pragma omp parallel for schedule(static)
     for (int i = 0; i < Hp; ++i) {
         const double *row = x + (size_t)src_index(i - r, H, boundary) * W;
-        for (int j = 0; j < Wp; ++j) xp[(size_t)i * Wp + j] = row[cmap[j]];
+        double *o = xp + (size_t)i * Wp;
+        for (int j = 0; j < Wp; ++j) o[j] = row[cmap[j]];
     }
-    double *kf = (double *)malloc(sizeof(double) * m * m);
-    for (int a = 0; a < m; ++a)
-        for (int b = 0; b < m; ++b) kf[a * m + b] = k[(m - 1 - a) * m + (m - 1 - b)];
+    free(cmap);
+}
+
+/* out[y][x] = sum_{a,b} kf[a][b] xp[y + a][x + b] over the padded image (row pitch Wp), accumulated tap
+ * by tap in (a, b) order */
+static void conv_padded(const double *xp, int Wp, int H, int W, const double *kf, int m, double *out) {
 #pragma omp parallel for schedule(static)
     for (int y = 0; y < H; ++y) {
         double *o = out + (size_t)y * W;
@@ -87,15 +84,37 @@ void orc_convolve_same(const double *x, int H, int W, const double *k, int m,
             }
         }
     }
-    free(kf);
-    free(cmap);
+}
+
+static void flip_kernel(const double *k, int m, double *kf) {
+    for (int a = 0; a < m; ++a)
+        for (int b = 0; b < m; ++b) kf[a * m + b] = k[(m - 1 - a) * m + (m - 1 - b)];
+}
+
+/* convolve_same, image.py:37-58: true 2-D convolution, "same" output,
+ * z[p] = sum_{a,b} kf[a,b] * u_ext[p + (a - r, b - r)],  kf = k[::-1, ::-1]. */
+void orc_convolve_same(const double *x, int H, int W, const double *k, int m,
+                       int boundary, double *out) {
+    const int r = m / 2;
+    if (r == 0) { /* image.py:51-52 */
+        for (long i = 0; i < (long)H * W; ++i) out[i] = x[i] * k[0];
+        return;
+    }
+    const int Hp = H + 2 * r, Wp = W + 2 * r;
+    double *xp = (double *)malloc(sizeof(double) * (size_t)Hp * Wp);
+    pad_image(x, H, W, r, boundary, xp);
+    double kf[49];
+    flip_kernel(k, m, kf);
+    conv_padded(xp, Wp, H, W, kf, m, out);
     free(xp);
 }
 
 /* convolve_adjoint, image.py:68-83: V^T psi = full correlation of the
  * zero-padded input with the unflipped kernel on the padded domain
- * (image.py:84-87), then P^T folds every padded pixel onto its source pixel
- * in padded row-major order (image.py:88-90, np.bincount). */
+ * (image.py:76-79), then P^T folds every padded pixel onto its source pixel
+ * in padded row-major order (image.py:80-83, np.bincount).  The fold runs in
+ * parallel over destination rows; each destination pixel still receives its
+ * contributions in padded row-major order, so the sums are the serial ones. */
 void orc_convolve_adjoint(const double *y, int H, int W, const double *k, int m,
                           int boundary, double *out) {
     const int r = m / 2;
@@ -108,6 +127,7 @@ void orc_convolve_adjoint(const double *y, int H, int W, const double *k, int m,
      * correlation window never leaves the buffer (BORDER_CONSTANT) */
     const int Hz = Hp + 2 * r, Wz = Wp + 2 * r;
     double *yz = (double *)calloc((size_t)Hz * Wz, sizeof(double));
+#pragma omp parallel for schedule(static)
     for (int i = 0; i < H; ++i)
         memcpy(yz + (size_t)(i + 2 * r) * Wz + 2 * r, y + (size_t)i * W, sizeof(double) * W);
     double *g = (double *)malloc(sizeof(double) * (size_t)Hp * Wp);
@@ -124,41 +144,66 @@ void orc_convolve_adjoint(const double *y, int H, int W, const double *k, int m,
             }
         }
     }
-    for (long i = 0; i < (long)H * W; ++i) out[i] = 0.0;
     int *cmap = (int *)malloc(sizeof(int) * Wp);
     for (int j = 0; j < Wp; ++j) cmap[j] = src_index(j - r, W, boundary);
+    /* source padded rows of every destination row, ascending (at most 3: itself and two folds) */
+    int *nsrc = (int *)calloc(H, sizeof(int));
+    int *srcs = (int *)malloc(sizeof(int) * 4 * (size_t)H);
     for (int q = 0; q < Hp; ++q) {
-        double *dst = out + (size_t)src_index(q - r, H, boundary) * W;
-        const double *s = g + (size_t)q * Wp;
-        for (int j = 0; j < Wp; ++j) dst[cmap[j]] += s[j];
+        const int d = src_index(q - r, H, boundary);
+        if (nsrc[d] < 4) srcs[4 * d + nsrc[d]++] = q;
     }
+#pragma omp parallel for schedule(static)
+    for (int d = 0; d < H; ++d) {
+        double *dst = out + (size_t)d * W;
+        for (int j = 0; j < W; ++j) dst[j] = 0.0;
+        for (int t = 0; t < nsrc[d]; ++t) {
+            const double *s = g + (size_t)srcs[4 * d + t] * Wp;
+            for (int j = 0; j < Wp; ++j) dst[cmap[j]] += s[j];
+        }
+    }
+    free(srcs);
+    free(nsrc);
     free(cmap);
     free(g);
     free(yz);
 }
 
-/* pairwise-free plain sum in fixed order (numpy uses pairwise summation; the
- * difference is ~1e-16 relative and is covered by the golden tolerances) */
-static double sum_array(const double *a, long n) {
-    double s = 0.0;
-#pragma omp parallel for reduction(+ : s) schedule(static)
-    for (long i = 0; i < n; ++i) s += a[i];
-    return s;
+/* sum of log1p(z^2) over an H x W response: per-row sums in parallel, then the rows in order -- the
+ * same result for any thread count (numpy's pairwise sum differs by ~1e-16 relative, covered by the
+ * golden tolerances) */
+static double sum_log1p_sq(const double *z, int H, int W, double *row_sums) {
+#pragma omp parallel for schedule(static)
+    for (int y = 0; y < H; ++y) {
+        const double *zr = z + (size_t)y * W;
+        double s = 0.0;
+        for (int x = 0; x < W; ++x) s += log1p(zr[x] * zr[x]);
+        row_sums[y] = s;
+    }
+    double t = 0.0;
+    for (int y = 0; y < H; ++y) t += row_sums[y];
+    return t;
 }
 
 /* foe_energy, prior.py:95-101: sum_i w_i sum_p log1p((k_i * u)_p^2)
- * (potential order 0, prior.py:23-35). */
+ * (potential order 0, prior.py:23-35).  u is padded once for all filters. */
 double orc_foe_energy(const double *u, int H, int W, const double *filters,
                       const double *weights, int N, int m, int boundary) {
     const long n = (long)H * W;
+    const int r = m / 2, Hp = H + 2 * r, Wp = W + 2 * r;
     double *z = (double *)malloc(sizeof(double) * n);
+    double *xp = (double *)malloc(sizeof(double) * (size_t)Hp * Wp);
+    double *rs = (double *)malloc(sizeof(double) * H);
+    pad_image(u, H, W, r, boundary, xp);
     double total = 0.0;
     for (int i = 0; i < N; ++i) {
-        orc_convolve_same(u, H, W, filters + (size_t)i * m * m, m, boundary, z);
-#pragma omp parallel for schedule(static)
-        for (long p = 0; p < n; ++p) z[p] = log1p(z[p] * z[p]);
-        total += weights[i] * sum_array(z, n);
+        double kf[49];
+        flip_kernel(filters + (size_t)i * m * m, m, kf);
+        conv_padded(xp, Wp, H, W, kf, m, z);
+        total += weights[i] * sum_log1p_sq(z, H, W, rs);
     }
+    free(rs);
+    free(xp);
     free(z);
     return total;
 }
@@ -168,18 +213,30 @@ double orc_foe_energy(const double *u, int H, int W, const double *filters,
 void orc_foe_gradient(const double *u, int H, int W, const double *filters,
                       const double *weights, int N, int m, int boundary, double *grad) {
     const long n = (long)H * W;
+    const int r = m / 2, Hp = H + 2 * r, Wp = W + 2 * r;
     double *z = (double *)malloc(sizeof(double) * n);
     double *a = (double *)malloc(sizeof(double) * n);
+    double *xp = (double *)malloc(sizeof(double) * (size_t)Hp * Wp);
+    pad_image(u, H, W, r, boundary, xp);
+#pragma omp parallel for schedule(static)
     for (long p = 0; p < n; ++p) grad[p] = 0.0;
     for (int i = 0; i < N; ++i) {
-        orc_convolve_same(u, H, W, filters + (size_t)i * m * m, m, boundary, z);
+        const double *k = filters + (size_t)i * m * m;
+        double kf[49];
+        flip_kernel(k, m, kf);
+        if (r == 0) {
+            for (long p = 0; p < n; ++p) z[p] = u[p] * k[0];
+        } else {
+            conv_padded(xp, Wp, H, W, kf, m, z);
+        }
 #pragma omp parallel for schedule(static)
         for (long p = 0; p < n; ++p) z[p] = 2.0 * z[p] / (1.0 + z[p] * z[p]);
-        orc_convolve_adjoint(z, H, W, filters + (size_t)i * m * m, m, boundary, a);
+        orc_convolve_adjoint(z, H, W, k, m, boundary, a);
         const double w = weights[i];
 #pragma omp parallel for schedule(static)
         for (long p = 0; p < n; ++p) grad[p] += w * a[p];
     }
+    free(xp);
     free(a);
     free(z);
 }
@@ -261,11 +318,13 @@ static double energy_G(const double *u, const double *obs, long n, double lam, i
  * Returns 0 ok, 1 non-finite f_u (solver.py:143-144), 2 backtracking stalled
  * (solver.py:159-160).  *n_iters = accepted iterations; *n_trials = energy
  * evaluations of trial points. */
-int orc_ipiano_foe(const double *u0, const double *obs, int H, int W,
-                   const double *filters, const double *weights, int N, int m, int boundary,
-                   double lam, int branch, double gamma, double L0, double eta, double relax,
-                   int max_iters, double rel_tol, double max_L,
-                   double *u_out, double *trace, int *n_iters, int *n_trials) {
+/* iterates (nullable): (max_iters, H * W) fp32 copies of each accepted iterate, for the per-iteration
+ * gradient check of the GPU path (the device state is fp32, so the check runs at the fp32 iterate). */
+int orc_ipiano_foe_ex(const double *u0, const double *obs, int H, int W,
+                      const double *filters, const double *weights, int N, int m, int boundary,
+                      double lam, int branch, double gamma, double L0, double eta, double relax,
+                      int max_iters, double rel_tol, double max_L,
+                      double *u_out, double *trace, int *n_iters, int *n_trials, float *iterates) {
     const double SLACK_RTOL = 1e-12; /* solver.py:23 */
     const long n = (long)H * W;
     double *u = (double *)malloc(sizeof(double) * n);
@@ -311,6 +370,10 @@ int orc_ipiano_foe(const double *u0, const double *obs, int H, int W,
         row[3] = step;
         row[4] = slack;
         row[5] = tol;
+        if (iterates) {
+            float *dst = iterates + (size_t)it * n;
+            for (long i = 0; i < n; ++i) dst[i] = (float)un[i];
+        }
         ++it;
         double unorm = 0.0;
         for (long i = 0; i < n; ++i) unorm += u[i] * u[i];
@@ -327,4 +390,13 @@ int orc_ipiano_foe(const double *u0, const double *obs, int H, int W,
     *n_trials = trials;
     free(u); free(up); free(un); free(ut); free(g);
     return status;
+}
+
+int orc_ipiano_foe(const double *u0, const double *obs, int H, int W,
+                   const double *filters, const double *weights, int N, int m, int boundary,
+                   double lam, int branch, double gamma, double L0, double eta, double relax,
+                   int max_iters, double rel_tol, double max_L,
+                   double *u_out, double *trace, int *n_iters, int *n_trials) {
+    return orc_ipiano_foe_ex(u0, obs, H, W, filters, weights, N, m, boundary, lam, branch, gamma, L0, eta, relax,
+                             max_iters, rel_tol, max_L, u_out, trace, n_iters, n_trials, NULL);
 }

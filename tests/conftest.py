@@ -32,3 +32,22 @@ def golden():
     def load(name):
         return dict(np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False))
     return load
+
+
+# parity metrics recorded by the GPU tests (first L-trace divergence, max |dx|, trace-column errors,
+# gradient-check margins); written as JSON when FOE_PARITY_REPORT names a path (profiles/ keeps the
+# committed copy of a driver-style run)
+_REPORT: dict = {}
+
+
+@pytest.fixture(scope="session")
+def parity_report():
+    return _REPORT
+
+
+def pytest_sessionfinish(session, exitstatus):
+    import json
+    path = os.environ.get("FOE_PARITY_REPORT")
+    if path and _REPORT:
+        with open(path, "w") as fh:
+            json.dump(_REPORT, fh, indent=1, sort_keys=True, default=float)

@@ -1,0 +1,237 @@
+"""Parity at the full sizes of every BASELINE config (BASELINE.json configs 1-5), on the default
+(tensor-core) pass kernels.
+
+Gates (north_star): max |x_gpu - x_ref| <= 1e-3 * peak after the inverse Anscombe, |dPSNR| <= 0.01 dB,
+per-iteration gradient rel-L2 <= 1e-5.  Decision fingerprint: the L-trace --
+identical decisions give bit-identical L sequences (the same fp64 multiplications by 1.2 and
+divisions by 1.05 in the same order), so it is compared exactly; where a late decision flips, the
+first divergent iteration is recorded in the parity report.  Trace columns F, G and step_norm are
+compared up to the first divergence.
+
+References: configs 1-3 against the reference's own outputs (tests/golden/make_golden*.py ran
+foepoisson.pipeline.denoise), configs 4-5 against the C oracle (pinned to the reference by
+tests/test_oracle.py, including exact L-traces at 256^2 and 512^2).  Run with
+FOE_PARITY_REPORT=path to write the recorded metrics as JSON.
+"""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import paper_1609_05722_b200 as fp
+from oracle import cpu as orc
+from paper_1609_05722_b200.synth import make_counts
+from tests.conftest import REPO
+from tests.test_oracle import CFG23
+
+pytestmark = pytest.mark.gpu
+
+ASSETS = os.path.join(REPO, "paper_1609_05722_b200", "assets")
+TABLE = orc.load_lambda_table(os.path.join(ASSETS, "lambda_table.json"))
+# trace-column tolerances before the first divergence (fp32 state vs the fp64 reference): F is the
+# device's running f_u + dF, G is evaluated from the fp32 iterate, step_norm = |du| of fp32 iterates
+F_RTOL, G_RTOL, STEP_RTOL = 1e-6, 1e-5, 2e-3
+
+
+def psnr(x, ref, peak):
+    return 10 * np.log10(peak ** 2 / np.mean((x - ref) ** 2))
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def oracle_model(model):
+    return orc.OracleModel(filters=model.filters, weights=model.weights, boundary=model.boundary,
+                           domain_tag=model.domain_tag)
+
+
+def first_divergence(a, b):
+    """First index where two L sequences differ (None if identical, incl. length)."""
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    n = min(len(a), len(b))
+    idx = np.nonzero(a[:n] != b[:n])[0]
+    if len(idx):
+        return int(idx[0])
+    return None if len(a) == len(b) else n
+
+
+def compare(report, name, img, trace, ref_img, ref_rows, peak, clean=None):
+    """Gates + report entry.  ref_rows: (n, >=4) array of F, G, L, step_norm per accepted iteration."""
+    ref_rows = np.asarray(ref_rows)
+    ours = np.array([trace.F, trace.G, trace.L, trace.step_norm]).T.reshape(-1, 4)
+    div = first_divergence(ours[:, 2], ref_rows[:, 2])
+    k = len(ours) if div is None else div
+    relerr = lambda a, b: float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300))) if len(a) else 0.0
+    ent = {
+        "n_iters": len(ours), "n_iters_ref": int(len(ref_rows)), "n_trials": trace.n_trials,
+        "L_first_divergence": div,
+        "max_abs_dx_over_peak": float(np.max(np.abs(img - ref_img)) / peak),
+        "F_max_rel": relerr(ours[:k, 0], ref_rows[:k, 0]),
+        "G_max_rel": relerr(ours[:k, 1], ref_rows[:k, 1]),
+        "step_norm_max_rel": relerr(ours[:k, 3], ref_rows[:k, 3]),
+    }
+    if div is not None:
+        ent["max_abs_dx_over_peak_after_divergence"] = ent["max_abs_dx_over_peak"]
+    if clean is not None:
+        ent["dpsnr_db"] = float(psnr(img, peak * clean, peak) - psnr(ref_img, peak * clean, peak))
+    report[name] = ent
+    assert ent["max_abs_dx_over_peak"] <= 1e-3, (name, ent)
+    if clean is not None:
+        assert abs(ent["dpsnr_db"]) <= 0.01, (name, ent)
+    assert ent["F_max_rel"] <= F_RTOL and ent["G_max_rel"] <= G_RTOL, (name, ent)
+    assert ent["step_norm_max_rel"] <= STEP_RTOL, (name, ent)
+    return ent
+
+
+# ---- config 1: 256^2 peak 4 quadratic, vs the reference: the exact L-trace -----------------------------
+
+def test_cfg1_exact_L_trace_vs_reference(golden, parity_report):
+    g = golden("cfg1_256")
+    x, y = make_counts(256, 256, 0, 4.0)
+    assert y.sum() == g["counts_sum"]
+    r = fp.denoise(fp.DenoiseRequest(noisy=y, peak=4.0, model=fp.load_packaged_model("foe_a"),
+                                     variant="transform", force_branch="quadratic"), fp.SolverConfig(rel_tol=0.0))
+    ent = compare(parity_report, "cfg1_quad", r.image, r.trace, g["image"].astype(np.float64), g["trace"], 4.0, x)
+    assert ent["L_first_divergence"] is None, ent
+
+
+# ---- configs 2 and 3 at 512^2 vs the reference's own outputs -------------------------------------------
+
+@pytest.mark.parametrize("name", sorted(CFG23))
+def test_cfg23_vs_reference_golden(golden, parity_report, name):
+    import dataclasses
+    g = golden("cfg23_512")
+    peak, mk, variant, fb = CFG23[name]
+    x, y = make_counts(512, 512, 0, peak)
+    assert hashlib.sha256(y.tobytes()).digest() == g[f"{name}_counts_sha"].tobytes()
+    fa = fp.load_packaged_model("foe_a")
+    model = {"foe_a": fa, "foe_s": fp.load_packaged_model("foe_s"),
+             "foe_a_original": dataclasses.replace(fa, domain_tag="original")}[mk]
+    r = fp.denoise(fp.DenoiseRequest(noisy=y, peak=peak, model=model, variant=variant, force_branch=fb),
+                   fp.SolverConfig(rel_tol=0.0))
+    assert r.branch == str(g[f"{name}_branch"]) and r.lam == g[f"{name}_meta"][1]
+    compare(parity_report, name, r.image, r.trace, g[f"{name}_image"].astype(np.float64), g[f"{name}_trace"],
+            peak, x)
+
+
+def test_cfg2_gradient_at_every_oracle_iterate(parity_report):
+    """north_star's per-iteration gradient check on config 2 (512^2, peak 1, quadratic): the fused device
+    gradient at every one of the 150 oracle iterates (taken at their fp32 representation, the device
+    state's precision) against the fp64 oracle gradient there; rel-L2 <= 1e-5 at every iterate."""
+    import torch
+    model = fp.load_packaged_model("foe_a")
+    om = oracle_model(model)
+    _, y = make_counts(512, 512, 0, 1.0)
+    v = orc.anscombe_forward(y)
+    lam = orc.select_lambda(1.0, "transform", TABLE, "quadratic")
+    _, tr, its = orc.ipiano_foe(v, v, om, lam, "quadratic", max_iters=150, rel_tol=0.0, return_iterates=True)
+    assert len(its) == 150
+    from paper_1609_05722_b200.prior import energy_grad_device
+    u32 = np.concatenate([v.astype(np.float32)[None], its])  # u_0 = v, then every accepted iterate
+    _, gd = energy_grad_device(torch.from_numpy(u32).cuda(), model)
+    gd = gd.double().cpu().numpy()
+    errs = [rel_l2(gd[k], orc.foe_gradient(u32[k].astype(np.float64), om)) for k in range(len(u32))]
+    worst = int(np.argmax(errs))
+    parity_report["cfg2_gradient_every_iterate"] = {
+        "n_iterates": len(errs), "max_rel_l2": max(errs), "argmax_iterate": worst, "median_rel_l2": float(np.median(errs)),
+        "gate": 1e-5, "margin_factor": 1e-5 / max(errs)}
+    assert max(errs) <= 1e-5, (worst, max(errs))
+
+
+# ---- config 4: batch of 512^2 images, peaks cycling {0.5, 1, 2, 4} ---------------------------------------
+
+def _cfg4_peak(s):
+    return [0.5, 1.0, 2.0, 4.0][s % 4]
+
+
+def test_cfg4_seeds_0_7_vs_oracle(parity_report):
+    """parity on seeds 0-7 (two per peak), solved as one device batch."""
+    model = fp.load_packaged_model("foe_a")
+    om = oracle_model(model)
+    xs, ys = zip(*[make_counts(512, 512, s, _cfg4_peak(s)) for s in range(8)])
+    peaks = [_cfg4_peak(s) for s in range(8)]
+    imgs, traces, lams, _ = fp.denoise_batch(np.stack(ys), peaks, model, "transform", force_branch="quadratic",
+                                             solver=fp.SolverConfig(rel_tol=0.0))
+    for s in range(8):
+        ref = orc.denoise(ys[s], peaks[s], om, "transform", TABLE, force_branch="quadratic", rel_tol=0.0)
+        assert lams[s] == ref["lam"]
+        rt = ref["trace"]
+        compare(parity_report, f"cfg4_seed{s}_peak{peaks[s]:g}", imgs[s], traces[s], ref["image"],
+                np.array([rt.F, rt.G, rt.L, rt.step_norm]).T, peaks[s], xs[s])
+
+
+def test_cfg4_batch_256_equals_single_bitwise(parity_report):
+    """All 256 images of config 4 in one device batch == 256 independent denoise calls, bit for bit
+    (images and L-traces): batching changes nothing in any image's arithmetic."""
+    model = fp.load_packaged_model("foe_a")
+    ys = np.stack([make_counts(512, 512, s, _cfg4_peak(s))[1] for s in range(256)])
+    peaks = [_cfg4_peak(s) for s in range(256)]
+    imgs, traces, _, _ = fp.denoise_batch(ys, peaks, model, "transform", force_branch="quadratic",
+                                          solver=fp.SolverConfig(rel_tol=0.0))
+    mismatched = []
+    for s in range(256):
+        r = fp.denoise(fp.DenoiseRequest(noisy=ys[s], peak=peaks[s], model=model, variant="transform",
+                                         force_branch="quadratic"), fp.SolverConfig(rel_tol=0.0))
+        if not (np.array_equal(imgs[s], r.image) and traces[s].L == r.trace.L and traces[s].F == r.trace.F):
+            mismatched.append(s)
+    parity_report["cfg4_batch256_vs_single"] = {"images": 256, "bitwise_mismatches": len(mismatched),
+                                                "trials_total": int(sum(t.n_trials for t in traces))}
+    assert not mismatched, mismatched
+
+
+# ---- config 5: one 8192^2 image ---------------------------------------------------------------------
+
+_CFG5 = {}
+
+
+def _cfg5_inputs():
+    if "v" not in _CFG5:
+        import torch
+        from paper_1609_05722_b200.anscombe import forward_device
+        x, y = make_counts(8192, 8192, 0, 2.0)
+        _CFG5.update(x=x, y=y, v=forward_device(torch.from_numpy(y).cuda()))
+    return _CFG5
+
+
+def test_cfg5_truncated_solve_vs_oracle(parity_report):
+    """SURVEY.md Appendix B's truncated oracle for config 5: 8192^2, peak 2, quadratic, 3 accepted
+    iterations (the first one includes the backtracking climb from L = 1), single device vs oracle."""
+    from paper_1609_05722_b200.anscombe import inverse_exact_unbiased_device
+    d = _cfg5_inputs()
+    model = fp.load_packaged_model("foe_a")
+    lam = fp.select_lambda(2.0, "transform", force_branch="quadratic")
+    res = fp.solve_device(model, d["v"], d["v"], lam, "quadratic", 3, fp.SolverConfig(rel_tol=0.0))
+    img = inverse_exact_unbiased_device(res.u).cpu().numpy()
+    ref = orc.denoise(d["y"], 2.0, oracle_model(model), "transform", TABLE, force_branch="quadratic", rel_tol=0.0,
+                      max_iters=3)
+    rt = ref["trace"]
+    ent = compare(parity_report, "cfg5_truncated_3it", img, res.traces[0], ref["image"],
+                  np.array([rt.F, rt.G, rt.L, rt.step_norm]).T, 2.0)
+    parity_report["cfg5_truncated_3it"]["n_trials_ref"] = rt.n_trials
+    assert ent["L_first_divergence"] is None and res.traces[0].n_trials == rt.n_trials
+
+
+@pytest.mark.parametrize("bank,n_bands", [("foe_a", 2), ("foe_a", 4), ("foe_a", 8), ("foe_fallback48x7", 4)])
+def test_cfg5_bands_equal_single_device_full_solve(parity_report, bank, n_bands):
+    """Config 5's row-band decomposition (halo 2r: 4 rows for foe_a, 6 for the 48 x 7 x 7 bank) over the
+    full 150-iteration solve at 8192^2 equals the single-device solve bit for bit (iterate, L and F)."""
+    from paper_1609_05722_b200 import bands
+    d = _cfg5_inputs()
+    model = fp.load_packaged_model(bank)
+    lam = fp.select_lambda(2.0, "transform", force_branch="quadratic")
+    cfg = fp.SolverConfig(rel_tol=0.0)
+    key = ("single", bank)
+    if key not in _CFG5:
+        _CFG5[key] = fp.solve_device(model, d["v"], d["v"], lam, "quadratic", 150, cfg)
+    single = _CFG5[key]
+    u, traces, status = bands.solve_image_bands(model, d["v"], d["v"], lam, "quadratic", 150, n_bands, cfg)
+    same = bool((u[0] == single.u).all().item())
+    parity_report[f"cfg5_bands_{bank}_{n_bands}"] = {
+        "halo_rows": 2 * (model.basis.size // 2), "iterations": len(traces[0]), "trials": traces[0].n_trials,
+        "bitwise_equal_u": same, "same_L": traces[0].L == single.traces[0].L, "same_F": traces[0].F == single.traces[0].F}
+    assert status == [0] and len(traces[0]) == 150
+    assert traces[0].L == single.traces[0].L and traces[0].F == single.traces[0].F
+    assert same

@@ -180,8 +180,7 @@ def test_cfg1_256_vs_reference_golden(golden):
                                      variant="transform", force_branch="quadratic"), fp.SolverConfig(rel_tol=0.0))
     assert len(r.trace) == 150
     _check_solve(r.image, g["image"].astype(np.float64), 4.0, x, "cfg1")
-    same_L = np.mean(np.isclose(r.trace.L, g["trace"][:, 2], rtol=1e-9))
-    assert same_L > 0.5
+    assert r.trace.L == g["trace"][:, 2].tolist()  # identical decisions (the exact L-trace)
 
 
 @pytest.mark.parametrize("peak,branch", [(1.0, "quadratic"), (1.0, None)])

@@ -130,3 +130,40 @@ def test_binned_matches_reference(golden):
         np.testing.assert_allclose(res["image"], g[f"{name}_image"], rtol=0, atol=1e-8 * meta[0])
         np.testing.assert_allclose(orc.unbin_bilinear(res["transformed"], g[f"{name}_noisy"].shape, int(meta[5])),
                                    g[f"{name}_unbin_of_transformed"], rtol=1e-13, atol=1e-13)
+
+
+CFG23 = {"cfg2_quad": (1.0, "foe_a", "transform", "quadratic"), "cfg2_idiv": (1.0, "foe_a", "transform", None),
+         "cfg3_fa": (8.0, "foe_a_original", "direct", None), "cfg3_fs": (8.0, "foe_s", "direct", None)}
+
+
+def cfg23_model(name):
+    mk = CFG23[name][1]
+    if mk == "foe_s":
+        return orc.read_foe(os.path.join(ASSETS, "foe_s.foe"))
+    fa = orc.read_foe(os.path.join(ASSETS, "foe_a.foe"))
+    if mk == "foe_a_original":
+        fa = orc.OracleModel(filters=fa.filters, weights=fa.weights, boundary=fa.boundary, domain_tag="original")
+    return fa
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", sorted(CFG23))
+def test_cfg23_full_size_matches_reference(golden, name):
+    """BASELINE configs 2 and 3 at 512^2 (tests/golden/make_golden_512.py ran the reference's own
+    denoise): identical L-trace (identical decisions), F to 1e-10, image to the fp32 storage of the
+    golden."""
+    import hashlib
+    from paper_1609_05722_b200.synth import make_counts
+    g = golden("cfg23_512")
+    peak, _, variant, fb = CFG23[name]
+    _, y = make_counts(512, 512, 0, peak)
+    assert hashlib.sha256(y.tobytes()).digest() == g[f"{name}_counts_sha"].tobytes()
+    table = orc.load_lambda_table(os.path.join(ASSETS, "lambda_table.json"))
+    res = orc.denoise(y, peak, cfg23_model(name), variant, table, force_branch=fb, rel_tol=0.0)
+    tr = g[f"{name}_trace"]
+    assert res["branch"] == str(g[f"{name}_branch"]) and res["lam"] == g[f"{name}_meta"][1]
+    np.testing.assert_allclose(res["trace"].L, tr[:, 2], rtol=1e-13)
+    np.testing.assert_allclose(res["trace"].F, tr[:, 0], rtol=1e-10)
+    np.testing.assert_allclose(res["trace"].G, tr[:, 1], rtol=1e-9)
+    np.testing.assert_allclose(res["trace"].step_norm, tr[:, 3], rtol=1e-7)
+    assert np.max(np.abs(res["image"] - g[f"{name}_image"])) <= 1e-5 * peak  # golden stored as float32
