@@ -229,6 +229,10 @@ int foe_band_trial(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_ba
                    void *workspace, size_t workspace_bytes, void *stream);
 int foe_band_commit(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_band_desc *d, int trace_cap,
                     int init, void *workspace, size_t workspace_bytes, void *stream);
+/* after the last pass: F at the final iterate, tile partials only (all-gather them as after a trial,
+ * then foe_band_end sums them in the fixed order and anchors the trace's F column as foe_solve does) */
+int foe_band_final_pass(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_band_desc *d, int trace_cap,
+                        void *workspace, size_t workspace_bytes, void *stream);
 /* u_owned: device (B, row1-row0, W) final iterate rows; status/trace as foe_solve */
 int foe_band_end(const foe_bank *bank, const foe_band_desc *d, int trace_cap, void *workspace,
                  size_t workspace_bytes, float *u_owned, foe_image_status *status, double *trace,

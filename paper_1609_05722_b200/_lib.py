@@ -147,5 +147,5 @@ EXPORTED_SYMBOLS = [
     "foe_bench_trial_pass", "foe_debug_pass_times", "foe_tc_selftest", "foe_pass_uses_tensor_cores",
     "foe_debug_tc_rate", "foe_measure_ffma_peak", "foe_debug_pass_times_seq", "foe_score_workspace_size", "foe_score",
     "foe_conv_bank64", "foe_adjoint_bank64", "foe_tile_grid", "foe_band_geometry", "foe_band_describe", "foe_band_workspace_size",
-    "foe_band_buffers_get", "foe_band_begin", "foe_band_trial", "foe_band_commit", "foe_band_end",
+    "foe_band_buffers_get", "foe_band_begin", "foe_band_trial", "foe_band_commit", "foe_band_final_pass", "foe_band_end",
 ]

@@ -57,6 +57,7 @@ def _bind():
                                  ctypes.c_size_t, vp]
     L.foe_band_commit.argtypes = [vp, ctypes.POINTER(_lib.SolverCfgC), ctypes.POINTER(BandDesc), i, i, vp,
                                   ctypes.c_size_t, vp]
+    L.foe_band_final_pass.argtypes = L.foe_band_trial.argtypes
     L.foe_band_end.argtypes = [vp, ctypes.POINTER(BandDesc), i, vp, ctypes.c_size_t, vp, vp, vp, vp]
     L._bands_bound = True
     return L
@@ -158,6 +159,12 @@ class Band:
                                           self.trace_cap, int(init), self.ws.data_ptr(), self.ws_bytes,
                                           self._stream()), "foe_band_commit")
 
+    def final_pass(self):
+        """F at the final iterate (partials only; exchanged like a trial's, summed by end())."""
+        _lib.check(self.L.foe_band_final_pass(self.bank.handle, ctypes.byref(self.cfg_c), ctypes.byref(self.desc),
+                                              self.trace_cap, self.ws.data_ptr(), self.ws_bytes, self._stream()),
+                   "foe_band_final_pass")
+
     def end(self):
         import torch
         d = self.desc
@@ -257,6 +264,9 @@ def solve_bands(bands, exchange, u0_locals, obs_locals, lam, branch, max_iters, 
             break
         if n > cap:
             raise RuntimeError("band solve did not terminate")
+    for b in bands:  # F(u_final) for the trace's F column (foe_solve's anchor, same partials and order)
+        b.final_pass()
+    exchange(bands)
     out = [b.end() for b in bands]
     if raise_on_failure:
         _u, traces, status, failed = out[0]

@@ -569,6 +569,16 @@ __global__ void __launch_bounds__(PassCfg<5>::NT) k_decide(const PassArgs a) {
 // boundary rows -> send buffer [dir][B][field][halo][W]; dir 0 = first owned rows (to the band
 // above), dir 1 = last owned rows (to the band below); field 0 = u, 1 = grad.  init: the gradient of
 // the start point (u halos come with the input); otherwise the trial slots.
+// the final-energy reduction of a band solve: image b's all-gathered tile partials in the fixed order
+__global__ void __launch_bounds__(PassCfg<5>::NT) k_band_energy(const PassArgs a, double *energy) {
+    constexpr int NT = PassCfg<5>::NT;
+    __shared__ double red[NT / 32][kNumPartials];
+    __shared__ double s_sum[kNumPartials];
+    const int b = blockIdx.x;
+    reduce_tiles<NT>(a.partials, a.tiles_x * a.tiles_y, a.B, b, red, s_sum);
+    if (threadIdx.x == 0) energy[b] = s_sum[0];
+}
+
 __global__ void k_band_pack(const PassArgs a, float *send, int halo, int row0, int row1, int init) {
     const int b = blockIdx.y;
     const ImgCtl &c = a.ctl[b];
@@ -762,7 +772,7 @@ void tile_counts(int m, int H, int W, int *tx, int *ty) {
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct SolveLayout {
-    size_t U, G, O, ctl, partials, tickets, trace, n_active, send, recv, total;
+    size_t U, G, O, ctl, partials, tickets, trace, n_active, energy, send, recv, total;
     size_t halo_floats;  // per direction
 };
 
@@ -782,6 +792,7 @@ SolveLayout solve_layout(int m, int B, int H, int W, int trace_cap, int Hl = -1,
     L.tickets = off; off = align_up(off + sizeof(unsigned) * B);
     L.trace = off; off = align_up(off + sizeof(double) * 6 * (size_t)B * trace_cap);
     L.n_active = off; off = align_up(off + sizeof(int) * 4);
+    L.energy = off; off = align_up(off + sizeof(double) * B);
     L.halo_floats = (size_t)B * 2 * halo * W;
     L.send = off; off = align_up(off + sizeof(float) * 2 * L.halo_floats);
     L.recv = off; off = align_up(off + sizeof(float) * 2 * L.halo_floats);
@@ -797,6 +808,22 @@ int check_dims(const foe_bank *bank, int B, int H, int W) {
     return FOE_OK;
 }
 
+
+// The trace's F column (solver.py:163) is the device's running f_u + dF: every dF is accurate to its own
+// scale, but their sum carries the absolute rounding of the large early energies (F falls ~150x over a
+// solve, so the last rows were ~3e-5 off relative).  Anchoring the column on F(u_final), evaluated
+// directly, turns F_k into F(u_final) - sum_{j > k} dF_j (the same dF values; the accept decisions,
+// which use dF only, are untouched).
+void anchor_f_column(double *trace, int trace_cap, const std::vector<ImgCtl> &hc, const std::vector<double> &e) {
+    for (size_t b = 0; b < hc.size(); ++b) {
+        const int n = hc[b].n;
+        if (n < 1 || !std::isfinite(e[b])) continue;
+        double *rows = trace + b * (size_t)trace_cap * 6;
+        const double delta = e[b] - rows[(size_t)(n - 1) * 6];
+        if (!std::isfinite(delta)) continue;
+        for (int k = 0; k < n; ++k) rows[(size_t)k * 6] += delta;
+    }
+}
 
 }  // namespace
 
@@ -1451,6 +1478,14 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     cudaGraphExec_t exec = nullptr;
     if ((rc = loop_graph(bank->m, bank->boundary == FOE_SYMMETRIC, a, cap, &exec))) return rc;
     FOE_CUDA(cudaGraphLaunch(exec, st));
+    // final-energy pass: F at each image's last accepted iterate, evaluated directly (INIT mode on the
+    // final slot, no decision), to anchor the trace's F column (anchor_f_column)
+    a.mode = MODE_INIT;
+    a.no_decide = 1;
+    a.energy_out = (double *)(ws + L.energy);
+    if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, st))) return rc;
+    a.no_decide = 0;
+    a.energy_out = nullptr;
     {
         dim3 grid(std::max(1, std::min(148, (int)((size_t)H * W / 1024 + 1))), B);
         g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1460,8 +1495,11 @@ int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, in
     FOE_CUDA(cudaMemcpyAsync(hc.data(), a.ctl, sizeof(ImgCtl) * B, cudaMemcpyDeviceToHost, st));
     FOE_CUDA(cudaMemcpyAsync(trace, a.trace, sizeof(double) * 6 * (size_t)B * trace_cap, cudaMemcpyDeviceToHost, st));
     int loop_info[4] = {0, 0, 0, 0};
+    std::vector<double> energy(B);
     FOE_CUDA(cudaMemcpyAsync(loop_info, a.n_active, sizeof(loop_info), cudaMemcpyDeviceToHost, st));
+    FOE_CUDA(cudaMemcpyAsync(energy.data(), ws + L.energy, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
     FOE_CUDA(cudaStreamSynchronize(st));
+    anchor_f_column(trace, trace_cap, hc, energy);
     g_launches.fetch_add(loop_info[1] + loop_info[1] / kGraphChunk, std::memory_order_relaxed);
     if (loop_info[2]) return fail(FOE_E_NUMERICAL, "solver did not terminate after %d passes", loop_info[1]);
     int any_fail = 0;
@@ -1657,6 +1695,17 @@ int foe_band_commit(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_b
     return FOE_OK;
 }
 
+int foe_band_final_pass(const foe_bank *bank, const foe_solver_cfg *cfg, const foe_band_desc *d, int trace_cap,
+                        void *workspace, size_t workspace_bytes, void *stream) {
+    PassArgs a;
+    SolveLayout L;
+    int rc = band_args(bank, d, trace_cap, workspace, workspace_bytes, a, L, cfg);
+    if (rc) return rc;
+    a.mode = MODE_INIT;  // F and its tile partials at every image's final slot, no decision
+    a.no_decide = 1;
+    return launch_pass(bank->m, true, a, (cudaStream_t)stream);
+}
+
 int foe_band_end(const foe_bank *bank, const foe_band_desc *d, int trace_cap, void *workspace, size_t workspace_bytes,
                  float *u_owned, foe_image_status *status, double *trace, void *stream) {
     PassArgs a;
@@ -1669,10 +1718,18 @@ int foe_band_end(const foe_bank *bank, const foe_band_desc *d, int trace_cap, vo
     g_launches.fetch_add(1, std::memory_order_relaxed);
     k_gather_band<<<dim3(64, B), 256, 0, st>>>(a.U, a.plane, a.ctl, u_owned, d->Hl, d->W, d->row0, d->row1, d->lrow0);
     FOE_CUDA(cudaGetLastError());
+    // final energy from the all-gathered partials of foe_band_final_pass (the same fixed order on every
+    // band and in the single-device solve), to anchor the F column exactly as foe_solve does
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_band_energy<<<B, PassCfg<5>::NT, 0, st>>>(a, (double *)((char *)workspace + L.energy));
+    FOE_CUDA(cudaGetLastError());
     std::vector<ImgCtl> hc(B);
+    std::vector<double> energy(B);
     FOE_CUDA(cudaMemcpyAsync(hc.data(), a.ctl, sizeof(ImgCtl) * B, cudaMemcpyDeviceToHost, st));
     FOE_CUDA(cudaMemcpyAsync(trace, a.trace, sizeof(double) * 6 * (size_t)B * trace_cap, cudaMemcpyDeviceToHost, st));
+    FOE_CUDA(cudaMemcpyAsync(energy.data(), (char *)workspace + L.energy, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
     FOE_CUDA(cudaStreamSynchronize(st));
+    anchor_f_column(trace, trace_cap, hc, energy);
     int any_fail = 0;
     for (int b = 0; b < B; ++b) {
         status[b].status = hc[b].status;

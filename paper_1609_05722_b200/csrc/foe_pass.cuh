@@ -585,9 +585,8 @@ __global__ void __launch_bounds__(PassCfg<M>::NT, 1) k_pass(const PassArgs a) {
     reduce_tiles<NT>(a.partials, a.tiles_x * a.tiles_y, a.B, b, red, s_sum);
     if (tid == 0) {
         a.tickets[b] = 0u;
-        if (a.mode == MODE_EVAL) {
-            a.energy_out[b] = s_sum[0];
-        } else if (!a.no_decide) {
+        if (a.energy_out) a.energy_out[b] = s_sum[0];  // EVAL, and a solve's final-energy pass
+        if (a.mode != MODE_EVAL && !a.no_decide) {
             ImgCtl c = s_ctl;  // = a.ctl[b]: read at this pass's start, written only by this decision
             decide_ctl(a, b, s_sum, c, true, a.mode);
             a.ctl[b] = c;
