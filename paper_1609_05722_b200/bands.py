@@ -183,6 +183,8 @@ class Band:
 class LocalExchange:
     """All bands live in this process (one or several devices): exchange by device copies."""
 
+    capturable = True  # stream-ordered device copies: a chunk of passes can be captured in a CUDA graph
+
     def __call__(self, bands):
         for p in bands:  # all-gather of the per-tile partials
             for q in bands:
@@ -196,7 +198,11 @@ class LocalExchange:
 
 
 class DistExchange:
-    """One band per rank over torch.distributed (NCCL between B200s; gloo works for CPU tensors)."""
+    """One band per rank over torch.distributed: NCCL between B200s (device buffers); gloo (CPU tests, or
+    several ranks sharing one GPU) stages the device buffers through host memory.  The gather buffers
+    are allocated once and reused every pass.  The NCCL exchange is stream-ordered and can be captured
+    with the passes in a CUDA graph (solve_bands(graph=True)); that is opt-in because no multi-GPU box
+    was available to validate NCCL capture for this build, and the host-driven loop is the tested one."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -204,31 +210,50 @@ class DistExchange:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        self._gather = None
+        self.backend = dist.get_backend(group)
+        self._bufs = {}
+
+    capturable = False  # see the class note; solve_bands(graph=True) opts in for NCCL
+
+    def _buf(self, name, n, dtype, device):
+        import torch
+        b = self._bufs.get(name)
+        if b is None or b.numel() != n or b.dtype != dtype or b.device != device:
+            b = self._bufs[name] = torch.zeros(n, dtype=dtype, device=device)
+        return b
 
     def exchange_arrays(self, partials, chunk, chunk_sizes, sendbuf, recvbuf):
         """partials: full array (this rank's chunk filled); chunk_sizes: per-rank (offset, count)."""
         import torch
         dist = self.dist
+        stage = self.backend == "gloo" and partials.is_cuda  # gloo moves host tensors only
+        dev = torch.device("cpu") if stage else partials.device
         maxc = max(c for _, c in chunk_sizes)
-        mine = torch.zeros(maxc, dtype=partials.dtype, device=partials.device)
+        mine = self._buf("mine", maxc, partials.dtype, dev)
         mine[:chunk.stop - chunk.start].copy_(partials[chunk])
-        if self._gather is None or self._gather.numel() != maxc * self.world or self._gather.device != partials.device:
-            self._gather = torch.empty(maxc * self.world, dtype=partials.dtype, device=partials.device)
-        dist.all_gather_into_tensor(self._gather, mine, group=self.group)
+        gathered = self._buf("gather", maxc * self.world, partials.dtype, dev)
+        dist.all_gather_into_tensor(gathered, mine, group=self.group)
         for r, (off, cnt) in enumerate(chunk_sizes):
             if r != self.rank:
-                partials[off:off + cnt].copy_(self._gather[r * maxc:r * maxc + cnt])
+                partials[off:off + cnt].copy_(gathered[r * maxc:r * maxc + cnt])
+        if stage:
+            send = self._buf("send", sendbuf.numel(), sendbuf.dtype, dev).view(sendbuf.shape)
+            recv = self._buf("recv", recvbuf.numel(), recvbuf.dtype, dev).view(recvbuf.shape)
+            send.copy_(sendbuf)
+        else:
+            send, recv = sendbuf, recvbuf
         ops = []
         if self.rank > 0:
-            ops.append(dist.P2POp(dist.isend, sendbuf[0], self._peer(self.rank - 1), self.group))
-            ops.append(dist.P2POp(dist.irecv, recvbuf[0], self._peer(self.rank - 1), self.group))
+            ops.append(dist.P2POp(dist.isend, send[0], self._peer(self.rank - 1), self.group))
+            ops.append(dist.P2POp(dist.irecv, recv[0], self._peer(self.rank - 1), self.group))
         if self.rank + 1 < self.world:
-            ops.append(dist.P2POp(dist.isend, sendbuf[1], self._peer(self.rank + 1), self.group))
-            ops.append(dist.P2POp(dist.irecv, recvbuf[1], self._peer(self.rank + 1), self.group))
+            ops.append(dist.P2POp(dist.isend, send[1], self._peer(self.rank + 1), self.group))
+            ops.append(dist.P2POp(dist.irecv, recv[1], self._peer(self.rank + 1), self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if stage:
+            recvbuf.copy_(recv)
 
     def _peer(self, r):
         return r if self.group is None else self.dist.get_global_rank(self.group, r)
@@ -238,14 +263,47 @@ class DistExchange:
         self.exchange_arrays(band.partials, band.chunk, self.chunks, band.sendbuf, band.recvbuf)
 
 
+def _one_pass(bands, exchange):
+    for b in bands:
+        b.trial()
+    exchange(bands)
+    for b in bands:
+        b.commit(False)
+
+
+def _pass_graph(bands, exchange, chunk):
+    """A CUDA graph of `chunk` trial passes (trial -> exchange -> commit on every band), captured once per
+    (band set, exchange) and replayed: no per-pass host orchestration.  Passes after an image is done are
+    no-ops on the device (the pass, the exchange of unchanged buffers and the decision skip it)."""
+    import torch
+    key = (id(exchange), tuple(id(b) for b in bands), chunk)
+    cache = bands[0].__dict__.setdefault("_graphs", {})
+    g = cache.get(key)
+    if g is None:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            for _ in range(chunk):
+                _one_pass(bands, exchange)
+        cache.clear()
+        cache[key] = g
+    return g
+
+
 def solve_bands(bands, exchange, u0_locals, obs_locals, lam, branch, max_iters, poll: int = 8,
-                raise_on_failure: bool = True):
+                raise_on_failure: bool = True, graph: bool | None = None):
     """Device-resident iPiano over row bands.  ``bands``: the bands this process drives (all of them
     for LocalExchange, its own one for DistExchange); ``u0_locals`` / ``obs_locals``: per band,
     (B, Hl, W) fp32 CUDA tensors holding rows [lrow0, lrow0 + Hl).  Returns per band (u_owned,
-    traces, status, failed_at)."""
+    traces, status, failed_at).
+
+    With a capturable exchange (device copies, NCCL) the pass loop runs as replays of a CUDA graph of
+    ``poll`` passes, the live-image count read once per replay; otherwise pass by pass from the host."""
     if isinstance(exchange, DistExchange):
         exchange.chunks = _all_chunks(bands[0], exchange)
+    if graph is None:
+        graph = bool(getattr(exchange, "capturable", False))
+    if graph and isinstance(exchange, DistExchange) and exchange.backend != "nccl":
+        raise ValueError("only device-side exchanges (LocalExchange, NCCL) can be captured in a CUDA graph")
     for b, u0, ob in zip(bands, u0_locals, obs_locals):
         b.begin(u0, ob, lam, branch, max_iters)
     exchange(bands)
@@ -253,13 +311,15 @@ def solve_bands(bands, exchange, u0_locals, obs_locals, lam, branch, max_iters, 
         b.commit(True)
     n = 0
     cap = max(int(np.max(max_iters)) * 200 + 64, 64)
+    if graph:
+        g = _pass_graph(bands, exchange, poll)
     while True:
-        for b in bands:
-            b.trial()
-        exchange(bands)
-        for b in bands:
-            b.commit(False)
-        n += 1
+        if graph:
+            g.replay()
+            n += poll
+        else:
+            _one_pass(bands, exchange)
+            n += 1
         if n % poll == 0 and int(bands[0].n_active.item()) == 0:
             break
         if n > cap:
