@@ -77,14 +77,17 @@ struct ImgCtl {
     double L, f_u, lam;
     int n, max_iters, trials, status, done, branch, failed_at;
     int iu, iup, inew, ig, ignew;
-    float tau, t;  // fp32 step size tau = step_num / L and prox weight tau * lam, kept in step with L
+    // step size tau = step_num / L (solver.py:64-65), prox weight t = tau * lam and 1 / (1 + t), kept in step
+    // with L: the trial point is formed in fp64 from these (trial_point) and rounded once to fp32
+    double tau, t, inv1pt;
 };
 
 // the trial step of the current L, computed once per change of L rather than by every thread of a pass
 __host__ __device__ inline void set_step(ImgCtl &c, double step_num) {
     const double tau = step_num / c.L;  // SolverConfig.step_size, solver.py:64-65
-    c.tau = (float)tau;
-    c.t = (float)(tau * c.lam);
+    c.tau = tau;
+    c.t = tau * c.lam;
+    c.inv1pt = 1.0 / (1.0 + c.t);
 }
 
 struct PassArgs {
@@ -162,6 +165,16 @@ __device__ __forceinline__ void load_row(const float *p, float (&r)[W]) {
 
 __device__ __forceinline__ float prox_quad(float ut, float t, float v) {
     return (ut + t * v) / (1.0f + t);  // solver.py:100
+}
+
+// prox_idiv (solver.py:103-125) in fp64 for the trial point
+__device__ __forceinline__ double prox_idv64(double ut, double t, double ob) {
+    if (t == 0.0) return ut;  // solver.py:119-120
+    const double a = ut - t;
+    const double root = sqrt(fma(a, a, 4.0 * t * ob));
+    double o = (a >= 0.0) ? 0.5 * (a + root) : (2.0 * t * ob) / (root - a);  // solver.py:121-124
+    if (ob == 0.0 && a < 0.0) o = 0.0;                                        // solver.py:125
+    return o;
 }
 
 __device__ __forceinline__ float prox_idv(float ut, float t, float ob) {

@@ -186,16 +186,28 @@ __device__ void zero_psi_ring(const Smem<M> &S) {
 // per-image trial parameters of one pass
 struct TrialParams {
     int iu, iup, inew, ig, ignew, branch;
-    float tau, t, gam;
+    double tau, t, inv1pt, gam;
 };
 
 __device__ __forceinline__ TrialParams trial_params(const PassArgs &a, const ImgCtl &c) {
     TrialParams p;
     p.iu = c.iu; p.iup = c.iup; p.inew = c.inew; p.ig = c.ig; p.ignew = c.ignew; p.branch = c.branch;
-    p.tau = c.tau;  // set_step: step_num / L (solver.py:64-65) and tau * lam
+    p.tau = c.tau;  // set_step: step_num / L (solver.py:64-65), tau * lam, 1 / (1 + tau * lam)
     p.t = c.t;
-    p.gam = (float)a.gamma;
+    p.inv1pt = c.inv1pt;
+    p.gam = a.gamma;
     return p;
+}
+
+// the trial point prox(u - tau g + gamma (u - u_prev)) (solver.py:146-149 with prox_quadratic / prox_idiv,
+// solver.py:92-125) of one pixel, in fp64 like the reference and rounded once to the fp32 state: the
+// state then tracks the reference's iterates to ~1/2 ulp per iteration (fp32 arithmetic here rounded
+// several times per pixel and moved the iterates ~2x further, enough to flip a late decision)
+__device__ __forceinline__ float trial_point(float u, float up, float g, float ob, const TrialParams &p) {
+    const double ud = (double)u;
+    const double ut = (ud - p.tau * (double)g) + p.gam * (ud - (double)up);
+    if (p.branch == FOE_QUADRATIC) return (float)((ut + p.t * (double)ob) * p.inv1pt);
+    return (float)prox_idv64(ut, p.t, (double)ob);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -234,8 +246,7 @@ __device__ void stage(const PassArgs &a, const TileGeom &g, const Smem<M> &S, co
         const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
         const float u = lu[q], gg = lg[q], ob = lob[q];
         // u - tau g + gamma (u - u_prev)  (solver.py:146-149)
-        const float ut = (u - p.tau * gg) + p.gam * (u - lup[q]);
-        const float un = (p.branch == FOE_QUADRATIC) ? prox_quad(ut, p.t, ob) : prox_idv(ut, p.t, ob);
+        const float un = trial_point(u, lup[q], gg, ob, p);
         const float du = un - u;
         S.Un[i * SW + j] = un - shift;
         S.Du[i * SW + j] = du;

@@ -311,8 +311,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             }
             const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
             const float u = lu[q], gg = lg[q], ob = lob[q];
-            const float ut = (u - p.tau * gg) + p.gam * (u - lup[q]);  // solver.py:146-149
-            const float un = (p.branch == FOE_QUADRATIC) ? prox_quad(ut, p.t, ob) : prox_idv(ut, p.t, ob);
+            const float un = trial_point(u, lup[q], gg, ob, p);  // solver.py:146-149
             const float du = un - u;
             const float x = un - shift, h = tf32_rn(x), hd = tf32_rn(du);
             S4[i * SW + j] = make_float4(h, tf32_rn_operand(x - h), hd, tf32_rn_operand(du - hd));
