@@ -31,14 +31,14 @@ pytestmark = pytest.mark.gpu
 ASSETS = os.path.join(REPO, "paper_1609_05722_b200", "assets")
 TABLE = orc.load_lambda_table(os.path.join(ASSETS, "lambda_table.json"))
 # trace-column tolerances before the first divergence (fp32 state vs the fp64 reference), set from the
-# measured errors (profiles/r02_parity_report.json) with ~2x margin:
+# measured errors (profiles/r02_parity_report.json: F <= 6.1e-7, G <= 2.9e-7, step_norm <= 3.3e-2):
 #  * F is anchored on the directly evaluated F(u_final) (anchor_f_column in foe_b200.cu): F_k's error is
-#    the accumulated rounding of the dF between k and the end -- each dF a net of +- per-pixel changes
-#    ~1e3 x larger than itself -- against F values that fall ~150x over a solve (measured <= 9.9e-6);
-#  * G is evaluated from the fp32 iterate (measured <= 6.1e-7);
-#  * step_norm = |du| of fp32 iterates: late steps are ~1e-4 of |u| and the fp32 rounding of u
-#    (2^-24 |u| per pixel) is then up to ~1e-2 of the step (measured <= 3.0e-2).
-F_RTOL, G_RTOL, STEP_RTOL = 2e-5, 2e-6, 5e-2
+#    the accumulated rounding of the dF between k and the end, each dF a net of +- per-pixel changes
+#    far larger than itself, against F values that fall ~150x over a solve;
+#  * G is evaluated from the fp32 iterate;
+#  * step_norm = |du| of fp32 iterates: late steps are ~1e-4 of |u|, and the fp32 rounding of u
+#    (2^-24 |u| per pixel) is then up to ~1e-2 of the step.
+F_RTOL, G_RTOL, STEP_RTOL = 2e-6, 1e-6, 5e-2
 
 
 def psnr(x, ref, peak):
