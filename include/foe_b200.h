@@ -152,6 +152,24 @@ int foe_conv_bank64(const double *filters, int n, int m, int boundary, const dou
 int foe_adjoint_bank64(const double *filters, int n, int m, int boundary, const double *y, double *out, int B, int H,
                        int W, void *stream);
 
+/* hessian_apply (training.py:158-174), fused fp64: out = H p (+ eps p), H = sum_i wgt_i K_i^T diag(rho''(K_i w))
+ * K_i + d2D, d2D = I (objective 0, anscombe_domain) or diag(lam f / max(w, 1e-150)^2 where f > 0) (objective 1,
+ * original_domain); free_mask (nullable, uint8 H x W): outside it H acts as the identity and p is zeroed
+ * inside the operator (solve_hessian_system's `free`, training.py:196-200).  filters: (n, m, m) reference
+ * orientation, device; w, f, p, out: device H x W fp64.  One kernel per call, no N x H x W intermediate. */
+int foe_hessian_apply64(const double *filters, const double *weights, int n, int m, int boundary, int objective,
+                        double lam, const double *w, const double *f, const unsigned char *free_mask, const double *p,
+                        double eps, double *out, int H, int W, void *stream);
+/* one conjugate-gradient attempt of solve_hessian_system (training.py:203-237) on (H + eps I) q = rhs, entirely on
+ * the device (rhs already masked by the caller's free set): status 1 converged (relative residual <= tol),
+ * 2 non-positive curvature (the caller restarts with a larger eps, as the reference), 3 iteration cap;
+ * residuals (host, max_iters + 1): relative residual history, [0] = 1; iterations = entries after [0]. */
+size_t foe_cg_workspace_size(int H, int W, int max_iters);
+int foe_cg_solve64(const double *filters, const double *weights, int n, int m, int boundary, int objective, double lam,
+                   const double *w, const double *f, const unsigned char *free_mask, const double *rhs, double eps,
+                   double tol, int max_iters, double *q, int *status, int *iterations, double *residuals,
+                   int H, int W, void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- scoring (metrics.py:30-102) ------------------------------------
  * Per image b of B (H x W fp64, row-major, device): psnr[b] and mssim[b] of x_hat against g after the
  * reference's convention (both scaled by 255 / peak, data_range 255; 11 x 11 Gaussian window,

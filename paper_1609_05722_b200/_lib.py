@@ -119,6 +119,14 @@ def lib():
     for fn in (L.foe_conv_bank64, L.foe_adjoint_bank64):
         fn.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, ctypes.c_int, ctypes.c_int,
                        ctypes.c_int, _vp]
+    L.foe_hessian_apply64.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                      _vp, _vp, _vp, _vp, ctypes.c_double, _vp, ctypes.c_int, ctypes.c_int, _vp]
+    L.foe_cg_workspace_size.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    L.foe_cg_workspace_size.restype = ctypes.c_size_t
+    L.foe_cg_solve64.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                 _vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_double, ctypes.c_int, _vp,
+                                 ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), _vp, ctypes.c_int,
+                                 ctypes.c_int, _vp, ctypes.c_size_t, _vp]
     L.foe_score_workspace_size.argtypes = [ctypes.c_int] * 3
     L.foe_score_workspace_size.restype = ctypes.c_size_t
     L.foe_score.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, _vp, _vp, _vp,
@@ -146,6 +154,6 @@ EXPORTED_SYMBOLS = [
     "foe_eval_workspace_size", "foe_energy_grad", "foe_solve_workspace_size", "foe_solve",
     "foe_bench_trial_pass", "foe_debug_pass_times", "foe_tc_selftest", "foe_pass_uses_tensor_cores",
     "foe_debug_tc_rate", "foe_measure_ffma_peak", "foe_debug_pass_times_seq", "foe_score_workspace_size", "foe_score",
-    "foe_conv_bank64", "foe_adjoint_bank64", "foe_tile_grid", "foe_band_geometry", "foe_band_describe", "foe_band_workspace_size",
+    "foe_conv_bank64", "foe_adjoint_bank64", "foe_hessian_apply64", "foe_cg_workspace_size", "foe_cg_solve64", "foe_tile_grid", "foe_band_geometry", "foe_band_describe", "foe_band_workspace_size",
     "foe_band_buffers_get", "foe_band_begin", "foe_band_trial", "foe_band_commit", "foe_band_final_pass", "foe_band_end",
 ]

@@ -1167,6 +1167,58 @@ int bank64(const double *kf, int n, int m, int boundary, const double *in, doubl
     }
 }
 
+#include "foe_train64.cuh"
+
+template <int M, bool SYM>
+int launch_cg_hvp(const CgArgs &a, cudaStream_t st) {
+    const dim3 grid((a.W + kHT - 1) / kHT, (a.H + kHT - 1) / kHT);
+    k_cg_hvp<M, SYM><<<grid, 256, 0, st>>>(a);
+    FOE_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return FOE_OK;
+}
+
+int cg_hvp(int m, bool sym, const CgArgs &a, cudaStream_t st) {
+    switch (m) {
+        case 1: return sym ? launch_cg_hvp<1, true>(a, st) : launch_cg_hvp<1, false>(a, st);
+        case 3: return sym ? launch_cg_hvp<3, true>(a, st) : launch_cg_hvp<3, false>(a, st);
+        case 5: return sym ? launch_cg_hvp<5, true>(a, st) : launch_cg_hvp<5, false>(a, st);
+        case 7: return sym ? launch_cg_hvp<7, true>(a, st) : launch_cg_hvp<7, false>(a, st);
+        default: return fail(FOE_E_UNSUPPORTED, "filter size %d not compiled (1,3,5,7)", m);
+    }
+}
+
+int check_cg_model(const double *filters, const double *weights, int n, int m, int boundary, int objective,
+                   const double *w, const double *f, int H, int W) {
+    if (!filters || !weights || !w) return fail(FOE_E_INVALID, "null argument");
+    if (n < 1 || m < 1 || m > 7 || m % 2 != 1) return fail(FOE_E_INVALID, "bad bank (%d filters, side %d)", n, m);
+    if (boundary != FOE_SYMMETRIC && boundary != FOE_PERIODIC) return fail(FOE_E_INVALID, "bad boundary");
+    if (objective != 0 && objective != 1) return fail(FOE_E_INVALID, "objective must be 0 (anscombe) or 1 (original)");
+    if (objective == 1 && !f) return fail(FOE_E_INVALID, "the original-domain objective needs the counts");
+    if (H < m || W < m) return fail(FOE_E_INVALID, "image shape (%d, %d) smaller than filter size %d", H, W, m);
+    return FOE_OK;
+}
+
+struct CgLayout {
+    size_t r, da, db, hp, part, tickets, state, resid, total;
+};
+CgLayout cg_layout(int H, int W, int max_iters) {
+    const size_t plane = sizeof(double) * (size_t)H * W;
+    const size_t nct = (size_t)((W + kHT - 1) / kHT) * ((H + kHT - 1) / kHT);
+    CgLayout L;
+    size_t off = 0;
+    L.r = off; off = align_up(off + plane);
+    L.da = off; off = align_up(off + plane);
+    L.db = off; off = align_up(off + plane);
+    L.hp = off; off = align_up(off + plane);
+    L.part = off; off = align_up(off + sizeof(double) * 2 * std::max<size_t>(nct, kCgUpdCtas));
+    L.tickets = off; off = align_up(off + 2 * sizeof(unsigned));
+    L.state = off; off = align_up(off + sizeof(CgState));
+    L.resid = off; off = align_up(off + sizeof(double) * ((size_t)max_iters + 1));
+    L.total = off;
+    return L;
+}
+
 // FP32 FFMA throughput probe: 8 independent FMA chains per thread, 4 warps per SMSP, enough CTAs for
 // every SM; the result feeds the roofline peak (MEASURED_PEAKS.json has no FP32 figure)
 __global__ void __launch_bounds__(512) k_ffma_peak(float *out, int iters, float a, float b) {
@@ -1851,6 +1903,107 @@ int foe_conv_bank64(const double *filters, int n, int m, int boundary, const dou
 int foe_adjoint_bank64(const double *filters, int n, int m, int boundary, const double *y, double *out, int B, int H,
                        int W, void *stream) {
     return bank64<true>(filters, n, m, boundary, y, out, B, H, W, stream);
+}
+
+int foe_hessian_apply64(const double *filters, const double *weights, int n, int m, int boundary, int objective,
+                        double lam, const double *w, const double *f, const unsigned char *free_mask, const double *p,
+                        double eps, double *out, int H, int W, void *stream) {
+    int rc = check_cg_model(filters, weights, n, m, boundary, objective, w, f, H, W);
+    if (rc) return rc;
+    if (!p || !out) return fail(FOE_E_INVALID, "null argument");
+    CgArgs a{};
+    a.H = H; a.W = W; a.n = n; a.objective = objective; a.lam = lam; a.eps = eps;
+    a.kf = filters; a.wgt = weights; a.w = w; a.f = f; a.free_mask = free_mask;
+    a.r = p; a.hp = out;
+    return cg_hvp(m, boundary == FOE_SYMMETRIC, a, (cudaStream_t)stream);
+}
+
+size_t foe_cg_workspace_size(int H, int W, int max_iters) {
+    if (H < 1 || W < 1 || max_iters < 0) return 0;
+    return cg_layout(H, W, max_iters).total;
+}
+
+int foe_cg_solve64(const double *filters, const double *weights, int n, int m, int boundary, int objective, double lam,
+                   const double *w, const double *f, const unsigned char *free_mask, const double *rhs, double eps,
+                   double tol, int max_iters, double *q, int *status, int *iterations, double *residuals,
+                   int H, int W, void *workspace, size_t workspace_bytes, void *stream) {
+    int rc = check_cg_model(filters, weights, n, m, boundary, objective, w, f, H, W);
+    if (rc) return rc;
+    if (!rhs || !q || !status || !iterations || !residuals || !workspace || max_iters < 1)
+        return fail(FOE_E_INVALID, "null argument or max_iters < 1");
+    const CgLayout L = cg_layout(H, W, max_iters);
+    if (workspace_bytes < L.total) return fail(FOE_E_INVALID, "workspace too small (%zu < %zu)", workspace_bytes, L.total);
+    cudaStream_t st = (cudaStream_t)stream;
+    char *ws = (char *)workspace;
+    CgArgs a{};
+    a.H = H; a.W = W; a.n = n; a.objective = objective; a.lam = lam; a.eps = eps;
+    a.kf = filters; a.wgt = weights; a.w = w; a.f = f; a.free_mask = free_mask;
+    a.r = (const double *)(ws + L.r);
+    a.r_mut = (double *)(ws + L.r);
+    a.d_prev = (const double *)(ws + L.da);
+    a.d_next = (double *)(ws + L.db);
+    a.hp = (double *)(ws + L.hp);
+    a.q = q;
+    a.part = (double *)(ws + L.part);
+    a.tickets = (unsigned *)(ws + L.tickets);
+    a.st = (CgState *)(ws + L.state);
+    a.residuals = (double *)(ws + L.resid);
+    const size_t npx = (size_t)H * W;
+    FOE_CUDA(cudaMemsetAsync(a.tickets, 0, 2 * sizeof(unsigned), st));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_cg_init<<<1, 256, 0, st>>>(a.st, rhs, a.r_mut, q, npx, tol, max_iters, a.residuals, a.part);
+    FOE_CUDA(cudaGetLastError());
+    // the iteration loop: a graph whose WHILE node repeats [H d, update] until k_cg_update clears it
+    cudaGraph_t g = nullptr;
+    FOE_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    FOE_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    FOE_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+    cudaStream_t cs;
+    FOE_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    FOE_CUDA(cudaStreamBeginCaptureToGraph(cs, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    a.cond = h;
+    a.use_cond = 1;
+    const long long before = g_launches.load();
+    rc = cg_hvp(m, boundary == FOE_SYMMETRIC, a, cs);
+    if (rc == FOE_OK) {
+        k_cg_update<<<kCgUpdCtas, 256, 0, cs>>>(a);
+        if (cudaGetLastError() != cudaSuccess) rc = fail(FOE_E_CUDA, "k_cg_update launch failed");
+    }
+    cudaGraph_t captured = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cs, &captured);
+    cudaStreamDestroy(cs);
+    g_launches.store(before);
+    cudaGraphExec_t exec = nullptr;
+    if (rc == FOE_OK && ce == cudaSuccess) {
+        const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+        if (ie != cudaSuccess) rc = fail(FOE_E_CUDA, "CG graph instantiate: %s", cudaGetErrorString(ie));
+    } else if (rc == FOE_OK) {
+        rc = fail(FOE_E_CUDA, "CG graph capture: %s", cudaGetErrorString(ce));
+    }
+    cudaGraphDestroy(g);
+    if (rc) return rc;
+    const cudaError_t le = cudaGraphLaunch(exec, st);
+    CgState hs{};
+    cudaError_t me = cudaMemcpyAsync(&hs, a.st, sizeof(CgState), cudaMemcpyDeviceToHost, st);
+    if (me == cudaSuccess)
+        me = cudaMemcpyAsync(residuals, a.residuals, sizeof(double) * ((size_t)max_iters + 1), cudaMemcpyDeviceToHost, st);
+    const cudaError_t se = cudaStreamSynchronize(st);
+    cudaGraphExecDestroy(exec);
+    FOE_CUDA(le);
+    FOE_CUDA(me);
+    FOE_CUDA(se);
+    g_launches.fetch_add(2LL * hs.it + (hs.status == CG_BREAKDOWN ? 2 : 0), std::memory_order_relaxed);
+    *status = hs.status;
+    *iterations = hs.it;
+    return FOE_OK;
 }
 
 int foe_pass_uses_tensor_cores(int m, int nf) { return (use_tc(m, nf) || use_tc7(m, nf)) ? 1 : 0; }

@@ -8,9 +8,13 @@ it, and the parameter-gradient reductions:
     dL/dbeta_ij = -wgt_i ( <rho'(K_i w), B_j q> + <rho''(K_i w) K_i q, B_j w> ),
     dL/dlog w_i = -wgt_i <rho'(K_i w), K_i q>,   q = H^-1 dL/dw           (training.py:317-356)
 
-The filter-bank convolutions and exact adjoints run in the library's fp64 kernels
-(``foe_conv_bank64`` / ``foe_adjoint_bank64``); the filter x atom reductions are fp64 GEMMs; the CG
-vectors stay on the device.  fp64 throughout because the reference trains with 1e-9 CG and
+The Hessian-vector product is one fused fp64 kernel per call (``foe_hessian_apply64``: K w and K p,
+the rho'' weighting and the exact adjoint per tile, no N x H x W intermediate); the conjugate-gradient
+solve runs on the device (``foe_cg_solve64``: dot products, step lengths, the residual test and the
+breakdown test in kernels, the iteration loop a CUDA graph) with one host synchronise per CG attempt;
+the reference's restart rule (H + eps I, eps escalating tenfold) stays on the host.  The gradient and
+the parameter-gradient reductions use the fp64 bank kernels (``foe_conv_bank64`` /
+``foe_adjoint_bank64``) and fp64 GEMMs.  fp64 throughout because the reference trains with 1e-9 CG and
 stationarity tolerances.  The L-BFGS driver, lower solve and checkpointing are out of scope.
 """
 from __future__ import annotations
@@ -179,22 +183,30 @@ def stationarity_residual(w, model, sample, objective, lam=1.0) -> float:
     return float(g.abs().max().item())
 
 
-def _hvp_dev(bank, wd, zw, p, sample, objective, lam, fd=None):
-    """H p on the device; zw = K w (cached across CG iterations)."""
+_OBJECTIVE_CODE = {"anscombe_domain": 0, "original_domain": 1}
+CG_CONVERGED, CG_BREAKDOWN, CG_MAXITER = 1, 2, 3
+
+
+def _hvp_fused(bank, wd, p, objective, lam, fd=None, free=None, eps=0.0):
+    """(H + eps I) p through foe_hessian_apply64 (one fused kernel); free: uint8 device mask or None."""
     import torch
-    out = bank.adjoint(bank.weights[None, :, None, None] * _rho2(zw) * bank.conv(p))[0]
-    if objective == "anscombe_domain":
-        return out + p
-    f = fd if fd is not None else _dev(sample.noisy)
-    diag = torch.where(f > 0, lam * f / torch.clamp(wd, min=1e-150) ** 2, torch.zeros_like(wd))
-    return out + diag * p
+
+    from . import _lib
+    H, W = p.shape
+    out = torch.empty_like(p)
+    _lib.check(_lib.lib().foe_hessian_apply64(
+        bank.filters.data_ptr(), bank.weights.data_ptr(), bank.filters.shape[0], bank.m, bank.boundary,
+        _OBJECTIVE_CODE[objective], float(lam), wd.data_ptr(), fd.data_ptr() if fd is not None else None,
+        free.data_ptr() if free is not None else None, p.contiguous().data_ptr(), float(eps), out.data_ptr(), H, W,
+        torch.cuda.current_stream().cuda_stream), "hessian_apply64")
+    return out
 
 
 def hessian_apply(w, model, objective, p, sample, lam=1.0) -> np.ndarray:
     """H p with H = sum_i wgt_i K_i^T diag(rho''(K_i w)) K_i + d2D, matrix-free (training.py:158-174)."""
     bank = _Bank64(model)
-    wd = _dev(w)
-    return _hvp_dev(bank, wd, bank.conv(wd), _dev(p), sample, objective, lam).cpu().numpy()
+    fd = _dev(sample.noisy) if objective == "original_domain" else None
+    return _hvp_fused(bank, _dev(w), _dev(p), objective, lam, fd).cpu().numpy()
 
 
 def solve_hessian_system(w, model, objective, rhs, sample, lam=1.0, tol=1e-9, max_iters=600, free=None):
@@ -202,21 +214,22 @@ def solve_hessian_system(w, model, objective, rhs, sample, lam=1.0, tol=1e-9, ma
 
     Same algorithm as the reference: restarts with H + eps I when a search direction has
     non-positive curvature (eps from the same Philox trace estimate, escalating tenfold), ``free``
-    restricting the system to unpinned pixels."""
+    restricting the system to unpinned pixels.  Each attempt is one device-resident CG
+    (``foe_cg_solve64``); the host reads its status and residual history once per attempt."""
+    import ctypes
+
     import torch
+
+    from . import _lib
     bank = _Bank64(model)
     wd = _dev(w)
-    zw = bank.conv(wd)
     fd = _dev(sample.noisy) if objective == "original_domain" else None
     rhs_d = _dev(rhs)
-    raw = lambda p: _hvp_dev(bank, wd, zw, p, sample, objective, lam, fd)  # noqa: E731
-    if free is None:
-        base = raw
-    else:
-        fr = torch.as_tensor(np.asarray(free), device="cuda")
-        rhs_d = torch.where(fr, rhs_d, torch.zeros_like(rhs_d))
-        base = lambda p: torch.where(fr, raw(torch.where(fr, p, torch.zeros_like(p))), p)  # noqa: E731
-    dot = lambda a, b: float(torch.dot(a.reshape(-1), b.reshape(-1)).item())  # noqa: E731
+    H, W = rhs_d.shape
+    fr = None
+    if free is not None:
+        fr = torch.as_tensor(np.ascontiguousarray(np.asarray(free, dtype=np.uint8)), device="cuda")
+        rhs_d = torch.where(fr.bool(), rhs_d, torch.zeros_like(rhs_d))
     rhs_norm = float(torch.linalg.vector_norm(rhs_d).item())
     info = {"iterations": 0, "residuals": [], "regularization": 0.0}
     if rhs_norm == 0:
@@ -224,37 +237,27 @@ def solve_hessian_system(w, model, objective, rhs, sample, lam=1.0, tol=1e-9, ma
     # stochastic trace estimate with the reference's Rademacher probe (training.py:177-180)
     zt = np.where(np.random.Generator(np.random.Philox(key=0xC0FFEE)).random(tuple(rhs_d.shape)) < 0.5, -1.0, 1.0)
     zt = _dev(zt)
+    tr_est = float(torch.dot(zt.reshape(-1), _hvp_fused(bank, wd, zt, objective, lam, fd, fr).reshape(-1)).item())
     eps = 0.0
-    eps_unit = 1e-6 * max(dot(zt, base(zt)), 0.0) / rhs_d.numel() + 1e-300
+    eps_unit = 1e-6 * max(tr_est, 0.0) / rhs_d.numel() + 1e-300
+    L = _lib.lib()
+    ws = torch.empty(L.foe_cg_workspace_size(H, W, max_iters), dtype=torch.uint8, device="cuda")
+    q = torch.empty_like(rhs_d)
     residuals = []
     for _ in range(6):
-        matvec = base if eps == 0.0 else (lambda p, e=eps: base(p) + e * p)
-        q = torch.zeros_like(rhs_d)
-        r = rhs_d.clone()
-        d = r.clone()
-        rs = dot(r, r)
-        residuals = [np.sqrt(rs) / rhs_norm]
-        broke = False
-        for it in range(max_iters):
-            hd = matvec(d)
-            dhd = dot(d, hd)
-            if dhd <= 1e-14 * dot(d, d):
-                broke = True
-                break
-            alpha = rs / dhd
-            q += alpha * d
-            r -= alpha * hd
-            rs_new = dot(r, r)
-            residuals.append(np.sqrt(rs_new) / rhs_norm)
-            if residuals[-1] <= tol:
-                info.update(iterations=it + 1, residuals=residuals, regularization=eps)
-                return q.cpu().numpy(), info
-            d = r + (rs_new / rs) * d
-            rs = rs_new
-        if not broke:
-            info.update(iterations=max_iters, residuals=residuals, regularization=eps)
+        status, iters = ctypes.c_int(), ctypes.c_int()
+        res = np.zeros(max_iters + 1)
+        _lib.check(L.foe_cg_solve64(
+            bank.filters.data_ptr(), bank.weights.data_ptr(), bank.filters.shape[0], bank.m, bank.boundary,
+            _OBJECTIVE_CODE[objective], float(lam), wd.data_ptr(), fd.data_ptr() if fd is not None else None,
+            fr.data_ptr() if fr is not None else None, rhs_d.data_ptr(), float(eps), float(tol), int(max_iters),
+            q.data_ptr(), ctypes.byref(status), ctypes.byref(iters), res.ctypes.data, H, W, ws.data_ptr(),
+            ws.numel(), torch.cuda.current_stream().cuda_stream), "cg_solve64")
+        residuals = res[:iters.value + 1].tolist()
+        if status.value in (CG_CONVERGED, CG_MAXITER):
+            info.update(iterations=iters.value, residuals=residuals, regularization=eps)
             return q.cpu().numpy(), info
-        eps = eps_unit if eps == 0.0 else eps * 10.0
+        eps = eps_unit if eps == 0.0 else eps * 10.0  # CG_BREAKDOWN: training.py:233-235
         warnings.warn(f"non-positive curvature in Hessian solve; regularizing with eps={eps:.3e}")
     info.update(iterations=max_iters, residuals=residuals, regularization=eps)
     return q.cpu().numpy(), info

@@ -505,3 +505,69 @@ def test_tc7_matches_ffma_7x7(monkeypatch):
         monkeypatch.setenv("FOE_TC7", k)
         g[k] = fp.foe_gradient(u, model)
     assert rel_l2(g["1"], g["0"]) <= 1e-5
+
+
+def test_device_cg_restarts_and_free_set_vs_reference_golden(golden):
+    """solve_hessian_system's restart rule (six escalating H + eps I attempts after non-positive curvature)
+    and its free set (pinned pixels act as the identity), run as device-resident CG attempts, vs the
+    reference's own outputs (tests/golden/make_golden_cg.py)."""
+    import warnings
+    from paper_1609_05722_b200 import training as tr
+    g = golden("cg")
+    smp = tr.TrainingSample.create(g["cg_clean"], g["cg_noisy"])
+    fs, fa = fp.load_packaged_model("foe_s"), fp.load_packaged_model("foe_a")
+    hp = tr.hessian_apply(g["brk_w"], fs, "original_domain", g["cg_rhs"], smp, lam=0.1)
+    assert rel_l2(hp, g["brk_hp"]) <= 1e-12
+    with warnings.catch_warnings(record=True) as wl:
+        warnings.simplefilter("always")
+        q, info = tr.solve_hessian_system(g["brk_w"], fs, "original_domain", g["cg_rhs"], smp, lam=0.1, tol=1e-9,
+                                          max_iters=80)
+    assert sum("non-positive curvature" in str(x.message) for x in wl) == 6
+    assert info["iterations"] == int(g["brk_iters"])
+    assert abs(info["regularization"] - float(g["brk_reg"])) <= 1e-12 * float(g["brk_reg"])
+    assert len(info["residuals"]) == len(g["brk_res"])
+    np.testing.assert_allclose(info["residuals"], g["brk_res"], rtol=1e-8)
+    assert rel_l2(q, g["brk_q"]) <= 1e-8
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        q, info = tr.solve_hessian_system(g["free_w"], fa, "anscombe_domain", g["cg_rhs"], smp, lam=1.0, tol=1e-9,
+                                          max_iters=600, free=g["free_mask"])
+    assert info["iterations"] == int(g["free_iters"])
+    assert abs(info["regularization"] - float(g["free_reg"])) <= 1e-12 * float(g["free_reg"])
+    assert len(info["residuals"]) == len(g["free_res"])
+    np.testing.assert_allclose(info["residuals"], g["free_res"], rtol=1e-6)
+    assert rel_l2(q, g["free_q"]) <= 1e-8
+    np.testing.assert_array_equal(q[~g["free_mask"]], g["free_q"][~g["free_mask"]])
+
+
+def test_fused_hessian_apply_matches_composed_bank_operators():
+    """foe_hessian_apply64 (one fused kernel) == the product composed from the fp64 bank kernels
+    (conv, rho'' weighting, adjoint) + d2D, for both objectives, both boundaries, m in {3, 5, 7}, a free
+    set and the eps term, to 1e-13 relative."""
+    import torch
+    from paper_1609_05722_b200 import training as tr
+    rng = np.random.default_rng(21)
+    for m, boundary, objective, shape in ((3, "symmetric", "original_domain", (37, 53)),
+                                          (5, "periodic", "anscombe_domain", (40, 33)),
+                                          (7, "symmetric", "anscombe_domain", (64, 70)),
+                                          (5, "symmetric", "original_domain", (17, 19))):
+        basis = fp.dct_basis(m)
+        model = fp.FoEModel(basis=basis, betas=rng.normal(scale=0.5, size=(6, basis.n_atoms)),
+                            weights=rng.uniform(0.5, 2, 6),
+                            domain_tag="original" if objective == "original_domain" else "anscombe", boundary=boundary)
+        bank = tr._Bank64(model)
+        w = tr._dev(np.abs(rng.normal(2.0, 1.0, shape)) + 0.1)
+        p = tr._dev(rng.normal(size=shape))
+        f = tr._dev(rng.poisson(2.0, shape).astype(np.float64))
+        free = torch.as_tensor(rng.random(shape) < 0.7, device="cuda")
+        lam, eps = 0.7, 0.3
+        pm = torch.where(free, p, torch.zeros_like(p))
+        raw = bank.adjoint(bank.weights[None, :, None, None] * tr._rho2(bank.conv(w)) * bank.conv(pm))[0]
+        if objective == "anscombe_domain":
+            raw = raw + pm
+        else:
+            raw = raw + torch.where(f > 0, lam * f / torch.clamp(w, min=1e-150) ** 2, torch.zeros_like(w)) * pm
+        want = torch.where(free, raw, p) + eps * p
+        got = tr._hvp_fused(bank, w, p, objective, lam, f if objective == "original_domain" else None,
+                            free.to(torch.uint8), eps)
+        assert rel_l2(got.cpu().numpy(), want.cpu().numpy()) <= 1e-13, (m, boundary, objective)
