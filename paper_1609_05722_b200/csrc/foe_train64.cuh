@@ -72,7 +72,7 @@ __device__ __forceinline__ void block_sum2(double &a, double &b, double (*red)[2
 template <int M, bool SYM>
 __global__ void __launch_bounds__(256) k_cg_hvp(const CgArgs a) {
     constexpr int R = M / 2, SP = kHT + 4 * R, SC = kHT + 2 * R;
-    __shared__ double ws[SP * SP], ps[SP * SP], cs[SC * SC], ks[M * M];
+    __shared__ double ws[SP * SP], ps[SP * SP], cs[SC * SC];
     __shared__ double red[8][2];
     __shared__ int s_last;
     const int tid = threadIdx.x, H = a.H, W = a.W;
@@ -108,28 +108,36 @@ __global__ void __launch_bounds__(256) k_cg_hvp(const CgArgs a) {
         else if (qx >= W - R) Qx[nqx++] = 2 * W - 1 - qx;
     }
     double acc = 0.0;
+    // c positions: thread t < SC * SC / 2 owns column t % SC, rows 2 (t / SC) and 2 (t / SC) + 1 (the two
+    // rows share M (M - 1) of their 2 M^2 staged operands); taps live in registers (warp-uniform loads)
+    static_assert(SC % 2 == 0 && SC * SC / 2 <= 256, "two c rows per thread");
+    const int ccol = tid % SC, crow = 2 * (tid / SC);
+    const bool cworker = tid < SC * SC / 2;
     for (int i = 0; i < a.n; ++i) {
+        double k[M * M];
+#pragma unroll
+        for (int e = 0; e < M * M; ++e) k[e] = __ldg(a.kf + (size_t)i * M * M + e);
+        const double wgt = __ldg(a.wgt + i);
         __syncthreads();  // staging done / previous filter's c consumed
-        if (tid < M * M) ks[tid] = a.kf[(size_t)i * M * M + tid];
-        __syncthreads();
-        const double wgt = a.wgt[i];
-        for (int e = tid; e < SC * SC; e += 256) {
-            const int t0 = e / SC, t1 = e % SC;
-            const int gy = y0 - R + t0, gx = x0 - R + t1;
-            double c = 0.0;
-            if (!SYM || (gy >= 0 && gy < H && gx >= 0 && gx < W)) {
-                double z = 0.0, kp = 0.0;  // z(x) = sum_{a,b} k[a,b] w_ext(x - (a - r, b - r))
+        if (cworker) {
+            double z0 = 0.0, z1 = 0.0, p0 = 0.0, p1 = 0.0;  // z(x) = sum_{a,b} k[a,b] w_ext(x - (a - r, b - r))
 #pragma unroll
-                for (int aa = 0; aa < M; ++aa)
+            for (int aa = 0; aa < M; ++aa)
 #pragma unroll
-                    for (int bb = 0; bb < M; ++bb) {
-                        const int s = (t0 + 2 * R - aa) * SP + (t1 + 2 * R - bb);
-                        z = fma(ks[aa * M + bb], ws[s], z);
-                        kp = fma(ks[aa * M + bb], ps[s], kp);
-                    }
-                c = wgt * rho2_64(z) * kp;
+                for (int bb = 0; bb < M; ++bb) {
+                    const int s0 = (crow + 2 * R - aa) * SP + (ccol + 2 * R - bb);
+                    const double kk = k[aa * M + bb];
+                    z0 = fma(kk, ws[s0], z0);
+                    z1 = fma(kk, ws[s0 + SP], z1);
+                    p0 = fma(kk, ps[s0], p0);
+                    p1 = fma(kk, ps[s0 + SP], p1);
+                }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int gy = y0 - R + crow + h, gx = x0 - R + ccol;
+                const bool in = !SYM || (gy >= 0 && gy < H && gx >= 0 && gx < W);  // psi_0 = 0 outside (symmetric)
+                cs[(crow + h) * SC + ccol] = in ? wgt * rho2_64(h ? z1 : z0) * (h ? p1 : p0) : 0.0;
             }
-            cs[e] = c;
         }
         __syncthreads();
         if (!inside) continue;
@@ -144,7 +152,7 @@ __global__ void __launch_bounds__(256) k_cg_hvp(const CgArgs a) {
                     for (int bb = 0; bb < M; ++bb) {
                         const int ix = lx + bb;
                         if (ix < 0 || ix >= SC) continue;
-                        acc = fma(ks[aa * M + bb], cs[iy * SC + ix], acc);
+                        acc = fma(k[aa * M + bb], cs[iy * SC + ix], acc);
                     }
                 }
             }
@@ -182,12 +190,14 @@ __global__ void __launch_bounds__(256) k_cg_hvp(const CgArgs a) {
         s_last = ticket_acq_rel(a.tickets) == (unsigned)(nct - 1);
     }
     __syncthreads();
-    if (!s_last || tid != 0) return;
-    double sdhd = 0.0, sdd = 0.0;  // fixed order over the CTAs
-    for (int k = 0; k < nct; ++k) {
+    if (!s_last) return;
+    double sdhd = 0.0, sdd = 0.0;  // fixed order: thread t sums CTAs t, t + 256, ..., then a fixed tree
+    for (int k = tid; k < nct; k += 256) {
         sdhd += __ldcg(a.part + k);
         sdd += __ldcg(a.part + nct + k);
     }
+    block_sum2(sdhd, sdd, red);
+    if (tid != 0) return;
     a.tickets[0] = 0u;
     CgState *st = a.st;
     if (sdhd <= 1e-14 * sdd) st->status = CG_BREAKDOWN;  // training.py:220-222
@@ -219,9 +229,11 @@ __global__ void __launch_bounds__(256) k_cg_update(const CgArgs a) {
         s_last = ticket_acq_rel(a.tickets + 1) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!s_last || tid != 0) return;
-    double rs_new = 0.0;
-    for (int k = 0; k < (int)gridDim.x; ++k) rs_new += __ldcg(a.part + k);
+    if (!s_last) return;
+    double rs_new = 0.0, unused2 = 0.0;  // fixed order, as in k_cg_hvp
+    for (int k = tid; k < (int)gridDim.x; k += 256) rs_new += __ldcg(a.part + k);
+    block_sum2(rs_new, unused2, red);
+    if (tid != 0) return;
     a.tickets[1] = 0u;
     const double res = sqrt(rs_new) / st->rhs_norm;  // training.py:226-227
     st->it += 1;
