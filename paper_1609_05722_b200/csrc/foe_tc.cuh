@@ -10,12 +10,13 @@
 //    A.B ~= A_hi.B_hi + A_lo.B_hi + A_hi.B_lo (3xTF32, the A_lo.B_lo term is below fp32 rounding).
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
-// nearest tf32 (ties away from zero): the 3xTF32 split x = hi + lo with hi = rn(x), lo = rn(x - hi)
-// leaves |lo| <= 2^-11 |x| and a lo error <= 2^-22 |x| (the MMA truncates fp32 inputs to tf32).
-// Integer form of cvt.rna.tf32.f32 (which sm_100a emulates with an extra infinity test): identical
-// for every finite x, and every operand split here is finite.
+// nearest tf32: the 3xTF32 split x = hi + lo with hi = rn(x), lo = rn(x - hi) leaves |lo| <= 2^-11 |x|
+// and a lo error <= 2^-22 |x| (the MMA truncates fp32 inputs to tf32).  cvt.rn.tf32.f32 is one
+// instruction on sm_100a (F2FP.TF32.F32), where cvt.rna (and the integer add-and-mask form) take two.
 __device__ __forceinline__ float tf32_rn(float x) {
-    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+    uint32_t r;
+    asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
 }
 
 // lo operand of a split: x + half a tf32 ulp, left for the MMA to truncate -- the tensor core reads the
