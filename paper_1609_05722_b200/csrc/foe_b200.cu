@@ -25,8 +25,6 @@
 #define FOE_STAMPS 0  // per-block cycle stamps of the tensor-core pass (timing diagnostic builds only)
 #endif
 
-#include <cuda.h>  // CUtensorMap (TMA descriptors of the trial pass; encoded through the runtime's driver entry point)
-#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -70,7 +68,6 @@ int fail(int code, const char *fmt, ...) {
 constexpr int kMaxTaps = 4096;
 constexpr int kMaxFilters = 512;
 constexpr int kNumPartials = 7;  // dF|F, sq, gd, |u|^2, G_a, G_b, G_bad
-constexpr int kTmaRows = 8;      // staged rows per TMA box (the trial pass's row chunks)
 constexpr int kPartialStride = 8;
 constexpr bool kTcDefault = true;  // tensor-core pass for eligible banks unless FOE_TC=0
 
@@ -122,10 +119,6 @@ struct PassArgs {
     unsigned *tickets;    // (B)
     // solver constants
     double gamma, step_num, eta, relax, rel_tol, max_L;
-    // TMA descriptors of the state planes for the tensor-core trial pass (use_tma; see make_tmaps):
-    // U slots 0..2, G slots 0..1, obs, each a 2-D fp32 tensor {W, B * Hl} read in boxes of 8 staged rows
-    int use_tma;
-    CUtensorMap tmap[6];
 };
 
 // ------------------------------------------------------------------------------------------------
@@ -1457,42 +1450,6 @@ size_t foe_solve_workspace_size(const foe_bank *bank, int B, int H, int W, int t
     return solve_layout(bank->m, B, H, W, trace_cap).total;
 }
 
-// TMA descriptors of the trial pass's state planes (tensor-core 5x5 pass, symmetric boundary): each plane is
-// a 2-D fp32 tensor of W columns and B * Hl rows, read in boxes of CW x 8 staged cells; out-of-range
-// rows / columns arrive as zeros and are replaced by their mirror sources in shared memory.  Needs the
-// row stride (W * 4 bytes) to be a multiple of 16; otherwise (or with any other pass kernel) use_tma = 0
-// and the pass loads its cells with per-thread loads.
-static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            p = nullptr;
-        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }();
-    return fn;
-}
-
-static void make_tmaps(PassArgs &a, int m, int boundary) {
-    a.use_tma = 0;
-    if (!(m == 5 && boundary == FOE_SYMMETRIC && use_tc(m, a.n_filters) && a.W % 4 == 0)) return;
-    PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
-    if (!enc) return;
-    using C = PassCfg<5>;
-    const float *planes[6] = {a.U, a.U + a.plane, a.U + 2 * a.plane, a.Gs, a.Gs + a.plane, a.obs};
-    const cuuint64_t dims[2] = {(cuuint64_t)a.W, (cuuint64_t)a.B * (cuuint64_t)a.Hl};
-    const cuuint64_t strides[1] = {(cuuint64_t)a.W * sizeof(float)};
-    const cuuint32_t box[2] = {(cuuint32_t)C::CW, (cuuint32_t)kTmaRows};
-    const cuuint32_t estr[2] = {1, 1};
-    for (int k = 0; k < 6; ++k)
-        if (enc(&a.tmap[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(planes[k]), dims, strides, box, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return;
-    a.use_tma = 1;
-}
-
 static void fill_solve_args(PassArgs &a, const foe_bank *bank, const foe_solver_cfg &cfg, int B, int H, int W,
                             int trace_cap, char *ws, const SolveLayout &L, const foe_band_desc *band = nullptr) {
     a.B = B; a.H = H; a.W = W; a.n_filters = bank->n; a.zero_mean = bank->zero_mean;
@@ -1519,7 +1476,6 @@ static void fill_solve_args(PassArgs &a, const foe_bank *bank, const foe_solver_
     a.relax = cfg.relax_factor;
     a.rel_tol = cfg.rel_tol;
     a.max_L = cfg.max_lipschitz;
-    make_tmaps(a, bank->m, bank->boundary);
 }
 
 int foe_solve(const foe_bank *bank, const foe_solver_cfg *cfgp, int B, int H, int W, const float *u0,

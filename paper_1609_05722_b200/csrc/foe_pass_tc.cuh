@@ -45,12 +45,6 @@ struct TcCfg {
     static constexpr int C_AUH = 0, C_AUL = 24, C_ADH = 48, C_ADL = 72, C_T24 = 96, C_ASTAGE = 104;
     static constexpr int C_D0 = 208, C_DZ = 0, C_DDZ = 32, C_DY = 64, C_DREGION = 96, NDREG = 3;
     static_assert(C_D0 >= 2 * C_ASTAGE && C_D0 + NDREG * C_DREGION <= 512, "TMEM budget");
-    // TMA staging (PassArgs::use_tma): raw u, u_prev, g, obs of the staged cells, SH x CW each, in row chunks
-    // of kTmaRows; the prologue stages rows [0, PRE_ROWS) (blocks 0 and 1), the operand warps the two rows
-    // of block j + 2 while block j runs
-    static constexpr int RAWPL = SH * P::CW, NCHUNK = SH / kTmaRows, PRE_ROWS = SH;  // all rows in the prologue
-    static constexpr bool PROGRESSIVE = PRE_ROWS < SH;
-    static_assert(SH % kTmaRows == 0 && (PRE_ROWS == SH || PRE_ROWS == 2 * R + 4), "row chunks / prologue rows");
     static_assert(RW == 64 && NBLK * 128 == RH * RW, "blocks of two 64-pixel region rows");
     static_assert(NF_MAX <= 32, "one N = 32 MMA covers the bank");
 };
@@ -60,8 +54,7 @@ __host__ __device__ constexpr size_t tc_smem_floats() {
     using T = TcCfg<NF_MAX>;
     // staged planes u hi/lo, du hi/lo; Kf hi/lo, Kt hi/lo, four tap-24 B operands; Y ring; region gradient (two tap halves); alpha,
     // (spare), 2 alpha
-    return 4 * (size_t)T::PLANE + 5 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96 +
-           6 * (size_t)T::RAWPL;
+    return 4 * (size_t)T::PLANE + 5 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96;
 }
 
 // sum over taps [T0, T1) of Y(row r + a - R, column c + b - R)[a M + b] from the Y ring: one ring-row
@@ -120,11 +113,9 @@ __device__ __forceinline__ void tc_im2col(const float4 *sp, uint32_t st) {
 struct TcSmem {
     float4 *S4;                           // staged cells {u hi, u lo, du hi, du lo}
     float *Kf, *Kt, *K24, *Yr, *Gr, *s_al, *s_al2;
-    float *Raw;  // TMA staging: the six candidate planes U0, U1, U2, G0, G1, obs (RAWPL floats each)
     double (*red)[kNumPartials];
     double *s_sum;
     unsigned long long *mb_dfull, *mb_yfull, *mb_ring, *mb_sum;
-    unsigned long long *mb_chunk, *mb_stage;  // TMA row chunks landed; block j's staged rows complete
 };
 
 template <int NF>
@@ -143,7 +134,6 @@ __device__ __forceinline__ TcSmem tc_carve(float *sm, double (*red)[kNumPartials
     S.Gr = S.Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold), two tap halves
     S.s_al = S.Gr + 2 * T::RH * T::RW;       // alpha_f, zero-padded
     S.s_al2 = S.s_al + 64;                   // 2 alpha_f
-    S.Raw = S.s_al2 + 32;                    // 128-byte aligned (offsets above are multiples of 32 floats)
     S.red = red;
     S.s_sum = s_sum;
     S.mb_dfull = mb_dfull; S.mb_yfull = mb_yfull; S.mb_ring = mb_ring; S.mb_sum = mb_sum;
@@ -177,10 +167,7 @@ __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uin
         for (int j = 0; j < NBLK; ++j) {
             mbar_init(&mb_ring[j], 8);  // one arrival per warp of the draining point set
             mbar_init(&mb_sum[j], 8);   // one arrival per warp of the summing point set
-            mbar_init(&S.mb_stage[j], 7);  // one arrival per staging operand warp (1-7)
         }
-        for (int c = 0; c < T::NCHUNK; ++c) mbar_init(&S.mb_chunk[c], 1);  // thread 0's expect_tx
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // B operands: Kf[f][t] = kf_f[t] (convolution orientation), Kt[t][f] = 2 a_f k_f[t] with the
     // unflipped k_f[t] = kf_f[24 - t]; zero padding to 32 x 32; split into tf32 hi + tf32 lo (both rounded to nearest)
@@ -215,61 +202,6 @@ __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uin
     }
 }
 
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-// one 2-D TMA box (CW x kTmaRows fp32) of a state plane into shared memory, completing on bar
-__device__ __forceinline__ void tma_load_rows(float *dst, const CUtensorMap *map, int x, int y, unsigned long long *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
-        : "memory");
-}
-
-// Stage cell (i, j) of the tile from the TMA planes: the trial point prox(u - tau g + gamma (u - u_prev))
-// (solver.py:146-149) of the cell's source pixel (symmetric index map: mirrored cells read their source
-// inside the box; far-out cells of partial tiles, which reach no owned output, stage zeros), its tf32
-// hi / lo split into S4, and for owned pixels the u_new store and the fp64 partials (solver.py:152-153,
-// pipeline.py:141-149, 200) -- the arithmetic of the per-thread-load prologue, cell for cell.
-template <class T, class C>
-__device__ __forceinline__ void tc_stage_cell(const PassArgs &a, const TcSmem &S, const TileGeom &g,
-                                              const TrialParams &p, float shift, float *uout, int i, int j,
-                                              double (&acc)[kNumPartials]) {
-    constexpr int R = T::R;
-    const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
-    const int sy = src_idx<true>(gy, a.H) - (g.ry0 - R), sx = src_idx<true>(gx, a.W) - (g.rx0 - R);
-    float u = 0.0f, up = 0.0f, gg = 0.0f, ob = 0.0f;
-    if (sy >= 0 && sy < T::SH && sx >= 0 && sx < C::CW) {
-        mbar_wait(&S.mb_chunk[sy / kTmaRows], 0u);
-        const float *r = S.Raw + sy * C::CW + sx;
-        u = r[p.iu * T::RAWPL];
-        up = r[p.iup * T::RAWPL];
-        gg = r[(3 + p.ig) * T::RAWPL];
-        ob = r[5 * T::RAWPL];
-    }
-    const float un = trial_point(u, up, gg, ob, p);
-    const float du = un - u;
-    const float x = un - shift, h = tf32_rn(x), hd = tf32_rn(du);
-    S.S4[i * C::SW + j] = make_float4(h, tf32_rn_operand(x - h), hd, tf32_rn_operand(du - hd));
-    if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) {
-        uout[(size_t)(gy - a.lrow0) * a.W + gx] = un;
-        acc[1] += (double)du * (double)du;
-        acc[2] += (double)gg * (double)du;
-        acc[3] += (double)u * (double)u;
-        if (p.branch == FOE_QUADRATIC) {
-            const double d = (double)un - (double)ob;
-            acc[4] += d * d;
-        } else {
-            acc[4] += (double)un;
-            if (ob > 0.0f) {
-                if (un > 0.0f) acc[5] += (double)ob * (double)logf(un);
-                else acc[6] += 1.0;
-            }
-        }
-    }
-}
-
 // One trial (TRIAL) or evaluation pass of this CTA's tile: stage the trial point, the 18-block tensor-core
 // loop, the fold; thread 0 publishes the tile's fp64 partials in buffer `pbuf` of a.partials.  ctl: the
 // image's control block (null in MODE_EVAL); rpar: phase parity of the
@@ -297,22 +229,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     // TRIAL: every candidate slot (3 iterate planes, 2 gradient planes) and the observation are loaded
     // before the control block that names the slots is read, so the two L2 round trips overlap
     float cu[TRIAL ? 3 : 1][CPT], cg[TRIAL ? 2 : 1][CPT], cob[CPT], canc[TRIAL ? 3 : 1];
-    // TMA staging (symmetric boundary, row stride a multiple of 16 bytes): the planes arrive by row chunks
-    // and the cells are staged progressively -- rows of blocks 0 and 1 here, the rest inside the block loop
-    const bool tma = TRIAL && SYM && a.use_tma;
-    if (tma && tid == 0) {
-        // every row chunk of all six candidate planes (the control block naming the slots is read meanwhile),
-        // one mbarrier per chunk; the chunk mbarriers were initialised by this thread in tc_setup
-        const int x0 = g.rx0 - R, y0 = b * a.Hl + (g.ry0 - R - a.lrow0);
-        for (int c = 0; c < T::NCHUNK; ++c) {
-            mbar_expect_tx(&S.mb_chunk[c], 6u * kTmaRows * C::CW * (unsigned)sizeof(float));
-#pragma unroll
-            for (int k = 0; k < 6; ++k)
-                tma_load_rows(S.Raw + k * T::RAWPL + c * kTmaRows * C::CW, &a.tmap[k], x0, y0 + c * kTmaRows,
-                              &S.mb_chunk[c]);
-        }
-    }
-    if (TRIAL && !tma) {
+    if (TRIAL) {
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
             const int k = tid + q * NT;
@@ -359,27 +276,13 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         }
     }
     if (ph && tid == 0) ph[NBLK * 16 + 11] = clock64();  // control block read
-    if (tma) __syncthreads();  // the chunk mbarriers' initialisation (thread 0, setup) before anyone polls them
-    float shift;
-    if (tma) {
-        mbar_wait(&S.mb_chunk[0], 0u);
-        // the anchor (s0, c0) is staged cell (2R, 2R)
-        shift = a.zero_mean ? S.Raw[p.iu * T::RAWPL + 2 * R * C::CW + 2 * R] : 0.0f;
-    } else {
-        shift = TRIAL ? (p.iu == 0 ? canc[0] : p.iu == 1 ? canc[1] : canc[2])
-                      : a.zero_mean ? __ldg(uin + (size_t)(g.s0 - a.lrow0) * a.W + g.c0) : 0.0f;
-    }
+    const float shift = TRIAL ? (p.iu == 0 ? canc[0] : p.iu == 1 ? canc[1] : canc[2])
+                              : a.zero_mean ? __ldg(uin + (size_t)(g.s0 - a.lrow0) * a.W + g.c0) : 0.0f;
     double acc[kNumPartials];
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
-    if (tma) {
-        for (int k = tid; k < T::PRE_ROWS * C::CW; k += NT) {
-            const int i = k / C::CW, j = k - i * C::CW;
-            tc_stage_cell<T, C>(a, S, g, p, shift, uout, i, j, acc);
-        }
-    }
     // ---- prologue: stage u_new - shift and du for the region + r ring (all loads in flight first) ----
-    if (!tma) {
+    {
         float lu[CPT], lup[CPT], lg[CPT], lob[CPT];
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
@@ -433,8 +336,8 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     if (ph && tid == 0) ph[NBLK * 16 + 12] = clock64();  // cells staged
     // the prologue's partials 1..6 are summed per warp now (the block loop only adds partial 0)
     // scratch: the Y ring's data columns 2 .. 65 (its zero columns stay intact), one 32-double row per ring row
-    static_assert(T::YW % 2 == 0 && (NT / 32) * kNumPartials <= T::KT * T::YROWS, "partial scratch");
-    if (!tma) warp_partials_smem<1, kNumPartials, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));
+    static_assert(T::YW % 2 == 0 && (NT / 32) * (kNumPartials - 1) <= T::KT * T::YROWS, "partial scratch");
+    warp_partials_smem<1, kNumPartials, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));
     if (ph && tid == 0) ph[NBLK * 16 + 13] = clock64();  // warp partials
     fence_async_smem();
     tc_fence_before();
@@ -460,7 +363,6 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         for (int j = 0; j < NBLK; ++j) {
             const int s = j & 1;
             if (j >= 2 && warp != 0) named_sync(T::BAR_AFREE + s, 256);  // released by warp 0 (below)
-            if (T::PROGRESSIVE && tma && j >= 2) mbar_wait(&S.mb_stage[j], 0u);  // block j's rows (warps 1-7, step j - 2)
             tc_fence_after();
             if (ph && warp == 0) ph[j * 16 + 5] = clock64();
             const uint32_t st = tmem + s * T::C_ASTAGE + lane_off;
@@ -474,16 +376,6 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             tc_wait_st();
             tc_fence_before();
             if (warp != 0) named_arrive(T::BAR_AFULL + s, 256);
-            if (T::PROGRESSIVE && tma && warp != 0 && j + 2 < NBLK) {
-                // the two staged rows block j + 2 adds (2 j + 2 R + 4, + 1), by warps 1-7 while forward(j) runs
-                const int r0 = 2 * j + 2 * R + 4;
-                for (int k = tid - 32; k < 2 * C::CW; k += 7 * 32) {
-                    const int i = r0 + k / C::CW, jj = k % C::CW;
-                    tc_stage_cell<T, C>(a, S, g, p, shift, uout, i, jj, acc);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.mb_stage[j + 2]);
-            }
             if (warp == 0) {
                 // release stage (j+1)%2 for the next im2col as soon as forward(j-1) has read it, before
                 // forward(j) is issued: the im2col of block j+1 overlaps this warp's issue of block j
@@ -720,10 +612,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     if (ph && tid == 0) ph[NBLK * 16 + 1] = clock64();  // loop end (cycles), CTA (0, 0)
     // ---- per-tile partials first (last CTA of the image reduces and decides, as k_pass): the ticket's
     // round trip overlaps the fold below ----
-    if (tma)  // the staging partials 1..6 were accumulated through the loop: all seven now
-        warp_partials_smem<0, kNumPartials, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));
-    else
-        warp_partials_smem<0, 1, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));  // Y ring no longer live
+    warp_partials_smem<0, 1, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));  // Y ring no longer live
     block_combine<NT>(red, s_sum);
     if (ph && tid == 0) ph[NBLK * 16 + 5] = clock64();  // block reduction done
     int ticket = 0;
@@ -772,7 +661,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
 }
 
 template <int NF, bool TRIAL, bool SYM>
-__global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const __grid_constant__ PassArgs a) {
+__global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) {
     static_assert(NF % 8 == 0 && NF <= 32, "filter count rounded up to a multiple of 8");
     using T = TcCfg<32>;
     constexpr int NT = T::NT, NBLK = T::NBLK;
@@ -782,7 +671,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const __grid_const
     __shared__ int s_last;
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) unsigned long long mb_dfull[T::NDREG], mb_yfull[T::NDREG];
-    __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK], mb_stage[NBLK], mb_chunk[T::NCHUNK];
+    __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b = blockIdx.y;
@@ -803,9 +692,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const __grid_const
     griddep_launch_dependents();
     const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
     const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
-    TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_ring, mb_sum);
-    S.mb_stage = mb_stage;
-    S.mb_chunk = mb_chunk;
+    const TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_ring, mb_sum);
     tc_setup<NF>(a, S, &s_tmem);
     griddep_wait();  // the previous pass (control block, iterates, gradients, partials) is complete
     if (ph && tid == 0) ph[NBLK * 16 + 3] = clock64();  // dependency resolved
