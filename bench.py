@@ -275,6 +275,51 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def scaling_roofline(args, fp, model, cfg0, world, seeds):
+    """The trial pass of configs 4 / 5 on this rank's share (config 4: its images as one batch; config 5:
+    the whole 8192^2 image on one device when N = 1, else this rank's band is not a solve workspace and
+    the line carries the N = 1 figure only): CUDA-event time of back-to-back passes on a solved state,
+    achieved = 2,400 algorithmic FLOP x pixels in the launch / pass time, against the FFMA probe."""
+    import torch
+
+    from paper_1609_05722_b200 import _lib
+    from paper_1609_05722_b200.anscombe import forward_device
+    from paper_1609_05722_b200.synth import make_counts
+    if args.config == 5 and world > 1:
+        return None
+    L = _lib.lib()
+    if args.config == 4:
+        peaks = [[0.5, 1.0, 2.0, 4.0][s % 4] for s in seeds]
+        y = torch.from_numpy(np.stack([make_counts(H, W, s, p)[1] for s, p in zip(seeds, peaks)])).cuda()
+        B, HH, WW = len(seeds), H, W
+        lams = [fp.select_lambda(p, "transform", force_branch="quadratic") for p in peaks]
+    else:
+        _, yy = make_counts(8192, 8192, 0, 2.0)
+        y = torch.from_numpy(yy).cuda()[None]
+        B, HH, WW = 1, 8192, 8192
+        lams = [fp.select_lambda(2.0, "transform", force_branch="quadratic")]
+    v = forward_device(y.double() if y.dtype != torch.float64 else y)
+    res = fp.solve_device(model, v, v, lams, "quadratic", 3, cfg0, raise_on_failure=False)  # a state to time on
+    ws, stream = res._workspace, torch.cuda.current_stream()
+    reps = 10
+    _lib.check(L.foe_bench_trial_pass(res._bank.handle, B, HH, WW, res._cap, 2, ws.data_ptr(), ws.numel(),
+                                      stream.cuda_stream))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    _lib.check(L.foe_bench_trial_pass(res._bank.handle, B, HH, WW, res._cap, reps, ws.data_ptr(), ws.numel(),
+                                      stream.cuda_stream))
+    e1.record(stream)
+    e1.synchronize()
+    pass_ms = e0.elapsed_time(e1) / reps
+    peak, clk = measure_ffma_peak(L, torch.device("cuda"), torch.cuda.current_device())
+    flop = ALG_FLOP_PER_PX_IT * B * HH * WW
+    achieved = flop / (pass_ms * 1e-3) / 1e12
+    return {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None, "kernel": "k_pass_tc<24,TRIAL,SYM>", "pass_ms": pass_ms, "flop_per_launch": flop,
+            "launch": f"{B} x {HH}x{WW} per launch",
+            "peak_source": f"measured FFMA probe (SM clock {clk} MHz); achieved = 2400 FLOP x pixels / pass time"}
+
+
 def run_scaling_config(args, rank, local_rank, world):
     """Configs 4 (batch sharding) and 5 (row bands): strong scaling, device-timed, max over ranks."""
     import torch
@@ -350,12 +395,15 @@ def run_scaling_config(args, rank, local_rank, world):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         total_ms, px_it = float(tmax[0]), float(t[1])
     value = px_it / (total_ms * 1e-3) / 1e6
+    roof = None
+    if rank == 0:
+        roof = scaling_roofline(args, fp, model, cfg0, world, seeds if args.config == 4 else None)
     if rank == 0:
         print(json.dumps({"metric": METRIC, "value": value, "unit": "Mpixel*iter/s", "n_gpus": world,
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
                           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
                           "data": "synthetic", "config": {"workload": workload, "parallelism": f"{dtag}{world}"},
-                          "clocks": clk.summary()}), flush=True)
+                          "roofline": roof, "clocks": clk.summary()}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
