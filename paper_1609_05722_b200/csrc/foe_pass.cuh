@@ -101,6 +101,37 @@ __device__ __forceinline__ float two_atanh(float t) {
     return __logf((1.0f + t) * rcp_approx(1.0f - t));
 }
 
+// sum over filter pairs i of alpha_i * 2 atanh(t_i) into (e0, e1) (even, odd filters) when a warp's |t| exceeds
+// the series range somewhere: two_atanh's two forms (series to t^9 for |t| <= 0.2, MUFU logarithm of
+// (1+t)/(1-t) otherwise) evaluated in packed fp32 for both filters of a pair, selected per lane -- the same
+// arithmetic without the divergent branch.  al / al2: alpha and 2 alpha of the n filters (shared memory).
+template <int N>
+__device__ __forceinline__ void two_atanh_pairs(const float *t, const float *al, const float *al2, float &e0,
+                                                float &e1) {
+    static_assert(N % 2 == 0, "filter pairs");
+    float2 e = make_float2(e0, e1);
+#pragma unroll
+    for (int i = 0; i < N; i += 2) {
+        const float2 t1 = make_float2(t[i], t[i + 1]);
+        const float2 w = __fmul2_rn(*reinterpret_cast<const float2 *>(al2 + i), t1);
+        const float2 sq = __fmul2_rn(t1, t1);
+        float2 pp = __ffma2_rn(sq, make_float2(1.0f / 9.0f, 1.0f / 9.0f), make_float2(1.0f / 7.0f, 1.0f / 7.0f));
+        pp = __ffma2_rn(sq, pp, make_float2(1.0f / 5.0f, 1.0f / 5.0f));
+        pp = __ffma2_rn(sq, pp, make_float2(1.0f / 3.0f, 1.0f / 3.0f));
+        pp = __ffma2_rn(sq, pp, make_float2(1.0f, 1.0f));
+        const float2 vs = __fmul2_rn(w, pp);
+        const float2 num = __fadd2_rn(make_float2(1.0f, 1.0f), t1);
+        const float2 den = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-t1.x, -t1.y));
+        const float2 q = __fmul2_rn(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
+        const float2 a2 = *reinterpret_cast<const float2 *>(al + i);
+        const float2 vl = __fmul2_rn(make_float2(__log2f(q.x), __log2f(q.y)),
+                                     __fmul2_rn(a2, make_float2(0.69314718f, 0.69314718f)));
+        e = __fadd2_rn(e, make_float2(fabsf(t1.x) <= 0.2f ? vs.x : vl.x, fabsf(t1.y) <= 0.2f ? vs.y : vl.y));
+    }
+    e0 = e.x;
+    e1 = e.y;
+}
+
 // ------------------------------------------------------------------------------------------------
 // tile geometry and shared-memory carve-up
 

@@ -581,31 +581,8 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                     e0 = e.x;
                     e1 = e.y;
                 };
-                if (wmax > 0.2f) {
-                    // lanes mix |t| <= 0.2 (series) and larger |t| (MUFU logarithm of (1+t)/(1-t)): both forms
-                    // on filter pairs in packed fp32 and a per-lane select -- two_atanh's arithmetic without its
-                    // divergent branch (the early, large-step trials of a solve)
-                    float2 e = make_float2(e0, e1);
-#pragma unroll
-                    for (int i = 0; i < FH; i += 2) {
-                        const float2 t1 = make_float2(dz[i], dz[i + 1]);
-                        const float2 w = __fmul2_rn(*reinterpret_cast<const float2 *>(s_al2 + f0 + i), t1);
-                        const float2 sq = __fmul2_rn(t1, t1);
-                        float2 pp = __ffma2_rn(sq, make_float2(1.0f / 9.0f, 1.0f / 9.0f), make_float2(1.0f / 7.0f, 1.0f / 7.0f));
-                        pp = __ffma2_rn(sq, pp, make_float2(1.0f / 5.0f, 1.0f / 5.0f));
-                        pp = __ffma2_rn(sq, pp, make_float2(1.0f / 3.0f, 1.0f / 3.0f));
-                        pp = __ffma2_rn(sq, pp, make_float2(1.0f, 1.0f));
-                        const float2 vs = __fmul2_rn(w, pp);
-                        const float2 num = __fadd2_rn(make_float2(1.0f, 1.0f), t1);
-                        const float2 den = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-t1.x, -t1.y));
-                        const float2 q = __fmul2_rn(num, make_float2(rcp_approx(den.x), rcp_approx(den.y)));
-                        const float2 al = *reinterpret_cast<const float2 *>(s_al + f0 + i);
-                        const float2 vl = __fmul2_rn(make_float2(__log2f(q.x), __log2f(q.y)),
-                                                     __fmul2_rn(al, make_float2(0.69314718f, 0.69314718f)));
-                        e = __fadd2_rn(e, make_float2(fabsf(t1.x) <= 0.2f ? vs.x : vl.x, fabsf(t1.y) <= 0.2f ? vs.y : vl.y));
-                    }
-                    e0 = e.x;
-                    e1 = e.y;
+                if (wmax > 0.2f) {  // lanes mix series-range and larger |t|: both forms, per-lane select
+                    two_atanh_pairs<FH>(dz, s_al + f0, s_al2 + f0, e0, e1);
                 } else if (wmax > 0.04f) {
                     series(std::integral_constant<int, 9>{});
                 } else if (wmax > 0.004f) {

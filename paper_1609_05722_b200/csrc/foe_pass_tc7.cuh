@@ -428,12 +428,8 @@ __global__ void __launch_bounds__(TcCfg7::NT, 1) k_pass_tc7(const PassArgs a) {
                             e0 = e.x;
                             e1 = e.y;
                         };
-                        if (wmax > 0.2f) {
-#pragma unroll
-                            for (int i = 0; i < 12; ++i) {
-                                const float term = s_al[f0 + i] * two_atanh(dz[i]);
-                                if (i & 1) e1 += term; else e0 += term;
-                            }
+                        if (wmax > 0.2f) {  // lanes mix series-range and larger |t|: both forms, per-lane select
+                            two_atanh_pairs<12>(dz, s_al + f0, s_al2 + f0, e0, e1);
                         } else if (wmax > 0.12f) {
                             series(std::integral_constant<int, 9>{});
                         } else if (wmax > 0.04f) {
