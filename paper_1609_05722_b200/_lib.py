@@ -18,8 +18,10 @@ LIB_PATH = os.path.join(PKG, "libfoe_b200.so")
 # diagnostic builds (e.g. -DFOE_STAMPS=1, built by tools/build_diag.py) load through FOE_LIB
 LOAD_PATH = os.environ.get("FOE_LIB", LIB_PATH)
 
+# host code (count validation, band geometry, descriptor setup) for x86-64-v3 (AVX2), as the oracle: the GPU
+# boxes' hosts support it
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared"]
+              "-Xcompiler", "-fPIC,-march=x86-64-v3", "-shared"]
 
 FOE_OK, FOE_E_INVALID, FOE_E_CUDA, FOE_E_NUMERICAL, FOE_E_UNSUPPORTED = 0, -1, -2, -3, -4
 
