@@ -444,7 +444,7 @@ __global__ void k_conv_adjoint(const float *__restrict__ yv, float *__restrict__
         const int64_t b = i / ((int64_t)H * W);
         const int p = (int)(i - b * H * W), y = p / W, xx = p - y * W;
         const float *img = yv + b * H * W;
-        // padded positions q with src(q) == p (image.py:88-90)
+        // padded positions q with src(q) == p (image.py:80-83)
         int qy[3], qx[3], ny = 0, nx = 0;
         const int cy[3] = {y, SYM ? -1 - y : y - H, SYM ? 2 * H - 1 - y : y + H};
         const int cx[3] = {xx, SYM ? -1 - xx : xx - W, SYM ? 2 * W - 1 - xx : xx + W};

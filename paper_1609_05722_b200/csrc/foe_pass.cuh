@@ -458,7 +458,7 @@ __device__ double filter_loop(const PassArgs &a, const TileGeom &g, const Smem<M
                     w[kk] = v.x; w[kk + 1] = v.y; w[kk + 2] = v.z; w[kk + 3] = v.w;
                 }
                 const float *pb = S.Psi + (grp * C::NBUF + kb) * C::PLANE + ly0 * SW + lx0;
-                // adjoint: gacc += K_f^T psi_f  (correlation with the unflipped kernel, image.py:84-87)
+                // adjoint: gacc += K_f^T psi_f  (correlation with the unflipped kernel, image.py:76-79)
 #pragma unroll
                 for (int i = 0; i < WR; ++i) {
                     float rp[WIN];
