@@ -42,6 +42,7 @@
 struct foe_bank {
     int n, m, boundary, device, zero_mean;
     float *d_kf, *d_alpha;
+    float *d_tc_img;  // operand image of the tensor-core 5x5 pass (foe_pass_tc.cuh), null for other banks
 };
 
 namespace {
@@ -102,6 +103,7 @@ struct PassArgs {
     size_t plane;  // B*H*W: distance between state slots
     const float *kf;     // (n, M*M) flipped taps (correlation orientation of the forward conv)
     const float *alpha;  // (n)
+    const float *tc_img; // k_pass_tc's shared-memory operand image (5x5 banks with <= 32 filters), else null
     // state (solve modes)
     float *U;        // 3 slots
     float *Gs;       // 2 slots
@@ -330,6 +332,25 @@ __device__ __forceinline__ void block_reduce(double (&v)[kNumPartials], double (
 // Up to kFastReduceTiles tiles (every single-image configuration up to ~2k x 2k) take the one-warp-
 // per-partial path below instead.
 constexpr int kReduceNT = 384, kFastReduceTiles = 1024;
+
+// lane l's ordered sum of partial k over tiles l, l + 32, ...: eight loads in flight at a time (a loop of
+// dependent load-add pairs costs one L2 round trip per tile: 4-5 of them, ~2 us, at 144 tiles), added in
+// the same order (absent tiles add an exact zero)
+__device__ __forceinline__ double lane_tile_sum(const double *partials, int ntiles, int B, int b, int k, int lane) {
+    double x = 0.0;
+    for (int base = 0; base < ntiles; base += 256) {
+        double v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int tt = base + lane + 32 * i;
+            v[i] = tt < ntiles ? __ldcg(partials + ((size_t)tt * B + b) * kPartialStride + k) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x += v[i];
+    }
+    return x;
+}
+
 template <int NT>
 __device__ void reduce_tiles(const double *partials, int ntiles, int B, int b, double (*red)[kNumPartials],
                              double *s_sum) {
@@ -340,9 +361,7 @@ __device__ void reduce_tiles(const double *partials, int ntiles, int B, int b, d
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         __syncthreads();
         if (warp < kNumPartials) {
-            double x = 0.0;
-#pragma unroll 8
-            for (int tt = lane; tt < ntiles; tt += 32) x += __ldcg(partials + ((size_t)tt * B + b) * kPartialStride + warp);
+            double x = lane_tile_sum(partials, ntiles, B, b, warp, lane);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
             if (lane == 0) s_sum[warp] = x;
@@ -1268,6 +1287,42 @@ int foe_device_sm_count(int device) {
     return v;
 }
 
+// Shared-memory operand image of k_pass_tc (TcCfg<32>::IMG_*), built once per bank: forward B1 / B2 (N = 32
+// filters x K = 56 A columns, K-major SWIZZLE_NONE), adjoint Kt hi / lo (N = 32 taps x K = 32 filters), alpha,
+// 2 alpha.  tf32 hi / lo both rounded to nearest-even, as cvt.rn.tf32.f32 does.
+static float tf32_rn_host(float x) {
+    uint32_t b;
+    memcpy(&b, &x, 4);
+    b += 0xFFFu + ((b >> 13) & 1u);
+    b &= 0xffffe000u;
+    memcpy(&x, &b, 4);
+    return x;
+}
+static std::vector<float> tc_operand_image(const float *kf, const float *al, int nf) {
+    using T = TcCfg<32>;
+    std::vector<float> img(T::IMG_FLOATS, 0.0f);
+    auto boff = [](int n, int k) { return (n & 7) * 4 + (k & 3) + (n >> 3) * 32 + (k >> 2) * 128; };  // bsw_offset<32>
+    for (int n = 0; n < nf; ++n)
+        for (int t = 0; t < T::KT; ++t) {
+            const float v = kf[n * T::KT + t], h = tf32_rn_host(v), l = tf32_rn_host(v - h);
+            img[T::IMG_B1 + boff(n, tc_acol(t, 0))] = h;  // u_hi k_hi
+            img[T::IMG_B1 + boff(n, tc_acol(t, 1))] = h;  // u_lo k_hi
+            img[T::IMG_B2 + boff(n, tc_acol(t, 0))] = l;  // u_hi k_lo
+        }
+    // Kt[t][f] = 2 a_f k_f[t] with the unflipped k_f[t] = kf_f[24 - t]
+    for (int t = 0; t < T::KT; ++t)
+        for (int f = 0; f < nf; ++f) {
+            const float v = 2.0f * al[f] * kf[f * T::KT + (T::KT - 1 - t)], h = tf32_rn_host(v);
+            img[T::IMG_KT + boff(t, f)] = h;
+            img[T::IMG_KT + T::BSZ + boff(t, f)] = tf32_rn_host(v - h);
+        }
+    for (int f = 0; f < nf; ++f) {
+        img[T::IMG_AL + f] = al[f];
+        img[T::IMG_AL2 + f] = 2.0f * al[f];
+    }
+    return img;
+}
+
 int foe_bank_create(const double *filters, const double *weights, int n, int m, int boundary, foe_bank **out) {
     if (!filters || !weights || !out) return fail(FOE_E_INVALID, "null argument");
     if (n < 1 || n > kMaxFilters) return fail(FOE_E_INVALID, "filter count %d out of range", n);
@@ -1316,6 +1371,14 @@ int foe_bank_create(const double *filters, const double *weights, int n, int m, 
     }
     FOE_CUDA(cudaMemcpy(bk->d_kf, kf.data(), kf.size() * sizeof(float), cudaMemcpyHostToDevice));
     FOE_CUDA(cudaMemcpy(bk->d_alpha, al.data(), al.size() * sizeof(float), cudaMemcpyHostToDevice));
+    if (m == 5 && n <= 32) {
+        const std::vector<float> img = tc_operand_image(kf.data(), al.data(), n);
+        if (cudaMalloc(&bk->d_tc_img, img.size() * sizeof(float)) != cudaSuccess) {
+            foe_bank_destroy(bk);
+            return fail(FOE_E_CUDA, "cudaMalloc failed for the operand image");
+        }
+        FOE_CUDA(cudaMemcpy(bk->d_tc_img, img.data(), img.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
     *out = bk;
     return FOE_OK;
 }
@@ -1324,6 +1387,7 @@ int foe_bank_destroy(foe_bank *bank) {
     if (!bank) return FOE_OK;
     cudaFree(bank->d_kf);
     cudaFree(bank->d_alpha);
+    cudaFree(bank->d_tc_img);
     delete bank;
     return FOE_OK;
 }
@@ -1437,7 +1501,7 @@ int foe_energy_grad(const foe_bank *bank, const float *u, float *grad, double *e
     tile_counts(bank->m, H, W, &a.tiles_x, &a.tiles_y);
     a.tiles_yl = a.tiles_y; a.ty0 = 0; a.lrow0 = 0; a.Hl = H; a.band = 0;
     a.mode = MODE_EVAL;
-    a.kf = bank->d_kf; a.alpha = bank->d_alpha;
+    a.kf = bank->d_kf; a.alpha = bank->d_alpha; a.tc_img = bank->d_tc_img;
     a.u_in = u; a.g_out = grad; a.energy_out = energy;
     a.partials = (double *)workspace;
     a.tickets = (unsigned *)((char *)workspace + align_up(sizeof(double) * kPartialStride * (size_t)B * a.tiles_x * a.tiles_y));
@@ -1460,7 +1524,7 @@ static void fill_solve_args(PassArgs &a, const foe_bank *bank, const foe_solver_
         a.ty0 = 0; a.tiles_yl = a.tiles_y; a.lrow0 = 0; a.Hl = H; a.band = 0;
     }
     a.plane = (size_t)B * a.Hl * W;
-    a.kf = bank->d_kf; a.alpha = bank->d_alpha;
+    a.kf = bank->d_kf; a.alpha = bank->d_alpha; a.tc_img = bank->d_tc_img;
     a.U = (float *)(ws + L.U);
     a.Gs = (float *)(ws + L.G);
     a.obs = (const float *)(ws + L.O);
@@ -1589,7 +1653,8 @@ int foe_debug_pass_times_seq(const foe_bank *bank, int B, int H, int W, int trac
     fill_solve_args(a, bank, cfg, B, H, W, trace_cap, (char *)workspace, L);
     a.mode = MODE_TRIAL;
     a.no_decide = 1;
-    const size_t stride = 3 * (size_t)a.tiles_x * a.tiles_y * B + 512;
+    // per pass: [cta][start, loop start, ticket seen] | 512 phase stamps | [cta] dependency released | [cta] decider done
+    const size_t stride = 5 * (size_t)a.tiles_x * a.tiles_y * B + 512;
     for (int k = 0; k < n_passes; ++k) {
         a.dbg_times = times + k * stride;
         if ((rc = launch_pass(bank->m, bank->boundary == FOE_SYMMETRIC, a, (cudaStream_t)stream))) return rc;

@@ -38,23 +38,36 @@ struct TcCfg {
     static constexpr int RING = 4;                       // Y ring: 4 blocks = 8 region rows
     static constexpr int YROWS = 2 * RING, YW = RW + 4;  // 2 zero columns each side
     static constexpr int BSZ = 32 * 32;                  // one 32 x 32 B operand (floats)
-    // TMEM columns: A stage s at 128 s (A_u hi/lo, A_du hi/lo); D region s at 256 + 96 s (D_z -> Psi hi,
-    // D_dz -> Psi lo, D_y)
-    // A stage: taps 0..23 of u hi / lo, du hi / lo (K = 24 each), then the tap-24 group {u hi, u lo, du hi,
-    // du lo, 0, 0, 0, 0} (one K = 8 step whose B operand selects the plane)
-    static constexpr int C_AUH = 0, C_AUL = 24, C_ADH = 48, C_ADL = 72, C_T24 = 96, C_ASTAGE = 104;
-    static constexpr int C_D0 = 208, C_DZ = 0, C_DDZ = 32, C_DY = 64, C_DREGION = 96, NDREG = 3;
+    // A stage (TMEM, lane = pixel): two quantities (u, du) of KA = 56 columns each.  Column order = the
+    // order the im2col loads deliver them, so every tcgen05.st takes consecutive registers: per filter row
+    // dy the pairs {hi, lo} of taps dx 0..3 (8 columns, two LDS.128 of the pair-replicated staged cells),
+    // then the {hi, lo} pairs of tap dx = 4 of the five rows (10 columns), then 6 zero columns.
+    //   column 8 dy + 2 dx + part (dx < 4);  40 + 2 dy + part (dx = 4);  part 0 = tf32 hi, 1 = tf32 lo
+    // B1[k][f] = k_hi[tap(k)] on both parts (u_hi k_hi + u_lo k_hi), B2[k][f] = k_lo[tap(k)] on part 0
+    // (u_hi k_lo): the 3xTF32 product is two K = 56 sweeps, 14 MMAs per quantity.
+    static constexpr int KA = 56, KSTEPS = KA / 8, BFSZ = 32 * KA;
+    static constexpr int C_AU = 0, C_AD = KA, C_ASTAGE = 2 * KA;
+    static constexpr int C_D0 = 2 * C_ASTAGE, C_DZ = 0, C_DDZ = 32, C_DY = 64, C_DREGION = 96, NDREG = 3;
+    // operand image built once per bank on the host (foe_bank_create) and copied into shared memory by one
+    // bulk copy per CTA: [B1 | B2 | Kt hi | Kt lo | alpha (64) | 2 alpha (32)] floats
+    static constexpr int IMG_B1 = 0, IMG_B2 = BFSZ, IMG_KT = 2 * BFSZ, IMG_AL = IMG_KT + 2 * BSZ, IMG_AL2 = IMG_AL + 64;
+    static constexpr int IMG_FLOATS = IMG_AL2 + 32;
+    static_assert(IMG_FLOATS % 4 == 0, "bulk copy: multiple of 16 bytes");
     static_assert(C_D0 >= 2 * C_ASTAGE && C_D0 + NDREG * C_DREGION <= 512, "TMEM budget");
     static_assert(RW == 64 && NBLK * 128 == RH * RW, "blocks of two 64-pixel region rows");
     static_assert(NF_MAX <= 32, "one N = 32 MMA covers the bank");
 };
 
+// A-stage column of (tap, part) in the order above
+__host__ __device__ constexpr int tc_acol(int tap, int part) {
+    return (tap % 5 < 4) ? 8 * (tap / 5) + 2 * (tap % 5) + part : 40 + 2 * (tap / 5) + part;
+}
+
 template <int NF_MAX>
 __host__ __device__ constexpr size_t tc_smem_floats() {
     using T = TcCfg<NF_MAX>;
-    // staged planes u hi/lo, du hi/lo; Kf hi/lo, Kt hi/lo, four tap-24 B operands; Y ring; region gradient (two tap halves); alpha,
-    // (spare), 2 alpha
-    return 4 * (size_t)T::PLANE + 5 * (size_t)T::BSZ + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW + 96;
+    // staged cells (u and du, pair-replicated: 4 floats each); operand image; Y ring; region gradient (two tap halves)
+    return 8 * (size_t)T::PLANE + (size_t)T::IMG_FLOATS + (size_t)T::KT * T::YROWS * T::YW + 2 * (size_t)T::RH * T::RW;
 }
 
 // sum over taps [T0, T1) of Y(row r + a - R, column c + b - R)[a M + b] from the Y ring: one ring-row
@@ -81,124 +94,112 @@ __device__ __forceinline__ float tc_tap_sum(const float *Yr, int r, int c) {
     return s0 + s1;
 }
 
-// im2col of one pixel's taps {8V..8V+7, 16+4V..16+4V+3} (and V = 1: the tap-24 group) from the interleaved staged cells (u hi, u lo,
-// du hi, du lo) into A stage columns (TMEM lane = pixel), 4 taps per round
-template <int V, bool TRIAL, class T>
-__device__ __forceinline__ void tc_im2col(const float4 *sp, uint32_t st) {
+// im2col of one pixel's 25 taps of one quantity (u or du) from its pair-replicated staged cells X[p] =
+// {hi(p), lo(p), hi(p+1), lo(p+1)} into the quantity's KA columns of an A stage (TMEM lane = pixel): per
+// filter row two LDS.128 (taps dx 0..3) and one LDS.64 (dx 4), five tcgen05.st of consecutive registers
+template <class T>
+__device__ __forceinline__ void tc_im2col(const float4 *xp, uint32_t st) {
+    float q[40], c[10];
 #pragma unroll
-    for (int rd = 0; rd < 3; ++rd) {
-        const int c0 = rd < 2 ? 8 * V + 4 * rd : 16 + 4 * V;
-        float uh[4], ul[4], dh[4], dl[4];
+    for (int dy = 0; dy < T::M; ++dy) {
+        const float4 a = xp[dy * T::SW], b = xp[dy * T::SW + 2];
+        const float2 e = *reinterpret_cast<const float2 *>(xp + dy * T::SW + 4);
+        q[8 * dy + 0] = a.x; q[8 * dy + 1] = a.y; q[8 * dy + 2] = a.z; q[8 * dy + 3] = a.w;
+        q[8 * dy + 4] = b.x; q[8 * dy + 5] = b.y; q[8 * dy + 6] = b.z; q[8 * dy + 7] = b.w;
+        c[2 * dy] = e.x; c[2 * dy + 1] = e.y;
+    }
+    tmem_st16(st, *reinterpret_cast<const float(*)[16]>(q));
+    tmem_st16(st + 16, *reinterpret_cast<const float(*)[16]>(q + 16));
+    tmem_st8(st + 32, *reinterpret_cast<const float(*)[8]>(q + 32));
+    tmem_st8(st + 40, *reinterpret_cast<const float(*)[8]>(c));
+    tmem_st2(st + 48, c[8], c[9]);
+}
+
+// 3xTF32 forward product of one quantity: D = A . B1^T + A . B2^T over the KA columns (issued by one thread)
+template <class T>
+__device__ __forceinline__ void tc_forward(uint32_t d_tmem, uint32_t a_tmem, uint64_t b1d, uint64_t b2d) {
+    constexpr uint32_t idesc = idesc_tf32(128, 32);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int t = c0 + i;
-            const float4 c = sp[(t / T::M) * T::SW + (t % T::M)];
-            uh[i] = c.x; ul[i] = c.y; dh[i] = c.z; dl[i] = c.w;
-        }
-        tmem_st4(st + T::C_AUH + c0, uh);
-        tmem_st4(st + T::C_AUL + c0, ul);
-        if (TRIAL) {
-            tmem_st4(st + T::C_ADH + c0, dh);
-            tmem_st4(st + T::C_ADL + c0, dl);
-        }
-    }
-    if (V == 1) {  // tap-24 group: {u hi, u lo, du hi, du lo, 0, 0, 0, 0}
-        const float4 c = sp[(24 / T::M) * T::SW + (24 % T::M)];
-        const float g24[8] = {c.x, c.y, c.z, c.w, 0.0f, 0.0f, 0.0f, 0.0f};
-        tmem_st8(st + T::C_T24, g24);
-    }
+    for (int j = 0; j < T::KSTEPS; ++j) umma_tf32_ts(d_tmem, a_tmem + 8 * j, b1d + (uint64_t)(j * 64), idesc, j > 0 ? 1u : 0u);
+#pragma unroll
+    for (int j = 0; j < T::KSTEPS; ++j) umma_tf32_ts(d_tmem, a_tmem + 8 * j, b2d + (uint64_t)(j * 64), idesc, 1u);
 }
 
 // shared-memory carve-up of the tensor-core pass (dynamic buffers + the static arrays of the kernel)
 struct TcSmem {
-    float4 *S4;                           // staged cells {u hi, u lo, du hi, du lo}
-    float *Kf, *Kt, *K24, *Yr, *Gr, *s_al, *s_al2;
+    float4 *XU, *XD;                      // staged cells, pair-replicated: {hi(p), lo(p), hi(p+1), lo(p+1)} of u / du
+    float *img, *Kt, *Yr, *Gr, *s_al, *s_al2;
     double (*red)[kNumPartials];
     double *s_sum;
-    unsigned long long *mb_dfull, *mb_yfull, *mb_ring, *mb_sum;
+    unsigned long long *mb_dfull, *mb_yfull, *mb_ring, *mb_sum, *mb_img;
 };
 
 template <int NF>
 __device__ __forceinline__ TcSmem tc_carve(float *sm, double (*red)[kNumPartials], double *s_sum,
                                            unsigned long long *mb_dfull, unsigned long long *mb_yfull,
-                                           unsigned long long *mb_ring, unsigned long long *mb_sum) {
+                                           unsigned long long *mb_ring, unsigned long long *mb_sum,
+                                           unsigned long long *mb_img) {
     using T = TcCfg<32>;
     TcSmem S;
-    // staged planes, split once into tf32 hi + lo (both rounded to nearest): u_new - shift and du
-    // (interleaved per cell as {u hi, u lo, du hi, du lo}: one 16-byte load per tap in the im2col)
-    S.S4 = reinterpret_cast<float4 *>(sm);
-    S.Kf = sm + 4 * T::PLANE;      // [hi | lo], forward B (N = filters, K = taps)
-    S.Kt = S.Kf + 2 * T::BSZ;      // [hi | lo], adjoint B (N = taps, K = filters)
-    S.K24 = S.Kt + 2 * T::BSZ;     // tap-24 B operands (K = 8 x N = 32): u hi+lo . hi, u hi . lo, du ..
-    S.Yr = S.K24 + T::BSZ;         // Y ring [tap][ring row][YW]
+    // staged planes, split once into tf32 hi + lo (both rounded to nearest): u_new - shift and du, each cell
+    // also carrying its right neighbour's pair (one 16-byte load = two taps in the im2col)
+    S.XU = reinterpret_cast<float4 *>(sm);
+    S.XD = S.XU + T::PLANE;
+    S.img = sm + 8 * T::PLANE;     // operand image (bulk-copied): forward B1 | B2, adjoint Kt hi | lo, alpha, 2 alpha
+    S.Kt = S.img + T::IMG_KT;      // [hi | lo], adjoint B (N = taps, K = filters)
+    S.s_al = S.img + T::IMG_AL;    // alpha_f, zero-padded
+    S.s_al2 = S.img + T::IMG_AL2;  // 2 alpha_f
+    S.Yr = S.img + T::IMG_FLOATS;  // Y ring [tap][ring row][YW]
     S.Gr = S.Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold), two tap halves
-    S.s_al = S.Gr + 2 * T::RH * T::RW;       // alpha_f, zero-padded
-    S.s_al2 = S.s_al + 64;                   // 2 alpha_f
     S.red = red;
     S.s_sum = s_sum;
-    S.mb_dfull = mb_dfull; S.mb_yfull = mb_yfull; S.mb_ring = mb_ring; S.mb_sum = mb_sum;
+    S.mb_dfull = mb_dfull; S.mb_yfull = mb_yfull; S.mb_ring = mb_ring; S.mb_sum = mb_sum; S.mb_img = mb_img;
     return S;
 }
 
-// once per CTA: TMEM, barriers, B operands, alpha, the Y ring's zero columns (launch arguments only)
+// once per CTA: TMEM, barriers, the operand image (one bulk copy), the Y ring's zero columns (launch
+// arguments only: runs before the dependency on the previous pass is awaited)
 template <int NF>
 __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uint32_t *s_tmem) {
     using T = TcCfg<32>;
-    using C = PassCfg<5>;
-    constexpr int NT = T::NT, R = T::R, SW = T::SW, NBLK = T::NBLK;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    float4 *S4 = S.S4;
-    float *Kf = S.Kf, *Kt = S.Kt, *K24 = S.K24, *Yr = S.Yr, *Gr = S.Gr, *s_al = S.s_al, *s_al2 = S.s_al2;
-    double(*red)[kNumPartials] = S.red;
-    double *s_sum = S.s_sum;
-    unsigned long long *mb_dfull = S.mb_dfull, *mb_yfull = S.mb_yfull, *mb_ring = S.mb_ring, *mb_sum = S.mb_sum;
-    (void)C::NCELL; (void)R; (void)SW; (void)lane; (void)Kf; (void)Kt; (void)K24; (void)s_al; (void)s_al2;
-    const int nf = a.n_filters;
+    constexpr int NT = T::NT, NBLK = T::NBLK;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (tid == 32) {  // warp 1: the bank's operand image, global -> shared (TMA bulk copy, completes on mb_img)
+        mbar_init(S.mb_img, 1);
+        fence_mbar_init();
+        mbar_expect_tx(S.mb_img, T::IMG_FLOATS * 4);
+        bulk_g2s(S.img, a.tc_img, T::IMG_FLOATS * 4, S.mb_img);
+    }
     if (warp == 0) tmem_alloc(s_tmem, 512);
     if (tid == 0) {
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&mb_dfull[s], 1);
-            mbar_init(&mb_yfull[s], 1);
-            if (s == 1) {
-                mbar_init(&mb_dfull[2], 1);
-                mbar_init(&mb_yfull[2], 1);
-            }
+        for (int s = 0; s < T::NDREG; ++s) {
+            mbar_init(&S.mb_dfull[s], 1);
+            mbar_init(&S.mb_yfull[s], 1);
         }
         for (int j = 0; j < NBLK; ++j) {
-            mbar_init(&mb_ring[j], 8);  // one arrival per warp of the draining point set
-            mbar_init(&mb_sum[j], 8);   // one arrival per warp of the summing point set
+            mbar_init(&S.mb_ring[j], 8);  // one arrival per warp of the draining point set
+            mbar_init(&S.mb_sum[j], 8);   // one arrival per warp of the summing point set
         }
-    }
-    // B operands: Kf[f][t] = kf_f[t] (convolution orientation), Kt[t][f] = 2 a_f k_f[t] with the
-    // unflipped k_f[t] = kf_f[24 - t]; zero padding to 32 x 32; split into tf32 hi + tf32 lo (both rounded to nearest)
-    for (int e = tid; e < 32 * 32; e += NT) {
-        const int n = e >> 5, k = e & 31;
-        const float vf = (n < nf && k < T::KT) ? a.kf[n * T::KT + k] : 0.0f;
-        const float vt = (k < nf && n < T::KT) ? 2.0f * a.alpha[k] * a.kf[k * T::KT + (T::KT - 1 - n)] : 0.0f;
-        const float hf = tf32_rn(vf), ht = tf32_rn(vt);
-        Kf[bsw_offset<32>(n, k)] = hf;
-        Kf[T::BSZ + bsw_offset<32>(n, k)] = tf32_rn(vf - hf);
-        Kt[bsw_offset<32>(n, k)] = ht;
-        Kt[T::BSZ + bsw_offset<32>(n, k)] = tf32_rn(vt - ht);
-    }
-    // tap-24 operands: the A group holds (u hi, u lo, du hi, du lo) in K rows 0..3; [0] rows 0, 1 = k24 hi,
-    // [1] row 0 = k24 lo (z = ... + uh.k24h + ul.k24h + uh.k24l), [2] / [3] the same on rows 2, 3 (dz)
-    for (int e = tid; e < 4 * 256; e += NT) {
-        const int mtx = e >> 8, n = (e >> 3) & 31, k = e & 7;
-        const float v24 = n < nf ? a.kf[n * T::KT + 24] : 0.0f, h24 = tf32_rn(v24);
-        const int row = mtx >> 1 ? k - 2 : k;  // row within the (hi, lo) pair of the plane
-        float val = 0.0f;
-        if (row == 0) val = (mtx & 1) ? tf32_rn(v24 - h24) : h24;
-        else if (row == 1 && !(mtx & 1)) val = h24;
-        K24[mtx * 256 + bsw_offset<32>(n, k)] = val;
-    }
-    for (int e = tid; e < 32; e += NT) {
-        s_al[e] = e < nf ? a.alpha[e] : 0.0f;
-        s_al2[e] = e < nf ? 2.0f * a.alpha[e] : 0.0f;
     }
     for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {  // zero columns of the Y ring
         const int col = e & 3, rr = e >> 2;
-        Yr[rr * T::YW + (col < 2 ? col : T::YW - 4 + col)] = 0.0f;
+        S.Yr[rr * T::YW + (col < 2 ? col : T::YW - 4 + col)] = 0.0f;
+    }
+}
+
+// staged cells per thread, and their source offsets within an image (np.pad index maps of image.py:61-65):
+// launch arguments only, so the kernel computes them before it awaits the previous pass
+struct TcCells {
+    static constexpr int CPT = (PassCfg<5>::NCELL + TcCfg<32>::NT - 1) / TcCfg<32>::NT;
+};
+template <bool SYM>
+__device__ __forceinline__ void tc_cell_offsets(const PassArgs &a, const TileGeom &g, int (&coff)[TcCells::CPT]) {
+    using C = PassCfg<5>;
+#pragma unroll
+    for (int q = 0; q < TcCells::CPT; ++q) {
+        const int k = threadIdx.x + q * TcCfg<32>::NT;
+        const int i = k / C::CW, j = k - i * C::CW;
+        coff[q] = k < C::NCELL ? (src_idx<SYM>(g.ry0 - C::R + i, a.H) - a.lrow0) * a.W + src_idx<SYM>(g.rx0 - C::R + j, a.W) : 0;
     }
 }
 
@@ -209,39 +210,43 @@ __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uin
 // and decides).  Returns -1, before touching shared state, if the image is done; else thread 0's ticket.
 template <int NF, bool TRIAL, bool SYM>
 __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const TileGeom &g, const ImgCtl *ctl,
-                                       unsigned rpar, int pbuf, bool take_ticket, int fold_t0,
-                                       unsigned long long *ph, ImgCtl *ctl_keep = nullptr) {
+                                       const int (&coff)[TcCells::CPT], const float (&pob)[TcCells::CPT], unsigned rpar,
+                                       int pbuf, bool take_ticket,
+                                       int fold_t0, unsigned long long *ph, ImgCtl *ctl_keep = nullptr) {
     using T = TcCfg<32>;
     using C = PassCfg<5>;
     constexpr int NT = T::NT, R = T::R, SW = T::SW, NBLK = T::NBLK;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b = blockIdx.y;
-    float4 *S4 = S.S4;
-    float *Kf = S.Kf, *Kt = S.Kt, *K24 = S.K24, *Yr = S.Yr, *Gr = S.Gr, *s_al = S.s_al, *s_al2 = S.s_al2;
+    float2 *xu2 = reinterpret_cast<float2 *>(S.XU), *xd2 = reinterpret_cast<float2 *>(S.XD);
+    float *Kt = S.Kt, *Yr = S.Yr, *Gr = S.Gr, *s_al = S.s_al, *s_al2 = S.s_al2;
     double(*red)[kNumPartials] = S.red;
     double *s_sum = S.s_sum;
     unsigned long long *mb_dfull = S.mb_dfull, *mb_yfull = S.mb_yfull, *mb_ring = S.mb_ring, *mb_sum = S.mb_sum;
-    (void)C::NCELL; (void)R; (void)SW; (void)lane; (void)Kf; (void)Kt; (void)K24; (void)s_al; (void)s_al2;
-    const int nf = a.n_filters;
-    (void)nf;
-    constexpr int CPT = (C::NCELL + NT - 1) / NT;
+    (void)C::NCELL; (void)R; (void)SW; (void)lane; (void)Kt; (void)s_al; (void)s_al2; (void)xd2;
+    static_assert(C::CW == SW, "staged cells are stored without row padding: cell index = i * SW + j");
+    constexpr int CPT = TcCells::CPT;
     const size_t ioff = (size_t)b * a.Hl * a.W;
+    // the control block's trial fields first: their L2 round trip overlaps the candidate loads below
+    TrialParams p{};
+    int c_done = 0;
+    if (a.mode != MODE_EVAL) {
+        p = trial_params(a, *ctl);
+        c_done = ctl->done;
+    }
     // TRIAL: every candidate slot (3 iterate planes, 2 gradient planes) and the observation are loaded
     // before the control block that names the slots is read, so the two L2 round trips overlap
-    float cu[TRIAL ? 3 : 1][CPT], cg[TRIAL ? 2 : 1][CPT], cob[CPT], canc[TRIAL ? 3 : 1];
+    float cu[TRIAL ? 3 : 1][CPT], cg[TRIAL ? 2 : 1][CPT], canc[TRIAL ? 3 : 1];
     if (TRIAL) {
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
             const int k = tid + q * NT;
             if (k < C::NCELL) {
-                const int i = k / C::CW, j = k - i * C::CW;
-                const size_t o = ioff + (size_t)(src_idx<SYM>(g.ry0 - R + i, a.H) - a.lrow0) * a.W +
-                                 src_idx<SYM>(g.rx0 - R + j, a.W);
+                const size_t o = ioff + (size_t)coff[q];
 #pragma unroll
                 for (int sl = 0; sl < 3; ++sl) cu[sl][q] = __ldg(a.U + sl * a.plane + o);
 #pragma unroll
                 for (int sl = 0; sl < 2; ++sl) cg[sl][q] = __ldg(a.Gs + sl * a.plane + o);
-                cob[q] = __ldg(a.obs + o);
             }
         }
         const size_t oa = ioff + (size_t)(g.s0 - a.lrow0) * a.W + g.c0;
@@ -249,14 +254,11 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         for (int sl = 0; sl < 3; ++sl) canc[sl] = a.zero_mean ? __ldg(a.U + sl * a.plane + oa) : 0.0f;
     }
     if (ph && tid == 0) ph[NBLK * 16 + 10] = clock64();  // candidate loads issued
-    TrialParams p{};
     if (a.mode != MODE_EVAL) {
-        const ImgCtl c = *ctl;
-        if (c.done && !a.no_decide) return -1;  // image converged
-        p = trial_params(a, c);
+        if (c_done && !a.no_decide) return -1;  // image converged
         // ctl_keep: the whole block parked in shared memory for this pass's decision (the deciding CTA then
         // needs no L2 round trip for it on the pass-to-pass critical path; only that CTA writes it)
-        if (ctl_keep && tid == 0) *ctl_keep = c;
+        if (ctl_keep && tid == 0) *ctl_keep = *ctl;
     }
     const float *uin, *upv = nullptr, *gin = nullptr, *obs = nullptr;
     float *gout, *uout = nullptr;
@@ -291,12 +293,9 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 lu[q] = p.iu == 0 ? cu[0][q] : p.iu == 1 ? cu[1][q] : cu[2][q];
                 lup[q] = p.iup == 0 ? cu[0][q] : p.iup == 1 ? cu[1][q] : cu[2][q];
                 lg[q] = p.ig == 0 ? cg[0][q] : cg[1][q];
-                lob[q] = cob[q];
+                lob[q] = pob[q];
             } else if (k < C::NCELL) {
-                const int i = k / C::CW, j = k - i * C::CW;
-                const size_t o = (size_t)(src_idx<SYM>(g.ry0 - R + i, a.H) - a.lrow0) * a.W +
-                                 src_idx<SYM>(g.rx0 - R + j, a.W);
-                lu[q] = __ldg(uin + o);
+                lu[q] = __ldg(uin + coff[q]);
             }
         }
 #pragma unroll
@@ -306,7 +305,9 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             const int i = k / C::CW, j = k - i * C::CW;
             if (!TRIAL) {
                 const float x = lu[q] - shift, h = tf32_rn(x);
-                S4[i * SW + j] = make_float4(h, tf32_rn_operand(x - h), 0.0f, 0.0f);
+                const float2 pu = make_float2(h, tf32_rn_operand(x - h));
+                xu2[2 * k] = pu;                  // cell k's own pair ...
+                if (k > 0) xu2[2 * k - 1] = pu;   // ... and its copy as cell k - 1's right neighbour
                 continue;
             }
             const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
@@ -314,7 +315,13 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             const float un = trial_point(u, lup[q], gg, ob, p);  // solver.py:146-149
             const float du = un - u;
             const float x = un - shift, h = tf32_rn(x), hd = tf32_rn(du);
-            S4[i * SW + j] = make_float4(h, tf32_rn_operand(x - h), hd, tf32_rn_operand(du - hd));
+            const float2 pu = make_float2(h, tf32_rn_operand(x - h)), pd = make_float2(hd, tf32_rn_operand(du - hd));
+            xu2[2 * k] = pu;
+            xd2[2 * k] = pd;
+            if (k > 0) {
+                xu2[2 * k - 1] = pu;
+                xd2[2 * k - 1] = pd;
+            }
             if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) {
                 uout[(size_t)(gy - a.lrow0) * a.W + gx] = un;
                 acc[1] += (double)du * (double)du;
@@ -343,6 +350,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    mbar_wait_sleep(S.mb_img, 0u);  // the operand image has landed (bulk copy issued in tc_setup)
     if (a.dbg_times && tid == 0) a.dbg_times[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 3 + 1] = globaltimer_ns();
     // the CTA owns all 512 columns (one CTA per SM), so the allocation starts at column 0: constant
     // TMEM addresses keep the MMA operands in uniform registers
@@ -352,14 +360,20 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
 
     if (warp < T::W_PT) {
         // ================= im2col: block j's A operands into stage j%2 =================
-        // warps 0-3 and 4-7 split the taps (warp 0 issues the forward MMAs)
-        const int pl = tid & 127, v = warp >> 2;  // pixel = TMEM lane; tap split
+        // warps 0-3 build the u columns, warps 4-7 the du columns (warp 0 issues the forward MMAs)
+        const int pl = tid & 127, v = warp >> 2;  // pixel = TMEM lane; quantity
         const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
-        BDescs<32, 3> kfd;
-        kfd.build(smem_u32(Kf), smem_u32(Kf + T::BSZ));
-        uint64_t k24d[4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) k24d[m] = umma_desc_kmajor(smem_u32(K24 + 256 * m), 512, 128);
+        // forward B operands: K-major, N = 32, 16-byte K chunks 512 B apart; K step j starts 1024 B further
+        const uint64_t b1d = umma_desc_kmajor(smem_u32(S.img + T::IMG_B1), 512, 128);
+        const uint64_t b2d = umma_desc_kmajor(smem_u32(S.img + T::IMG_B2), 512, 128);
+        {  // zero columns KA-8 .. KA-1 of both stages once (48, 49 are rewritten per block; the rest pad K to 56)
+            const float z8[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+            if (v == 0 || TRIAL) {
+                tmem_st8(tmem + lane_off + v * T::KA + T::KA - 8, z8);
+                tmem_st8(tmem + lane_off + T::C_ASTAGE + v * T::KA + T::KA - 8, z8);
+                tc_wait_st();
+            }
+        }
         for (int j = 0; j < NBLK; ++j) {
             const int s = j & 1;
             if (j >= 2 && warp != 0) named_sync(T::BAR_AFREE + s, 256);  // released by warp 0 (below)
@@ -367,12 +381,10 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             if (ph && warp == 0) ph[j * 16 + 5] = clock64();
             const uint32_t st = tmem + s * T::C_ASTAGE + lane_off;
             const int lr = 2 * j + (pl >> 6), lc = pl & 63;
-            // taps {0..7, 16..19} (warps 0-3) / {8..15, 20..23} (warps 4-7) of all four planes (compile-time
-            // tap offsets: one LDS.128 with an immediate offset per tap); warps 4-7 also the tap-24 group
             if (v == 0)
-                tc_im2col<0, TRIAL, T>(S4 + lr * SW + lc, st);
-            else
-                tc_im2col<1, TRIAL, T>(S4 + lr * SW + lc, st);
+                tc_im2col<T>(S.XU + lr * SW + lc, st + T::C_AU);
+            else if (TRIAL)
+                tc_im2col<T>(S.XD + lr * SW + lc, st + T::C_AD);
             tc_wait_st();
             tc_fence_before();
             if (warp != 0) named_arrive(T::BAR_AFULL + s, 256);
@@ -391,15 +403,8 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 tc_fence_after();
                 if (ph) ph[j * 16 + 7] = clock64();
                 if (elect_one()) {
-                    constexpr uint32_t idesc = idesc_tf32(128, 32);
-                    umma_3xtf32_pre<32, 3>(sd + T::C_DZ, sa + T::C_AUH, sa + T::C_AUL, kfd, 3);
-                    umma_tf32_ts(sd + T::C_DZ, sa + T::C_T24, k24d[0], idesc, 1u);
-                    umma_tf32_ts(sd + T::C_DZ, sa + T::C_T24, k24d[1], idesc, 1u);
-                    if (TRIAL) {
-                        umma_3xtf32_pre<32, 3>(sd + T::C_DDZ, sa + T::C_ADH, sa + T::C_ADL, kfd, 3);
-                        umma_tf32_ts(sd + T::C_DDZ, sa + T::C_T24, k24d[2], idesc, 1u);
-                        umma_tf32_ts(sd + T::C_DDZ, sa + T::C_T24, k24d[3], idesc, 1u);
-                    }
+                    tc_forward<T>(sd + T::C_DZ, sa + T::C_AU, b1d, b2d);
+                    if (TRIAL) tc_forward<T>(sd + T::C_DDZ, sa + T::C_AD, b1d, b2d);
                     umma_commit(&mb_dfull[rg]);
                 }
                 __syncwarp();
@@ -609,6 +614,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     // ---- per-tile partials first (last CTA of the image reduces and decides, as k_pass): the ticket's
     // round trip overlaps the fold below ----
     warp_partials_smem<0, 1, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));  // Y ring no longer live
+    if (ph && tid == 0) ph[NBLK * 16 + 14] = clock64();  // warp partial of the energy change
     block_combine<NT>(red, s_sum);
     if (ph && tid == 0) ph[NBLK * 16 + 5] = clock64();  // block reduction done
     int ticket = 0;
@@ -667,7 +673,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     __shared__ int s_last;
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) unsigned long long mb_dfull[T::NDREG], mb_yfull[T::NDREG];
-    __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK];
+    __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK], mb_img;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b = blockIdx.y;
@@ -688,9 +694,17 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     griddep_launch_dependents();
     const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
     const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
-    const TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_ring, mb_sum);
+    const TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_ring, mb_sum, &mb_img);
     tc_setup<NF>(a, S, &s_tmem);
+    int coff[TcCells::CPT];
+    tc_cell_offsets<SYM>(a, g, coff);
+    // the observation never changes during a solve: its cells are loaded before the dependency is awaited
+    float pob[TcCells::CPT];
+#pragma unroll
+    for (int q = 0; q < TcCells::CPT; ++q)
+        pob[q] = (TRIAL && tid + q * NT < PassCfg<5>::NCELL) ? __ldg(a.obs + (size_t)b * a.Hl * a.W + coff[q]) : 0.0f;
     griddep_wait();  // the previous pass (control block, iterates, gradients, partials) is complete
+    if (a.dbg_times && tid == 0) a.dbg_times[3 * (size_t)gridDim.x * gridDim.y + 512 + cta] = globaltimer_ns();
     if (ph && tid == 0) ph[NBLK * 16 + 3] = clock64();  // dependency resolved
     if (tid == 0 && s_tmem != 0u) __trap();
     constexpr uint32_t tmem = 0u;
@@ -699,7 +713,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     // reduces and decides while warps 8-23 fold (RW * 8 = 512 items, one each)
     const bool split = !a.band && nlaunch <= kFastReduceTiles && T::RW * 8 <= NT - 256;
     __shared__ ImgCtl s_ctl;
-    const int ticket = tc_body<NF, TRIAL, SYM>(a, S, g, a.mode == MODE_EVAL ? nullptr : a.ctl + b, 0u, 0, !a.band,
+    const int ticket = tc_body<NF, TRIAL, SYM>(a, S, g, a.mode == MODE_EVAL ? nullptr : a.ctl + b, coff, pob, 0u, 0, !a.band,
                                                split ? 256 : 0, ph, &s_ctl);
     if (ticket < 0) {
         __syncthreads();  // image converged: release TMEM and leave
@@ -718,19 +732,22 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         named_sync(T::BAR_EPI, 256);
         if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
         if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket seen
-        if (warp == 0) tmem_dealloc(tmem, 512);
+        // TMEM is released by warp 7, which takes no part in the reduction (tcgen05.dealloc blocks its warp:
+        // on warp 0 it sat on the deciding CTA's critical path)
+        static_assert(kNumPartials <= 7, "warp 7 is free of the tile reduction");
+        if (warp == 7) {
+            tmem_dealloc(tmem, 512);
+            return;
+        }
         if (!s_last) return;
         // (no fence: thread 0's acquiring ticket and the barrier above order the loads below)
-        if (warp < kNumPartials) {  // the fixed order of reduce_tiles' fast path
-            double x = 0.0;
-#pragma unroll 8
-            for (int tt = lane; tt < nlaunch; tt += 32)
-                x += __ldcg(a.partials + ((size_t)tt * a.B + b) * kPartialStride + warp);
+        {  // warps 0..6: the fixed order of reduce_tiles' fast path
+            double x = lane_tile_sum(a.partials, nlaunch, a.B, b, warp, lane);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
             if (lane == 0) s_sum[warp] = x;
         }
-        named_sync(T::BAR_EPI, 256);
+        named_sync(T::BAR_EPI, 224);
     } else {
         if (tid == 0) s_last = ticket == nlaunch - 1;
         __syncthreads();
@@ -748,5 +765,6 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             decide_ctl(a, b, s_sum, c, true, a.mode);
             a.ctl[b] = c;
         }
+        if (a.dbg_times) a.dbg_times[4 * (size_t)gridDim.x * gridDim.y + 512 + cta] = globaltimer_ns();  // decider done
     }
 }

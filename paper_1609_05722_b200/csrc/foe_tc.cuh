@@ -99,6 +99,10 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
                  : "memory");
 }
 
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, float v0, float v1) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "f"(v0), "f"(v1) : "memory");
+}
+
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, const float (&v)[4]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "f"(v[0]), "f"(v[1]),
                  "f"(v[2]), "f"(v[3])
@@ -133,6 +137,19 @@ __device__ __forceinline__ void mbar_wait_sleep(unsigned long long *bar, unsigne
     while (!mbar_test(bar, parity)) {
         if (FOE_SLEEP_NS > 0) __nanosleep(FOE_SLEEP_NS);
     }
+}
+
+// TMA bulk copy global -> shared (cp.async.bulk, no tensor map): one thread issues it, the bytes land through
+// the async proxy and complete the transaction count armed on the mbarrier
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst_smem)),
+                 "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 // hardware named barriers: producers arrive without blocking, the consumer warp blocks in sync

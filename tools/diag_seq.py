@@ -24,7 +24,7 @@ L.foe_debug_pass_times_seq.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_i
                                        ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 ws = res._workspace
 ncta = (-(-H // 32)) * (-(-W // 60))
-stride = 3 * ncta + 512
+stride = 5 * ncta + 512
 t = torch.zeros(NP * stride, dtype=torch.int64, device="cuda")
 for _ in range(3):
     _lib.check(L.foe_debug_pass_times_seq(res._bank.handle, 1, H, W, res._cap, ws.data_ptr(), ws.numel(), t.data_ptr(),
@@ -38,6 +38,10 @@ for k in range(NP):
     start, loop, end = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, (a[:, 2] - t0) / 1e3
     line = (f"pass {k}: first start {start.min():8.2f}  last start {start.max():8.2f}  median loop-start "
             f"{np.median(loop):8.2f}  median exit {np.median(end):8.2f}  last exit {end.max():8.2f} us")
+    rel = (full[k * stride + 3 * ncta + 512:k * stride + 4 * ncta + 512] - t0) / 1e3
+    dec = full[k * stride + 4 * ncta + 512:k * stride + 5 * ncta + 512]
+    dec = (dec[dec > 0].max() - t0) / 1e3 if (dec > 0).any() else float("nan")
+    line += f"\n        released: first {rel.min():8.2f} median {np.median(rel):8.2f} last {rel.max():8.2f}  decider done {dec:8.2f}"
     if prev_exit is not None:
         line += f"  | gap last-exit(k-1) -> median loop-start(k) {np.median(loop) - prev_exit:6.2f}"
     print(line)

@@ -19,7 +19,7 @@ res = fp.solve_device(model, v, v, 0.6075, "quadratic", 150, fp.SolverConfig(rel
 L = _lib.lib()
 ws = res._workspace
 ncta = (-(-H // 32)) * (-(-W // 60))
-t = torch.zeros(ncta * 3 + 18 * 16 + 16, dtype=torch.int64, device="cuda")
+t = torch.zeros(ncta * 5 + 512, dtype=torch.int64, device="cuda")
 for _ in range(3):
     _lib.check(L.foe_debug_pass_times(res._bank.handle, 1, H, W, res._cap, ws.data_ptr(), ws.numel(), t.data_ptr(),
                                       torch.cuda.current_stream().cuda_stream))
@@ -28,9 +28,9 @@ full = t.cpu().numpy()
 a = full[:ncta * 3].reshape(ncta, 3).astype(np.float64)
 phs = full[ncta * 3:ncta * 3 + 18 * 16].reshape(18, 16).astype(np.float64)
 loop0 = float(full[ncta * 3 + 18 * 16])
-ext = full[ncta * 3 + 18 * 16: ncta * 3 + 18 * 16 + 14].astype(np.float64)
+ext = full[ncta * 3 + 18 * 16: ncta * 3 + 18 * 16 + 15].astype(np.float64)
 if ext[2]:
-    names = ["loop start", "loop end", "kernel start", "griddep done", "fold done", "block reduce done", "ticket", "tmem released", "first fold value", "first fold store", "loads issued", "ctl read", "cells staged", "warp partials"]
+    names = ["loop start", "loop end", "kernel start", "griddep done", "fold done", "block reduce done", "ticket", "tmem released", "first fold value", "first fold store", "loads issued", "ctl read", "cells staged", "warp partials", "dF warp partial"]
     print("CTA (0,0) phase stamps, cycles from kernel start:",
           {n: int(ext[i] - ext[2]) for i, n in enumerate(names) if ext[i]})
 if phs.any():
