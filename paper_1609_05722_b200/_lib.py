@@ -133,7 +133,8 @@ def lib():
     L.foe_score_workspace_size.restype = ctypes.c_size_t
     L.foe_score.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, _vp, _vp, _vp,
                             ctypes.c_size_t, _vp]
-    L.foe_debug_tc_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
+    L.foe_debug_tc_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
+    L.foe_debug_tmem_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
     L.foe_debug_pass_times.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
                                        ctypes.c_size_t, _vp, _vp]
     _lib = L
@@ -155,7 +156,7 @@ EXPORTED_SYMBOLS = [
     "foe_prox_quadratic", "foe_prox_idiv", "foe_bin", "foe_unbin_bilinear", "foe_estimate_peak", "foe_convolve_same", "foe_convolve_adjoint",
     "foe_eval_workspace_size", "foe_energy_grad", "foe_solve_workspace_size", "foe_solve",
     "foe_bench_trial_pass", "foe_debug_pass_times", "foe_tc_selftest", "foe_pass_uses_tensor_cores",
-    "foe_debug_tc_rate", "foe_measure_ffma_peak", "foe_debug_pass_times_seq", "foe_score_workspace_size", "foe_score",
+    "foe_debug_tc_rate", "foe_debug_tmem_rate", "foe_measure_ffma_peak", "foe_debug_pass_times_seq", "foe_score_workspace_size", "foe_score",
     "foe_conv_bank64", "foe_adjoint_bank64", "foe_hessian_apply64", "foe_cg_workspace_size", "foe_cg_solve64", "foe_tile_grid", "foe_band_geometry", "foe_band_describe", "foe_band_workspace_size",
     "foe_band_buffers_get", "foe_band_begin", "foe_band_trial", "foe_band_commit", "foe_band_final_pass", "foe_band_end",
 ]

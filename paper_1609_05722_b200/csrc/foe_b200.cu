@@ -2073,17 +2073,27 @@ int foe_cg_solve64(const double *filters, const double *weights, int n, int m, i
 
 int foe_pass_uses_tensor_cores(int m, int nf) { return (use_tc(m, nf) || use_tc7(m, nf)) ? 1 : 0; }
 
-int foe_debug_tc_rate(int n, int ts, int nmma, long long *out_cycles, void *stream) {
+int foe_debug_tmem_rate(int nwarps, int store, int iters, long long *out_cycles, void *stream) {
+    if (nwarps < 4 || nwarps > 32 || nwarps % 4) return fail(FOE_E_INVALID, "nwarps must be a multiple of 4 in 4..32");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (store) k_tmem_rate<true><<<1, 32 * nwarps, 0, st>>>(iters, out_cycles);
+    else k_tmem_rate<false><<<1, 32 * nwarps, 0, st>>>(iters, out_cycles);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_debug_tc_rate(int n, int ts, int nmma, int nchain, long long *out_cycles, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n != 32 && n != 64 && n != 128) return fail(FOE_E_INVALID, "n must be 32, 64 or 128");
+    if (nchain < 1 || nchain * n > 256) return fail(FOE_E_INVALID, "nchain accumulators of n columns must fit 256 columns");
     if (ts) {
-        if (n == 32) k_tc_rate<32, true><<<1, 128, 0, st>>>(nmma, out_cycles);
-        if (n == 64) k_tc_rate<64, true><<<1, 128, 0, st>>>(nmma, out_cycles);
-        if (n == 128) k_tc_rate<128, true><<<1, 128, 0, st>>>(nmma, out_cycles);
+        if (n == 32) k_tc_rate<32, true><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
+        if (n == 64) k_tc_rate<64, true><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
+        if (n == 128) k_tc_rate<128, true><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
     } else {
-        if (n == 32) k_tc_rate<32, false><<<1, 128, 0, st>>>(nmma, out_cycles);
-        if (n == 64) k_tc_rate<64, false><<<1, 128, 0, st>>>(nmma, out_cycles);
-        if (n == 128) k_tc_rate<128, false><<<1, 128, 0, st>>>(nmma, out_cycles);
+        if (n == 32) k_tc_rate<32, false><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
+        if (n == 64) k_tc_rate<64, false><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
+        if (n == 128) k_tc_rate<128, false><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
     }
     FOE_CUDA(cudaGetLastError());
     return FOE_OK;

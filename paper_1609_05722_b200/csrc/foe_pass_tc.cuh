@@ -31,10 +31,10 @@ struct TcCfg {
     static constexpr int R = 2, M = 5, KT = 25;
     static constexpr int RH = P::RH, RW = P::RW, SH = P::SH, SW = P::SW, PLANE = P::PLANE;
     static constexpr int NBLK = RH * RW / 128;  // 128-pixel blocks (two region rows each)
-    static constexpr int W_PT = 8, NWARPS = 24, NT = NWARPS * 32;
-    // named barriers, one per stage / set: A complete, Psi complete, D region free, forward done (relayed
-    // to the set), adjoint done (relayed to the set), A stage free (relayed to the im2col warps)
-    static constexpr int BAR_AFULL = 1, BAR_PFULL = 3, BAR_DFULL = 5, BAR_AFREE = 9, BAR_DFREE = 11, BAR_EPI = 14;
+    // warps 0-7 movers (im2col, Y drain, shifted sums), 8-15 / 16-23 the two point sets, 24 the MMA issuer
+    static constexpr int W_PT = 8, W_MMA = 24, NWARPS = 25, NT = NWARPS * 32;
+    // named barriers: the movers' per-block barrier (ring writes before ring reads), the epilogue's
+    static constexpr int BAR_MOVERS = 1, BAR_EPI = 14;
     static constexpr int RING = 4;                       // Y ring: 4 blocks = 8 region rows
     static constexpr int YROWS = 2 * RING, YW = RW + 4;  // 2 zero columns each side
     static constexpr int BSZ = 32 * 32;                  // one 32 x 32 B operand (floats)
@@ -131,14 +131,14 @@ struct TcSmem {
     float *img, *Kt, *Yr, *Gr, *s_al, *s_al2;
     double (*red)[kNumPartials];
     double *s_sum;
-    unsigned long long *mb_dfull, *mb_yfull, *mb_ring, *mb_sum, *mb_img;
+    unsigned long long *mb_dfull, *mb_yfull, *mb_afull, *mb_pfull, *mb_dfree, *mb_img;
 };
 
 template <int NF>
 __device__ __forceinline__ TcSmem tc_carve(float *sm, double (*red)[kNumPartials], double *s_sum,
                                            unsigned long long *mb_dfull, unsigned long long *mb_yfull,
-                                           unsigned long long *mb_ring, unsigned long long *mb_sum,
-                                           unsigned long long *mb_img) {
+                                           unsigned long long *mb_afull, unsigned long long *mb_pfull,
+                                           unsigned long long *mb_dfree, unsigned long long *mb_img) {
     using T = TcCfg<32>;
     TcSmem S;
     // staged planes, split once into tf32 hi + lo (both rounded to nearest): u_new - shift and du, each cell
@@ -153,7 +153,8 @@ __device__ __forceinline__ TcSmem tc_carve(float *sm, double (*red)[kNumPartials
     S.Gr = S.Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold), two tap halves
     S.red = red;
     S.s_sum = s_sum;
-    S.mb_dfull = mb_dfull; S.mb_yfull = mb_yfull; S.mb_ring = mb_ring; S.mb_sum = mb_sum; S.mb_img = mb_img;
+    S.mb_dfull = mb_dfull; S.mb_yfull = mb_yfull; S.mb_afull = mb_afull; S.mb_pfull = mb_pfull; S.mb_dfree = mb_dfree;
+    S.mb_img = mb_img;
     return S;
 }
 
@@ -162,7 +163,7 @@ __device__ __forceinline__ TcSmem tc_carve(float *sm, double (*red)[kNumPartials
 template <int NF>
 __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uint32_t *s_tmem) {
     using T = TcCfg<32>;
-    constexpr int NT = T::NT, NBLK = T::NBLK;
+    constexpr int NT = T::NT;
     const int tid = threadIdx.x, warp = tid >> 5;
     if (tid == 32) {  // warp 1: the bank's operand image, global -> shared (TMA bulk copy, completes on mb_img)
         mbar_init(S.mb_img, 1);
@@ -173,12 +174,13 @@ __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uin
     if (warp == 0) tmem_alloc(s_tmem, 512);
     if (tid == 0) {
         for (int s = 0; s < T::NDREG; ++s) {
-            mbar_init(&S.mb_dfull[s], 1);
-            mbar_init(&S.mb_yfull[s], 1);
+            mbar_init(&S.mb_dfull[s], 1);  // forward MMAs of the region's block committed
+            mbar_init(&S.mb_yfull[s], 1);  // adjoint MMAs committed
+            mbar_init(&S.mb_dfree[s], 8);  // Y drained: one arrival per mover warp
         }
-        for (int j = 0; j < NBLK; ++j) {
-            mbar_init(&S.mb_ring[j], 8);  // one arrival per warp of the draining point set
-            mbar_init(&S.mb_sum[j], 8);   // one arrival per warp of the summing point set
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&S.mb_afull[s], 8);  // A stage built: one arrival per mover warp
+            mbar_init(&S.mb_pfull[s], 8);  // Psi written: one arrival per warp of the point set
         }
     }
     for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {  // zero columns of the Y ring
@@ -222,7 +224,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     float *Kt = S.Kt, *Yr = S.Yr, *Gr = S.Gr, *s_al = S.s_al, *s_al2 = S.s_al2;
     double(*red)[kNumPartials] = S.red;
     double *s_sum = S.s_sum;
-    unsigned long long *mb_dfull = S.mb_dfull, *mb_yfull = S.mb_yfull, *mb_ring = S.mb_ring, *mb_sum = S.mb_sum;
+    unsigned long long *mb_dfull = S.mb_dfull, *mb_yfull = S.mb_yfull;
     (void)C::NCELL; (void)R; (void)SW; (void)lane; (void)Kt; (void)s_al; (void)s_al2; (void)xd2;
     static_assert(C::CW == SW, "staged cells are stored without row padding: cell index = i * SW + j");
     constexpr int CPT = TcCells::CPT;
@@ -358,139 +360,141 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     // per-block role stamps: [block][im2col, fwd, point, sum]
     if (ph && tid == 0) ph[NBLK * 16] = clock64();  // loop start (cycles)
 
-    if (warp < T::W_PT) {
-        // ================= im2col: block j's A operands into stage j%2 =================
-        // warps 0-3 build the u columns, warps 4-7 the du columns (warp 0 issues the forward MMAs)
-        const int pl = tid & 127, v = warp >> 2;  // pixel = TMEM lane; quantity
-        const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+    // warp-uniform role index (a shuffle result lets the compiler keep it, and the TMEM addresses derived from
+    // it, in uniform registers)
+    const int wu = __shfl_sync(0xffffffffu, warp, 0);
+    if (wu == T::W_MMA) {
+        // ================= MMA issuer: forward(j), then adjoint(j-1) =================
         // forward B operands: K-major, N = 32, 16-byte K chunks 512 B apart; K step j starts 1024 B further
         const uint64_t b1d = umma_desc_kmajor(smem_u32(S.img + T::IMG_B1), 512, 128);
         const uint64_t b2d = umma_desc_kmajor(smem_u32(S.img + T::IMG_B2), 512, 128);
-        {  // zero columns KA-8 .. KA-1 of both stages once (48, 49 are rewritten per block; the rest pad K to 56)
-            const float z8[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-            if (v == 0 || TRIAL) {
-                tmem_st8(tmem + lane_off + v * T::KA + T::KA - 8, z8);
-                tmem_st8(tmem + lane_off + T::C_ASTAGE + v * T::KA + T::KA - 8, z8);
-                tc_wait_st();
-            }
-        }
-        for (int j = 0; j < NBLK; ++j) {
-            const int s = j & 1;
-            if (j >= 2 && warp != 0) named_sync(T::BAR_AFREE + s, 256);  // released by warp 0 (below)
-            tc_fence_after();
-            if (ph && warp == 0) ph[j * 16 + 5] = clock64();
-            const uint32_t st = tmem + s * T::C_ASTAGE + lane_off;
-            const int lr = 2 * j + (pl >> 6), lc = pl & 63;
-            if (v == 0)
-                tc_im2col<T>(S.XU + lr * SW + lc, st + T::C_AU);
-            else if (TRIAL)
-                tc_im2col<T>(S.XD + lr * SW + lc, st + T::C_AD);
-            tc_wait_st();
-            tc_fence_before();
-            if (warp != 0) named_arrive(T::BAR_AFULL + s, 256);
-            if (warp == 0) {
-                // release stage (j+1)%2 for the next im2col as soon as forward(j-1) has read it, before
-                // forward(j) is issued: the im2col of block j+1 overlaps this warp's issue of block j
-                if (j >= 1 && j + 1 < NBLK) {
-                    mbar_wait_sleep(&mb_dfull[(j - 1) % T::NDREG], ((j - 1) / T::NDREG) & 1);
-                    named_arrive(T::BAR_AFREE + (s ^ 1), 256);
-                }
-                // forward(j) once A is complete and block j-3 left D region j%3
-                const int rg = j % T::NDREG;
-                const uint32_t sa = tmem + s * T::C_ASTAGE, sd = tmem + T::C_D0 + rg * T::C_DREGION;
-                named_sync(T::BAR_AFULL + s, 256);
-                if (j >= T::NDREG) named_sync(T::BAR_DFREE + rg, 288);  // Y(j-3) drained by its point set
+        BDescs<32, NF / 8> ktd;
+        ktd.build(smem_u32(Kt), smem_u32(Kt + T::BSZ));
+        for (int j = 0; j <= NBLK; ++j) {
+            if (j < NBLK) {  // forward(j) once its A stage is built and block j-3's Y has left D region j%3
+                const int s = j & 1, rg = j % T::NDREG;
+                mbar_wait(&S.mb_afull[s], (j >> 1) & 1);
+                if (j >= T::NDREG) mbar_wait(&S.mb_dfree[rg], ((j - T::NDREG) / T::NDREG) & 1);
                 tc_fence_after();
-                if (ph) ph[j * 16 + 7] = clock64();
                 if (elect_one()) {
+                    const uint32_t sa = tmem + s * T::C_ASTAGE, sd = tmem + T::C_D0 + rg * T::C_DREGION;
                     tc_forward<T>(sd + T::C_DZ, sa + T::C_AU, b1d, b2d);
                     if (TRIAL) tc_forward<T>(sd + T::C_DDZ, sa + T::C_AD, b1d, b2d);
                     umma_commit(&mb_dfull[rg]);
                 }
                 __syncwarp();
-                if (ph) ph[j * 16 + 0] = clock64();
+                if (ph) ph[j * 16 + 0] = clock64();  // forward issued
+            }
+            if (j >= 1) {  // adjoint(j-1) once its point set wrote Psi over z / dz
+                const int jj = j - 1, rg = jj % T::NDREG;
+                mbar_wait(&S.mb_pfull[jj & 1], (jj >> 1) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t sb = tmem + T::C_D0 + rg * T::C_DREGION;
+                    umma_3xtf32_pre<32, NF / 8>(sb + T::C_DY, sb + T::C_DZ, sb + T::C_DDZ, ktd, NF / 8);
+                    umma_commit(&mb_yfull[rg]);
+                }
+                __syncwarp();
+                if (ph) ph[jj * 16 + 2] = clock64();  // adjoint issued
             }
         }
-    } else {
-        // ================= point sets: drain Y one block late, shifted sums, psi, energy terms =========
-        // set s handles blocks j = s (mod 2); at step j it first drains Y(j-2) -- its own previous block,
-        // whose adjoint ran while it evaluated that block's energy terms -- into the ring (freeing D region
-        // (j+1)%3 for forward(j+1)), sums g(j-3) over its tap half once Y(j-4 .. j-2) are in the ring, and
-        // then evaluates block j: psi' -> adjoint(j) issued, energy terms.  Steps j >= NBLK only drain/sum.
-        const int q4 = warp & 3, hf = ((warp - T::W_PT) >> 2) & 1;  // lane quarter; filter / tap half
-        const int set = (warp - T::W_PT) >> 3;                        // blocks j = set (mod 2)
-        const bool issuer = warp == T::W_PT + 8 * set;  // whole warp; one elected lane issues
-        BDescs<32, NF / 8> ktd;
-        ktd.build(smem_u32(Kt), smem_u32(Kt + T::BSZ));
-        const int pl = 32 * q4 + lane;
-        const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
-        constexpr int FH = NF / 2;  // filters per half, in chunks of 4
-        const int f0 = FH * hf;
-        double e_own = 0.0;
-        for (int j = set; j < NBLK + 3; j += 2) {
-            const int s = set, jd = j - 2, js = j - 3;  // block to drain, block to sum
-            const bool comp = j < NBLK, drain = jd >= 0 && jd < NBLK, sum = js >= 0 && js < NBLK;
-            const int rg = j % T::NDREG;  // D region of block j
-            if (issuer) {  // forward(j) and adjoint(j-2) complete: polled by the set's first warp, relayed
-                if (comp) mbar_wait_sleep(&mb_dfull[rg], (j / T::NDREG) & 1);
-                if (drain) mbar_wait_sleep(&mb_yfull[jd % T::NDREG], (jd / T::NDREG) & 1);
-                named_arrive(T::BAR_DFULL + s, 256);
-            } else {
-                named_sync(T::BAR_DFULL + s, 256);
+    } else if (wu < T::W_PT) {
+        // ================= movers: im2col(j), drain Y(j-2) into the ring, shifted sum g(j-3) =================
+        // warps 0-3 build the u columns, warps 4-7 the du columns; warps w and w+4 share a TMEM lane quarter and
+        // split the taps of the drain (16 + 9) and of the sum (12 + 13)
+        const int pl = tid & 127, hf = wu >> 2;
+        const uint32_t lane_off = (uint32_t)(32 * (wu & 3)) << 16;
+        {  // zero columns KA-8 .. KA-1 of both stages once (48, 49 are rewritten per block; the rest pad K to 56)
+            const float z8[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+            if (hf == 0 || TRIAL) {
+                tmem_st8(tmem + lane_off + hf * T::KA + T::KA - 8, z8);
+                tmem_st8(tmem + lane_off + T::C_ASTAGE + hf * T::KA + T::KA - 8, z8);
+                tc_wait_st();
             }
-            tc_fence_after();
-            if (drain) {  // Y(jd): half 0 taps 0..15, half 1 taps 16..24, into ring slot jd % RING
+        }
+        const float4 *xsrc = (hf == 0 ? S.XU : S.XD) + (pl >> 6) * SW + (pl & 63);
+        const int prow = pl >> 6, pcol = pl & 63;
+        for (int j = 0; j < NBLK + 3; ++j) {
+            if (j < NBLK) {
+                const int s = j & 1;
+                // forward(j-2) has read stage s
+                if (j >= 2) mbar_wait_sleep(&mb_dfull[(j - 2) % T::NDREG], ((j - 2) / T::NDREG) & 1);
+                tc_fence_after();
+                if (ph && wu == 0) ph[j * 16 + 5] = clock64();  // im2col start
+                if (hf == 0 || TRIAL) {
+                    tc_im2col<T>(xsrc + 2 * j * SW, tmem + s * T::C_ASTAGE + lane_off + hf * T::KA);
+                    tc_wait_st();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.mb_afull[s]);
+                if (ph && wu == 0) ph[j * 16 + 7] = clock64();  // A stage built
+            }
+            const int jd = j - 2, js = j - 3;
+            if (jd >= 0 && jd < NBLK) {  // Y(jd): half 0 taps 0..15, half 1 taps 16..24, into ring slot jd % RING
+                const int rg = jd % T::NDREG;
+                mbar_wait_sleep(&mb_yfull[rg], (jd / T::NDREG) & 1);
+                tc_fence_after();
+                if (ph && wu == 0) ph[jd * 16 + 8] = clock64();  // adjoint seen
                 float y[16];
-                tmem_ld16(tmem + T::C_D0 + (jd % T::NDREG) * T::C_DREGION + lane_off + T::C_DY + 16 * hf, y);
+                tmem_ld16(tmem + T::C_D0 + rg * T::C_DREGION + lane_off + T::C_DY + 16 * hf, y);
                 tc_wait_ld();
                 tc_fence_before();
-                if (jd + T::NDREG < NBLK) named_arrive(T::BAR_DFREE + jd % T::NDREG, 288);  // for forward(jd + 3)
-                // the slot held Y(jd - 4), read by g(jd - 5) .. g(jd - 3): g(jd - 5) and g(jd - 3) were summed
-                // by this set (steps j - 4, j - 2), g(jd - 4) by the other one
-                if (jd >= T::RING) mbar_wait_sleep(&mb_sum[jd - T::RING], rpar);
-                const int lr = 2 * jd + (pl >> 6), lc = pl & 63;
-                float *yrow = Yr + (lr & (T::YROWS - 1)) * T::YW + 2 + lc;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.mb_dfree[rg]);  // for forward(jd + 3)
+                float *yrow = Yr + ((2 * jd + prow) & (T::YROWS - 1)) * T::YW + 2 + pcol;
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int t = 16 * hf + i;
                     if (t < T::KT) yrow[t * T::YROWS * T::YW] = y[i];
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&mb_ring[jd]);
-                if (ph && (warp - T::W_PT) % 8 == 0) ph[jd * 16 + 3] = clock64();
+                if (ph && wu == 0) ph[jd * 16 + 3] = clock64();  // Y in the ring
             }
-            if (sum) {  // g(js) over this warp's tap half (0..11 / 12..24) once Y(js-1 .. js+1) are in the ring
-                for (int n = js - 1; n <= js + 1; ++n)
-                    if (n >= 0 && n < NBLK) mbar_wait_sleep(&mb_ring[n], rpar);
-                const int r = 2 * js + (pl >> 6), c = pl & 63;
+            // ring slot jd % RING held Y(jd-4), last read by g(jd-3) = g(j-5) two iterations ago; this iteration's
+            // ring writes are ordered before its reads by the movers' barrier
+            named_sync(T::BAR_MOVERS, 256);
+            if (js >= 0 && js < NBLK) {  // g(js) over this warp's tap half once Y(js-1 .. js+1) are in the ring
+                const int r = 2 * js + prow;
                 float gsum;
                 if (js == 0 || js == NBLK - 1)
-                    gsum = hf ? tc_tap_sum<12, 25, true, T>(Yr, r, c) : tc_tap_sum<0, 12, true, T>(Yr, r, c);
+                    gsum = hf ? tc_tap_sum<12, 25, true, T>(Yr, r, pcol) : tc_tap_sum<0, 12, true, T>(Yr, r, pcol);
                 else
-                    gsum = hf ? tc_tap_sum<12, 25, false, T>(Yr, r, c) : tc_tap_sum<0, 12, false, T>(Yr, r, c);
-                Gr[hf * T::RH * T::RW + r * T::RW + c] = gsum;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&mb_sum[js]);
-                if (ph && (warp - T::W_PT) % 8 == 0) ph[js * 16 + 4] = clock64();
+                    gsum = hf ? tc_tap_sum<12, 25, false, T>(Yr, r, pcol) : tc_tap_sum<0, 12, false, T>(Yr, r, pcol);
+                Gr[hf * T::RH * T::RW + r * T::RW + pcol] = gsum;
+                if (ph && wu == 0) ph[js * 16 + 4] = clock64();  // g summed
             }
-            if (!comp) continue;
+        }
+    } else {
+        // ================= point sets: psi', energy terms =================
+        // set s handles blocks j = s (mod 2): z, dz -> psi' (tf32 hi / lo written over them as the adjoint's A
+        // operand) -> p_full; then the energy terms while the adjoint runs.  Warps w and w+4 of a set share a
+        // TMEM lane quarter (same 32 pixels) and split the filters.
+        const int q4 = wu & 3, hf = ((wu - T::W_PT) >> 2) & 1;  // lane quarter; filter half
+        const int set = (wu - T::W_PT) >> 3;                     // blocks j = set (mod 2)
+        const int pl = 32 * q4 + lane;
+        const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
+        constexpr int FH = NF / 2;  // filters per half
+        const int f0 = FH * hf;
+        const int lc = pl & 63, gx = g.rx0 + lc;
+        const bool col_in = !SYM || (gx >= 0 && gx < a.W), col_own = gx >= g.c0 && gx < g.c1;
+        double e_own = 0.0;
+        for (int j = set; j < NBLK; j += 2) {
+            const int rg = j % T::NDREG;  // D region of block j
+            mbar_wait_sleep(&mb_dfull[rg], (j / T::NDREG) & 1);
+            tc_fence_after();
+            const bool pst = ph && (wu - T::W_PT) % 8 == 0;
+            if (pst) ph[j * 16 + 1] = clock64();  // forward seen
             const uint32_t sd = tmem + T::C_D0 + rg * T::C_DREGION + lane_off;
-            const int lr = 2 * j + (pl >> 6), lc = pl & 63;
-            const int gy = g.ry0 + lr, gx = g.rx0 + lc;
-            const bool in_img = !SYM || (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W);
-            const bool owned = gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1;
-            const bool pst = ph && (warp - T::W_PT) % 8 == 0;
-            if (pst) ph[j * 16 + 1] = clock64();
+            const int gy = g.ry0 + 2 * j + (pl >> 6);
+            const bool in_img = col_in && (!SYM || (gy >= 0 && gy < a.H));
+            const bool owned = col_own && gy >= g.s0 && gy < g.s1;
             // this half's filters: all z / dz loads in flight at once; psi' (tf32 hi / lo, written over
             // the z / dz columns as the adjoint's A operand, whose K covers filters < NF only) and the
             // atanh arguments for every filter with full ILP; Psi is handed to the adjoint MMA before
             // the energy series are evaluated
             float z[FH], dz[FH];
-#pragma unroll
-            for (int c = 0; c < FH / 4; ++c) {
-                tmem_ld4(sd + T::C_DZ + f0 + 4 * c, *reinterpret_cast<float(*)[4]>(&z[4 * c]));
-                if (TRIAL) tmem_ld4(sd + T::C_DDZ + f0 + 4 * c, *reinterpret_cast<float(*)[4]>(&dz[4 * c]));
-            }
+            tmem_ldn<FH>(sd + T::C_DZ + f0, z);
+            if (TRIAL) tmem_ldn<FH>(sd + T::C_DDZ + f0, dz);
             tc_wait_ld();
             float tmax = 0.0f;
             // psi' (zero on padded cells outside the image: a warp-uniform test, edge tiles only)
@@ -499,14 +503,15 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
 #pragma unroll
                     for (int i = 0; i < FH; i += 2) {
                         const float2 zz = make_float2(z[i], z[i + 1]), d = make_float2(dz[i], dz[i + 1]);
-                        const float2 zo = __fadd2_rn(zz, make_float2(-d.x, -d.y));
-                        // psi' = z / (1+z^2) and t = (z^2 - zo^2) / (2+z^2+zo^2): two MUFU reciprocals (the
-                        // XU pipe has room; fewer issue slots than one reciprocal of the product)
+                        // psi' = z / (1+z^2) and t = (z^2 - zo^2) / (2+z^2+zo^2) with zo = z - d:
+                        // z^2 - zo^2 = d (2z - d) and 2+z^2+zo^2 = 2 (1+z^2) - (z^2 - zo^2); two MUFU
+                        // reciprocals (the XU pipe has room; fewer issue slots than one reciprocal of the product)
                         const float2 a1 = __ffma2_rn(zz, zz, make_float2(1.0f, 1.0f));
-                        const float2 b1 = __fadd2_rn(__ffma2_rn(zo, zo, a1), make_float2(1.0f, 1.0f));
+                        const float2 s2 = __ffma2_rn(zz, make_float2(2.0f, 2.0f), make_float2(-d.x, -d.y));
+                        const float2 nm = __fmul2_rn(d, s2);
+                        const float2 b1 = __ffma2_rn(a1, make_float2(2.0f, 2.0f), make_float2(-nm.x, -nm.y));
                         const float2 ps = __fmul2_rn(zz, make_float2(rcp_approx(a1.x), rcp_approx(a1.y)));
-                        const float2 tt = __fmul2_rn(__fmul2_rn(d, __fadd2_rn(zz, zo)),
-                                                     make_float2(rcp_approx(b1.x), rcp_approx(b1.y)));
+                        const float2 tt = __fmul2_rn(nm, make_float2(rcp_approx(b1.x), rcp_approx(b1.y)));
                         dz[i] = tt.x;
                         dz[i + 1] = tt.y;
                         tmax = fmaxf(tmax, fmaxf(fabsf(tt.x), fabsf(tt.y)));
@@ -527,32 +532,25 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 point(std::true_type{});
             else
                 point(std::false_type{});
+            {
+                float hi[FH], lo[FH];
 #pragma unroll
-            for (int c = 0; c < FH / 4; ++c) {
-                float hi[4], lo[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    hi[i] = tf32_rn(z[4 * c + i]);
-                    lo[i] = tf32_rn_operand(z[4 * c + i] - hi[i]);
+                for (int i = 0; i < FH; i += 2) {
+                    hi[i] = tf32_rn(z[i]);
+                    hi[i + 1] = tf32_rn(z[i + 1]);
+                    const float2 l2 = __fadd2_rn(make_float2(z[i], z[i + 1]), make_float2(-hi[i], -hi[i + 1]));
+                    lo[i] = tf32_rn_operand(l2.x);
+                    lo[i + 1] = tf32_rn_operand(l2.y);
                 }
-                tmem_st4(sd + T::C_DZ + f0 + 4 * c, hi);
-                tmem_st4(sd + T::C_DDZ + f0 + 4 * c, lo);
+                tmem_stn<FH>(sd + T::C_DZ + f0, hi);
+                tmem_stn<FH>(sd + T::C_DDZ + f0, lo);
             }
             tc_wait_st();
             tc_fence_before();
-            if (!issuer) named_arrive(T::BAR_PFULL + s, 256);
-            if (issuer) {  // adjoint(j) once both halves of all four lane quarters wrote Psi
-                const uint32_t sb = tmem + T::C_D0 + rg * T::C_DREGION;
-                named_sync(T::BAR_PFULL + s, 256);
-                tc_fence_after();
-                if (elect_one()) {
-                    umma_3xtf32_pre<32, NF / 8>(sb + T::C_DY, sb + T::C_DZ, sb + T::C_DDZ, ktd, NF / 8);
-                    umma_commit(&mb_yfull[rg]);
-                }
-                __syncwarp();
-                if (ph) ph[j * 16 + 2] = clock64();
-            }
-            // energy terms while the adjoint MMAs run (Y(j) is drained at step j + 2)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.mb_pfull[set]);
+            if (pst) ph[j * 16 + 6] = clock64();  // Psi handed over
+            // energy terms while the adjoint MMAs run
             float e0 = 0.0f, e1 = 0.0f;
             if (TRIAL) {
                 // 2 a atanh(t) = 2 a (t + t^3/3 + ...): the series is cut where the next term is below fp32
@@ -605,6 +603,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 }
             }
             if (owned) e_own += (double)(e0 + e1);
+            if (pst) ph[j * 16 + 9] = clock64();  // energy terms done
         }
         acc[0] = e_own;
     }
@@ -673,7 +672,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     __shared__ int s_last;
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) unsigned long long mb_dfull[T::NDREG], mb_yfull[T::NDREG];
-    __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK], mb_img;
+    __shared__ __align__(8) unsigned long long mb_afull[2], mb_pfull[2], mb_dfree[T::NDREG], mb_img;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b = blockIdx.y;
@@ -694,7 +693,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     griddep_launch_dependents();
     const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
     const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
-    const TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_ring, mb_sum, &mb_img);
+    const TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_afull, mb_pfull, mb_dfree, &mb_img);
     tc_setup<NF>(a, S, &s_tmem);
     int coff[TcCells::CPT];
     tc_cell_offsets<SYM>(a, g, coff);

@@ -116,6 +116,30 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
                  : "memory");
 }
 
+// N = 4, 8, 12 or 16 consecutive columns in the fewest instructions (12 = 8 + 4)
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, float (&v)[N]) {
+    static_assert(N == 4 || N == 8 || N == 12 || N == 16, "column count");
+    if constexpr (N == 16) tmem_ld16(taddr, v);
+    if constexpr (N == 8) tmem_ld8(taddr, v);
+    if constexpr (N == 4) tmem_ld4(taddr, v);
+    if constexpr (N == 12) {
+        tmem_ld8(taddr, *reinterpret_cast<float(*)[8]>(&v[0]));
+        tmem_ld4(taddr + 8, *reinterpret_cast<float(*)[4]>(&v[8]));
+    }
+}
+template <int N>
+__device__ __forceinline__ void tmem_stn(uint32_t taddr, const float (&v)[N]) {
+    static_assert(N == 4 || N == 8 || N == 12 || N == 16, "column count");
+    if constexpr (N == 16) tmem_st16(taddr, v);
+    if constexpr (N == 8) tmem_st8(taddr, v);
+    if constexpr (N == 4) tmem_st4(taddr, v);
+    if constexpr (N == 12) {
+        tmem_st8(taddr, *reinterpret_cast<const float(*)[8]>(&v[0]));
+        tmem_st4(taddr + 8, *reinterpret_cast<const float(*)[4]>(&v[8]));
+    }
+}
+
 // mbarrier wait: a non-blocking probe, then probes with a short nanosleep backoff so waiting warps
 // leave the issue slots to the working ones
 __device__ __forceinline__ bool mbar_test(unsigned long long *bar, unsigned parity) {
@@ -326,7 +350,7 @@ __device__ __forceinline__ void umma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, u
 }
 
 template <int N, bool TS>
-__global__ void __launch_bounds__(128) k_tc_rate(int nmma, long long *out) {
+__global__ void __launch_bounds__(128) k_tc_rate(int nmma, int nchain, long long *out) {
     __shared__ __align__(128) float sA[128 * 8];
     __shared__ __align__(128) float sB[N * 8];
     __shared__ uint32_t s_tmem;
@@ -347,9 +371,12 @@ __global__ void __launch_bounds__(128) k_tc_rate(int nmma, long long *out) {
         const uint32_t idesc = idesc_tf32(128, N);
         const long long c0 = clock64();
         if (elect_one()) {
+            // nchain independent accumulators (D columns 256 + N c), issued round robin: a dependent chain of
+            // small MMAs exposes the pipeline's accumulate latency, independent chains overlap
             for (int i = 0; i < nmma; ++i) {
-                if (TS) umma_tf32_ts(t0 + 256, t0, bd, idesc, i > 0);
-                else umma_tf32_ss(t0 + 256, ad, bd, idesc, i > 0);
+                const uint32_t d = t0 + 256 + (uint32_t)((i % nchain) * N);
+                if (TS) umma_tf32_ts(d, t0, bd, idesc, i >= nchain);
+                else umma_tf32_ss(d, ad, bd, idesc, i >= nchain);
             }
             umma_commit(&s_mbar);
         }
@@ -361,5 +388,56 @@ __global__ void __launch_bounds__(128) k_tc_rate(int nmma, long long *out) {
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(t0, 512);
+}
+
+// ------------------------------------------------------------------------------------------------
+// TMEM read / write throughput probe: nwarps warps (4 per lane quarter group) each issue `iters` rounds of four
+// tcgen05.ld (or st) .32x32b.x32 (512 bytes per lane quarter per instruction); clock64 cycles -> out[0]
+template <bool STORE>
+__global__ void __launch_bounds__(1024) k_tmem_rate(int iters, long long *out) {
+    __shared__ uint32_t s_tmem;
+    __shared__ long long s_t[32];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) tmem_alloc(&s_tmem, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t base = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+    tmem_st32(base, v);
+    tmem_st32(base + 32, v);
+    tmem_st32(base + 64, v);
+    tmem_st32(base + 96, v);
+    tc_wait_st();
+    __syncthreads();
+    const long long c0 = clock64();
+    float acc = 0.0f;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (STORE) {
+                tmem_st32(base + 32 * k, v);
+            } else {
+                float w[32];
+                tmem_ld32(base + 32 * k, w);
+                tc_wait_ld();
+                acc += w[0] + w[31];
+            }
+        }
+        if (STORE) tc_wait_st();
+    }
+    const long long c1 = clock64();
+    if ((tid & 31) == 0) s_t[warp] = c1 - c0;
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+        long long m = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = s_t[w] > m ? s_t[w] : m;
+        out[0] = m;
+        out[1] = (long long)acc;
+    }
+    if (warp == 0) tmem_dealloc(s_tmem, 512);
 }
 

@@ -36,8 +36,8 @@ if ext[2]:
 if phs.any():
     np.set_printoptions(precision=0, suppress=True, linewidth=200)
     cols = [0, 1, 2, 3, 4, 5, 6, 7, 8, 9]
-    print("block stamps (cycles from loop start), TC pass: fwd-issued, fwd-seen (point), adj-issued, Y-in-ring, "
-          "g-done, im2col-start, sum-loads-done, d_free-seen, sum-start, ring-seen")
+    print("block stamps (cycles from loop start): fwd issued (MMA), fwd seen (point), adj issued (MMA), Y in ring (mover), "
+          "g summed (mover), im2col start (mover), Psi handed over (point), A built (mover), adj seen (mover), energy done (point)")
     tab = phs[:, cols] - loop0
     tab[phs[:, cols] == 0] = -1
     print(tab.astype(np.int64))

@@ -11,11 +11,15 @@ L = _lib.lib()
 out = torch.zeros(1, dtype=torch.int64, device="cuda")
 for ts in (1, 0):
     for n in (32, 64, 128):
-        res = []
-        for nm in (1, 9, 27, 108):
-            for _ in range(2):
-                _lib.check(L.foe_debug_tc_rate(n, ts, nm, out.data_ptr(), torch.cuda.current_stream().cuda_stream))
-            torch.cuda.synchronize()
-            res.append((nm, int(out.item())))
-        per = (res[-1][1] - res[1][1]) / (res[-1][0] - res[1][0])
-        print(f"{'TS' if ts else 'SS'} N={n}: " + ", ".join(f"{nm}->{c}" for nm, c in res) + f"  => {per:.1f} cycles/MMA")
+        for nchain in (1, 2, 3, 4):
+            if nchain * n > 256:
+                continue
+            res = []
+            for nm in (1, 12, 36, 108):
+                for _ in range(2):
+                    _lib.check(L.foe_debug_tc_rate(n, ts, nm, nchain, out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+                torch.cuda.synchronize()
+                res.append((nm, int(out.item())))
+            per = (res[-1][1] - res[1][1]) / (res[-1][0] - res[1][0])
+            print(f"{'TS' if ts else 'SS'} N={n} chains={nchain}: " + ", ".join(f"{nm}->{c}" for nm, c in res) +
+                  f"  => {per:.1f} cycles/MMA")
