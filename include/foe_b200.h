@@ -190,7 +190,7 @@ int foe_pass_uses_tensor_cores(int m, int nf);
 /* diagnostics: cycles (clock64, into device out_cycles[0]) for one thread to issue `nmma`
  * accumulating kind::tf32 MMAs of M = 128, N = n (32 / 64 / 128), K = 8, A in TMEM (ts = 1) or
  * shared memory (ts = 0), and observe their commit */
-int foe_debug_tc_rate(int n, int ts, int nmma, int nchain, long long *out_cycles, void *stream);
+int foe_debug_tc_rate(int n, int ts, int nmma, int nchain, int every, long long *out_cycles, void *stream);
 /* diagnostics: tcgen05.ld / st throughput with nwarps warps (out_cycles[0] = cycles for iters x 4 x 512 B per warp) */
 int foe_debug_tmem_rate(int nwarps, int store, int iters, long long *out_cycles, void *stream);
 /* diagnostics: the tcgen05 / TMEM primitives of the tensor-core pass on one 128 x 32 x 32 product,

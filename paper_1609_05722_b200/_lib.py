@@ -133,7 +133,7 @@ def lib():
     L.foe_score_workspace_size.restype = ctypes.c_size_t
     L.foe_score.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, _vp, _vp, _vp,
                             ctypes.c_size_t, _vp]
-    L.foe_debug_tc_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
+    L.foe_debug_tc_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
     L.foe_debug_tmem_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
     L.foe_debug_pass_times.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
                                        ctypes.c_size_t, _vp, _vp]

@@ -1256,6 +1256,56 @@ __global__ void __launch_bounds__(512) k_ffma_peak(float *out, int iters, float 
     if (s == 1234.5f) out[0] = s;  // keeps the chains live
 }
 
+// Shared-memory operand image of k_pass_tc (TcCfg<32>::IMG_*), built once per bank: forward B1 / B2 (N = 32
+// filters x K = 56 A columns, K-major SWIZZLE_NONE), adjoint Kt hi / lo (N = 32 taps x K = 32 filters), alpha,
+// 2 alpha.  tf32 hi / lo both rounded to nearest-even, as cvt.rn.tf32.f32 does.
+namespace {
+float tf32_rn_host(float x) {
+    uint32_t b;
+    memcpy(&b, &x, 4);
+    b += 0xFFFu + ((b >> 13) & 1u);
+    b &= 0xffffe000u;
+    memcpy(&x, &b, 4);
+    return x;
+}
+template <int NF>
+void tc_operand_image_t(std::vector<float> &img, const float *kf, const float *al, int nf) {
+    using T = TcCfg<32>;
+    using CL = TcCols<NF>;
+    // K-major SWIZZLE_NONE operand of N rows: 8-row groups 128 B apart, 16-byte K chunks (N / 8) * 128 B apart
+    auto boff = [](int N, int n, int k) { return (n & 7) * 4 + (k & 3) + (n >> 3) * 32 + (k >> 2) * (N / 8) * 32; };
+    for (int f = 0; f < nf; ++f)
+        for (int t = 0; t < T::KT; ++t) {
+            const float v = kf[f * T::KT + t], h = tf32_rn_host(v), l = tf32_rn_host(v - h);
+            img[T::IMG_BF + boff(CL::NZ, CL::brow(f, 0), tc_acol(t, 0))] = h;  // z1: u_hi k_hi
+            img[T::IMG_BF + boff(CL::NZ, CL::brow(f, 0), tc_acol(t, 1))] = h;  //     u_lo k_hi
+            img[T::IMG_BF + boff(CL::NZ, CL::brow(f, 1), tc_acol(t, 0))] = l;  // z2: u_hi k_lo
+        }
+    // adjoint: Kt[t][f] = 2 a_f k_f[t] with the unflipped k_f[t] = kf_f[24 - t]; K1 and K2 are N = 32 row operands
+    for (int t = 0; t < T::KT; ++t)
+        for (int f = 0; f < nf; ++f) {
+            const float v = 2.0f * al[f] * kf[f * T::KT + (T::KT - 1 - t)], h = tf32_rn_host(v), l = tf32_rn_host(v - h);
+            img[T::IMG_KT + boff(32, t, CL::kcol(f, 0))] = h;   // K1: psi_hi kt_hi
+            img[T::IMG_KT + boff(32, t, CL::kcol(f, 1))] = h;   //     psi_lo kt_hi
+            img[T::IMG_KT2 + boff(32, t, CL::kcol(f, 0))] = l;  // K2: psi_hi kt_lo
+        }
+    for (int f = 0; f < nf; ++f) {
+        img[T::IMG_AL + f] = al[f];
+        img[T::IMG_AL2 + f] = 2.0f * al[f];
+    }
+}
+std::vector<float> tc_operand_image(const float *kf, const float *al, int nf) {
+    std::vector<float> img(TcCfg<32>::IMG_FLOATS, 0.0f);
+    switch ((nf + 7) / 8) {  // the kernel instantiation (launch_pass)
+        case 1: tc_operand_image_t<8>(img, kf, al, nf); break;
+        case 2: tc_operand_image_t<16>(img, kf, al, nf); break;
+        case 3: tc_operand_image_t<24>(img, kf, al, nf); break;
+        default: tc_operand_image_t<32>(img, kf, al, nf); break;
+    }
+    return img;
+}
+}  // namespace
+
 extern "C" {
 
 int foe_abi_version(void) { return 1; }
@@ -1285,42 +1335,6 @@ int foe_device_sm_count(int device) {
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
     return v;
-}
-
-// Shared-memory operand image of k_pass_tc (TcCfg<32>::IMG_*), built once per bank: forward B1 / B2 (N = 32
-// filters x K = 56 A columns, K-major SWIZZLE_NONE), adjoint Kt hi / lo (N = 32 taps x K = 32 filters), alpha,
-// 2 alpha.  tf32 hi / lo both rounded to nearest-even, as cvt.rn.tf32.f32 does.
-static float tf32_rn_host(float x) {
-    uint32_t b;
-    memcpy(&b, &x, 4);
-    b += 0xFFFu + ((b >> 13) & 1u);
-    b &= 0xffffe000u;
-    memcpy(&x, &b, 4);
-    return x;
-}
-static std::vector<float> tc_operand_image(const float *kf, const float *al, int nf) {
-    using T = TcCfg<32>;
-    std::vector<float> img(T::IMG_FLOATS, 0.0f);
-    auto boff = [](int n, int k) { return (n & 7) * 4 + (k & 3) + (n >> 3) * 32 + (k >> 2) * 128; };  // bsw_offset<32>
-    for (int n = 0; n < nf; ++n)
-        for (int t = 0; t < T::KT; ++t) {
-            const float v = kf[n * T::KT + t], h = tf32_rn_host(v), l = tf32_rn_host(v - h);
-            img[T::IMG_B1 + boff(n, tc_acol(t, 0))] = h;  // u_hi k_hi
-            img[T::IMG_B1 + boff(n, tc_acol(t, 1))] = h;  // u_lo k_hi
-            img[T::IMG_B2 + boff(n, tc_acol(t, 0))] = l;  // u_hi k_lo
-        }
-    // Kt[t][f] = 2 a_f k_f[t] with the unflipped k_f[t] = kf_f[24 - t]
-    for (int t = 0; t < T::KT; ++t)
-        for (int f = 0; f < nf; ++f) {
-            const float v = 2.0f * al[f] * kf[f * T::KT + (T::KT - 1 - t)], h = tf32_rn_host(v);
-            img[T::IMG_KT + boff(t, f)] = h;
-            img[T::IMG_KT + T::BSZ + boff(t, f)] = tf32_rn_host(v - h);
-        }
-    for (int f = 0; f < nf; ++f) {
-        img[T::IMG_AL + f] = al[f];
-        img[T::IMG_AL2 + f] = 2.0f * al[f];
-    }
-    return img;
 }
 
 int foe_bank_create(const double *filters, const double *weights, int n, int m, int boundary, foe_bank **out) {
@@ -2082,18 +2096,18 @@ int foe_debug_tmem_rate(int nwarps, int store, int iters, long long *out_cycles,
     return FOE_OK;
 }
 
-int foe_debug_tc_rate(int n, int ts, int nmma, int nchain, long long *out_cycles, void *stream) {
+int foe_debug_tc_rate(int n, int ts, int nmma, int nchain, int every, long long *out_cycles, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (n != 32 && n != 64 && n != 128) return fail(FOE_E_INVALID, "n must be 32, 64 or 128");
     if (nchain < 1 || nchain * n > 256) return fail(FOE_E_INVALID, "nchain accumulators of n columns must fit 256 columns");
     if (ts) {
-        if (n == 32) k_tc_rate<32, true><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
-        if (n == 64) k_tc_rate<64, true><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
-        if (n == 128) k_tc_rate<128, true><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
+        if (n == 32) k_tc_rate<32, true><<<1, 128, 0, st>>>(nmma, nchain, every, out_cycles);
+        if (n == 64) k_tc_rate<64, true><<<1, 128, 0, st>>>(nmma, nchain, every, out_cycles);
+        if (n == 128) k_tc_rate<128, true><<<1, 128, 0, st>>>(nmma, nchain, every, out_cycles);
     } else {
-        if (n == 32) k_tc_rate<32, false><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
-        if (n == 64) k_tc_rate<64, false><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
-        if (n == 128) k_tc_rate<128, false><<<1, 128, 0, st>>>(nmma, nchain, out_cycles);
+        if (n == 32) k_tc_rate<32, false><<<1, 128, 0, st>>>(nmma, nchain, every, out_cycles);
+        if (n == 64) k_tc_rate<64, false><<<1, 128, 0, st>>>(nmma, nchain, every, out_cycles);
+        if (n == 128) k_tc_rate<128, false><<<1, 128, 0, st>>>(nmma, nchain, every, out_cycles);
     }
     FOE_CUDA(cudaGetLastError());
     return FOE_OK;

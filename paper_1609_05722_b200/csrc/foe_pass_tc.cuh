@@ -25,37 +25,72 @@
 // Within a point set, warps w and w+4 share a TMEM lane quarter (same 32 pixels) and split the
 // filters (forward side, NF/2 each) and taps (adjoint side, 16 + 9).  24 warps: 80 registers/thread.
 
+#ifndef FOE_MMA_SLEEP
+#define FOE_MMA_SLEEP 0  // ns between the MMA warp's polls of its mbarriers
+#endif
+#ifndef FOE_ABLATE
+#define FOE_ABLATE 0  // timing diagnostics only (results wrong): 1 no shifted sums, 2 no energy series, 4 no psi math, 8 one MMA per sweep, 16 no im2col loads
+#endif
+
 template <int NF_MAX>
 struct TcCfg {
     using P = PassCfg<5>;
     static constexpr int R = 2, M = 5, KT = 25;
     static constexpr int RH = P::RH, RW = P::RW, SH = P::SH, SW = P::SW, PLANE = P::PLANE;
     static constexpr int NBLK = RH * RW / 128;  // 128-pixel blocks (two region rows each)
-    // warps 0-7 movers (im2col, Y drain, shifted sums), 8-15 / 16-23 the two point sets, 24 the MMA issuer
-    static constexpr int W_PT = 8, W_MMA = 24, NWARPS = 25, NT = NWARPS * 32;
+    // warps 0-7 movers (im2col, shifted sums), 8-15 / 16-23 the two point sets (psi', energy terms, Y drain),
+    // 24 / 25 / 26 the MMA issuers of z, dz and the adjoint
+    static constexpr int W_PT = 8, W_MMA = 24, NWARPS = 27, NT = NWARPS * 32;
     // named barriers: the movers' per-block barrier (ring writes before ring reads), the epilogue's
     static constexpr int BAR_MOVERS = 1, BAR_EPI = 14;
     static constexpr int RING = 4;                       // Y ring: 4 blocks = 8 region rows
+    static constexpr int SUMLAG = 4;                     // the movers sum g(j - SUMLAG) after im2col(j)
     static constexpr int YROWS = 2 * RING, YW = RW + 4;  // 2 zero columns each side
     static constexpr int BSZ = 32 * 32;                  // one 32 x 32 B operand (floats)
-    // A stage (TMEM, lane = pixel): two quantities (u, du) of KA = 56 columns each.  Column order = the
+    // A operands (TMEM, lane = pixel): two quantities (u, du) of KA = 56 columns each.  Column order = the
     // order the im2col loads deliver them, so every tcgen05.st takes consecutive registers: per filter row
     // dy the pairs {hi, lo} of taps dx 0..3 (8 columns, two LDS.128 of the pair-replicated staged cells),
     // then the {hi, lo} pairs of tap dx = 4 of the five rows (10 columns), then 6 zero columns.
     //   column 8 dy + 2 dx + part (dx < 4);  40 + 2 dy + part (dx = 4);  part 0 = tf32 hi, 1 = tf32 lo
-    // B1[k][f] = k_hi[tap(k)] on both parts (u_hi k_hi + u_lo k_hi), B2[k][f] = k_lo[tap(k)] on part 0
-    // (u_hi k_lo): the 3xTF32 product is two K = 56 sweeps, 14 MMAs per quantity.
-    static constexpr int KA = 56, KSTEPS = KA / 8, BFSZ = 32 * KA;
-    static constexpr int C_AU = 0, C_AD = KA, C_ASTAGE = 2 * KA;
-    static constexpr int C_D0 = 2 * C_ASTAGE, C_DZ = 0, C_DDZ = 32, C_DY = 64, C_DREGION = 96, NDREG = 3;
+    static constexpr int KA = 56, KSTEPS = KA / 8, NDREG = 3;
+    // A tcgen05.mma of this shape (M = 128, K = 8, tf32) occupies the tensor pipe ~51 cycles for any N <= 64
+    // (tools/tc_rate.py), so the block loop is bound by the MMA *count*: the two sweeps of a 3xTF32 product
+    // are merged along N instead of being issued one after the other --
+    //   forward  [z1 | z2] = A . [B1 | B2]^T,  B1[k] = k_hi[tap(k)] on both parts (u_hi k_hi + u_lo k_hi),
+    //            B2[k] = k_lo[tap(k)] on part 0 (u_hi k_lo): N = 2 NF, 7 MMAs per quantity, z = z1 + z2
+    //   adjoint  Y = Psi . K1^T + Psi . K2^T, Psi = {hi, lo} pairs per filter (K = 2 NF), K1 = Kt_hi on both
+    //            parts, K2 = Kt_lo on part 0: N = 32, two sweeps of NF / 4 MMAs into the same columns (a merged
+    //            N = 64 adjoint would cost 16 more TMEM columns per D region -- the second du stage)
+    // (26 MMAs per 128-pixel block at NF = 24; ~23 / 28 / 32 pipe cycles per MMA at N = 32 / 48 / 64, tools/tc_rate.py).
     // operand image built once per bank on the host (foe_bank_create) and copied into shared memory by one
-    // bulk copy per CTA: [B1 | B2 | Kt hi | Kt lo | alpha (64) | 2 alpha (32)] floats
-    static constexpr int IMG_B1 = 0, IMG_B2 = BFSZ, IMG_KT = 2 * BFSZ, IMG_AL = IMG_KT + 2 * BSZ, IMG_AL2 = IMG_AL + 64;
+    // bulk copy per CTA: [forward (2 NF x 56) | adjoint K1 (32 x 2 NF) | K2 | alpha (64) | 2 alpha (32)] floats,
+    // sized for NF = 32
+    static constexpr int IMG_BF = 0, IMG_KT = 64 * KA, IMG_KT2 = IMG_KT + 32 * 64, IMG_AL = IMG_KT2 + 32 * 64, IMG_AL2 = IMG_AL + 64;
     static constexpr int IMG_FLOATS = IMG_AL2 + 32;
     static_assert(IMG_FLOATS % 4 == 0, "bulk copy: multiple of 16 bytes");
-    static_assert(C_D0 >= 2 * C_ASTAGE && C_D0 + NDREG * C_DREGION <= 512, "TMEM budget");
     static_assert(RW == 64 && NBLK * 128 == RH * RW, "blocks of two 64-pixel region rows");
     static_assert(NF_MAX <= 32, "one N = 32 MMA covers the bank");
+};
+
+// TMEM plan for a bank of NF (multiple of 8) filters.  D region of a block: [Z: z1 | z2 per filter half, then Psi
+// pairs in place, 2 NF columns][W: dz1 | dz2 per filter half, then Y (32 columns) over them].  Within Z (and
+// W) the point thread of filter half h owns columns [h NF, (h + 1) NF): part p of its filter i at h NF + p NF/2 + i,
+// its Psi pair at h NF + 2 i + part -- so a thread overwrites only what it has read itself.  Three regions at
+// the top of TMEM, the A operands below them: NU u stages and ND du stages of KA columns.
+template <int NF>
+struct TcCols {
+    using T = TcCfg<32>;
+    static constexpr int FH = NF / 2, NZ = 2 * NF, REGION = NZ + (NZ > 32 ? NZ : 32), C_Z = 0, C_W = NZ;
+    static constexpr int C_D0 = 512 - T::NDREG * REGION;
+    // both quantities double-buffered when TMEM allows (a single du stage puts im2col -> dz -> its completion
+    // on a one-block cycle)
+    static constexpr int NU = C_D0 >= 4 * T::KA ? 2 : 1, ND = NU;
+    static constexpr int C_AU = 0, C_AD = NU * T::KA;
+    static_assert(NF % 8 == 0 && NF <= 32, "filter count rounded up to a multiple of 8");
+    static_assert((NU + ND) * T::KA <= C_D0 && NZ <= 64, "TMEM budget");
+    // forward operand row of (filter f, part p); adjoint operand K column of (filter f, part)
+    __host__ __device__ static constexpr int brow(int f, int p) { return (f / FH) * NF + p * FH + f % FH; }
+    __host__ __device__ static constexpr int kcol(int f, int part) { return 2 * f + part; }
 };
 
 // A-stage column of (tap, part) in the order above
@@ -115,14 +150,15 @@ __device__ __forceinline__ void tc_im2col(const float4 *xp, uint32_t st) {
     tmem_st2(st + 48, c[8], c[9]);
 }
 
-// 3xTF32 forward product of one quantity: D = A . B1^T + A . B2^T over the KA columns (issued by one thread)
-template <class T>
-__device__ __forceinline__ void tc_forward(uint32_t d_tmem, uint32_t a_tmem, uint64_t b1d, uint64_t b2d) {
-    constexpr uint32_t idesc = idesc_tf32(128, 32);
+// forward product of one quantity, both 3xTF32 sweeps in one N = 2 NF operand: [z1 | z2] = A . [B1 | B2]^T over the
+// KA columns, one MMA per K step (issued by one thread); bd: descriptor of K step 0, the next 16-byte K chunk
+// pair LBO2 bytes further
+template <class T, int N>
+__device__ __forceinline__ void tc_forward(uint32_t d_tmem, uint32_t a_tmem, uint64_t bd) {
+    constexpr uint32_t idesc = idesc_tf32(128, N);
+    constexpr uint64_t step = (uint64_t)(2 * (N / 8) * 128 / 16);  // two K chunks, in 16-byte units
 #pragma unroll
-    for (int j = 0; j < T::KSTEPS; ++j) umma_tf32_ts(d_tmem, a_tmem + 8 * j, b1d + (uint64_t)(j * 64), idesc, j > 0 ? 1u : 0u);
-#pragma unroll
-    for (int j = 0; j < T::KSTEPS; ++j) umma_tf32_ts(d_tmem, a_tmem + 8 * j, b2d + (uint64_t)(j * 64), idesc, 1u);
+    for (int j = 0; j < ((FOE_ABLATE & 8) ? 1 : T::KSTEPS); ++j) umma_tf32_ts(d_tmem, a_tmem + 8 * j, bd + j * step, idesc, j > 0 ? 1u : 0u);
 }
 
 // shared-memory carve-up of the tensor-core pass (dynamic buffers + the static arrays of the kernel)
@@ -131,29 +167,32 @@ struct TcSmem {
     float *img, *Kt, *Yr, *Gr, *s_al, *s_al2;
     double (*red)[kNumPartials];
     double *s_sum;
-    unsigned long long *mb_dfull, *mb_yfull, *mb_afull, *mb_pfull, *mb_dfree, *mb_img;
+    unsigned long long *mb_dfull, *mb_yfull, *mb_aufull, *mb_adfull, *mb_zfull, *mb_pfull, *mb_dfree, *mb_ring, *mb_sum, *mb_img;
 };
 
 template <int NF>
 __device__ __forceinline__ TcSmem tc_carve(float *sm, double (*red)[kNumPartials], double *s_sum,
                                            unsigned long long *mb_dfull, unsigned long long *mb_yfull,
-                                           unsigned long long *mb_afull, unsigned long long *mb_pfull,
-                                           unsigned long long *mb_dfree, unsigned long long *mb_img) {
+                                           unsigned long long *mb_aufull, unsigned long long *mb_adfull,
+                                           unsigned long long *mb_zfull, unsigned long long *mb_pfull,
+                                           unsigned long long *mb_dfree, unsigned long long *mb_ring,
+                                           unsigned long long *mb_sum, unsigned long long *mb_img) {
     using T = TcCfg<32>;
     TcSmem S;
     // staged planes, split once into tf32 hi + lo (both rounded to nearest): u_new - shift and du, each cell
     // also carrying its right neighbour's pair (one 16-byte load = two taps in the im2col)
     S.XU = reinterpret_cast<float4 *>(sm);
     S.XD = S.XU + T::PLANE;
-    S.img = sm + 8 * T::PLANE;     // operand image (bulk-copied): forward B1 | B2, adjoint Kt hi | lo, alpha, 2 alpha
-    S.Kt = S.img + T::IMG_KT;      // [hi | lo], adjoint B (N = taps, K = filters)
+    S.img = sm + 8 * T::PLANE;     // operand image (bulk-copied): forward [B1 | B2], adjoint [K1 | K2], alpha, 2 alpha
+    S.Kt = S.img + T::IMG_KT;      // adjoint B operands K1 | K2 (N = 32 taps, K = {hi, lo} pairs of the filters)
     S.s_al = S.img + T::IMG_AL;    // alpha_f, zero-padded
     S.s_al2 = S.img + T::IMG_AL2;  // 2 alpha_f
     S.Yr = S.img + T::IMG_FLOATS;  // Y ring [tap][ring row][YW]
     S.Gr = S.Yr + T::KT * T::YROWS * T::YW;  // region gradient (before the fold), two tap halves
     S.red = red;
     S.s_sum = s_sum;
-    S.mb_dfull = mb_dfull; S.mb_yfull = mb_yfull; S.mb_afull = mb_afull; S.mb_pfull = mb_pfull; S.mb_dfree = mb_dfree;
+    S.mb_dfull = mb_dfull; S.mb_yfull = mb_yfull; S.mb_aufull = mb_aufull; S.mb_adfull = mb_adfull; S.mb_zfull = mb_zfull;
+    S.mb_pfull = mb_pfull; S.mb_dfree = mb_dfree; S.mb_ring = mb_ring; S.mb_sum = mb_sum;
     S.mb_img = mb_img;
     return S;
 }
@@ -176,11 +215,17 @@ __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uin
         for (int s = 0; s < T::NDREG; ++s) {
             mbar_init(&S.mb_dfull[s], 1);  // forward MMAs of the region's block committed
             mbar_init(&S.mb_yfull[s], 1);  // adjoint MMAs committed
-            mbar_init(&S.mb_dfree[s], 8);  // Y drained: one arrival per mover warp
+            mbar_init(&S.mb_dfree[s], 8);  // Y drained: one arrival per warp of the block's point set
+            mbar_init(&S.mb_zfull[s], 1);  // z MMAs of the region's block committed
+            mbar_init(&S.mb_pfull[s], 8);  // Psi written: one arrival per warp of the block's point set
         }
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&S.mb_afull[s], 8);  // A stage built: one arrival per mover warp
-            mbar_init(&S.mb_pfull[s], 8);  // Psi written: one arrival per warp of the point set
+            mbar_init(&S.mb_aufull[s], 4);  // u stage built: one arrival per u mover warp
+            mbar_init(&S.mb_adfull[s], 4);  // du stage built: one arrival per du mover warp
+        }
+        for (int j = 0; j < T::NBLK; ++j) {
+            mbar_init(&S.mb_ring[j], 8);  // Y(j) in the ring: one arrival per warp of the block's point set
+            mbar_init(&S.mb_sum[j], 8);   // g(j) summed: one arrival per mover warp
         }
     }
     for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {  // zero columns of the Y ring
@@ -216,6 +261,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                                        int pbuf, bool take_ticket,
                                        int fold_t0, unsigned long long *ph, ImgCtl *ctl_keep = nullptr) {
     using T = TcCfg<32>;
+    using CL = TcCols<NF>;
     using C = PassCfg<5>;
     constexpr int NT = T::NT, R = T::R, SW = T::SW, NBLK = T::NBLK;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -359,113 +405,125 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     constexpr uint32_t tmem = 0u;
     // per-block role stamps: [block][im2col, fwd, point, sum]
     if (ph && tid == 0) ph[NBLK * 16] = clock64();  // loop start (cycles)
+    unsigned long long *pw = ph ? ph + 304 + 8 * warp : nullptr;  // per-warp stamps of blocks 8 / 9
+    (void)pw;
 
     // warp-uniform role index (a shuffle result lets the compiler keep it, and the TMEM addresses derived from
     // it, in uniform registers)
     const int wu = __shfl_sync(0xffffffffu, warp, 0);
-    if (wu == T::W_MMA) {
-        // ================= MMA issuer: forward(j), then adjoint(j-1) =================
-        // forward B operands: K-major, N = 32, 16-byte K chunks 512 B apart; K step j starts 1024 B further
-        const uint64_t b1d = umma_desc_kmajor(smem_u32(S.img + T::IMG_B1), 512, 128);
-        const uint64_t b2d = umma_desc_kmajor(smem_u32(S.img + T::IMG_B2), 512, 128);
-        BDescs<32, NF / 8> ktd;
-        ktd.build(smem_u32(Kt), smem_u32(Kt + T::BSZ));
-        for (int j = 0; j <= NBLK; ++j) {
-            if (j < NBLK) {  // forward(j) once its A stage is built and block j-3's Y has left D region j%3
-                const int s = j & 1, rg = j % T::NDREG;
-                mbar_wait(&S.mb_afull[s], (j >> 1) & 1);
-                if (j >= T::NDREG) mbar_wait(&S.mb_dfree[rg], ((j - T::NDREG) / T::NDREG) & 1);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t sa = tmem + s * T::C_ASTAGE, sd = tmem + T::C_D0 + rg * T::C_DREGION;
-                    tc_forward<T>(sd + T::C_DZ, sa + T::C_AU, b1d, b2d);
-                    if (TRIAL) tc_forward<T>(sd + T::C_DDZ, sa + T::C_AD, b1d, b2d);
-                    umma_commit(&mb_dfull[rg]);
+    if (wu >= T::W_MMA) {
+        // ================= MMA issuers: one warp each for z(j), dz(j) and the adjoint(j) =================
+        // A warp that has issued a batch of tcgen05.mma stalls on its next uniform-datapath instructions until the
+        // batch has consumed its descriptors, so a single issuer serialises its own polling and fences with the
+        // tensor pipe (measured: ~450 cycles of overhead per batch, three batches per block); three issuers
+        // overlap theirs.  forward operand: K-major, N = 2 NF rows; adjoint operands K1, K2: N = 32 rows, K = 2 NF
+        const int role = wu - T::W_MMA;  // 0: z, 1: dz, 2: adjoint
+        if (role < 2) {
+            const uint64_t bfd = umma_desc_kmajor(smem_u32(S.img + T::IMG_BF), (CL::NZ / 8) * 128, 128);
+            if (role == 0 || TRIAL) {
+                for (int j = 0; j < NBLK; ++j) {
+                    // its A stage is built and block j-3's Y has left D region j%3
+                    const int rg = j % T::NDREG, st = j % CL::NU;
+                    const uint32_t sd = tmem + CL::C_D0 + rg * CL::REGION;
+                    mbar_wait(role == 0 ? &S.mb_aufull[st] : &S.mb_adfull[st], (j / CL::NU) & 1);
+                    if (j >= T::NDREG) mbar_wait(&S.mb_dfree[rg], ((j - T::NDREG) / T::NDREG) & 1);
+                    tc_fence_after();
+                    if (ph) ph[j * 16 + (role == 0 ? 10 : 12)] = clock64();  // z / dz issue starts
+                    if (elect_one()) {
+                        if (role == 0) {
+                            tc_forward<T, CL::NZ>(sd + CL::C_Z, tmem + CL::C_AU + st * T::KA, bfd);
+                            umma_commit(&S.mb_zfull[rg]);
+                        } else {
+                            tc_forward<T, CL::NZ>(sd + CL::C_W, tmem + CL::C_AD + st * T::KA, bfd);
+                            umma_commit(&mb_dfull[rg]);
+                        }
+                    }
+                    __syncwarp();
+                    if (ph) ph[j * 16 + (role == 0 ? 11 : 0)] = clock64();  // z / dz issued
                 }
-                __syncwarp();
-                if (ph) ph[j * 16 + 0] = clock64();  // forward issued
             }
-            if (j >= 1) {  // adjoint(j-1) once its point set wrote Psi over z / dz
-                const int jj = j - 1, rg = jj % T::NDREG;
-                mbar_wait(&S.mb_pfull[jj & 1], (jj >> 1) & 1);
+        } else {
+            const uint64_t ktd = umma_desc_kmajor(smem_u32(Kt), 512, 128);
+            const uint64_t kt2d = umma_desc_kmajor(smem_u32(S.img + T::IMG_KT2), 512, 128);
+            for (int j = 0; j < NBLK; ++j) {  // adjoint(j) once its point set wrote the Psi pairs over z1 | z2
+                const int rg = j % T::NDREG;
+                mbar_wait(&S.mb_pfull[rg], (j / T::NDREG) & 1);
                 tc_fence_after();
+                if (ph) ph[j * 16 + 13] = clock64();  // adjoint issue starts
                 if (elect_one()) {
-                    const uint32_t sb = tmem + T::C_D0 + rg * T::C_DREGION;
-                    umma_3xtf32_pre<32, NF / 8>(sb + T::C_DY, sb + T::C_DZ, sb + T::C_DDZ, ktd, NF / 8);
+                    const uint32_t sb = tmem + CL::C_D0 + rg * CL::REGION;
+                    constexpr uint32_t idesc = idesc_tf32(128, 32);
+#pragma unroll
+                    for (int k = 0; k < ((FOE_ABLATE & 8) ? 1 : CL::NZ / 8); ++k)  // K = 2 NF; two 16-byte K chunks (2 x 512 B) per step
+                        umma_tf32_ts(sb + CL::C_W, sb + CL::C_Z + 8 * k, ktd + (uint64_t)(k * 64), idesc, k > 0 ? 1u : 0u);
+#pragma unroll
+                    for (int k = 0; k < ((FOE_ABLATE & 8) ? 1 : CL::NZ / 8); ++k)
+                        umma_tf32_ts(sb + CL::C_W, sb + CL::C_Z + 8 * k, kt2d + (uint64_t)(k * 64), idesc, 1u);
                     umma_commit(&mb_yfull[rg]);
                 }
                 __syncwarp();
-                if (ph) ph[jj * 16 + 2] = clock64();  // adjoint issued
+                if (ph) ph[j * 16 + 2] = clock64();  // adjoint issued
             }
         }
     } else if (wu < T::W_PT) {
-        // ================= movers: im2col(j), drain Y(j-2) into the ring, shifted sum g(j-3) =================
-        // warps 0-3 build the u columns, warps 4-7 the du columns; warps w and w+4 share a TMEM lane quarter and
-        // split the taps of the drain (16 + 9) and of the sum (12 + 13)
+        // ================= movers: im2col(j), shifted sum g(j-3) =================
+        // warps 0-3 build the u columns, warps 4-7 the du columns; warps w and w+4 share a TMEM lane quarter (the
+        // same 128 pixels) and split the taps of the sum (12 + 13)
         const int pl = tid & 127, hf = wu >> 2;
         const uint32_t lane_off = (uint32_t)(32 * (wu & 3)) << 16;
-        {  // zero columns KA-8 .. KA-1 of both stages once (48, 49 are rewritten per block; the rest pad K to 56)
+        const int nst = hf == 0 ? CL::NU : CL::ND;
+        const uint32_t abase = tmem + lane_off + (hf == 0 ? CL::C_AU : CL::C_AD);
+        {  // zero columns KA-8 .. KA-1 of every stage once (48, 49 are rewritten per block; the rest pad K to 56)
             const float z8[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
             if (hf == 0 || TRIAL) {
-                tmem_st8(tmem + lane_off + hf * T::KA + T::KA - 8, z8);
-                tmem_st8(tmem + lane_off + T::C_ASTAGE + hf * T::KA + T::KA - 8, z8);
+                for (int st = 0; st < nst; ++st) tmem_st8(abase + st * T::KA + T::KA - 8, z8);
                 tc_wait_st();
             }
         }
         const float4 *xsrc = (hf == 0 ? S.XU : S.XD) + (pl >> 6) * SW + (pl & 63);
         const int prow = pl >> 6, pcol = pl & 63;
-        for (int j = 0; j < NBLK + 3; ++j) {
+        for (int j = 0; j < NBLK + T::SUMLAG; ++j) {
             if (j < NBLK) {
-                const int s = j & 1;
-                // forward(j-2) has read stage s
-                if (j >= 2) mbar_wait_sleep(&mb_dfull[(j - 2) % T::NDREG], ((j - 2) / T::NDREG) & 1);
+                const int s = j % nst, jp = j - nst;  // block jp used this stage last
+                if (jp >= 0) {  // its MMAs have read it: the z MMAs (u stage) / the whole forward (du stage)
+                    if (hf == 0) mbar_wait_sleep(&S.mb_zfull[jp % T::NDREG], (jp / T::NDREG) & 1);
+                    else if (TRIAL) mbar_wait_sleep(&mb_dfull[jp % T::NDREG], (jp / T::NDREG) & 1);
+                }
                 tc_fence_after();
                 if (ph && wu == 0) ph[j * 16 + 5] = clock64();  // im2col start
-                if (hf == 0 || TRIAL) {
-                    tc_im2col<T>(xsrc + 2 * j * SW, tmem + s * T::C_ASTAGE + lane_off + hf * T::KA);
+                if (pw && j == 8) pw[0] = clock64();
+                if ((hf == 0 || TRIAL) && !(FOE_ABLATE & 16)) {
+                    tc_im2col<T>(xsrc + 2 * j * SW, abase + s * T::KA);
                     tc_wait_st();
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&S.mb_afull[s]);
+                if (lane == 0) mbar_arrive(hf == 0 ? &S.mb_aufull[s] : &S.mb_adfull[s]);
                 if (ph && wu == 0) ph[j * 16 + 7] = clock64();  // A stage built
+                if (pw && j == 8) pw[1] = clock64();
             }
-            const int jd = j - 2, js = j - 3;
-            if (jd >= 0 && jd < NBLK) {  // Y(jd): half 0 taps 0..15, half 1 taps 16..24, into ring slot jd % RING
-                const int rg = jd % T::NDREG;
-                mbar_wait_sleep(&mb_yfull[rg], (jd / T::NDREG) & 1);
-                tc_fence_after();
-                if (ph && wu == 0) ph[jd * 16 + 8] = clock64();  // adjoint seen
-                float y[16];
-                tmem_ld16(tmem + T::C_D0 + rg * T::C_DREGION + lane_off + T::C_DY + 16 * hf, y);
-                tc_wait_ld();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.mb_dfree[rg]);  // for forward(jd + 3)
-                float *yrow = Yr + ((2 * jd + prow) & (T::YROWS - 1)) * T::YW + 2 + pcol;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int t = 16 * hf + i;
-                    if (t < T::KT) yrow[t * T::YROWS * T::YW] = y[i];
-                }
-                if (ph && wu == 0) ph[jd * 16 + 3] = clock64();  // Y in the ring
-            }
-            // ring slot jd % RING held Y(jd-4), last read by g(jd-3) = g(j-5) two iterations ago; this iteration's
-            // ring writes are ordered before its reads by the movers' barrier
-            named_sync(T::BAR_MOVERS, 256);
+            const int js = j - T::SUMLAG;
             if (js >= 0 && js < NBLK) {  // g(js) over this warp's tap half once Y(js-1 .. js+1) are in the ring
+                for (int n = js - 1; n <= js + 1; ++n)
+                    if (n >= 0 && n < NBLK) mbar_wait_sleep(&S.mb_ring[n], rpar);
+                if (pw && j == 8) pw[2] = clock64();
                 const int r = 2 * js + prow;
                 float gsum;
-                if (js == 0 || js == NBLK - 1)
+                if (FOE_ABLATE & 1)
+                    gsum = 0.0f;
+                else if (js == 0 || js == NBLK - 1)
                     gsum = hf ? tc_tap_sum<12, 25, true, T>(Yr, r, pcol) : tc_tap_sum<0, 12, true, T>(Yr, r, pcol);
                 else
                     gsum = hf ? tc_tap_sum<12, 25, false, T>(Yr, r, pcol) : tc_tap_sum<0, 12, false, T>(Yr, r, pcol);
                 Gr[hf * T::RH * T::RW + r * T::RW + pcol] = gsum;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.mb_sum[js]);
                 if (ph && wu == 0) ph[js * 16 + 4] = clock64();  // g summed
+                if (pw && j == 8) pw[3] = clock64();
             }
         }
     } else {
-        // ================= point sets: psi', energy terms =================
+        // ================= point sets: psi', energy terms, shifted sums =================
         // set s handles blocks j = s (mod 2): z, dz -> psi' (tf32 hi / lo written over them as the adjoint's A
         // operand) -> p_full; then the energy terms while the adjoint runs.  Warps w and w+4 of a set share a
         // TMEM lane quarter (same 32 pixels) and split the filters.
@@ -475,16 +533,19 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
         constexpr int FH = NF / 2;  // filters per half
         const int f0 = FH * hf;
+        const uint32_t own = (uint32_t)(hf * NF);  // this thread's columns within Z and W
         const int lc = pl & 63, gx = g.rx0 + lc;
         const bool col_in = !SYM || (gx >= 0 && gx < a.W), col_own = gx >= g.c0 && gx < g.c1;
         double e_own = 0.0;
         for (int j = set; j < NBLK; j += 2) {
             const int rg = j % T::NDREG;  // D region of block j
-            mbar_wait_sleep(&mb_dfull[rg], (j / T::NDREG) & 1);
+            mbar_wait_sleep(&S.mb_zfull[rg], (j / T::NDREG) & 1);            // z(j) committed
+            if (TRIAL) mbar_wait_sleep(&mb_dfull[rg], (j / T::NDREG) & 1);  // dz(j) committed
             tc_fence_after();
             const bool pst = ph && (wu - T::W_PT) % 8 == 0;
             if (pst) ph[j * 16 + 1] = clock64();  // forward seen
-            const uint32_t sd = tmem + T::C_D0 + rg * T::C_DREGION + lane_off;
+            if (pw && (j >> 1) == 4) pw[0] = clock64();
+            const uint32_t sd = tmem + CL::C_D0 + rg * CL::REGION + lane_off + own;
             const int gy = g.ry0 + 2 * j + (pl >> 6);
             const bool in_img = col_in && (!SYM || (gy >= 0 && gy < a.H));
             const bool owned = col_own && gy >= g.s0 && gy < g.s1;
@@ -493,9 +554,24 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             // atanh arguments for every filter with full ILP; Psi is handed to the adjoint MMA before
             // the energy series are evaluated
             float z[FH], dz[FH];
-            tmem_ldn<FH>(sd + T::C_DZ + f0, z);
-            if (TRIAL) tmem_ldn<FH>(sd + T::C_DDZ + f0, dz);
-            tc_wait_ld();
+            {  // z = z1 + z2, dz = dz1 + dz2 (the two sweeps of the 3xTF32 products)
+                float zz[NF], dd[TRIAL ? NF : 2];
+                tmem_ldn<NF>(sd + CL::C_Z, zz);
+                if (TRIAL) tmem_ldn<NF>(sd + CL::C_W, *reinterpret_cast<float(*)[NF]>(dd));
+                tc_wait_ld();
+                if (pw && (j >> 1) == 4) pw[1] = clock64();
+#pragma unroll
+                for (int i = 0; i < FH; i += 2) {
+                    const float2 t2 = __fadd2_rn(make_float2(zz[i], zz[i + 1]), make_float2(zz[FH + i], zz[FH + i + 1]));
+                    z[i] = t2.x;
+                    z[i + 1] = t2.y;
+                    if (TRIAL) {
+                        const float2 d2 = __fadd2_rn(make_float2(dd[i], dd[i + 1]), make_float2(dd[FH + i], dd[FH + i + 1]));
+                        dz[i] = d2.x;
+                        dz[i + 1] = d2.y;
+                    }
+                }
+            }
             float tmax = 0.0f;
             // psi' (zero on padded cells outside the image: a warp-uniform test, edge tiles only)
             auto point = [&](auto keep_all) {
@@ -528,31 +604,34 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                     z[i] = (decltype(keep_all)::value || in_img) ? ps : 0.0f;
                 }
             };
-            if (__all_sync(0xffffffffu, in_img))
+            if (FOE_ABLATE & 4) {
+            } else if (__all_sync(0xffffffffu, in_img))
                 point(std::true_type{});
             else
                 point(std::false_type{});
-            {
-                float hi[FH], lo[FH];
+            {  // Psi pairs {hi, lo} per filter over this thread's z1 | z2 columns
+                float pr[NF];
 #pragma unroll
                 for (int i = 0; i < FH; i += 2) {
-                    hi[i] = tf32_rn(z[i]);
-                    hi[i + 1] = tf32_rn(z[i + 1]);
-                    const float2 l2 = __fadd2_rn(make_float2(z[i], z[i + 1]), make_float2(-hi[i], -hi[i + 1]));
-                    lo[i] = tf32_rn_operand(l2.x);
-                    lo[i + 1] = tf32_rn_operand(l2.y);
+                    const float h0 = tf32_rn(z[i]), h1 = tf32_rn(z[i + 1]);
+                    const float2 l2 = __fadd2_rn(make_float2(z[i], z[i + 1]), make_float2(-h0, -h1));
+                    pr[2 * i] = h0;
+                    pr[2 * i + 1] = tf32_rn_operand(l2.x);
+                    pr[2 * i + 2] = h1;
+                    pr[2 * i + 3] = tf32_rn_operand(l2.y);
                 }
-                tmem_stn<FH>(sd + T::C_DZ + f0, hi);
-                tmem_stn<FH>(sd + T::C_DDZ + f0, lo);
+                tmem_stn<NF>(sd + CL::C_Z, pr);
             }
             tc_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&S.mb_pfull[set]);
+            if (lane == 0) mbar_arrive(&S.mb_pfull[rg]);
             if (pst) ph[j * 16 + 6] = clock64();  // Psi handed over
+            if (pw && (j >> 1) == 4) pw[2] = clock64();
             // energy terms while the adjoint MMAs run
             float e0 = 0.0f, e1 = 0.0f;
-            if (TRIAL) {
+            if (FOE_ABLATE & 2) {
+            } else if (TRIAL) {
                 // 2 a atanh(t) = 2 a (t + t^3/3 + ...): the series is cut where the next term is below fp32
                 // rounding for the warp's largest |t| (degree 9 up to 0.2, then 5, 3, 1); MUFU log beyond
                 const float wmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(tmax)));  // tmax >= 0
@@ -604,6 +683,31 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             }
             if (owned) e_own += (double)(e0 + e1);
             if (pst) ph[j * 16 + 9] = clock64();  // energy terms done
+            if (pw && (j >> 1) == 4) pw[3] = clock64();
+            {  // Y(j) (the adjoint ran meanwhile): half 0 taps 0..15, half 1 taps 16..24, into ring slot j % RING
+                mbar_wait_sleep(&mb_yfull[rg], (j / T::NDREG) & 1);
+                tc_fence_after();
+                if (pst) ph[j * 16 + 8] = clock64();  // adjoint seen
+                if (pw && (j >> 1) == 4) pw[4] = clock64();
+                float y[16];
+                tmem_ld16(tmem + CL::C_D0 + rg * CL::REGION + lane_off + CL::C_W + 16 * hf, y);
+                tc_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.mb_dfree[rg]);  // for forward(j + 3)
+                // the slot held Y(j - 4), read by g(j - 5) .. g(j - 3), which the movers sum in that order
+                if (j >= T::RING) mbar_wait_sleep(&S.mb_sum[j - 3], rpar);
+                float *yrow = Yr + ((2 * j + (pl >> 6)) & (T::YROWS - 1)) * T::YW + 2 + lc;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int t = 16 * hf + i;
+                    if (t < T::KT) yrow[t * T::YROWS * T::YW] = y[i];
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.mb_ring[j]);
+                if (pst) ph[j * 16 + 3] = clock64();  // Y in the ring
+                if (pw && (j >> 1) == 4) pw[5] = clock64();
+            }
         }
         acc[0] = e_own;
     }
@@ -672,7 +776,8 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     __shared__ int s_last;
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) unsigned long long mb_dfull[T::NDREG], mb_yfull[T::NDREG];
-    __shared__ __align__(8) unsigned long long mb_afull[2], mb_pfull[2], mb_dfree[T::NDREG], mb_img;
+    __shared__ __align__(8) unsigned long long mb_aufull[2], mb_adfull[2], mb_zfull[T::NDREG], mb_pfull[T::NDREG], mb_dfree[T::NDREG], mb_img;
+    __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int b = blockIdx.y;
@@ -693,7 +798,7 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     griddep_launch_dependents();
     const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
     const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
-    const TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_afull, mb_pfull, mb_dfree, &mb_img);
+    const TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_aufull, mb_adfull, mb_zfull, mb_pfull, mb_dfree, mb_ring, mb_sum, &mb_img);
     tc_setup<NF>(a, S, &s_tmem);
     int coff[TcCells::CPT];
     tc_cell_offsets<SYM>(a, g, coff);

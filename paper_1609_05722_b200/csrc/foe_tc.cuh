@@ -116,27 +116,35 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
                  : "memory");
 }
 
-// N = 4, 8, 12 or 16 consecutive columns in the fewest instructions (12 = 8 + 4)
+// N = 4 .. 32 (multiple of 4) consecutive columns in the fewest instructions
 template <int N>
 __device__ __forceinline__ void tmem_ldn(uint32_t taddr, float (&v)[N]) {
-    static_assert(N == 4 || N == 8 || N == 12 || N == 16, "column count");
-    if constexpr (N == 16) tmem_ld16(taddr, v);
-    if constexpr (N == 8) tmem_ld8(taddr, v);
-    if constexpr (N == 4) tmem_ld4(taddr, v);
-    if constexpr (N == 12) {
+    static_assert(N % 4 == 0 && N >= 4 && N <= 32, "column count");
+    if constexpr (N == 32) {
+        tmem_ld32(taddr, v);
+    } else if constexpr (N >= 16) {
+        tmem_ld16(taddr, *reinterpret_cast<float(*)[16]>(&v[0]));
+        if constexpr (N > 16) tmem_ldn<N - 16>(taddr + 16, *reinterpret_cast<float(*)[N - 16]>(&v[16]));
+    } else if constexpr (N >= 8) {
         tmem_ld8(taddr, *reinterpret_cast<float(*)[8]>(&v[0]));
-        tmem_ld4(taddr + 8, *reinterpret_cast<float(*)[4]>(&v[8]));
+        if constexpr (N > 8) tmem_ldn<N - 8>(taddr + 8, *reinterpret_cast<float(*)[N - 8]>(&v[8]));
+    } else {
+        tmem_ld4(taddr, v);
     }
 }
 template <int N>
 __device__ __forceinline__ void tmem_stn(uint32_t taddr, const float (&v)[N]) {
-    static_assert(N == 4 || N == 8 || N == 12 || N == 16, "column count");
-    if constexpr (N == 16) tmem_st16(taddr, v);
-    if constexpr (N == 8) tmem_st8(taddr, v);
-    if constexpr (N == 4) tmem_st4(taddr, v);
-    if constexpr (N == 12) {
+    static_assert(N % 4 == 0 && N >= 4 && N <= 32, "column count");
+    if constexpr (N == 32) {
+        tmem_st32(taddr, v);
+    } else if constexpr (N >= 16) {
+        tmem_st16(taddr, *reinterpret_cast<const float(*)[16]>(&v[0]));
+        if constexpr (N > 16) tmem_stn<N - 16>(taddr + 16, *reinterpret_cast<const float(*)[N - 16]>(&v[16]));
+    } else if constexpr (N >= 8) {
         tmem_st8(taddr, *reinterpret_cast<const float(*)[8]>(&v[0]));
-        tmem_st4(taddr + 8, *reinterpret_cast<const float(*)[4]>(&v[8]));
+        if constexpr (N > 8) tmem_stn<N - 8>(taddr + 8, *reinterpret_cast<const float(*)[N - 8]>(&v[8]));
+    } else {
+        tmem_st4(taddr, v);
     }
 }
 
@@ -350,14 +358,15 @@ __device__ __forceinline__ void umma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, u
 }
 
 template <int N, bool TS>
-__global__ void __launch_bounds__(128) k_tc_rate(int nmma, int nchain, long long *out) {
+__global__ void __launch_bounds__(128) k_tc_rate(int nmma, int nchain, int every, long long *out) {
     __shared__ __align__(128) float sA[128 * 8];
     __shared__ __align__(128) float sB[N * 8];
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) unsigned long long s_mbar;
+    __shared__ __align__(8) unsigned long long s_mbar, s_mid[128];
     const int tid = threadIdx.x, warp = tid >> 5;
     if (warp == 0) tmem_alloc(&s_tmem, 512);
     if (tid == 0) mbar_init(&s_mbar, 1);
+    mbar_init(&s_mid[tid], 1);
     for (int e = tid; e < 128 * 8; e += 128) sA[e] = 0.0f;
     for (int e = tid; e < N * 8; e += 128) sB[e] = 0.0f;
     fence_async_smem();
@@ -373,10 +382,23 @@ __global__ void __launch_bounds__(128) k_tc_rate(int nmma, int nchain, long long
         if (elect_one()) {
             // nchain independent accumulators (D columns 256 + N c), issued round robin: a dependent chain of
             // small MMAs exposes the pipeline's accumulate latency, independent chains overlap
-            for (int i = 0; i < nmma; ++i) {
-                const uint32_t d = t0 + 256 + (uint32_t)((i % nchain) * N);
-                if (TS) umma_tf32_ts(d, t0, bd, idesc, i >= nchain);
-                else umma_tf32_ss(d, ad, bd, idesc, i >= nchain);
+            if (every <= 0) {
+                int c = 0;
+                for (int i = 0; i < nmma; ++i) {
+                    const uint32_t d = t0 + 256 + (uint32_t)(c * N);
+                    if (TS) umma_tf32_ts(d, t0, bd, idesc, i >= nchain);
+                    else umma_tf32_ss(d, ad, bd, idesc, i >= nchain);
+                    c = c + 1 == nchain ? 0 : c + 1;
+                }
+            } else {
+                // a tcgen05.commit (to an mbarrier nobody waits on) after each group of `every` MMAs
+                for (int g = 0; g * every < nmma; ++g) {
+                    for (int k = 0; k < every; ++k) {
+                        if (TS) umma_tf32_ts(t0 + 256, t0, bd, idesc, (g | k) != 0);
+                        else umma_tf32_ss(t0 + 256, ad, bd, idesc, (g | k) != 0);
+                    }
+                    if ((g + 1) * every < nmma) umma_commit(&s_mid[g & 127]);
+                }
             }
             umma_commit(&s_mbar);
         }

@@ -41,9 +41,17 @@ if phs.any():
     tab = phs[:, cols] - loop0
     tab[phs[:, cols] == 0] = -1
     print(tab.astype(np.int64))
-    cyc = phs[:, 10:16]
-    print("point set cycles from fwd-seen: wait_ld, compute+st issued, wait_st, p_full seen (issuer), y_full seen")
-    print(np.stack([cyc[:, k] - cyc[:, 0] for k in range(1, 6)], axis=1).astype(np.int64))
+    print("MMA warp (cycles from loop start): z issue start, z issued, dz issue start, dz issued, adj issue start, adj issued")
+    m = phs[:, [10, 11, 12, 0, 13, 2]] - loop0
+    m[phs[:, [10, 11, 12, 0, 13, 2]] == 0] = -1
+    print(m.astype(np.int64))
+pw = full[ncta * 3 + 304: ncta * 3 + 304 + 200].reshape(25, 8)  # the first 25 warps.astype(np.float64)
+if pw.any():
+    t = pw - loop0
+    t[pw == 0] = -1
+    print("per-warp stamps, block 8 (movers, point set 0) / 9 (set 1): movers [im2col start, A built, sum start, sum done]; "
+          "point [fwd seen, z/dz loaded, Psi handed, energy done, adj seen, Y in ring]")
+    print(t[:, :6].astype(np.int64))
 a -= a[:, 0].min()
 start, comp, end = a[:, 0] / 1e3, a[:, 1] / 1e3, a[:, 2] / 1e3
 dur = comp - start

@@ -17,9 +17,20 @@ for ts in (1, 0):
             res = []
             for nm in (1, 12, 36, 108):
                 for _ in range(2):
-                    _lib.check(L.foe_debug_tc_rate(n, ts, nm, nchain, out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+                    _lib.check(L.foe_debug_tc_rate(n, ts, nm, nchain, 0, out.data_ptr(), torch.cuda.current_stream().cuda_stream))
                 torch.cuda.synchronize()
                 res.append((nm, int(out.item())))
             per = (res[-1][1] - res[1][1]) / (res[-1][0] - res[1][0])
             print(f"{'TS' if ts else 'SS'} N={n} chains={nchain}: " + ", ".join(f"{nm}->{c}" for nm, c in res) +
                   f"  => {per:.1f} cycles/MMA")
+
+# a tcgen05.commit after every group of MMAs: does the commit stall the pipe?
+for every in (0, 18, 9, 6, 3, 1):
+    res = []
+    for nm in (36, 108):
+        for _ in range(2):
+            _lib.check(L.foe_debug_tc_rate(64, 1, nm, 1, every, out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        res.append((nm, int(out.item())))
+    print(f"TS N=64 commit every {every}: " + ", ".join(f"{nm}->{c}" for nm, c in res) +
+          f"  => {(res[1][1] - res[0][1]) / 72:.1f} cycles/MMA")
