@@ -75,7 +75,7 @@ struct TcCfg {
 // TMEM plan for a bank of NF (multiple of 8) filters.  D region of a block: [Z: z1 | z2 per filter half, then Psi
 // pairs in place, 2 NF columns][W: dz1 | dz2 per filter half, then Y (32 columns) over them].  Within Z (and
 // W) the point thread of filter half h owns columns [h NF, (h + 1) NF): part p of its filter i at h NF + p NF/2 + i,
-// its Psi pair at h NF + 2 i + part -- so a thread overwrites only what it has read itself.  Three regions at
+// its Psi pairs at h NF + 4 (i / 2) + 2 part + i % 2 -- so a thread overwrites only what it has read itself.  Three regions at
 // the top of TMEM, the A operands below them: NU u stages and ND du stages of KA columns.
 template <int NF>
 struct TcCols {
@@ -90,7 +90,8 @@ struct TcCols {
     static_assert((NU + ND) * T::KA <= C_D0 && NZ <= 64, "TMEM budget");
     // forward operand row of (filter f, part p); adjoint operand K column of (filter f, part)
     __host__ __device__ static constexpr int brow(int f, int p) { return (f / FH) * NF + p * FH + f % FH; }
-    __host__ __device__ static constexpr int kcol(int f, int part) { return 2 * f + part; }
+    // (filter pairs as {hi, hi, lo, lo}: the order the point code produces them in, no register shuffles)
+    __host__ __device__ static constexpr int kcol(int f, int part) { return 4 * (f / 2) + 2 * part + f % 2; }
 };
 
 // A-stage column of (tap, part) in the order above
@@ -469,7 +470,9 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         // ================= movers: im2col(j), shifted sum g(j-3) =================
         // warps 0-3 build the u columns, warps 4-7 the du columns; warps w and w+4 share a TMEM lane quarter (the
         // same 128 pixels) and split the taps of the sum (12 + 13)
-        const int pl = tid & 127, hf = wu >> 2;
+        auto mover = [&](auto HFc) {
+        constexpr int hf = decltype(HFc)::value;  // 0: u columns, taps 0..11; 1: du columns, taps 12..24
+        const int pl = tid & 127;
         const uint32_t lane_off = (uint32_t)(32 * (wu & 3)) << 16;
         const int nst = hf == 0 ? CL::NU : CL::ND;
         const uint32_t abase = tmem + lane_off + (hf == 0 ? CL::C_AU : CL::C_AD);
@@ -504,8 +507,9 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             }
             const int js = j - T::SUMLAG;
             if (js >= 0 && js < NBLK) {  // g(js) over this warp's tap half once Y(js-1 .. js+1) are in the ring
-                for (int n = js - 1; n <= js + 1; ++n)
-                    if (n >= 0 && n < NBLK) mbar_wait_sleep(&S.mb_ring[n], rpar);
+                // (Y(js-1) and Y(js) were awaited by the two previous sums)
+                if (js == 0) mbar_wait_sleep(&S.mb_ring[0], rpar);
+                if (js + 1 < NBLK) mbar_wait_sleep(&S.mb_ring[js + 1], rpar);
                 if (pw && j == 8) pw[2] = clock64();
                 const int r = 2 * js + prow;
                 float gsum;
@@ -522,6 +526,9 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 if (pw && j == 8) pw[3] = clock64();
             }
         }
+        };
+        if (wu >> 2) mover(std::integral_constant<int, 1>{});
+        else mover(std::integral_constant<int, 0>{});
     } else {
         // ================= point sets: psi', energy terms, shifted sums =================
         // set s handles blocks j = s (mod 2): z, dz -> psi' (tf32 hi / lo written over them as the adjoint's A
@@ -609,15 +616,15 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 point(std::true_type{});
             else
                 point(std::false_type{});
-            {  // Psi pairs {hi, lo} per filter over this thread's z1 | z2 columns
+            {  // Psi {hi, hi, lo, lo} per filter pair over this thread's z1 | z2 columns
                 float pr[NF];
 #pragma unroll
                 for (int i = 0; i < FH; i += 2) {
                     const float h0 = tf32_rn(z[i]), h1 = tf32_rn(z[i + 1]);
                     const float2 l2 = __fadd2_rn(make_float2(z[i], z[i + 1]), make_float2(-h0, -h1));
                     pr[2 * i] = h0;
-                    pr[2 * i + 1] = tf32_rn_operand(l2.x);
-                    pr[2 * i + 2] = h1;
+                    pr[2 * i + 1] = h1;
+                    pr[2 * i + 2] = tf32_rn_operand(l2.x);
                     pr[2 * i + 3] = tf32_rn_operand(l2.y);
                 }
                 tmem_stn<NF>(sd + CL::C_Z, pr);
