@@ -212,22 +212,18 @@ __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uin
         bulk_g2s(S.img, a.tc_img, T::IMG_FLOATS * 4, S.mb_img);
     }
     if (warp == 0) tmem_alloc(s_tmem, 512);
-    if (tid == 0) {
-        for (int s = 0; s < T::NDREG; ++s) {
-            mbar_init(&S.mb_dfull[s], 1);  // forward MMAs of the region's block committed
-            mbar_init(&S.mb_yfull[s], 1);  // adjoint MMAs committed
-            mbar_init(&S.mb_dfree[s], 8);  // Y drained: one arrival per warp of the block's point set
-            mbar_init(&S.mb_zfull[s], 1);  // z MMAs of the region's block committed
-            mbar_init(&S.mb_pfull[s], 8);  // Psi written: one arrival per warp of the block's point set
-        }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&S.mb_aufull[s], 4);  // u stage built: one arrival per u mover warp
-            mbar_init(&S.mb_adfull[s], 4);  // du stage built: one arrival per du mover warp
-        }
-        for (int j = 0; j < T::NBLK; ++j) {
-            mbar_init(&S.mb_ring[j], 8);  // Y(j) in the ring: one arrival per warp of the block's point set
-            mbar_init(&S.mb_sum[j], 8);   // g(j) summed: one arrival per mover warp
-        }
+    if (tid < T::NBLK) {
+        // one single-phase barrier per block and event (no index arithmetic or phase bookkeeping in the loop)
+        const int j = tid;
+        mbar_init(&S.mb_aufull[j], 4);  // u columns of the block's A stage built: one arrival per u mover warp
+        mbar_init(&S.mb_adfull[j], 4);  // du columns built: one arrival per du mover warp
+        mbar_init(&S.mb_zfull[j], 1);   // z MMAs committed
+        mbar_init(&S.mb_dfull[j], 1);   // dz MMAs committed
+        mbar_init(&S.mb_pfull[j], 8);   // Psi written: one arrival per warp of the block's point set
+        mbar_init(&S.mb_yfull[j], 1);   // adjoint MMAs committed
+        mbar_init(&S.mb_dfree[j], 8);   // Y drained from its D region: one arrival per warp of the point set
+        mbar_init(&S.mb_ring[j], 8);    // Y(j) in the ring: one arrival per warp of the point set
+        mbar_init(&S.mb_sum[j], 8);     // g(j) summed: one arrival per mover warp
     }
     for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {  // zero columns of the Y ring
         const int col = e & 3, rr = e >> 2;
@@ -422,21 +418,22 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         if (role < 2) {
             const uint64_t bfd = umma_desc_kmajor(smem_u32(S.img + T::IMG_BF), (CL::NZ / 8) * 128, 128);
             if (role == 0 || TRIAL) {
-                for (int j = 0; j < NBLK; ++j) {
+                uint32_t sd = tmem + CL::C_D0;  // D region j % 3
+                int st = 0;                     // A stage j % NU
+                for (int j = 0; j < NBLK; ++j, sd = sd + CL::REGION == tmem + CL::C_D0 + T::NDREG * CL::REGION ? tmem + CL::C_D0 : sd + CL::REGION,
+                         st = st + 1 == CL::NU ? 0 : st + 1) {
                     // its A stage is built and block j-3's Y has left D region j%3
-                    const int rg = j % T::NDREG, st = j % CL::NU;
-                    const uint32_t sd = tmem + CL::C_D0 + rg * CL::REGION;
-                    mbar_wait(role == 0 ? &S.mb_aufull[st] : &S.mb_adfull[st], (j / CL::NU) & 1);
-                    if (j >= T::NDREG) mbar_wait(&S.mb_dfree[rg], ((j - T::NDREG) / T::NDREG) & 1);
+                    mbar_wait(role == 0 ? &S.mb_aufull[j] : &S.mb_adfull[j], 0u);
+                    if (j >= T::NDREG) mbar_wait(&S.mb_dfree[j - T::NDREG], 0u);
                     tc_fence_after();
                     if (ph) ph[j * 16 + (role == 0 ? 10 : 12)] = clock64();  // z / dz issue starts
                     if (elect_one()) {
                         if (role == 0) {
                             tc_forward<T, CL::NZ>(sd + CL::C_Z, tmem + CL::C_AU + st * T::KA, bfd);
-                            umma_commit(&S.mb_zfull[rg]);
+                            umma_commit(&S.mb_zfull[j]);
                         } else {
                             tc_forward<T, CL::NZ>(sd + CL::C_W, tmem + CL::C_AD + st * T::KA, bfd);
-                            umma_commit(&mb_dfull[rg]);
+                            umma_commit(&mb_dfull[j]);
                         }
                     }
                     __syncwarp();
@@ -446,13 +443,13 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         } else {
             const uint64_t ktd = umma_desc_kmajor(smem_u32(Kt), 512, 128);
             const uint64_t kt2d = umma_desc_kmajor(smem_u32(S.img + T::IMG_KT2), 512, 128);
-            for (int j = 0; j < NBLK; ++j) {  // adjoint(j) once its point set wrote the Psi pairs over z1 | z2
-                const int rg = j % T::NDREG;
-                mbar_wait(&S.mb_pfull[rg], (j / T::NDREG) & 1);
+            uint32_t sb = tmem + CL::C_D0;  // D region j % 3
+            for (int j = 0; j < NBLK; ++j, sb = sb + CL::REGION == tmem + CL::C_D0 + T::NDREG * CL::REGION ? tmem + CL::C_D0 : sb + CL::REGION) {
+                // adjoint(j) once its point set wrote the Psi pairs over z1 | z2
+                mbar_wait(&S.mb_pfull[j], 0u);
                 tc_fence_after();
                 if (ph) ph[j * 16 + 13] = clock64();  // adjoint issue starts
                 if (elect_one()) {
-                    const uint32_t sb = tmem + CL::C_D0 + rg * CL::REGION;
                     constexpr uint32_t idesc = idesc_tf32(128, 32);
 #pragma unroll
                     for (int k = 0; k < ((FOE_ABLATE & 8) ? 1 : CL::NZ / 8); ++k)  // K = 2 NF; two 16-byte K chunks (2 x 512 B) per step
@@ -460,7 +457,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
 #pragma unroll
                     for (int k = 0; k < ((FOE_ABLATE & 8) ? 1 : CL::NZ / 8); ++k)
                         umma_tf32_ts(sb + CL::C_W, sb + CL::C_Z + 8 * k, kt2d + (uint64_t)(k * 64), idesc, 1u);
-                    umma_commit(&mb_yfull[rg]);
+                    umma_commit(&mb_yfull[j]);
                 }
                 __syncwarp();
                 if (ph) ph[j * 16 + 2] = clock64();  // adjoint issued
@@ -487,10 +484,10 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         const int prow = pl >> 6, pcol = pl & 63;
         for (int j = 0; j < NBLK + T::SUMLAG; ++j) {
             if (j < NBLK) {
-                const int s = j % nst, jp = j - nst;  // block jp used this stage last
+                const int s = nst == 2 ? (j & 1) : 0, jp = j - nst;  // block jp used this stage last
                 if (jp >= 0) {  // its MMAs have read it: the z MMAs (u stage) / the whole forward (du stage)
-                    if (hf == 0) mbar_wait_sleep(&S.mb_zfull[jp % T::NDREG], (jp / T::NDREG) & 1);
-                    else if (TRIAL) mbar_wait_sleep(&mb_dfull[jp % T::NDREG], (jp / T::NDREG) & 1);
+                    if (hf == 0) mbar_wait_sleep(&S.mb_zfull[jp], 0u);
+                    else if (TRIAL) mbar_wait_sleep(&mb_dfull[jp], 0u);
                 }
                 tc_fence_after();
                 if (ph && wu == 0) ph[j * 16 + 5] = clock64();  // im2col start
@@ -501,7 +498,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(hf == 0 ? &S.mb_aufull[s] : &S.mb_adfull[s]);
+                if (lane == 0) mbar_arrive(hf == 0 ? &S.mb_aufull[j] : &S.mb_adfull[j]);
                 if (ph && wu == 0) ph[j * 16 + 7] = clock64();  // A stage built
                 if (pw && j == 8) pw[1] = clock64();
             }
@@ -544,10 +541,10 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         const int lc = pl & 63, gx = g.rx0 + lc;
         const bool col_in = !SYM || (gx >= 0 && gx < a.W), col_own = gx >= g.c0 && gx < g.c1;
         double e_own = 0.0;
-        for (int j = set; j < NBLK; j += 2) {
-            const int rg = j % T::NDREG;  // D region of block j
-            mbar_wait_sleep(&S.mb_zfull[rg], (j / T::NDREG) & 1);            // z(j) committed
-            if (TRIAL) mbar_wait_sleep(&mb_dfull[rg], (j / T::NDREG) & 1);  // dz(j) committed
+        int rg = set;  // D region of block j: j % 3
+        for (int j = set; j < NBLK; j += 2, rg = rg == 0 ? 2 : rg - 1) {
+            mbar_wait_sleep(&S.mb_zfull[j], 0u);            // z(j) committed
+            if (TRIAL) mbar_wait_sleep(&mb_dfull[j], 0u);  // dz(j) committed
             tc_fence_after();
             const bool pst = ph && (wu - T::W_PT) % 8 == 0;
             if (pst) ph[j * 16 + 1] = clock64();  // forward seen
@@ -632,7 +629,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             tc_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&S.mb_pfull[rg]);
+            if (lane == 0) mbar_arrive(&S.mb_pfull[j]);
             if (pst) ph[j * 16 + 6] = clock64();  // Psi handed over
             if (pw && (j >> 1) == 4) pw[2] = clock64();
             // energy terms while the adjoint MMAs run
@@ -692,7 +689,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             if (pst) ph[j * 16 + 9] = clock64();  // energy terms done
             if (pw && (j >> 1) == 4) pw[3] = clock64();
             {  // Y(j) (the adjoint ran meanwhile): half 0 taps 0..15, half 1 taps 16..24, into ring slot j % RING
-                mbar_wait_sleep(&mb_yfull[rg], (j / T::NDREG) & 1);
+                mbar_wait_sleep(&mb_yfull[j], 0u);
                 tc_fence_after();
                 if (pst) ph[j * 16 + 8] = clock64();  // adjoint seen
                 if (pw && (j >> 1) == 4) pw[4] = clock64();
@@ -701,7 +698,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 tc_wait_ld();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&S.mb_dfree[rg]);  // for forward(j + 3)
+                if (lane == 0) mbar_arrive(&S.mb_dfree[j]);  // for forward(j + 3)
                 // the slot held Y(j - 4), read by g(j - 5) .. g(j - 3), which the movers sum in that order
                 if (j >= T::RING) mbar_wait_sleep(&S.mb_sum[j - 3], rpar);
                 float *yrow = Yr + ((2 * j + (pl >> 6)) & (T::YROWS - 1)) * T::YW + 2 + lc;
@@ -782,8 +779,8 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     __shared__ double s_sum[kNumPartials];
     __shared__ int s_last;
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) unsigned long long mb_dfull[T::NDREG], mb_yfull[T::NDREG];
-    __shared__ __align__(8) unsigned long long mb_aufull[2], mb_adfull[2], mb_zfull[T::NDREG], mb_pfull[T::NDREG], mb_dfree[T::NDREG], mb_img;
+    __shared__ __align__(8) unsigned long long mb_dfull[NBLK], mb_yfull[NBLK], mb_aufull[NBLK], mb_adfull[NBLK], mb_zfull[NBLK];
+    __shared__ __align__(8) unsigned long long mb_pfull[NBLK], mb_dfree[NBLK], mb_img;
     __shared__ __align__(8) unsigned long long mb_ring[NBLK], mb_sum[NBLK];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
