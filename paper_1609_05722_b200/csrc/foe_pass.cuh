@@ -81,9 +81,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
     asm volatile(
         "{ .reg .pred p;\n"
-        "WAIT_%=: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n"
+        "WAIT_%=: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra WAIT_%=; }" ::"r"(a),
-        "r"(parity), "r"(2000u)
+        "r"(parity)
         : "memory");
 }
 

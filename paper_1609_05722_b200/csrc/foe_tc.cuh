@@ -162,9 +162,6 @@ __device__ __forceinline__ bool mbar_test(unsigned long long *bar, unsigned pari
         : "memory");
     return ok != 0u;
 }
-#ifndef FOE_SUSPEND_NS
-#define FOE_SUSPEND_NS 2000  // suspend-time hint of the hardware-suspended wait (ns)
-#endif
 #ifndef FOE_SLEEP_NS
 #define FOE_SLEEP_NS -1  // < 0: mbarrier.try_wait (hardware-suspended; measured best: 5.40 vs 5.52 ms per cfg2 solve with 32 ns sleeps, 5.44 spinning)
 #endif
@@ -174,9 +171,9 @@ __device__ __forceinline__ void mbar_wait_sleep(unsigned long long *bar, unsigne
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
     asm volatile(
         "{ .reg .pred p;\n"
-        "WAITS_%=: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n"
+        "WAITS_%=: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra WAITS_%=; }" ::"r"(a),
-        "r"(parity), "r"((unsigned)FOE_SUSPEND_NS)
+        "r"(parity)
         : "memory");
 #else
     while (!mbar_test(bar, parity)) {
