@@ -520,10 +520,10 @@ def main():
     traffic = pass_traffic("k_pass_tc<24, 1, 1>" if use_tc else "k_pass<5, 1, 1>")
     tensor = None
     if use_tc:
-        # executed tcgen05 work of one trial pass: per 128-pixel block 2 x 9 forward (u, du) + 9 adjoint
-        # kind::tf32 MMAs of 128 x 32 x 8 (3xTF32, K = 24 taps / 24 filters), 18 blocks per 32 x 60 tile
+        # executed tcgen05 work of one trial pass: per 128-pixel block 2 x 7 forward (u, du) kind::tf32 MMAs of
+        # 128 x 48 x 8 (both 3xTF32 sweeps merged along N) + 6 + 4 adjoint MMAs of 128 x 32 x 8, 18 blocks per tile
         ctas = -(-H // 32) * -(-W // 60)
-        mma_flop = ctas * 18 * 27 * 2 * 128 * 32 * 8
+        mma_flop = ctas * 18 * (14 * 48 + 10 * 32) * 2 * 128 * 8
         tf32_peak = PEAKS.get("bf16_tflops", 2 * 1125.0) / 2
         tensor = {"executed_tflops": mma_flop / (pass_ms * 1e-3) / 1e12, "mma_flop_per_launch": mma_flop,
                   "peak_tf32_tflops": tf32_peak, "frac": mma_flop / (pass_ms * 1e-3) / 1e12 / tf32_peak,

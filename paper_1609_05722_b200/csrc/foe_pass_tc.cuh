@@ -59,9 +59,10 @@ struct TcCfg {
     //   forward  [z1 | z2] = A . [B1 | B2]^T,  B1[k] = k_hi[tap(k)] on both parts (u_hi k_hi + u_lo k_hi),
     //            B2[k] = k_lo[tap(k)] on part 0 (u_hi k_lo): N = 2 NF, 7 MMAs per quantity, z = z1 + z2
     //   adjoint  Y = Psi . K1^T + Psi . K2^T, Psi = {hi, lo} pairs per filter (K = 2 NF), K1 = Kt_hi on both
-    //            parts, K2 = Kt_lo on part 0: N = 32, two sweeps of NF / 4 MMAs into the same columns (a merged
-    //            N = 64 adjoint would cost 16 more TMEM columns per D region -- the second du stage)
-    // (26 MMAs per 128-pixel block at NF = 24; ~23 / 28 / 32 pipe cycles per MMA at N = 32 / 48 / 64, tools/tc_rate.py).
+    //            parts, K2 = Kt_lo on part 0: N = 32, a sweep of NF / 4 MMAs and one over the K steps that hold a hi
+    //            column (4 of 6 at NF = 24) into the same columns (a merged N = 64 adjoint would cost 16 more TMEM
+    //            columns per D region -- the second du stage)
+    // (24 MMAs per 128-pixel block at NF = 24; ~23 / 28 / 32 pipe cycles per MMA at N = 32 / 48 / 64, tools/tc_rate.py).
     // operand image built once per bank on the host (foe_bank_create) and copied into shared memory by one
     // bulk copy per CTA: [forward (2 NF x 56) | adjoint K1 (32 x 2 NF) | K2 | alpha (64) | 2 alpha (32)] floats,
     // sized for NF = 32
@@ -75,7 +76,7 @@ struct TcCfg {
 // TMEM plan for a bank of NF (multiple of 8) filters.  D region of a block: [Z: z1 | z2 per filter half, then Psi
 // pairs in place, 2 NF columns][W: dz1 | dz2 per filter half, then Y (32 columns) over them].  Within Z (and
 // W) the point thread of filter half h owns columns [h NF, (h + 1) NF): part p of its filter i at h NF + p NF/2 + i,
-// its Psi pairs at h NF + 4 (i / 2) + 2 part + i % 2 -- so a thread overwrites only what it has read itself.  Three regions at
+// its Psi parts at h NF + part NF/2 + i (the same columns) -- so a thread overwrites only what it has read itself.  Three regions at
 // the top of TMEM, the A operands below them: NU u stages and ND du stages of KA columns.
 template <int NF>
 struct TcCols {
@@ -90,8 +91,10 @@ struct TcCols {
     static_assert((NU + ND) * T::KA <= C_D0 && NZ <= 64, "TMEM budget");
     // forward operand row of (filter f, part p); adjoint operand K column of (filter f, part)
     __host__ __device__ static constexpr int brow(int f, int p) { return (f / FH) * NF + p * FH + f % FH; }
-    // (filter pairs as {hi, hi, lo, lo}: the order the point code produces them in, no register shuffles)
-    __host__ __device__ static constexpr int kcol(int f, int part) { return 4 * (f / 2) + 2 * part + f % 2; }
+    // (per filter half: the FH hi parts, then the FH lo parts -- a thread's own columns, and the K steps of the
+    // second adjoint sweep, which multiplies hi parts only, shrink to those that hold a hi column)
+    __host__ __device__ static constexpr int kcol(int f, int part) { return (f / FH) * NF + part * FH + f % FH; }
+    __host__ __device__ static constexpr bool kstep_has_hi(int k) { return (8 * k) % NF < FH; }
 };
 
 // A-stage column of (tap, part) in the order above
@@ -136,10 +139,13 @@ __device__ __forceinline__ float tc_tap_sum(const float *Yr, int r, int c) {
 template <class T>
 __device__ __forceinline__ void tc_im2col(const float4 *xp, uint32_t st) {
     float q[40], c[10];
+    const int e2 = 8 - ((threadIdx.x >> 3) & 1);
 #pragma unroll
     for (int dy = 0; dy < T::M; ++dy) {
         const float4 a = xp[dy * T::SW], b = xp[dy * T::SW + 2];
-        const float2 e = *reinterpret_cast<const float2 *>(xp + dy * T::SW + 4);
+        // the pair of p + 4: the left half of cell p + 4 or the right half of cell p + 3 (the same values), by
+        // groups of 8 lanes -- 8-byte loads at a 16-byte stride alone use half the banks (2-way conflict)
+        const float2 e = reinterpret_cast<const float2 *>(xp + dy * T::SW)[e2];
         q[8 * dy + 0] = a.x; q[8 * dy + 1] = a.y; q[8 * dy + 2] = a.z; q[8 * dy + 3] = a.w;
         q[8 * dy + 4] = b.x; q[8 * dy + 5] = b.y; q[8 * dy + 6] = b.z; q[8 * dy + 7] = b.w;
         c[2 * dy] = e.x; c[2 * dy + 1] = e.y;
@@ -348,11 +354,14 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             const int k = tid + q * NT;
             if (k >= C::NCELL) continue;
             const int i = k / C::CW, j = k - i * C::CW;
+            const int k1 = (tid & 8) ? 2 * k - 1 : 2 * k, k2 = (tid & 8) ? 2 * k : 2 * k - 1;
             if (!TRIAL) {
                 const float x = lu[q] - shift, h = tf32_rn(x);
                 const float2 pu = make_float2(h, tf32_rn_operand(x - h));
-                xu2[2 * k] = pu;                  // cell k's own pair ...
-                if (k > 0) xu2[2 * k - 1] = pu;   // ... and its copy as cell k - 1's right neighbour
+                // cell k's own pair and its copy as cell k - 1's right neighbour: lanes 8..15 / 24..31 store
+                // the copy first, so that each half-warp's 8-byte stores cover all 32 banks (no 2-way conflict)
+                if (k1 >= 0) xu2[k1] = pu;
+                if (k2 >= 0) xu2[k2] = pu;
                 continue;
             }
             const int gy = g.ry0 - R + i, gx = g.rx0 - R + j;
@@ -361,11 +370,13 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             const float du = un - u;
             const float x = un - shift, h = tf32_rn(x), hd = tf32_rn(du);
             const float2 pu = make_float2(h, tf32_rn_operand(x - h)), pd = make_float2(hd, tf32_rn_operand(du - hd));
-            xu2[2 * k] = pu;
-            xd2[2 * k] = pd;
-            if (k > 0) {
-                xu2[2 * k - 1] = pu;
-                xd2[2 * k - 1] = pd;
+            if (k1 >= 0) {
+                xu2[k1] = pu;
+                xd2[k1] = pd;
+            }
+            if (k2 >= 0) {
+                xu2[k2] = pu;
+                xd2[k2] = pd;
             }
             if (gy >= g.s0 && gy < g.s1 && gx >= g.c0 && gx < g.c1) {
                 uout[(size_t)(gy - a.lrow0) * a.W + gx] = un;
@@ -455,8 +466,8 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                     for (int k = 0; k < ((FOE_ABLATE & 8) ? 1 : CL::NZ / 8); ++k)  // K = 2 NF; two 16-byte K chunks (2 x 512 B) per step
                         umma_tf32_ts(sb + CL::C_W, sb + CL::C_Z + 8 * k, ktd + (uint64_t)(k * 64), idesc, k > 0 ? 1u : 0u);
 #pragma unroll
-                    for (int k = 0; k < ((FOE_ABLATE & 8) ? 1 : CL::NZ / 8); ++k)
-                        umma_tf32_ts(sb + CL::C_W, sb + CL::C_Z + 8 * k, kt2d + (uint64_t)(k * 64), idesc, 1u);
+                    for (int k = 0; k < ((FOE_ABLATE & 8) ? 1 : CL::NZ / 8); ++k)  // K2 is zero on the lo parts: hi steps only
+                        if (CL::kstep_has_hi(k)) umma_tf32_ts(sb + CL::C_W, sb + CL::C_Z + 8 * k, kt2d + (uint64_t)(k * 64), idesc, 1u);
                     umma_commit(&mb_yfull[j]);
                 }
                 __syncwarp();
@@ -613,16 +624,16 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 point(std::true_type{});
             else
                 point(std::false_type{});
-            {  // Psi {hi, hi, lo, lo} per filter pair over this thread's z1 | z2 columns
+            {  // Psi: the FH hi parts, then the FH lo parts, over this thread's z1 | z2 columns
                 float pr[NF];
 #pragma unroll
                 for (int i = 0; i < FH; i += 2) {
                     const float h0 = tf32_rn(z[i]), h1 = tf32_rn(z[i + 1]);
                     const float2 l2 = __fadd2_rn(make_float2(z[i], z[i + 1]), make_float2(-h0, -h1));
-                    pr[2 * i] = h0;
-                    pr[2 * i + 1] = h1;
-                    pr[2 * i + 2] = tf32_rn_operand(l2.x);
-                    pr[2 * i + 3] = tf32_rn_operand(l2.y);
+                    pr[i] = h0;
+                    pr[i + 1] = h1;
+                    pr[FH + i] = tf32_rn_operand(l2.x);
+                    pr[FH + i + 1] = tf32_rn_operand(l2.y);
                 }
                 tmem_stn<NF>(sd + CL::C_Z, pr);
             }
