@@ -297,22 +297,29 @@ __device__ __forceinline__ void warp_partials_smem(const double (&v)[kNumPartial
     __syncwarp();
 }
 
+// one warp (any) combines the NT / 32 per-warp sums in a fixed tree; the result is in lane 0's x (and in out)
+template <int NT>
+__device__ __forceinline__ void warp_combine(double (*red)[kNumPartials], double *out, double (&x)[kNumPartials]) {
+    const int lane = threadIdx.x & 31;
+    static_assert(NT / 32 <= 32, "one warp combines the per-warp sums");
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) x[k] = lane < NT / 32 ? red[lane][k] : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int k = 0; k < kNumPartials; ++k) x[k] += __shfl_down_sync(0xffffffffu, x[k], off);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < kNumPartials; ++k) out[k] = x[k];
+}
+
 template <int NT>
 __device__ __forceinline__ void block_combine(double (*red)[kNumPartials], double *out) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5;
     __syncthreads();
-    static_assert(NT / 32 <= 32, "one warp combines the per-warp sums");
     if (warp == 0) {
         double x[kNumPartials];
-#pragma unroll
-        for (int k = 0; k < kNumPartials; ++k) x[k] = lane < NT / 32 ? red[lane][k] : 0.0;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-            for (int k = 0; k < kNumPartials; ++k) x[k] += __shfl_down_sync(0xffffffffu, x[k], off);
-        if (lane == 0)
-#pragma unroll
-            for (int k = 0; k < kNumPartials; ++k) out[k] = x[k];
+        warp_combine<NT>(red, out, x);
     }
     __syncthreads();
 }

@@ -174,7 +174,8 @@ struct TcSmem {
     float *img, *Kt, *Yr, *Gr, *s_al, *s_al2;
     double (*red)[kNumPartials];
     double *s_sum;
-    unsigned long long *mb_dfull, *mb_yfull, *mb_aufull, *mb_adfull, *mb_zfull, *mb_pfull, *mb_dfree, *mb_ring, *mb_sum, *mb_img;
+    unsigned long long *mb_dfull, *mb_yfull, *mb_aufull, *mb_adfull, *mb_zfull, *mb_pfull, *mb_dfree, *mb_ring, *mb_sum, *mb_img, *mb_edone;
+    int *s_ticket;
 };
 
 template <int NF>
@@ -183,7 +184,8 @@ __device__ __forceinline__ TcSmem tc_carve(float *sm, double (*red)[kNumPartials
                                            unsigned long long *mb_aufull, unsigned long long *mb_adfull,
                                            unsigned long long *mb_zfull, unsigned long long *mb_pfull,
                                            unsigned long long *mb_dfree, unsigned long long *mb_ring,
-                                           unsigned long long *mb_sum, unsigned long long *mb_img) {
+                                           unsigned long long *mb_sum, unsigned long long *mb_img,
+                                           unsigned long long *mb_edone, int *s_ticket) {
     using T = TcCfg<32>;
     TcSmem S;
     // staged planes, split once into tf32 hi + lo (both rounded to nearest): u_new - shift and du, each cell
@@ -201,6 +203,8 @@ __device__ __forceinline__ TcSmem tc_carve(float *sm, double (*red)[kNumPartials
     S.mb_dfull = mb_dfull; S.mb_yfull = mb_yfull; S.mb_aufull = mb_aufull; S.mb_adfull = mb_adfull; S.mb_zfull = mb_zfull;
     S.mb_pfull = mb_pfull; S.mb_dfree = mb_dfree; S.mb_ring = mb_ring; S.mb_sum = mb_sum;
     S.mb_img = mb_img;
+    S.mb_edone = mb_edone;
+    S.s_ticket = s_ticket;
     return S;
 }
 
@@ -231,6 +235,7 @@ __device__ __forceinline__ void tc_setup(const PassArgs &a, const TcSmem &S, uin
         mbar_init(&S.mb_ring[j], 8);    // Y(j) in the ring: one arrival per warp of the point set
         mbar_init(&S.mb_sum[j], 8);     // g(j) summed: one arrival per mover warp
     }
+    if (tid == T::NBLK) mbar_init(S.mb_edone, 16);  // the energy change summed per warp: one arrival per point warp
     for (int e = tid; e < T::KT * T::YROWS * 4; e += NT) {  // zero columns of the Y ring
         const int col = e & 3, rr = e >> 2;
         S.Yr[rr * T::YW + (col < 2 ? col : T::YW - 4 + col)] = 0.0f;
@@ -254,10 +259,11 @@ __device__ __forceinline__ void tc_cell_offsets(const PassArgs &a, const TileGeo
 }
 
 // One trial (TRIAL) or evaluation pass of this CTA's tile: stage the trial point, the 18-block tensor-core
-// loop, the fold; thread 0 publishes the tile's fp64 partials in buffer `pbuf` of a.partials.  ctl: the
-// image's control block (null in MODE_EVAL); rpar: phase parity of the
-// once-per-pass ring mbarriers; take_ticket: thread 0 then takes the image's ticket (the last CTA reduces
-// and decides).  Returns -1, before touching shared state, if the image is done; else thread 0's ticket.
+// loop, the fold; the z issuer's lane 0 publishes the tile's fp64 partials in buffer `pbuf` of a.partials.
+// ctl: the image's control block (null in MODE_EVAL); rpar: phase parity of the once-per-pass ring
+// mbarriers; take_ticket: that lane then takes the image's ticket (the last CTA reduces and decides) and
+// parks it in *S.s_ticket, valid after the caller's next CTA-wide or BAR_EPI barrier.  Returns -1, before
+// touching shared state, if the image is done; else 0.
 template <int NF, bool TRIAL, bool SYM>
 __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const TileGeom &g, const ImgCtl *ctl,
                                        const int (&coff)[TcCells::CPT], const float (&pob)[TcCells::CPT], unsigned rpar,
@@ -401,6 +407,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     // scratch: the Y ring's data columns 2 .. 65 (its zero columns stay intact), one 32-double row per ring row
     static_assert(T::YW % 2 == 0 && (NT / 32) * (kNumPartials - 1) <= T::KT * T::YROWS, "partial scratch");
     warp_partials_smem<1, kNumPartials, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));
+    if (lane == 0 && (warp < T::W_PT || warp >= T::W_MMA)) red[warp][0] = 0.0;  // partial 0 comes from the point sets
     if (ph && tid == 0) ph[NBLK * 16 + 13] = clock64();  // warp partials
     fence_async_smem();
     tc_fence_before();
@@ -419,6 +426,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     // warp-uniform role index (a shuffle result lets the compiler keep it, and the TMEM addresses derived from
     // it, in uniform registers)
     const int wu = __shfl_sync(0xffffffffu, warp, 0);
+    int early_ticket = 0;
     if (wu >= T::W_MMA) {
         // ================= MMA issuers: one warp each for z(j), dz(j) and the adjoint(j) =================
         // A warp that has issued a batch of tcgen05.mma stalls on its next uniform-datapath instructions until the
@@ -450,6 +458,22 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                     __syncwarp();
                     if (ph) ph[j * 16 + (role == 0 ? 11 : 0)] = clock64();  // z / dz issued
                 }
+            }
+            if (role == 0) {
+                // the z issuer is idle from here: it publishes the tile's partials and takes the image's ticket as
+                // soon as the point sets have summed the last energy terms -- the movers' last shifted sums, the
+                // fold and the ticket's round trip then overlap (the ticket is read after the loop's barrier)
+                mbar_wait(S.mb_edone, 0u);
+                double x[kNumPartials];
+                warp_combine<NT>(red, s_sum, x);
+                if (lane == 0) {
+                    double *parts = a.partials + (((size_t)pbuf * a.tiles_x * a.tiles_y + g.t) * a.B + b) * kPartialStride;
+#pragma unroll
+                    for (int k = 0; k < kNumPartials; ++k) parts[k] = x[k];
+                    // release: this thread's partial stores; acquire: every earlier CTA's
+                    if (take_ticket) early_ticket = (int)ticket_acq_rel(a.tickets + b);
+                }
+                if (ph && lane == 0) ph[NBLK * 16 + 5] = clock64();  // partials published, ticket requested
             }
         } else {
             const uint64_t ktd = umma_desc_kmajor(smem_u32(Kt), 512, 128);
@@ -725,30 +749,23 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             }
         }
         acc[0] = e_own;
+        // the set's warp sums of the energy change, for the z issuer (scratch: the staged u cells, dead once the
+        // last block's operands are built)
+        mbar_wait_sleep(&S.mb_aufull[NBLK - 1], 0u);
+        warp_partials_smem<0, 1, 32>(acc, red, reinterpret_cast<double *>(S.XU));
+        if (lane == 0) mbar_arrive(S.mb_edone);
     }
     tc_fence_before();
     __syncthreads();
     if (ph && tid == 0) ph[NBLK * 16 + 1] = clock64();  // loop end (cycles), CTA (0, 0)
-    // ---- per-tile partials first (last CTA of the image reduces and decides, as k_pass): the ticket's
-    // round trip overlaps the fold below ----
-    warp_partials_smem<0, 1, T::YW / 2>(acc, red, reinterpret_cast<double *>(Yr + 2));  // Y ring no longer live
-    if (ph && tid == 0) ph[NBLK * 16 + 14] = clock64();  // warp partial of the energy change
-    block_combine<NT>(red, s_sum);
-    if (ph && tid == 0) ph[NBLK * 16 + 5] = clock64();  // block reduction done
-    int ticket = 0;
-    if (tid == 0) {  // thread 0 publishes the tile's partials (and takes the ticket); the rest fold meanwhile
-        double *parts = a.partials + (((size_t)pbuf * a.tiles_x * a.tiles_y + g.t) * a.B + b) * kPartialStride;
-#pragma unroll
-        for (int k = 0; k < kNumPartials; ++k) parts[k] = s_sum[k];
-        if (take_ticket) {  // release: this thread's partial stores; acquire: every earlier CTA's
-            ticket = (int)ticket_acq_rel(a.tickets + b);
-        }
-    }
+    // ---- the tile's partials were published and the ticket requested by the z issuer (above); its lane 0 parks
+    // the ticket in shared memory for the CTA's decision path ----
+    if (tid == T::W_MMA * 32) *S.s_ticket = early_ticket;
 
-    // ---- fold padded pixels (symmetric rule) and write the owned gradient: threads [fold_t0, NT) (the
+    // ---- fold padded pixels (symmetric rule) and write the owned gradient: threads [fold_t0, 32 W_MMA) (the
     // rest return to run the image's reduction and decision meanwhile if this CTA is the last) ----
-    if (tid < fold_t0) return ticket;
-    for (int k = tid - fold_t0; k < T::RW * 8; k += NT - fold_t0) {
+    if (tid < fold_t0 || tid >= T::W_MMA * 32) return 0;
+    for (int k = tid - fold_t0; k < T::RW * 8; k += T::W_MMA * 32 - fold_t0) {
         const int xx = k % T::RW, rows0 = k / T::RW;
         const int gx = g.c0 + xx;
         if (gx >= g.c1) continue;
@@ -777,7 +794,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     }
 
     if (ph && tid == fold_t0) ph[NBLK * 16 + 4] = clock64();  // fold done
-    return ticket;
+    return 0;
 }
 
 template <int NF, bool TRIAL, bool SYM>
@@ -788,7 +805,6 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     extern __shared__ __align__(128) float sm[];
     __shared__ double red[NT / 32][kNumPartials];
     __shared__ double s_sum[kNumPartials];
-    __shared__ int s_last;
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) unsigned long long mb_dfull[NBLK], mb_yfull[NBLK], mb_aufull[NBLK], mb_adfull[NBLK], mb_zfull[NBLK];
     __shared__ __align__(8) unsigned long long mb_pfull[NBLK], mb_dfree[NBLK], mb_img;
@@ -813,7 +829,10 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     griddep_launch_dependents();
     const int tyl = blockIdx.x / a.tiles_x, txi = blockIdx.x - tyl * a.tiles_x;
     const TileGeom g = tile_geom<5, SYM>(a, tyl, txi);
-    const TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_aufull, mb_adfull, mb_zfull, mb_pfull, mb_dfree, mb_ring, mb_sum, &mb_img);
+    __shared__ __align__(8) unsigned long long mb_edone;
+    __shared__ int s_ticket;
+    const TcSmem S = tc_carve<NF>(sm, red, s_sum, mb_dfull, mb_yfull, mb_aufull, mb_adfull, mb_zfull, mb_pfull, mb_dfree, mb_ring, mb_sum, &mb_img,
+                                  &mb_edone, &s_ticket);
     tc_setup<NF>(a, S, &s_tmem);
     int coff[TcCells::CPT];
     tc_cell_offsets<SYM>(a, g, coff);
@@ -832,9 +851,9 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
     // reduces and decides while warps 8-23 fold (RW * 8 = 512 items, one each)
     const bool split = !a.band && nlaunch <= kFastReduceTiles && T::RW * 8 <= NT - 256;
     __shared__ ImgCtl s_ctl;
-    const int ticket = tc_body<NF, TRIAL, SYM>(a, S, g, a.mode == MODE_EVAL ? nullptr : a.ctl + b, coff, pob, 0u, 0, !a.band,
-                                               split ? 256 : 0, ph, &s_ctl);
-    if (ticket < 0) {
+    const int live = tc_body<NF, TRIAL, SYM>(a, S, g, a.mode == MODE_EVAL ? nullptr : a.ctl + b, coff, pob, 0u, 0, !a.band,
+                                             split ? 256 : 0, ph, &s_ctl);
+    if (live < 0) {
         __syncthreads();  // image converged: release TMEM and leave
         if (warp == 0) tmem_dealloc(tmem, 512);
         return;
@@ -846,9 +865,10 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         return;
     }
     if (split) {
-        if (warp >= 8) return;  // folded
-        if (tid == 0) s_last = ticket == nlaunch - 1;
-        named_sync(T::BAR_EPI, 256);
+        // warps 8..23 folded, the dz / adjoint issuers are idle; the movers wait for the z issuer's ticket
+        if (warp >= 8 && warp != T::W_MMA) return;
+        named_sync(T::BAR_EPI, 288);
+        if (warp == T::W_MMA) return;
         if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
         if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket seen
         // TMEM is released by warp 7, which takes no part in the reduction (tcgen05.dealloc blocks its warp:
@@ -858,8 +878,8 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
             tmem_dealloc(tmem, 512);
             return;
         }
-        if (!s_last) return;
-        // (no fence: thread 0's acquiring ticket and the barrier above order the loads below)
+        if (s_ticket != nlaunch - 1) return;
+        // (no fence: the z issuer's acquiring ticket and the barrier above order the loads below)
         {  // warps 0..6: the fixed order of reduce_tiles' fast path
             double x = lane_tile_sum(a.partials, nlaunch, a.B, b, warp, lane);
 #pragma unroll
@@ -868,12 +888,11 @@ __global__ void __launch_bounds__(TcCfg<32>::NT, 1) k_pass_tc(const PassArgs a) 
         }
         named_sync(T::BAR_EPI, 224);
     } else {
-        if (tid == 0) s_last = ticket == nlaunch - 1;
         __syncthreads();
         if (a.dbg_times && tid == 0) a.dbg_times[cta * 3 + 2] = globaltimer_ns();
         if (ph && tid == 0) ph[NBLK * 16 + 6] = clock64();  // ticket seen
         if (warp == 0) tmem_dealloc(tmem, 512);
-        if (!s_last) return;
+        if (s_ticket != nlaunch - 1) return;
         reduce_tiles<NT>(a.partials, nlaunch, a.B, b, red, s_sum);
     }
     if (tid == 0) {
