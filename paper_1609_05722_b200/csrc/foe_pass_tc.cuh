@@ -29,7 +29,7 @@
 #define FOE_MMA_SLEEP 0  // ns between the MMA warp's polls of its mbarriers
 #endif
 #ifndef FOE_ABLATE
-#define FOE_ABLATE 0  // timing diagnostics only (results wrong): 1 no shifted sums, 2 no energy series, 4 no psi math, 8 one MMA per sweep, 16 no im2col loads
+#define FOE_ABLATE 0  // timing diagnostics only (results wrong): 1 no shifted sums, 2 no energy series, 4 no psi math, 8 one MMA per sweep, 16 no im2col, 32 im2col without its shared-memory loads, 64 im2col without its TMEM stores
 #endif
 
 template <int NF_MAX>
@@ -142,6 +142,12 @@ __device__ __forceinline__ void tc_im2col(const float4 *xp, uint32_t st) {
     const int e2 = 8 - ((threadIdx.x >> 3) & 1);
 #pragma unroll
     for (int dy = 0; dy < T::M; ++dy) {
+        if (FOE_ABLATE & 32) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) q[8 * dy + i] = __int_as_float(st + i);
+            c[2 * dy] = c[2 * dy + 1] = __int_as_float(st);
+            continue;
+        }
         const float4 a = xp[dy * T::SW], b = xp[dy * T::SW + 2];
         // the pair of p + 4: the left half of cell p + 4 or the right half of cell p + 3 (the same values), by
         // groups of 8 lanes -- 8-byte loads at a 16-byte stride alone use half the banks (2-way conflict)
@@ -149,6 +155,15 @@ __device__ __forceinline__ void tc_im2col(const float4 *xp, uint32_t st) {
         q[8 * dy + 0] = a.x; q[8 * dy + 1] = a.y; q[8 * dy + 2] = a.z; q[8 * dy + 3] = a.w;
         q[8 * dy + 4] = b.x; q[8 * dy + 5] = b.y; q[8 * dy + 6] = b.z; q[8 * dy + 7] = b.w;
         c[2 * dy] = e.x; c[2 * dy + 1] = e.y;
+    }
+    if (FOE_ABLATE & 64) {  // keep the loads live
+        float s = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 40; ++i) s += q[i];
+#pragma unroll
+        for (int i = 0; i < 10; ++i) s += c[i];
+        if (s == 1234.5f) tmem_st2(st + 48, s, s);
+        return;
     }
     tmem_st16(st, *reinterpret_cast<const float(*)[16]>(q));
     tmem_st16(st + 16, *reinterpret_cast<const float(*)[16]>(q + 16));
@@ -517,7 +532,9 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         }
         const float4 *xsrc = (hf == 0 ? S.XU : S.XD) + (pl >> 6) * SW + (pl & 63);
         const int prow = pl >> 6, pcol = pl & 63;
-        for (int j = 0; j < NBLK + T::SUMLAG; ++j) {
+        // (the last iteration sums the last two blocks together: both wait for Y(NBLK-1) and each sum is a
+        // latency-bound step of its own)
+        for (int j = 0; j < NBLK + T::SUMLAG - 1; ++j) {
             if (j < NBLK) {
                 const int s = nst == 2 ? (j & 1) : 0, jp = j - nst;  // block jp used this stage last
                 if (jp >= 0) {  // its MMAs have read it: the z MMAs (u stage) / the whole forward (du stage)
@@ -551,6 +568,10 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                     gsum = hf ? tc_tap_sum<12, 25, true, T>(Yr, r, pcol) : tc_tap_sum<0, 12, true, T>(Yr, r, pcol);
                 else
                     gsum = hf ? tc_tap_sum<12, 25, false, T>(Yr, r, pcol) : tc_tap_sum<0, 12, false, T>(Yr, r, pcol);
+                if (js == NBLK - 2) {
+                    const float gl = hf ? tc_tap_sum<12, 25, true, T>(Yr, r + 2, pcol) : tc_tap_sum<0, 12, true, T>(Yr, r + 2, pcol);
+                    Gr[hf * T::RH * T::RW + (r + 2) * T::RW + pcol] = (FOE_ABLATE & 1) ? 0.0f : gl;
+                }
                 Gr[hf * T::RH * T::RW + r * T::RW + pcol] = gsum;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&S.mb_sum[js]);
