@@ -682,6 +682,13 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 }
                 tmem_stn<NF>(sd + CL::C_Z, pr);
             }
+            // the series' 2 alpha, loaded while the Psi stores drain (the asm statements below are compiler
+            // barriers: left after them, these loads queue behind the movers' im2col traffic on the energy path)
+            float2 al2r[TRIAL ? FH / 2 : 1];
+            if (TRIAL) {
+#pragma unroll
+                for (int i = 0; i < FH; i += 2) al2r[i / 2] = *reinterpret_cast<const float2 *>(s_al2 + f0 + i);
+            }
             tc_wait_st();
             tc_fence_before();
             __syncwarp();
@@ -701,7 +708,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
 #pragma unroll
                     for (int i = 0; i < FH; i += 2) {
                         const float2 t1 = make_float2(dz[i], dz[i + 1]);
-                        const float2 w = __fmul2_rn(*reinterpret_cast<const float2 *>(s_al2 + f0 + i), t1);  // 2 alpha t
+                        const float2 w = __fmul2_rn(al2r[i / 2], t1);  // 2 alpha t
                         if (D == 1) {
                             e = __fadd2_rn(e, w);
                             continue;
