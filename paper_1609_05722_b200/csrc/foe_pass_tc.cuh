@@ -28,6 +28,34 @@
 #ifndef FOE_MMA_SLEEP
 #define FOE_MMA_SLEEP 0  // ns between the MMA warp's polls of its mbarriers
 #endif
+#ifndef FOE_ISSUER_SPIN
+#define FOE_ISSUER_SPIN 1  // MMA issuers: mbarrier.test_wait spin instead of try_wait (a suspended try_wait wakes
+                            // ~300 cycles after the phase completes: 21.25 -> 20.8 us per pass)
+#endif
+__device__ __forceinline__ void tc_issuer_wait(unsigned long long *bar) {
+#if FOE_ISSUER_SPIN
+    while (!mbar_test(bar, 0u)) {
+    }
+#else
+    mbar_wait(bar, 0u);
+#endif
+}
+#ifndef FOE_SPIN_POINT
+#define FOE_SPIN_POINT 2  // point sets' waits for MMA completions spin: bit 0 forward (z, dz), bit 1 adjoint (Y)
+                          // (measured, with spinning issuers: 0 -> 20.8, 1 -> 20.75, 2 -> 20.5, 3 -> 20.6 us per pass)
+#endif
+#ifndef FOE_SPIN_MOVER
+#define FOE_SPIN_MOVER 0  // movers' waits spin: bit 0 stage free, bit 1 ring (measured no different: 20.76 us)
+#endif
+template <bool SPIN>
+__device__ __forceinline__ void tc_wait(unsigned long long *bar, unsigned parity) {
+    if (SPIN) {
+        while (!mbar_test(bar, parity)) {
+        }
+    } else {
+        mbar_wait_sleep(bar, parity);
+    }
+}
 #ifndef FOE_ABLATE
 #define FOE_ABLATE 0  // timing diagnostics only (results wrong): 1 no shifted sums, 2 no energy series, 4 no psi math, 8 one MMA per sweep, 16 no im2col, 32 im2col without its shared-memory loads, 64 im2col without its TMEM stores
 #endif
@@ -457,8 +485,8 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 for (int j = 0; j < NBLK; ++j, sd = sd + CL::REGION == tmem + CL::C_D0 + T::NDREG * CL::REGION ? tmem + CL::C_D0 : sd + CL::REGION,
                          st = st + 1 == CL::NU ? 0 : st + 1) {
                     // its A stage is built and block j-3's Y has left D region j%3
-                    mbar_wait(role == 0 ? &S.mb_aufull[j] : &S.mb_adfull[j], 0u);
-                    if (j >= T::NDREG) mbar_wait(&S.mb_dfree[j - T::NDREG], 0u);
+                    tc_issuer_wait(role == 0 ? &S.mb_aufull[j] : &S.mb_adfull[j]);
+                    if (j >= T::NDREG) tc_issuer_wait(&S.mb_dfree[j - T::NDREG]);
                     tc_fence_after();
                     if (ph) ph[j * 16 + (role == 0 ? 10 : 12)] = clock64();  // z / dz issue starts
                     if (elect_one()) {
@@ -496,7 +524,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             uint32_t sb = tmem + CL::C_D0;  // D region j % 3
             for (int j = 0; j < NBLK; ++j, sb = sb + CL::REGION == tmem + CL::C_D0 + T::NDREG * CL::REGION ? tmem + CL::C_D0 : sb + CL::REGION) {
                 // adjoint(j) once its point set wrote the Psi pairs over z1 | z2
-                mbar_wait(&S.mb_pfull[j], 0u);
+                tc_issuer_wait(&S.mb_pfull[j]);
                 tc_fence_after();
                 if (ph) ph[j * 16 + 13] = clock64();  // adjoint issue starts
                 if (elect_one()) {
@@ -538,8 +566,8 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             if (j < NBLK) {
                 const int s = nst == 2 ? (j & 1) : 0, jp = j - nst;  // block jp used this stage last
                 if (jp >= 0) {  // its MMAs have read it: the z MMAs (u stage) / the whole forward (du stage)
-                    if (hf == 0) mbar_wait_sleep(&S.mb_zfull[jp], 0u);
-                    else if (TRIAL) mbar_wait_sleep(&mb_dfull[jp], 0u);
+                    if (hf == 0) tc_wait<(FOE_SPIN_MOVER & 1) != 0>(&S.mb_zfull[jp], 0u);
+                    else if (TRIAL) tc_wait<(FOE_SPIN_MOVER & 1) != 0>(&mb_dfull[jp], 0u);
                 }
                 tc_fence_after();
                 if (ph && wu == 0) ph[j * 16 + 5] = clock64();  // im2col start
@@ -557,8 +585,8 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             const int js = j - T::SUMLAG;
             if (js >= 0 && js < NBLK) {  // g(js) over this warp's tap half once Y(js-1 .. js+1) are in the ring
                 // (Y(js-1) and Y(js) were awaited by the two previous sums)
-                if (js == 0) mbar_wait_sleep(&S.mb_ring[0], rpar);
-                if (js + 1 < NBLK) mbar_wait_sleep(&S.mb_ring[js + 1], rpar);
+                if (js == 0) tc_wait<(FOE_SPIN_MOVER & 2) != 0>(&S.mb_ring[0], rpar);
+                if (js + 1 < NBLK) tc_wait<(FOE_SPIN_MOVER & 2) != 0>(&S.mb_ring[js + 1], rpar);
                 if (pw && j == 8) pw[2] = clock64();
                 const int r = 2 * js + prow;
                 float gsum;
@@ -599,8 +627,8 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
         double e_own = 0.0;
         int rg = set;  // D region of block j: j % 3
         for (int j = set; j < NBLK; j += 2, rg = rg == 0 ? 2 : rg - 1) {
-            mbar_wait_sleep(&S.mb_zfull[j], 0u);            // z(j) committed
-            if (TRIAL) mbar_wait_sleep(&mb_dfull[j], 0u);  // dz(j) committed
+            tc_wait<(FOE_SPIN_POINT & 1) != 0>(&S.mb_zfull[j], 0u);            // z(j) committed
+            if (TRIAL) tc_wait<(FOE_SPIN_POINT & 1) != 0>(&mb_dfull[j], 0u);  // dz(j) committed
             tc_fence_after();
             const bool pst = ph && (wu - T::W_PT) % 8 == 0;
             if (pst) ph[j * 16 + 1] = clock64();  // forward seen
@@ -752,7 +780,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
             if (pst) ph[j * 16 + 9] = clock64();  // energy terms done
             if (pw && (j >> 1) == 4) pw[3] = clock64();
             {  // Y(j) (the adjoint ran meanwhile): half 0 taps 0..15, half 1 taps 16..24, into ring slot j % RING
-                mbar_wait_sleep(&mb_yfull[j], 0u);
+                tc_wait<(FOE_SPIN_POINT & 2) != 0>(&mb_yfull[j], 0u);
                 tc_fence_after();
                 if (pst) ph[j * 16 + 8] = clock64();  // adjoint seen
                 if (pw && (j >> 1) == 4) pw[4] = clock64();
