@@ -506,7 +506,7 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 // the z issuer is idle from here: it publishes the tile's partials and takes the image's ticket as
                 // soon as the point sets have summed the last energy terms -- the movers' last shifted sums, the
                 // fold and the ticket's round trip then overlap (the ticket is read after the loop's barrier)
-                mbar_wait(S.mb_edone, 0u);
+                tc_issuer_wait(S.mb_edone);
                 double x[kNumPartials];
                 warp_combine<NT>(red, s_sum, x);
                 if (lane == 0) {
