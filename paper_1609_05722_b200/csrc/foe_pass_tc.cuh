@@ -56,6 +56,10 @@ __device__ __forceinline__ void tc_wait(unsigned long long *bar, unsigned parity
         mbar_wait_sleep(bar, parity);
     }
 }
+#ifndef FOE_TAPSPLIT
+#define FOE_TAPSPLIT 10  // the u movers sum taps [0, FOE_TAPSPLIT), the du movers the rest (whole filter rows; the u
+                         // movers are the later ones: measured 8 -> 20.45, 10 -> 20.38, 12 -> 20.54, 15 -> 20.43 us per pass)
+#endif
 #ifndef FOE_ABLATE
 #define FOE_ABLATE 0  // timing diagnostics only (results wrong): 1 no shifted sums, 2 no energy series, 4 no psi math, 8 one MMA per sweep, 16 no im2col, 32 im2col without its shared-memory loads, 64 im2col without its TMEM stores
 #endif
@@ -544,9 +548,9 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
     } else if (wu < T::W_PT) {
         // ================= movers: im2col(j), shifted sum g(j-3) =================
         // warps 0-3 build the u columns, warps 4-7 the du columns; warps w and w+4 share a TMEM lane quarter (the
-        // same 128 pixels) and split the taps of the sum (12 + 13)
+        // same 128 pixels) and split the taps of the sum (10 + 15)
         auto mover = [&](auto HFc) {
-        constexpr int hf = decltype(HFc)::value;  // 0: u columns, taps 0..11; 1: du columns, taps 12..24
+        constexpr int hf = decltype(HFc)::value;  // 0: u columns, taps 0..9; 1: du columns, taps 10..24
         const int pl = tid & 127;
         const uint32_t lane_off = (uint32_t)(32 * (wu & 3)) << 16;
         const int nst = hf == 0 ? CL::NU : CL::ND;
@@ -593,11 +597,11 @@ __device__ __forceinline__ int tc_body(const PassArgs &a, const TcSmem &S, const
                 if (FOE_ABLATE & 1)
                     gsum = 0.0f;
                 else if (js == 0 || js == NBLK - 1)
-                    gsum = hf ? tc_tap_sum<12, 25, true, T>(Yr, r, pcol) : tc_tap_sum<0, 12, true, T>(Yr, r, pcol);
+                    gsum = hf ? tc_tap_sum<FOE_TAPSPLIT, 25, true, T>(Yr, r, pcol) : tc_tap_sum<0, FOE_TAPSPLIT, true, T>(Yr, r, pcol);
                 else
-                    gsum = hf ? tc_tap_sum<12, 25, false, T>(Yr, r, pcol) : tc_tap_sum<0, 12, false, T>(Yr, r, pcol);
+                    gsum = hf ? tc_tap_sum<FOE_TAPSPLIT, 25, false, T>(Yr, r, pcol) : tc_tap_sum<0, FOE_TAPSPLIT, false, T>(Yr, r, pcol);
                 if (js == NBLK - 2) {
-                    const float gl = hf ? tc_tap_sum<12, 25, true, T>(Yr, r + 2, pcol) : tc_tap_sum<0, 12, true, T>(Yr, r + 2, pcol);
+                    const float gl = hf ? tc_tap_sum<FOE_TAPSPLIT, 25, true, T>(Yr, r + 2, pcol) : tc_tap_sum<0, FOE_TAPSPLIT, true, T>(Yr, r + 2, pcol);
                     Gr[hf * T::RH * T::RW + (r + 2) * T::RW + pcol] = (FOE_ABLATE & 1) ? 0.0f : gl;
                 }
                 Gr[hf * T::RH * T::RW + r * T::RW + pcol] = gsum;
