@@ -587,7 +587,9 @@ def main():
                                             "figure); achieved = algorithmic fp32 flops (forward + adjoint, 2400 "
                                             "per pixel) / pass time"},
                 "e2e": {"value": e2e_value, "unit": "Mpixel*iter/s", "ms_per_denoise": float(e2e_t.item()),
-                        "h2d_bytes_per_step": int(y.nbytes),
+                        # the request's validation pass stages the counts as exact floats in page-locked
+                        # memory (_host.stage_counts): the H2D copy moves 4 bytes per pixel
+                        "h2d_bytes_per_step": int(y.size * 4),
                         "d2h_bytes_per_step": int(H * W * (8 + 8))},  # image (f64) + transformed (f64, cast on the device)
                 "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
                 "clocks": clk.summary(),

@@ -71,6 +71,10 @@ int foe_device_sm_count(int device);
 /* DenoiseRequest's count validation (pipeline.py:50-56) on a host float64 array: 0 if every value
  * is >= 0 and integral, 1 otherwise (negative, NaN or fractional); host only, no device work. */
 int foe_counts_check(const double *x, size_t n);
+/* the same validation that also writes every count as a float into dst (a page-locked staging buffer of the
+ * binding: the H2D copy of the counts then needs no separate host pass): 0 valid, 1 invalid, 2 valid but some
+ * count >= 2^24 (not exact as a float: stage the doubles instead); host only. */
+int foe_counts_check_stage(const double *x, size_t n, float *dst);
 /* number of CUDA kernels this library has launched in the process (launch accounting for bench.py) */
 long long foe_kernel_launch_count(void);
 
@@ -86,6 +90,8 @@ int foe_bank_info(const foe_bank *bank, int *n, int *m, int *boundary);
 /* ---- elementwise ------------------------------------------------------------------------------ */
 /* anscombe_forward, anscombe.py:19-24: v = 2 sqrt(y + 3/8) (y validated >= 0 by the caller) */
 int foe_anscombe_forward(const double *y, float *v, int64_t n, void *stream);
+/* the same from counts staged as exact floats (foe_counts_check_stage) */
+int foe_anscombe_forward_f32(const float *y, float *v, int64_t n, void *stream);
 /* denoise_direct obs, pipeline.py:165: obs = where(y == 0, c, y) */
 int foe_direct_obs(const double *y, float *obs, double c, int64_t n, void *stream);
 /* anscombe_inverse_exact_unbiased, anscombe.py:33-51; fp64 output from fp32 z.

@@ -8,6 +8,7 @@ streams, and an event is only ever recorded on the device it was created for.
 """
 from __future__ import annotations
 
+import os
 import threading
 
 import numpy as np
@@ -48,6 +49,47 @@ def upload(arr: np.ndarray):
     np.copyto(host, arr)
     out = torch.empty(arr.shape, dtype=torch.from_numpy(host[:0]).dtype, device=f"cuda:{dev}")
     out.copy_(torch.from_numpy(host), non_blocking=True)
+    ev.record()
+    return out
+
+
+def stage_counts(noisy: np.ndarray):
+    """DenoiseRequest's count validation fused with the staging of the counts (as exact floats) in this thread's
+    page-locked upload buffer: one native pass instead of a validation pass plus a host copy, and an H2D copy of
+    4 bytes per pixel.  Returns (valid, token): token identifies the staged copy for `upload_staged` (None when
+    nothing usable was staged: no CUDA device, or a count too large for an exact float)."""
+    from . import _lib
+    L = _lib.lib()
+    try:
+        import torch
+        cuda = torch.cuda.is_available()
+    except Exception:  # noqa: BLE001 -- validation must work without a usable torch / CUDA
+        cuda = False
+    if not cuda or noisy.size == 0:
+        return (not (noisy.size and L.foe_counts_check(noisy.ctypes.data, noisy.size))), None
+    dev = torch.cuda.current_device()
+    buf, ev = _pinned("upf", noisy.size * 4, dev)
+    ev.synchronize()  # the previous upload from this buffer has been consumed
+    rc = L.foe_counts_check_stage(noisy.ctypes.data, noisy.size, buf.data_ptr())
+    gen = _tls.stage_gen = getattr(_tls, "stage_gen", 0) + 1  # a later staging invalidates this one
+    if rc == 1:
+        return False, None
+    return True, ((os.getpid(), threading.get_ident(), dev, gen) if rc == 0 else None)
+
+
+def upload_staged(token, shape):
+    """The float32 CUDA tensor of counts staged by `stage_counts`, or None if that copy is gone (another request
+    was staged since, or this is another thread or device)."""
+    import torch
+    if token is None:
+        return None
+    pid, tid, dev, gen = token
+    if pid != os.getpid() or tid != threading.get_ident() or dev != torch.cuda.current_device() or gen != getattr(_tls, "stage_gen", 0):
+        return None
+    n = int(np.prod(shape))
+    buf, ev = _pinned("upf", n * 4, dev)
+    out = torch.empty(tuple(shape), dtype=torch.float32, device=f"cuda:{dev}")
+    out.copy_(buf[: n * 4].view(torch.float32).view(tuple(shape)), non_blocking=True)
     ev.record()
     return out
 

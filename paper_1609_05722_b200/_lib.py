@@ -90,11 +90,13 @@ def lib():
     L.foe_abi_version.restype = ctypes.c_int
     L.foe_device_sm_count.argtypes = [ctypes.c_int]
     L.foe_counts_check.argtypes = [_vp, ctypes.c_size_t]
+    L.foe_counts_check_stage.argtypes = [_vp, ctypes.c_size_t, _vp]
     L.foe_kernel_launch_count.restype = ctypes.c_longlong
     L.foe_bank_create.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)]
     L.foe_bank_destroy.argtypes = [_vp]
     L.foe_bank_info.argtypes = [_vp, _vp, _vp, _vp]
     L.foe_anscombe_forward.argtypes = [_vp, _vp, _i64, _vp]
+    L.foe_anscombe_forward_f32.argtypes = [_vp, _vp, _i64, _vp]
     L.foe_direct_obs.argtypes = [_vp, _vp, ctypes.c_double, _i64, _vp]
     L.foe_anscombe_inverse_exact_unbiased.argtypes = [_vp, _vp, _i64, _vp, _vp]
     L.foe_prox_quadratic.argtypes = [_vp, _vp, _vp, ctypes.c_double, _i64, _vp]
@@ -151,8 +153,8 @@ def check(rc: int, what: str = "") -> int:
 
 
 EXPORTED_SYMBOLS = [
-    "foe_abi_version", "foe_last_error", "foe_device_sm_count", "foe_counts_check", "foe_kernel_launch_count", "foe_bank_create", "foe_bank_destroy",
-    "foe_bank_info", "foe_anscombe_forward", "foe_direct_obs", "foe_anscombe_inverse_exact_unbiased",
+    "foe_abi_version", "foe_last_error", "foe_device_sm_count", "foe_counts_check", "foe_counts_check_stage", "foe_kernel_launch_count", "foe_bank_create", "foe_bank_destroy",
+    "foe_bank_info", "foe_anscombe_forward", "foe_anscombe_forward_f32", "foe_direct_obs", "foe_anscombe_inverse_exact_unbiased",
     "foe_prox_quadratic", "foe_prox_idiv", "foe_bin", "foe_unbin_bilinear", "foe_estimate_peak", "foe_convolve_same", "foe_convolve_adjoint",
     "foe_eval_workspace_size", "foe_energy_grad", "foe_solve_workspace_size", "foe_solve",
     "foe_bench_trial_pass", "foe_debug_pass_times", "foe_tc_selftest", "foe_pass_uses_tensor_cores",

@@ -18,6 +18,15 @@ def forward_device(y64, out=None):
     return v
 
 
+def forward_device_f32(y32):
+    """The same from counts staged as exact float32 values (a CUDA tensor) -> float32."""
+    import torch
+    v = torch.empty(y32.shape, dtype=torch.float32, device=y32.device)
+    _lib.check(_lib.lib().foe_anscombe_forward_f32(y32.data_ptr(), v.data_ptr(), y32.numel(),
+                                                   torch.cuda.current_stream().cuda_stream), "anscombe_forward_f32")
+    return v
+
+
 def inverse_exact_unbiased_device(z32, counts=None):
     """Closed-form exact unbiased inverse (anscombe.py:33-51) -> float64 CUDA tensor."""
     import torch

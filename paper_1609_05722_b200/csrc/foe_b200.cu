@@ -400,6 +400,11 @@ __global__ void k_anscombe_fwd(const double *__restrict__ y, float *__restrict__
         v[i] = (float)(2.0 * sqrt(y[i] + 0.375));  // anscombe.py:24
 }
 
+__global__ void k_anscombe_fwd_f32(const float *__restrict__ y, float *__restrict__ v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = (float)(2.0 * sqrt((double)y[i] + 0.375));  // anscombe.py:24, counts staged as exact floats
+}
+
 __global__ void k_direct_obs(const double *__restrict__ y, float *__restrict__ obs, double c, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         obs[i] = (float)(y[i] == 0.0 ? c : y[i]);  // pipeline.py:165
@@ -1338,6 +1343,29 @@ int foe_counts_check(const double *x, size_t n) {
     return 0;
 }
 
+// The same check, writing every count as a float into dst (the caller's page-locked staging buffer) in the same
+// pass: the H2D copy then moves 4 bytes per pixel and needs no separate host copy.  Returns 1 for invalid
+// counts, 2 if every count is valid but one is too large for an exact float (>= 2^24; dst is then unusable),
+// else 0.
+int foe_counts_check_stage(const double *x, size_t n, float *dst) {
+    if ((!x || !dst) && n) return fail(FOE_E_INVALID, "null argument");
+    constexpr double k52 = 4503599627370496.0;
+    int big = 0;
+    for (size_t i0 = 0; i0 < n; i0 += 8192) {
+        const size_t i1 = std::min(n, i0 + 8192);
+        int bad = 0;
+        for (size_t i = i0; i < i1; ++i) {
+            const double v = x[i];
+            const double r = (v + k52) - k52;
+            bad |= !(v >= 0.0) | ((v < k52) & (r != v));
+            big |= !(v < 16777216.0);
+            dst[i] = (float)v;
+        }
+        if (bad) return 1;
+    }
+    return big ? 2 : 0;
+}
+
 int foe_device_sm_count(int device) {
     int v = 0;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
@@ -1425,6 +1453,14 @@ int foe_anscombe_forward(const double *y, float *v, int64_t n, void *stream) {
     if (n <= 0) return FOE_OK;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     k_anscombe_fwd<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(y, v, n);
+    FOE_CUDA(cudaGetLastError());
+    return FOE_OK;
+}
+
+int foe_anscombe_forward_f32(const float *y, float *v, int64_t n, void *stream) {
+    if (n <= 0) return FOE_OK;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_anscombe_fwd_f32<<<grid_1d(n), 256, 0, (cudaStream_t)stream>>>(y, v, n);
     FOE_CUDA(cudaGetLastError());
     return FOE_OK;
 }

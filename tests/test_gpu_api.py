@@ -204,3 +204,29 @@ def test_concurrent_denoise_calls_equal_serial_bitwise():
     for a, b in zip(serial, results):
         np.testing.assert_array_equal(a.image, b.image)
         assert a.trace.L == b.trace.L and a.trace.F == b.trace.F
+
+
+def test_staged_upload_equals_plain_upload_bitwise():
+    """The counts staged by the request's validation pass (float32 in page-locked memory) give exactly the result
+    of the plain float64 upload, which a request falls back to once a later request has reused the staging buffer;
+    counts too large for an exact float are never staged."""
+    from paper_1609_05722_b200 import _host
+
+    model = fp.load_packaged_model("foe_a")
+    _, y = make_counts(96, 80, 3, 2.0)
+    first = fp.DenoiseRequest(noisy=y, peak=2.0, model=model, variant="transform")
+    assert first._staged is not None
+    later = fp.DenoiseRequest(noisy=make_counts(96, 80, 4, 2.0)[1], peak=2.0, model=model, variant="transform")
+    assert _host.upload_staged(first._staged, y.shape) is None  # superseded by `later`: plain upload
+    plain = fp.denoise(first)
+    fresh = fp.DenoiseRequest(noisy=y, peak=2.0, model=model, variant="transform")
+    assert _host.upload_staged(fresh._staged, y.shape) is not None
+    staged = fp.denoise(fresh)
+    again = fp.denoise(fresh)  # the staged copy survives its own use
+    np.testing.assert_array_equal(plain.image, staged.image)
+    np.testing.assert_array_equal(plain.image, again.image)
+    assert plain.trace.L == staged.trace.L and plain.trace.F == staged.trace.F
+    assert later._staged is not None
+    big = y.copy()
+    big[0, 0] = 2.0 ** 24
+    assert fp.DenoiseRequest(noisy=big, peak=2.0, model=model, variant="transform")._staged is None

@@ -197,3 +197,28 @@ def test_cli_exit_codes_without_a_gpu(tmp_path, capsys):
     np.save(tmp_path / "neg.npy", -np.ones((8, 8)))  # invalid counts: a usage-class ValueError
     assert main(["denoise", str(tmp_path / "neg.npy"), str(tmp_path / "o.npy"), "--peak", "1"]) == EXIT_USAGE
     assert main(["denoise", str(tmp_path / "y.npy"), str(tmp_path / "o.npy"), "--peak", "0"]) == EXIT_USAGE
+
+
+def test_counts_check_stage_validates_and_stages():
+    """foe_counts_check_stage: the same verdicts as foe_counts_check, every count written as an exact float,
+    and code 2 (valid, not stageable) as soon as a count needs more than a float's 24 bits."""
+    L = _lib.lib()
+    rng = np.random.default_rng(5)
+    base = rng.poisson(3.0, size=20000).astype(np.float64)
+    dst = np.full(base.size, -1.0, dtype=np.float32)
+    assert L.foe_counts_check_stage(base.ctypes.data, base.size, dst.ctypes.data) == 0
+    np.testing.assert_array_equal(dst.astype(np.float64), base)
+    for pos in (0, 8191, 8192, 19999):
+        for bad in (-1.0, 0.25, np.nan):
+            y = base.copy()
+            y[pos] = bad
+            assert L.foe_counts_check_stage(y.ctypes.data, y.size, dst.ctypes.data) == 1, (pos, bad)
+    for big in (2.0 ** 24, 2.0 ** 24 + 1, 1e300, np.inf):
+        y = base.copy()
+        y[17] = big
+        assert L.foe_counts_check_stage(y.ctypes.data, y.size, dst.ctypes.data) == 2, big
+    y = base.copy()
+    y[17] = 2.0 ** 24 - 1
+    assert L.foe_counts_check_stage(y.ctypes.data, y.size, dst.ctypes.data) == 0
+    assert dst[17] == 2.0 ** 24 - 1
+    assert L.foe_counts_check_stage(None, 0, None) == 0
